@@ -1,0 +1,142 @@
+/* nnb.h -- C ABI of the B200 runtime (libnnb.so) behind the CompiledNN path.
+ *
+ * The reference crosses into native code at exactly one place: the generated
+ * x86 function  void f(float *arena, const float *pool)  that
+ * CompiledNetwork.apply() calls through ctypes
+ *   - pkg/src/nnjit/codegen/executable.py:28      ENTRY_SIGNATURE = CFUNCTYPE(None, c_void_p, c_void_p)
+ *   - pkg/src/nnjit/codegen/executable.py:34-47   ExecutableBuffer(code): map RW, copy, flip RX
+ *   - pkg/src/nnjit/codegen/executable.py:49-50   ExecutableBuffer.__call__(arena, pool)
+ *   - pkg/src/nnjit/runtime.py:44-49              arena + constant-pool allocation
+ *   - pkg/src/nnjit/runtime.py:71-73              CompiledNetwork.apply()
+ *   - pkg/src/nnjit/codegen/hostcheck.py:9-23     check_host() capability gate
+ * This header replaces that boundary one-for-one:
+ *   check_host()              -> nnb_device_check()
+ *   ExecutableBuffer(code)    -> nnb_compile() / nnb_create()  (NVRTC -> cubin -> module)
+ *   arena / pool allocation   -> nnb_create()                  (device arena, weight pool upload)
+ *   entry(arena, pool)        -> nnb_apply()                   (one CUDA-graph replay)
+ *   arena views               -> nnb_arena_ptr()               (device pointers for tensor views)
+ *   CompiledNetwork.run(xs)   -> nnb_run_host()                (H2D, replay, D2H)
+ *   ExecutableBuffer.close()  -> nnb_destroy()
+ * Plain C types only; no torch or CUDA types cross the boundary (streams are
+ * passed as void*).  Every call returns an nnb_status; the message of the
+ * last failure on the calling thread is available from nnb_last_error().
+ */
+#ifndef NNB_H_
+#define NNB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNB_ABI_VERSION 1
+
+typedef enum {
+  NNB_OK = 0,
+  NNB_ERR_ARGUMENT = 1,     /* bad argument / descriptor                  -> ValueError      */
+  NNB_ERR_NO_DRIVER = 2,    /* libcuda.so.1 missing or cuInit failed       -> UnsupportedDevice */
+  NNB_ERR_NO_DEVICE = 3,    /* device index out of range                   -> UnsupportedDevice */
+  NNB_ERR_ARCH = 4,         /* device is not compute capability 10.0       -> UnsupportedDevice */
+  NNB_ERR_NVRTC = 5,        /* libnvrtc missing or compilation failed      -> CompileError    */
+  NNB_ERR_CUDA = 6,         /* a CUDA driver call failed                   -> DeviceError     */
+  NNB_ERR_OOM = 7,          /* device allocation failed                    -> DeviceError     */
+  NNB_ERR_BATCH = 8         /* batch outside [1, max_batch]                -> InputShapeMismatch */
+} nnb_status;
+
+/* One kernel launch of the schedule.  The grid is
+ *   grid.x = ceil(n * items_per_image / items_per_block) * grid_mult
+ * for a replay over n images; the launch is part of the replay only when
+ * n_min <= n <= n_max.  Every kernel has the signature
+ *   void k(const float *pool, float *arena, int n). */
+typedef struct {
+  int32_t kernel;            /* index into the kernel-name list             */
+  uint32_t block;            /* threads per block                           */
+  uint32_t smem_bytes;       /* dynamic shared memory                       */
+  uint32_t grid_mult;
+  uint64_t items_per_image;
+  uint64_t items_per_block;
+  int32_t n_min, n_max;
+} nnb_launch;
+
+/* A network I/O tensor: byte offset in the arena and bytes per image. */
+typedef struct {
+  uint64_t offset;
+  uint64_t image_bytes;
+} nnb_io;
+
+typedef struct {
+  int32_t device;
+  /* kernels: CUDA C++ translation unit + the extern "C" kernel names */
+  const char *source;
+  const char *include_dir;   /* directory of the kernel headers               */
+  const char *cache_dir;     /* cubin cache directory, NULL = no cache        */
+  const char *const *kernel_names;
+  int32_t n_kernels;
+  /* schedule */
+  const nnb_launch *launches;
+  int32_t n_launches;
+  /* memory */
+  const void *pool;          /* weight pool bytes (host)                     */
+  uint64_t pool_bytes;
+  uint64_t arena_bytes;      /* per-image arena * capacity                   */
+  int32_t max_batch;
+  const nnb_io *inputs;
+  int32_t n_inputs;
+  const nnb_io *outputs;
+  int32_t n_outputs;
+} nnb_net_desc;
+
+typedef struct nnb_net nnb_net;
+
+/* Capability gate (replaces hostcheck.check_host): driver present, device
+ * index valid, compute capability 10.x.  Any output pointer may be NULL. */
+nnb_status nnb_device_check(int32_t device, int32_t *cc_major, int32_t *cc_minor,
+                            int32_t *sm_count);
+
+/* Compile a translation unit to an sm_100a cubin with NVRTC (no GPU needed).
+ * When cubin_out is non-NULL it receives a malloc'd buffer the caller frees
+ * with nnb_free().  Used by nnb_create() and by the CPU build check. */
+nnb_status nnb_compile(const char *source, const char *include_dir, const char *cache_dir,
+                       void **cubin_out, uint64_t *cubin_bytes, double *compile_ms);
+
+/* Build a network: compile (or load from cache), upload the pool, allocate
+ * and zero the arena.  CUDA graphs are captured lazily per batch size. */
+nnb_status nnb_create(const nnb_net_desc *desc, nnb_net **out);
+
+/* Device address of arena byte `offset` (for zero-copy tensor views). */
+nnb_status nnb_arena_ptr(nnb_net *net, uint64_t offset, void **dptr);
+
+/* Replay the schedule over the first n images on `stream` (CUstream or NULL
+ * for the legacy default stream).  Asynchronous. */
+nnb_status nnb_apply(nnb_net *net, int32_t n, void *stream);
+
+/* Host-buffer call: copy n images of every input in, replay, copy every
+ * output out, wait for completion.  inputs[i] / outputs[i] are host
+ * pointers (pinned memory is fastest, see nnb_host_alloc). */
+nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs,
+                        void *const *outputs, void *stream);
+
+nnb_status nnb_sync(nnb_net *net, void *stream);
+
+/* Seconds of the last replay measured with CUDA events on `stream`:
+ * nnb_time_apply replays `iters` times between two events. */
+nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms);
+
+nnb_status nnb_host_alloc(uint64_t bytes, void **ptr);
+void nnb_host_free(void *ptr);
+void nnb_free(void *ptr);
+
+/* Introspection */
+nnb_status nnb_net_info(nnb_net *net, uint64_t *arena_bytes, uint64_t *pool_bytes,
+                        int32_t *n_kernels, double *compile_ms, int32_t *cache_hit);
+
+const char *nnb_last_error(void);
+int32_t nnb_abi_version(void);
+void nnb_destroy(nnb_net *net);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNB_H_ */

@@ -1,0 +1,7 @@
+// nnb_kernels.cuh -- umbrella header included by every generated translation
+// unit (paper_1906_05737_b200/kernels.py).
+#pragma once
+#include "nnb_common.cuh"
+#include "nnb_softmax.cuh"
+#include "nnb_small.cuh"
+#include "nnb_gemm_simt.cuh"

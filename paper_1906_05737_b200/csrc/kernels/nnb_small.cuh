@@ -1,0 +1,285 @@
+// nnb_small.cuh -- memory-bound launch units (one thread per output vector).
+//
+// Every kernel here is HBM-bound at the BASELINE shapes, so
+// the design rules are: one pass over the data, float4 along the innermost
+// (channel) axis whenever C % 4 == 0, consecutive threads on consecutive
+// addresses, and no shared memory.  Arithmetic is written with explicit *_rn
+// intrinsics in the reference's operation order, which makes depthwise,
+// pooling, BatchNorm, Add, upsample and concat bit-identical to the
+// interpreter (pkg/src/nnjit/interpreter.py:65-99, 121-122, 166-172).
+#pragma once
+#include "nnb_common.cuh"
+#include "nnb_softmax.cuh"
+
+namespace nnb {
+
+template <int V> struct Vec;
+template <> struct Vec<1> { typedef float T; };
+template <> struct Vec<4> { typedef float4 T; };
+
+__device__ __forceinline__ float lane(const float& v, int) { return v; }
+__device__ __forceinline__ float lane(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set_lane(float& v, int, float x) { v = x; }
+__device__ __forceinline__ void set_lane(float4& v, int i, float x) {
+  if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+}
+template <int V> __device__ __forceinline__ typename Vec<V>::T vzero();
+template <> __device__ __forceinline__ float vzero<1>() { return 0.f; }
+template <> __device__ __forceinline__ float4 vzero<4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+__device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + threadIdx.x; }
+
+// ---------------------------------------------------------------------------
+// Dense for a handful of rows (batch-1 latency path): 32 output columns per
+// block, KS warps split K, partial sums reduced in a fixed order.
+template <class C>
+struct DenseSmallM {
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    __shared__ float red[C::KS][C::MB][32];
+    const int lane_ = threadIdx.x & 31, ks = threadIdx.x >> 5;
+    constexpr int NJ = (C::CO + 31) / 32;
+    const int jb = blockIdx.x % NJ;
+    const int row0 = (blockIdx.x / NJ) * C::MB;
+    const int j = jb * 32 + lane_;
+    const float* x = at<float>(arena, C::IN_OFF);
+    const float* w = at<float>(pool, C::W_OFF);
+    constexpr int KPER = (C::K + C::KS - 1) / C::KS;
+    const int k0 = ks * KPER;
+    const int k1 = k0 + KPER < C::K ? k0 + KPER : C::K;
+    float acc[C::MB];
+#pragma unroll
+    for (int r = 0; r < C::MB; ++r) acc[r] = 0.f;
+    if (j < C::CO) {
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        float wv = __ldg(w + (i64)k * C::CO + j);
+#pragma unroll
+        for (int r = 0; r < C::MB; ++r)
+          if (row0 + r < n) acc[r] = fmaf(__ldg(x + (i64)(row0 + r) * (C::IN_IMG / 4) + k), wv, acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < C::MB; ++r) red[ks][r][lane_] = acc[r];
+    __syncthreads();
+    if (ks != 0) return;                       // warp 0 finishes all rows
+    const bool live = j < C::CO;
+    const float* ps = at<float>(pool, C::PS_OFF);
+    const float* po = at<float>(pool, C::PO_OFF);
+    float* out = at<float>(arena, C::OUT_OFF);
+    const float b = live ? __ldg(at<float>(pool, C::B_OFF) + j) : 0.f;
+#pragma unroll
+    for (int r = 0; r < C::MB; ++r) {
+      if (row0 + r >= n) break;
+      float s = b;
+      for (int q = 0; q < C::KS; ++q) s = s + red[q][r][lane_];
+      float v = finish<C::ACT, C::MODE, C::POST>(s, ps, po, live ? j : 0);
+      if (C::RES && live)
+        v = add(v, __ldg(at<float>(arena, C::RES_OFF) + (i64)(row0 + r) * (C::OUT_IMG / 4) + j));
+      if (C::SOFTMAX) v = softmax_warp_row<C::SMEXP>(v, live);   // CO <= 32
+      if (live) out[(i64)(row0 + r) * (C::OUT_IMG / 4) + j] = v;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// DepthwiseConv2D: acc = bias; taps (ky, kx) in order; mul then add.
+template <class C>
+struct Depthwise {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    constexpr int CG = C::C / V;
+    const i64 t = gtid();
+    if (t >= (i64)n * C::HO * C::WO * CG) return;
+    const int cg = (int)(t % CG);
+    const i64 p = t / CG;
+    const int ox = (int)(p % C::WO);
+    const int oy = (int)((p / C::WO) % C::HO);
+    const i64 img = p / ((i64)C::HO * C::WO);
+    const T* in = at<T>(arena, C::IN_OFF + img * C::IN_IMG);
+    const T* wk = at<T>(pool, C::W_OFF);
+    T acc = at<T>(pool, C::B_OFF)[cg];
+    const int iy0 = oy * C::S - C::PT, ix0 = ox * C::S - C::PL;
+#pragma unroll
+    for (int ky = 0; ky < C::KH; ++ky) {
+      const int iy = iy0 + ky;
+      if (iy < 0 || iy >= C::H) continue;
+#pragma unroll
+      for (int kx = 0; kx < C::KW; ++kx) {
+        const int ix = ix0 + kx;
+        if (ix < 0 || ix >= C::W) continue;
+        T xv = __ldg(in + ((i64)iy * C::W + ix) * CG + cg);
+        T wv = __ldg(wk + (ky * C::KW + kx) * CG + cg);
+#pragma unroll
+        for (int l = 0; l < V; ++l) set_lane(acc, l, add(lane(acc, l), mul(lane(xv, l), lane(wv, l))));
+      }
+    }
+    const float* ps = at<float>(pool, C::PS_OFF);
+    const float* po = at<float>(pool, C::PO_OFF);
+#pragma unroll
+    for (int l = 0; l < V; ++l)
+      set_lane(acc, l, finish<C::ACT, C::MODE, C::POST>(lane(acc, l), ps, po, cg * V + l));
+    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[p % ((i64)C::HO * C::WO) * CG + cg] = acc;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Max / average pooling over in-bounds taps (avg divides by their count,
+// pkg/src/nnjit/interpreter.py:85-95).  Global average pooling is the
+// whole-image window.
+template <class C>
+struct Pool {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    constexpr int CG = C::C / V;
+    const i64 t = gtid();
+    if (t >= (i64)n * C::HO * C::WO * CG) return;
+    const int cg = (int)(t % CG);
+    const i64 p = t / CG;
+    const int ox = (int)(p % C::WO);
+    const int oy = (int)((p / C::WO) % C::HO);
+    const i64 img = p / ((i64)C::HO * C::WO);
+    const T* in = at<T>(arena, C::IN_OFF + img * C::IN_IMG);
+    const int iy0 = oy * C::S - C::PT, ix0 = ox * C::S - C::PL;
+    T acc;
+    const float ninf = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int l = 0; l < V; ++l) set_lane(acc, l, C::AVG ? 0.f : ninf);
+    int count = 0;
+    for (int ky = 0; ky < C::PH; ++ky) {
+      const int iy = iy0 + ky;
+      if (iy < 0 || iy >= C::H) continue;
+      for (int kx = 0; kx < C::PW; ++kx) {
+        const int ix = ix0 + kx;
+        if (ix < 0 || ix >= C::W) continue;
+        T xv = __ldg(in + ((i64)iy * C::W + ix) * CG + cg);
+        ++count;
+#pragma unroll
+        for (int l = 0; l < V; ++l)
+          set_lane(acc, l, C::AVG ? add(lane(acc, l), lane(xv, l)) : fmaxf(lane(acc, l), lane(xv, l)));
+      }
+    }
+    if (C::AVG) {
+      const float cf = (float)count;
+#pragma unroll
+      for (int l = 0; l < V; ++l) set_lane(acc, l, dvd(lane(acc, l), cf));
+    }
+    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[p % ((i64)C::HO * C::WO) * CG + cg] = acc;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Elementwise: n-ary Add (left to right), BatchNorm affine (x*s + o, two
+// roundings), activation -- in the order of emitters.py:115-121.
+template <class C>
+struct Elementwise {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    const i64 t = gtid();
+    constexpr i64 PER = C::ELEMS / V;
+    if (t >= (i64)n * PER) return;
+    const i64 img = t / PER, e = t % PER;
+    T v = at<T>(arena, C::IN0_OFF + img * C::IMG)[e];
+    if (C::NIN > 1) { T w = at<T>(arena, C::IN1_OFF + img * C::IMG)[e];
+#pragma unroll
+      for (int l = 0; l < V; ++l) set_lane(v, l, add(lane(v, l), lane(w, l))); }
+    if (C::NIN > 2) { T w = at<T>(arena, C::IN2_OFF + img * C::IMG)[e];
+#pragma unroll
+      for (int l = 0; l < V; ++l) set_lane(v, l, add(lane(v, l), lane(w, l))); }
+    if (C::NIN > 3) { T w = at<T>(arena, C::IN3_OFF + img * C::IMG)[e];
+#pragma unroll
+      for (int l = 0; l < V; ++l) set_lane(v, l, add(lane(v, l), lane(w, l))); }
+    const float* sc = at<float>(pool, C::S_OFF);
+    const float* of = at<float>(pool, C::O_OFF);
+#pragma unroll
+    for (int l = 0; l < V; ++l) {
+      float x = lane(v, l);
+      if (C::AFFINE) {
+        const int ch = (int)((e * V + l) % C::CH);
+        x = add(mul(x, __ldg(sc + ch)), __ldg(of + ch));
+      }
+      set_lane(v, l, activate<C::ACT, C::MODE>(x));
+    }
+    at<T>(arena, C::OUT_OFF + img * C::IMG)[e] = v;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Nearest-neighbour upsampling by an integer factor.
+template <class C>
+struct Upsample {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    constexpr int CG = C::C / V;
+    constexpr int HO = C::H * C::F, WO = C::W * C::F;
+    const i64 t = gtid();
+    if (t >= (i64)n * HO * WO * CG) return;
+    const int cg = (int)(t % CG);
+    const i64 p = t / CG;
+    const int ox = (int)(p % WO), oy = (int)((p / WO) % HO);
+    const i64 img = p / ((i64)HO * WO);
+    const T* in = at<T>(arena, C::IN_OFF + img * C::IN_IMG);
+    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[((i64)oy * WO + ox) * CG + cg] =
+        in[((i64)(oy / C::F) * C::W + ox / C::F) * CG + cg];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Channel concatenation of up to four sources (rank-1 concat is P == 1).
+template <class C>
+struct Concat {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    constexpr int CG = C::CT / V;
+    const i64 t = gtid();
+    if (t >= (i64)n * C::P * CG) return;
+    const int cg = (int)(t % CG);
+    const i64 p = t / CG;
+    const i64 img = p / C::P, q = p % C::P;
+    int c = cg * V;
+    T v;
+    if (c < C::C0) {
+      v = at<T>(arena, C::OFF0 + img * C::C0 * C::P * 4)[(q * C::C0 + c) / V];
+    } else if (C::NIN < 3 || c < C::C0 + C::C1) {
+      c -= C::C0;
+      v = at<T>(arena, C::OFF1 + img * C::C1 * C::P * 4)[(q * C::C1 + c) / V];
+    } else if (C::NIN < 4 || c < C::C0 + C::C1 + C::C2) {
+      c -= C::C0 + C::C1;
+      v = at<T>(arena, C::OFF2 + img * C::C2 * C::P * 4)[(q * C::C2 + c) / V];
+    } else {
+      c -= C::C0 + C::C1 + C::C2;
+      v = at<T>(arena, C::OFF3 + img * C::C3 * C::P * 4)[(q * C::C3 + c) / V];
+    }
+    at<T>(arena, C::OUT_OFF + img * C::CT * C::P * 4)[p % C::P * CG + cg] = v;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// ZeroPadding2D (and plain copies when all pads are zero).
+template <class C>
+struct Pad {
+  static constexpr int V = C::VEC;
+  typedef typename Vec<V>::T T;
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    constexpr int CG = C::C / V;
+    const i64 t = gtid();
+    if (t >= (i64)n * C::HO * C::WO * CG) return;
+    const int cg = (int)(t % CG);
+    const i64 p = t / CG;
+    const int ox = (int)(p % C::WO), oy = (int)((p / C::WO) % C::HO);
+    const i64 img = p / ((i64)C::HO * C::WO);
+    const int iy = oy - C::PT, ix = ox - C::PL;
+    T v = vzero<V>();
+    if (iy >= 0 && iy < C::H && ix >= 0 && ix < C::W)
+      v = at<T>(arena, C::IN_OFF + img * C::IN_IMG)[((i64)iy * C::W + ix) * CG + cg];
+    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[((i64)oy * C::WO + ox) * CG + cg] = v;
+  }
+};
+
+}  // namespace nnb

@@ -1,0 +1,542 @@
+// nnb_runtime.cpp -- native runtime behind include/nnb.h.
+//
+// Responsibilities:
+//   * capability gate           (replaces pkg/src/nnjit/codegen/hostcheck.py:9-23)
+//   * NVRTC -> sm_100a cubin, with an on-disk cache keyed by the source, the
+//     kernel headers, the NVRTC version and the options
+//     (replaces the x86 encoder + ExecutableBuffer, codegen/executable.py:31-62)
+//   * device weight pool upload and arena allocation (runtime.py:44-49)
+//   * CUDA-graph capture per batch size and replay (runtime.py:71-73)
+//   * host-buffer end-to-end call (runtime.py:75-87)
+//
+// libcuda and libnvrtc are opened with dlopen on first use, so the library
+// loads (and reports a clean status) on machines without a GPU or driver --
+// that is how the CPU test-suite checks the ABI.
+#include "../../include/nnb.h"
+
+#include <cuda.h>
+#include <nvrtc.h>
+#include <dirent.h>
+#include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+nnb_status fail(nnb_status st, const char *fmt, ...) {
+  char buf[4096];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define XSTR(x) STR_(x)
+#define STR_(x) #x
+
+// ---------------------------------------------------------------- driver ----
+struct Cu {
+  void *h = nullptr;
+  bool ok = false;
+  std::string why;
+#define CU_FN(name) decltype(&name) p_##name = nullptr;
+  CU_FN(cuInit) CU_FN(cuDriverGetVersion) CU_FN(cuDeviceGet) CU_FN(cuDeviceGetCount)
+  CU_FN(cuDeviceGetAttribute) CU_FN(cuDevicePrimaryCtxRetain) CU_FN(cuCtxSetCurrent)
+  CU_FN(cuModuleLoadData) CU_FN(cuModuleUnload) CU_FN(cuModuleGetFunction)
+  CU_FN(cuFuncSetAttribute) CU_FN(cuMemAlloc) CU_FN(cuMemFree) CU_FN(cuMemcpyHtoD)
+  CU_FN(cuMemsetD8) CU_FN(cuMemAllocHost) CU_FN(cuMemFreeHost) CU_FN(cuMemcpyHtoDAsync)
+  CU_FN(cuMemcpyDtoHAsync) CU_FN(cuLaunchKernel) CU_FN(cuStreamCreate) CU_FN(cuStreamDestroy)
+  CU_FN(cuStreamSynchronize) CU_FN(cuStreamBeginCapture) CU_FN(cuStreamEndCapture)
+  CU_FN(cuGraphInstantiateWithFlags) CU_FN(cuGraphLaunch) CU_FN(cuGraphDestroy)
+  CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
+  CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
+  CU_FN(cuGetErrorString)
+#undef CU_FN
+  void load() {
+    const char *names[] = {"libcuda.so.1", "libcuda.so"};
+    for (const char *n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { why = "libcuda.so.1 not found (no NVIDIA driver in this process)"; return; }
+#define CU_LOAD(name)                                                        \
+  p_##name = reinterpret_cast<decltype(&name)>(dlsym(h, XSTR(name)));        \
+  if (!p_##name) { why = "libcuda lacks " XSTR(name); return; }
+    CU_LOAD(cuInit) CU_LOAD(cuDriverGetVersion) CU_LOAD(cuDeviceGet) CU_LOAD(cuDeviceGetCount)
+    CU_LOAD(cuDeviceGetAttribute) CU_LOAD(cuDevicePrimaryCtxRetain) CU_LOAD(cuCtxSetCurrent)
+    CU_LOAD(cuModuleLoadData) CU_LOAD(cuModuleUnload) CU_LOAD(cuModuleGetFunction)
+    CU_LOAD(cuFuncSetAttribute) CU_LOAD(cuMemAlloc) CU_LOAD(cuMemFree) CU_LOAD(cuMemcpyHtoD)
+    CU_LOAD(cuMemsetD8) CU_LOAD(cuMemAllocHost) CU_LOAD(cuMemFreeHost) CU_LOAD(cuMemcpyHtoDAsync)
+    CU_LOAD(cuMemcpyDtoHAsync) CU_LOAD(cuLaunchKernel) CU_LOAD(cuStreamCreate)
+    CU_LOAD(cuStreamDestroy) CU_LOAD(cuStreamSynchronize) CU_LOAD(cuStreamBeginCapture)
+    CU_LOAD(cuStreamEndCapture) CU_LOAD(cuGraphInstantiateWithFlags) CU_LOAD(cuGraphLaunch)
+    CU_LOAD(cuGraphDestroy) CU_LOAD(cuGraphExecDestroy) CU_LOAD(cuEventCreate)
+    CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
+    CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString)
+#undef CU_LOAD
+    CUresult r = p_cuInit(0);
+    if (r != CUDA_SUCCESS) {
+      why = "cuInit failed (code " + std::to_string((int)r) + ")";
+      return;
+    }
+    ok = true;
+  }
+};
+
+// ----------------------------------------------------------------- nvrtc ----
+struct Nvrtc {
+  void *h = nullptr;
+  bool ok = false;
+  std::string why;
+#define NV_FN(name) decltype(&name) p_##name = nullptr;
+  NV_FN(nvrtcVersion) NV_FN(nvrtcCreateProgram) NV_FN(nvrtcCompileProgram)
+  NV_FN(nvrtcGetProgramLogSize) NV_FN(nvrtcGetProgramLog) NV_FN(nvrtcGetCUBINSize)
+  NV_FN(nvrtcGetCUBIN) NV_FN(nvrtcDestroyProgram) NV_FN(nvrtcGetErrorString)
+#undef NV_FN
+  void load() {
+    std::vector<std::string> cands;
+    if (const char *e = getenv("NNB_NVRTC")) cands.push_back(e);
+    if (const char *c = getenv("CUDA_HOME")) cands.push_back(std::string(c) + "/lib64/libnvrtc.so.12");
+    cands.push_back("/usr/local/cuda/lib64/libnvrtc.so.12");
+    cands.push_back("libnvrtc.so.12");
+    cands.push_back("libnvrtc.so");
+    for (auto &n : cands) {
+      h = dlopen(n.c_str(), RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) { why = "libnvrtc.so.12 not found"; return; }
+#define NV_LOAD(name)                                                        \
+  p_##name = reinterpret_cast<decltype(&name)>(dlsym(h, XSTR(name)));        \
+  if (!p_##name) { why = "libnvrtc lacks " XSTR(name); return; }
+    NV_LOAD(nvrtcVersion) NV_LOAD(nvrtcCreateProgram) NV_LOAD(nvrtcCompileProgram)
+    NV_LOAD(nvrtcGetProgramLogSize) NV_LOAD(nvrtcGetProgramLog) NV_LOAD(nvrtcGetCUBINSize)
+    NV_LOAD(nvrtcGetCUBIN) NV_LOAD(nvrtcDestroyProgram) NV_LOAD(nvrtcGetErrorString)
+#undef NV_LOAD
+    ok = true;
+  }
+};
+
+std::once_flag g_cu_once, g_nv_once;
+Cu g_cu;
+Nvrtc g_nv;
+
+Cu *cu() {
+  std::call_once(g_cu_once, [] { g_cu.load(); });
+  return &g_cu;
+}
+Nvrtc *nv() {
+  std::call_once(g_nv_once, [] { g_nv.load(); });
+  return &g_nv;
+}
+
+#define CU_CHECK(call)                                                          \
+  do {                                                                          \
+    CUresult r_ = (call);                                                       \
+    if (r_ != CUDA_SUCCESS) {                                                   \
+      const char *s_ = "?";                                                     \
+      if (cu()->p_cuGetErrorString) cu()->p_cuGetErrorString(r_, &s_);          \
+      return fail(r_ == CUDA_ERROR_OUT_OF_MEMORY ? NNB_ERR_OOM : NNB_ERR_CUDA,  \
+                  "%s failed: %s (%d)", #call, s_, (int)r_);                    \
+    }                                                                           \
+  } while (0)
+
+// ------------------------------------------------------------- hashing ----
+uint64_t fnv1a(const std::string &s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
+  return h;
+}
+
+std::string read_file(const std::string &p, bool *ok) {
+  std::ifstream f(p, std::ios::binary);
+  if (!f) { *ok = false; return {}; }
+  std::stringstream ss;
+  ss << f.rdbuf();
+  *ok = true;
+  return ss.str();
+}
+
+std::string headers_digest(const char *dir) {
+  std::vector<std::string> names;
+  if (DIR *d = opendir(dir)) {
+    while (dirent *e = readdir(d)) {
+      std::string n = e->d_name;
+      if (n.size() > 4 && (n.substr(n.size() - 4) == ".cuh" || n.substr(n.size() - 2) == ".h"))
+        names.push_back(n);
+    }
+    closedir(d);
+  }
+  std::sort(names.begin(), names.end());
+  std::string all;
+  for (auto &n : names) {
+    bool ok;
+    all += n + "\n" + read_file(std::string(dir) + "/" + n, &ok);
+  }
+  return all;
+}
+
+const char *kArchOpt = "--gpu-architecture=sm_100a";
+
+nnb_status compile_cubin(const char *source, const char *include_dir, const char *cache_dir,
+                         std::string *cubin, double *ms, bool *hit) {
+  auto t0 = std::chrono::steady_clock::now();
+  *hit = false;
+  Nvrtc *N = nv();
+  if (!N->ok) return fail(NNB_ERR_NVRTC, "%s", N->why.c_str());
+  int vmaj = 0, vmin = 0;
+  N->p_nvrtcVersion(&vmaj, &vmin);
+  std::string inc = std::string("--include-path=") + (include_dir ? include_dir : ".");
+  std::vector<std::string> opts = {kArchOpt, "--std=c++17", inc, "--generate-line-info",
+                                   "-DNNB_NVRTC=1"};
+  std::string key_src = std::string(source) + "\x1f" + headers_digest(include_dir ? include_dir : ".");
+  for (auto &o : opts) key_src += "\x1f" + o;
+  key_src += "\x1f" + std::to_string(vmaj) + "." + std::to_string(vmin);
+  char key[40];
+  snprintf(key, sizeof key, "%016llx%016llx", (unsigned long long)fnv1a(key_src),
+           (unsigned long long)fnv1a(key_src, 0x9e3779b97f4a7c15ull));
+  std::string cpath;
+  if (cache_dir && *cache_dir) {
+    cpath = std::string(cache_dir) + "/" + key + ".cubin";
+    bool ok;
+    std::string c = read_file(cpath, &ok);
+    if (ok && !c.empty()) {
+      *cubin = c;
+      *hit = true;
+      *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      return NNB_OK;
+    }
+  }
+  nvrtcProgram prog;
+  nvrtcResult r = N->p_nvrtcCreateProgram(&prog, source, "nnb_net.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(NNB_ERR_NVRTC, "nvrtcCreateProgram: %s", N->p_nvrtcGetErrorString(r));
+  std::vector<const char *> copts;
+  for (auto &o : opts) copts.push_back(o.c_str());
+  r = N->p_nvrtcCompileProgram(prog, (int)copts.size(), copts.data());
+  size_t logn = 0;
+  N->p_nvrtcGetProgramLogSize(prog, &logn);
+  std::string log(logn, '\0');
+  if (logn) N->p_nvrtcGetProgramLog(prog, &log[0]);
+  if (r != NVRTC_SUCCESS) {
+    N->p_nvrtcDestroyProgram(&prog);
+    if (log.size() > 3500) log = log.substr(0, 3500) + "...";
+    return fail(NNB_ERR_NVRTC, "NVRTC compile failed: %s", log.c_str());
+  }
+  size_t n = 0;
+  N->p_nvrtcGetCUBINSize(prog, &n);
+  cubin->assign(n, '\0');
+  N->p_nvrtcGetCUBIN(prog, &(*cubin)[0]);
+  N->p_nvrtcDestroyProgram(&prog);
+  if (!cpath.empty()) {
+    mkdir(cache_dir, 0755);
+    std::string tmp = cpath + ".tmp." + std::to_string(getpid());
+    {
+      std::ofstream f(tmp, std::ios::binary);
+      f.write(cubin->data(), (std::streamsize)cubin->size());
+    }
+    rename(tmp.c_str(), cpath.c_str());
+  }
+  *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return NNB_OK;
+}
+
+nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
+  Cu *C = cu();
+  if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());
+  int count = 0;
+  CU_CHECK(C->p_cuDeviceGetCount(&count));
+  if (device < 0 || device >= count)
+    return fail(NNB_ERR_NO_DEVICE, "device %d out of range (%d visible)", device, count);
+  CU_CHECK(C->p_cuDeviceGet(dev, device));
+  int maj = 0;
+  CU_CHECK(C->p_cuDeviceGetAttribute(&maj, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, *dev));
+  if (maj != 10)
+    return fail(NNB_ERR_ARCH, "device %d has compute capability %d.x; kernels target sm_100a", device, maj);
+  CU_CHECK(C->p_cuDevicePrimaryCtxRetain(ctx, *dev));
+  CU_CHECK(C->p_cuCtxSetCurrent(*ctx));
+  return NNB_OK;
+}
+
+}  // namespace
+
+struct nnb_net {
+  int device = 0;
+  CUcontext ctx = nullptr;
+  CUmodule mod = nullptr;
+  std::vector<CUfunction> fns;
+  std::vector<nnb_launch> launches;
+  CUdeviceptr arena = 0, pool = 0;
+  uint64_t arena_bytes = 0, pool_bytes = 0;
+  int max_batch = 1;
+  std::vector<nnb_io> inputs, outputs;
+  CUstream capture_stream = nullptr;
+  std::map<int, CUgraphExec> graphs;
+  double compile_ms = 0;
+  bool cache_hit = false;
+  CUevent ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+nnb_status enqueue(nnb_net *net, int n, CUstream s) {
+  Cu *C = cu();
+  for (const nnb_launch &l : net->launches) {
+    if (n < l.n_min || n > l.n_max) continue;
+    uint64_t items = (uint64_t)n * l.items_per_image;
+    uint64_t gx = (items + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
+    if (gx == 0) continue;
+    if (gx > 0x7fffffffull) return fail(NNB_ERR_ARGUMENT, "grid too large (%llu)", (unsigned long long)gx);
+    CUdeviceptr pool = net->pool, arena = net->arena;
+    int nn = n;
+    void *args[] = {&pool, &arena, &nn};
+    CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
+                                 l.smem_bytes, s, args, nullptr));
+  }
+  return NNB_OK;
+}
+
+nnb_status graph_for(nnb_net *net, int n, CUgraphExec *out) {
+  auto it = net->graphs.find(n);
+  if (it != net->graphs.end()) { *out = it->second; return NNB_OK; }
+  Cu *C = cu();
+  CU_CHECK(C->p_cuStreamBeginCapture(net->capture_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+  nnb_status st = enqueue(net, n, net->capture_stream);
+  CUgraph g = nullptr;
+  CUresult r = C->p_cuStreamEndCapture(net->capture_stream, &g);
+  if (st != NNB_OK) { if (g) C->p_cuGraphDestroy(g); return st; }
+  if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "cuStreamEndCapture failed (%d)", (int)r);
+  CUgraphExec ex = nullptr;
+  r = C->p_cuGraphInstantiateWithFlags(&ex, g, 0);
+  C->p_cuGraphDestroy(g);
+  if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "cuGraphInstantiate failed (%d)", (int)r);
+  net->graphs[n] = ex;
+  *out = ex;
+  return NNB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t nnb_abi_version(void) { return NNB_ABI_VERSION; }
+
+const char *nnb_last_error(void) { return g_err.c_str(); }
+
+nnb_status nnb_device_check(int32_t device, int32_t *cc_major, int32_t *cc_minor, int32_t *sm_count) {
+  Cu *C = cu();
+  if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());
+  int count = 0;
+  CU_CHECK(C->p_cuDeviceGetCount(&count));
+  if (device < 0 || device >= count)
+    return fail(NNB_ERR_NO_DEVICE, "device %d out of range (%d visible)", device, count);
+  CUdevice dev;
+  CU_CHECK(C->p_cuDeviceGet(&dev, device));
+  int maj = 0, mnr = 0, sms = 0;
+  CU_CHECK(C->p_cuDeviceGetAttribute(&maj, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, dev));
+  CU_CHECK(C->p_cuDeviceGetAttribute(&mnr, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, dev));
+  CU_CHECK(C->p_cuDeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
+  if (cc_major) *cc_major = maj;
+  if (cc_minor) *cc_minor = mnr;
+  if (sm_count) *sm_count = sms;
+  if (maj != 10)
+    return fail(NNB_ERR_ARCH, "device %d has compute capability %d.%d; kernels target sm_100a",
+                device, maj, mnr);
+  return NNB_OK;
+}
+
+nnb_status nnb_compile(const char *source, const char *include_dir, const char *cache_dir,
+                       void **cubin_out, uint64_t *cubin_bytes, double *compile_ms) {
+  if (!source) return fail(NNB_ERR_ARGUMENT, "source is NULL");
+  std::string cubin;
+  double ms = 0;
+  bool hit = false;
+  nnb_status st = compile_cubin(source, include_dir, cache_dir, &cubin, &ms, &hit);
+  if (st != NNB_OK) return st;
+  if (cubin_bytes) *cubin_bytes = cubin.size();
+  if (compile_ms) *compile_ms = ms;
+  if (cubin_out) {
+    void *p = malloc(cubin.size());
+    if (!p) return fail(NNB_ERR_OOM, "malloc(%zu) failed", cubin.size());
+    memcpy(p, cubin.data(), cubin.size());
+    *cubin_out = p;
+  }
+  return NNB_OK;
+}
+
+void nnb_free(void *p) { free(p); }
+
+nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
+  if (!d || !out || !d->source || d->n_kernels < 0 || d->n_launches < 0 || d->max_batch < 1)
+    return fail(NNB_ERR_ARGUMENT, "invalid nnb_net_desc");
+  for (int i = 0; i < d->n_launches; ++i) {
+    const nnb_launch &l = d->launches[i];
+    if (l.kernel < 0 || l.kernel >= d->n_kernels || l.block == 0 || l.block > 1024 ||
+        l.items_per_block == 0 || l.grid_mult == 0)
+      return fail(NNB_ERR_ARGUMENT, "launch %d is malformed", i);
+  }
+  Cu *C = cu();
+  nnb_net *net = new nnb_net();
+  net->device = d->device;
+  net->max_batch = d->max_batch;
+  CUdevice dev;
+  nnb_status st = device_ctx(d->device, &net->ctx, &dev);
+  if (st != NNB_OK) { delete net; return st; }
+
+  std::string cubin;
+  st = compile_cubin(d->source, d->include_dir, d->cache_dir, &cubin, &net->compile_ms, &net->cache_hit);
+  if (st != NNB_OK) { delete net; return st; }
+  auto bail = [&](nnb_status s) { nnb_destroy(net); return s; };
+  CUresult r = C->p_cuModuleLoadData(&net->mod, cubin.data());
+  if (r != CUDA_SUCCESS) { g_err = "cuModuleLoadData failed (" + std::to_string((int)r) + ")"; return bail(NNB_ERR_CUDA); }
+  net->fns.resize(d->n_kernels);
+  for (int i = 0; i < d->n_kernels; ++i) {
+    r = C->p_cuModuleGetFunction(&net->fns[i], net->mod, d->kernel_names[i]);
+    if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "kernel %s not in module", d->kernel_names[i]); return bail(NNB_ERR_CUDA); }
+  }
+  net->launches.assign(d->launches, d->launches + d->n_launches);
+  for (auto &l : net->launches) {
+    if (l.smem_bytes > 48 * 1024) {
+      r = C->p_cuFuncSetAttribute(net->fns[l.kernel], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                  (int)l.smem_bytes);
+      if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "smem %u bytes rejected", l.smem_bytes); return bail(NNB_ERR_CUDA); }
+    }
+  }
+  net->pool_bytes = d->pool_bytes;
+  net->arena_bytes = d->arena_bytes;
+  r = C->p_cuMemAlloc(&net->pool, std::max<uint64_t>(d->pool_bytes, 256));
+  if (r != CUDA_SUCCESS) { fail(NNB_ERR_OOM, "pool alloc %llu bytes failed", (unsigned long long)d->pool_bytes); return bail(NNB_ERR_OOM); }
+  if (d->pool_bytes) {
+    r = C->p_cuMemcpyHtoD(net->pool, d->pool, d->pool_bytes);
+    if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "pool upload failed (%d)", (int)r); return bail(NNB_ERR_CUDA); }
+  }
+  r = C->p_cuMemAlloc(&net->arena, std::max<uint64_t>(d->arena_bytes, 256));
+  if (r != CUDA_SUCCESS) { fail(NNB_ERR_OOM, "arena alloc %llu bytes failed", (unsigned long long)d->arena_bytes); return bail(NNB_ERR_OOM); }
+  r = C->p_cuMemsetD8(net->arena, 0, std::max<uint64_t>(d->arena_bytes, 256));
+  if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "arena memset failed (%d)", (int)r); return bail(NNB_ERR_CUDA); }
+  net->inputs.assign(d->inputs, d->inputs + d->n_inputs);
+  net->outputs.assign(d->outputs, d->outputs + d->n_outputs);
+  r = C->p_cuStreamCreate(&net->capture_stream, CU_STREAM_NON_BLOCKING);
+  if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "stream create failed"); return bail(NNB_ERR_CUDA); }
+  C->p_cuEventCreate(&net->ev0, CU_EVENT_DEFAULT);
+  C->p_cuEventCreate(&net->ev1, CU_EVENT_DEFAULT);
+  *out = net;
+  return NNB_OK;
+}
+
+nnb_status nnb_arena_ptr(nnb_net *net, uint64_t offset, void **dptr) {
+  if (!net || !dptr || offset > net->arena_bytes) return fail(NNB_ERR_ARGUMENT, "bad arena offset");
+  *dptr = reinterpret_cast<void *>(net->arena + offset);
+  return NNB_OK;
+}
+
+nnb_status nnb_apply(nnb_net *net, int32_t n, void *stream) {
+  if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
+  if (n < 1 || n > net->max_batch)
+    return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
+  Cu *C = cu();
+  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CUgraphExec ex;
+  nnb_status st = graph_for(net, n, &ex);
+  if (st != NNB_OK) return st;
+  CU_CHECK(C->p_cuGraphLaunch(ex, reinterpret_cast<CUstream>(stream)));
+  return NNB_OK;
+}
+
+nnb_status nnb_sync(nnb_net *net, void *stream) {
+  if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
+  CU_CHECK(cu()->p_cuStreamSynchronize(reinterpret_cast<CUstream>(stream)));
+  return NNB_OK;
+}
+
+nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs, void *const *outputs,
+                        void *stream) {
+  if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
+  if (n < 1 || n > net->max_batch)
+    return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
+  Cu *C = cu();
+  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  for (size_t i = 0; i < net->inputs.size(); ++i)
+    CU_CHECK(C->p_cuMemcpyHtoDAsync(net->arena + net->inputs[i].offset, inputs[i],
+                                    (size_t)n * net->inputs[i].image_bytes, s));
+  nnb_status st = nnb_apply(net, n, stream);
+  if (st != NNB_OK) return st;
+  for (size_t i = 0; i < net->outputs.size(); ++i)
+    CU_CHECK(C->p_cuMemcpyDtoHAsync(outputs[i], net->arena + net->outputs[i].offset,
+                                    (size_t)n * net->outputs[i].image_bytes, s));
+  CU_CHECK(C->p_cuStreamSynchronize(s));
+  return NNB_OK;
+}
+
+nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms) {
+  if (!net || iters < 1 || !ms) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  Cu *C = cu();
+  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  CUgraphExec ex;
+  nnb_status st = graph_for(net, n, &ex);
+  if (st != NNB_OK) return st;
+  CU_CHECK(C->p_cuEventRecord(net->ev0, s));
+  for (int i = 0; i < iters; ++i) CU_CHECK(C->p_cuGraphLaunch(ex, s));
+  CU_CHECK(C->p_cuEventRecord(net->ev1, s));
+  CU_CHECK(C->p_cuEventSynchronize(net->ev1));
+  float f = 0;
+  CU_CHECK(C->p_cuEventElapsedTime(&f, net->ev0, net->ev1));
+  *ms = f / iters;
+  return NNB_OK;
+}
+
+nnb_status nnb_host_alloc(uint64_t bytes, void **ptr) {
+  Cu *C = cu();
+  if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());
+  CU_CHECK(C->p_cuMemAllocHost(ptr, bytes));
+  return NNB_OK;
+}
+
+void nnb_host_free(void *ptr) {
+  if (ptr && cu()->ok) cu()->p_cuMemFreeHost(ptr);
+}
+
+nnb_status nnb_net_info(nnb_net *net, uint64_t *arena_bytes, uint64_t *pool_bytes, int32_t *n_kernels,
+                        double *compile_ms, int32_t *cache_hit) {
+  if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
+  if (arena_bytes) *arena_bytes = net->arena_bytes;
+  if (pool_bytes) *pool_bytes = net->pool_bytes;
+  if (n_kernels) *n_kernels = (int32_t)net->fns.size();
+  if (compile_ms) *compile_ms = net->compile_ms;
+  if (cache_hit) *cache_hit = net->cache_hit ? 1 : 0;
+  return NNB_OK;
+}
+
+void nnb_destroy(nnb_net *net) {
+  if (!net) return;
+  Cu *C = cu();
+  if (C->ok) {
+    C->p_cuCtxSetCurrent(net->ctx);
+    for (auto &kv : net->graphs) C->p_cuGraphExecDestroy(kv.second);
+    if (net->ev0) C->p_cuEventDestroy(net->ev0);
+    if (net->ev1) C->p_cuEventDestroy(net->ev1);
+    if (net->capture_stream) C->p_cuStreamDestroy(net->capture_stream);
+    if (net->arena) C->p_cuMemFree(net->arena);
+    if (net->pool) C->p_cuMemFree(net->pool);
+    if (net->mod) C->p_cuModuleUnload(net->mod);
+  }
+  delete net;
+}
+
+}  // extern "C"

@@ -1,0 +1,402 @@
+"""compile() back half: specialise every launch unit into sm_100a CUDA.
+
+This replaces the reference's machine-code emitters (pkg/src/nnjit/codegen/
+compile.py:25-51, emitters.py:651-667).  Where the reference bakes arena and
+constant-pool displacements into x86 instructions, we bake them into a
+``struct Cfg_uNN`` of ``constexpr`` members and instantiate one of the kernel
+templates under ``csrc/kernels`` with it.  NVRTC (inside the C-ABI runtime)
+compiles the whole translation unit for sm_100a, so every loop bound, stride,
+offset and padding split is a compile-time constant -- the paper's runtime
+specialisation idea, with the device doing the arithmetic.
+
+Every kernel has the same entry signature as the reference's generated
+function (``f(arena, pool)``, pkg/README.md:187) plus the batch count:
+``void k(const float* pool, float* arena, int n)``.
+
+Outputs: the CUDA source, a list of :class:`Launch` records and the device
+weight pool (a deduplicated, 256-byte aligned blob, cf. codegen/pool.py).
+"""
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import UnsupportedLayer
+from .graph import same_padding
+
+F32 = np.float32
+
+ACT_CODE = {"linear": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "relu6": 4, "elu": 5}
+MODE_CODE = {"rational": 0, "fast": 1, "exact": 2}
+SMEXP_CODE = {"fast": 0, "precise": 1, "exact": 2}
+
+SMALL_M = 8           # Dense rows at or below this use the split-K GEMV kernel
+ELEM_BLOCK = 256
+
+
+@dataclass
+class Launch:
+    """One kernel launch of the schedule (mirrors ``nnb_launch`` in
+    include/nnb.h)."""
+    kernel: str
+    block: int
+    smem: int
+    items_per_image: int
+    items_per_block: int
+    grid_mult: int = 1
+    n_min: int = 1
+    n_max: int = 1 << 30
+    unit: int = -1
+    note: str = ""
+
+
+class DevicePool:
+    """Deduplicated weight/constant blob; every entry 256-byte aligned."""
+
+    def __init__(self):
+        self.data = bytearray()
+        self._seen = {}
+
+    def add(self, arr):
+        raw = np.ascontiguousarray(arr, dtype="<f4").tobytes()
+        key = hashlib.sha1(raw).digest() + len(raw).to_bytes(8, "little")
+        if key in self._seen:
+            return self._seen[key]
+        off = len(self.data)
+        self.data += raw
+        self.data += bytes((-len(self.data)) % 256)
+        self._seen[key] = off
+        return off
+
+    def zeros_offset(self, n):
+        return self.add(np.zeros(max(n, 1), F32))
+
+
+@dataclass
+class Specialization:
+    source: str
+    launches: list
+    pool: bytes
+    kernel_names: list
+    notes: dict = field(default_factory=dict)
+
+
+def _cfg_struct(name, fields):
+    lines = [f"struct {name} {{"]
+    for k, v in fields.items():
+        if isinstance(v, bool):
+            v = int(v)
+        lines.append(f"  static constexpr long long {k} = {int(v)}LL;")
+    lines.append("};")
+    return "\n".join(lines)
+
+
+def _pad4(x):
+    return (x + 3) // 4 * 4
+
+
+class Specializer:
+    def __init__(self, plan, assignment, options, max_batch, capacity):
+        self.plan = plan
+        self.asg = assignment
+        self.opt = options
+        self.max_batch = max_batch
+        self.cap = capacity
+        self.pool = DevicePool()
+        self.chunks = []
+        self.launches = []
+        self.names = []
+
+    # -- helpers -----------------------------------------------------------
+    def arena_off(self, tid):
+        return self.asg.offsets[tid][0] * self.cap
+
+    def img_bytes(self, tid):
+        return 4 * self.plan.tensors[tid].elements
+
+    def emit(self, unit_pos, tag, template, fields, block, smem, ipi, ipb,
+             grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note=""):
+        kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
+        cfg = f"Cfg_{len(self.names)}"
+        body = _cfg_struct(cfg, fields)
+        if dynamic_smem:
+            call = (f"  extern __shared__ __align__(16) unsigned char nnb_smem[];\n"
+                    f"  {template}<{cfg}>::run(pool, arena, n, "
+                    f"*reinterpret_cast<{template}<{cfg}>::Smem*>(nnb_smem));\n")
+        else:
+            call = f"  {template}<{cfg}>::run(pool, arena, n);\n"
+        body += (f"\nextern \"C\" __global__ void __launch_bounds__({block}) {kname}("
+                 f"const float* __restrict__ pool, float* __restrict__ arena, int n) {{\n"
+                 + call + "}\n")
+        self.chunks.append(body)
+        self.names.append(kname)
+        self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min,
+                                    n_max, unit_pos, note))
+
+    def epilogue_fields(self, u, co):
+        ps = po = self.pool.zeros_offset(co)
+        post = u.post_scale is not None
+        if post:
+            ps, po = self.pool.add(u.post_scale), self.pool.add(u.post_offset)
+        return dict(ACT=ACT_CODE[u.activation], MODE=MODE_CODE[self.opt.activation_mode],
+                    POST=post, PS_OFF=ps, PO_OFF=po)
+
+    # -- unit kinds ----------------------------------------------------------
+    def gemm(self, pos, u):
+        """Conv2D (any window) and Dense through the FFMA implicit GEMM."""
+        x = u.input_shapes[0]
+        if u.kind == "Dense":
+            H = W = 1
+            CI = x.elements
+            KH = KW = S = 1
+            PT = PL = 0
+            CO = u.kernel.shape[1]
+            HO = WO = 1
+            wmat = np.asarray(u.kernel, F32)
+        else:
+            H, W, CI = x.dims
+            KH, KW = u.kernel_hw
+            S = u.stride
+            conv_out = u.pre_pool_shape if u.pool_after else u.output_shape
+            HO, WO, CO = conv_out.dims
+            if u.padding == "same":
+                PT, PL = same_padding(H, KH, S)[0], same_padding(W, KW, S)[0]
+            else:
+                PT = PL = 0
+            wmat = np.asarray(u.kernel, F32).reshape(KH * KW * CI, CO)
+        K = KH * KW * CI
+        pool_fused = bool(u.pool_after)
+        if pool_fused:
+            PHO, PWO = u.output_shape.h, u.output_shape.w
+            rows = PHO * PWO * 4
+        else:
+            PHO = PWO = 1
+            rows = HO * WO
+        softmax = bool(u.softmax_after)
+
+        if u.kind == "Dense" and self.max_batch > 0:
+            # batch-1 latency path: split-K GEMV (also used for tiny batches)
+            self._dense_small(pos, u, wmat, CI, CO, softmax,
+                              n_max=min(SMALL_M, self.max_batch))
+            if self.max_batch <= SMALL_M:
+                return
+            n_min = SMALL_M + 1
+        else:
+            n_min = 1
+
+        # tile shape
+        if softmax:
+            TN = _pad4(CO)
+            NTX = 1
+            TM = 4 if TN <= 16 else 2
+        elif CO <= 4:
+            TN, NTX, TM = 4, 1, 4
+        elif CO <= 8:
+            TN, NTX, TM = 8, 1, 4 if K > 32 else 2
+        elif CO <= 16:
+            TN, NTX, TM = 8, 2, 4
+        elif CO <= 32:
+            TN, NTX, TM = 8, 4, 8
+        else:
+            TN, NTX, TM = 8, 8, 8
+        if pool_fused and TM % 4:
+            TM = 4
+        NT = 128
+        BN = TN * NTX
+        BM = TM * (NT // NTX)
+        if K <= 16:
+            BK = _pad4(K)
+        else:
+            BK = 8 if BM >= 256 else 16
+        avec = CI % 4 == 0 and BK % 4 == 0
+        akv = 4 if avec else 1
+        while (BM * BK) % (akv * NT):
+            BK += 4 if avec else 1
+        ntile_n = (CO + BN - 1) // BN
+        smem = 4 * (2 * BK * (BM + 4) + 2 * BK * (BN + 4))
+
+        wo = self.pool.add(wmat)
+        bo = self.pool.add(u.bias)
+        fields = dict(
+            H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
+            K=K, ROWS=rows, POOL=pool_fused, PHO=PHO, PWO=PWO,
+            IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+            OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+            W_OFF=wo, B_OFF=bo,
+            RES=u.residual_id is not None,
+            RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
+            RES_FIRST=False,
+            SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
+            BM=BM, BN=BN, BK=BK, TM=TM, TN=TN)
+        fields.update(self.epilogue_fields(u, CO))
+        tag = "dense" if u.kind == "Dense" else f"conv{KH}x{KW}"
+        self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
+                  grid_mult=ntile_n, n_min=n_min, dynamic_smem=True,
+                  note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
+
+    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max):
+        MB = n_max
+        KS = max(1, min(32, K // 32))
+        fields = dict(K=K, CO=CO, MB=MB, KS=KS,
+                      IN_OFF=self.arena_off(u.input_ids[0]),
+                      IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                      W_OFF=self.pool.add(wmat), B_OFF=self.pool.add(u.bias),
+                      SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
+                      RES=u.residual_id is not None,
+                      RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
+        fields.update(self.epilogue_fields(u, CO))
+        if softmax and CO > 32:
+            raise UnsupportedLayer("fused softmax needs <= 32 units")
+        nj = (CO + 31) // 32
+        self.emit(pos, "gemv", "nnb::DenseSmallM", fields, 32 * KS, 0, 1, MB,
+                  grid_mult=nj, n_max=n_max, note=f"gemv K={K} N={CO} ks={KS}")
+
+    def depthwise(self, pos, u):
+        H, W, C = u.input_shapes[0].dims
+        HO, WO, _ = u.output_shape.dims
+        KH, KW = u.kernel_hw
+        S = u.stride
+        PT = same_padding(H, KH, S)[0] if u.padding == "same" else 0
+        PL = same_padding(W, KW, S)[0] if u.padding == "same" else 0
+        vec = 4 if C % 4 == 0 else 1
+        fields = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
+                      VEC=vec, IN_OFF=self.arena_off(u.input_ids[0]),
+                      IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                      W_OFF=self.pool.add(u.kernel), B_OFF=self.pool.add(u.bias))
+        fields.update(self.epilogue_fields(u, C))
+        self.emit(pos, f"dw{KH}x{KW}", "nnb::Depthwise", fields, ELEM_BLOCK, 0,
+                  HO * WO * (C // vec), ELEM_BLOCK)
+
+    def pool_unit(self, pos, u):
+        H, W, C = u.input_shapes[0].dims
+        PH, PW = u.kernel_hw
+        S = u.stride
+        if u.output_shape.rank == 1:
+            HO = WO = 1
+        else:
+            HO, WO = u.output_shape.h, u.output_shape.w
+        PT = same_padding(H, PH, S)[0] if u.padding == "same" else 0
+        PL = same_padding(W, PW, S)[0] if u.padding == "same" else 0
+        vec = 4 if C % 4 == 0 else 1
+        fields = dict(H=H, W=W, C=C, HO=HO, WO=WO, PH=PH, PW=PW, S=S, PT=PT, PL=PL,
+                      AVG=u.pool_op == "avg", VEC=vec,
+                      IN_OFF=self.arena_off(u.input_ids[0]),
+                      IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id))
+        tag = ("gap" if (HO, WO) == (1, 1) and (PH, PW) == (H, W)
+               else f"{u.pool_op}pool{PH}x{PW}")
+        self.emit(pos, tag, "nnb::Pool", fields, ELEM_BLOCK, 0,
+                  HO * WO * (C // vec), ELEM_BLOCK)
+
+    def elementwise(self, pos, u):
+        shape = u.output_shape
+        elems = shape.elements
+        ch = shape.dims[-1]
+        vec = 4 if (elems % 4 == 0 and (u.scale is None or ch % 4 == 0)) else 1
+        ins = list(u.input_ids)
+        first = True
+        out = u.output_id
+        while ins:
+            take = ins[:4] if first else ins[:3]
+            ins = ins[len(take):]
+            srcs = take if first else [out] + take
+            fields = dict(ELEMS=elems, IMG=4 * elems, VEC=vec, NIN=len(srcs),
+                          OUT_OFF=self.arena_off(out), CH=ch)
+            for k in range(4):
+                fields[f"IN{k}_OFF"] = self.arena_off(srcs[k]) if k < len(srcs) else 0
+            last = not ins
+            affine = u.scale is not None and last
+            fields.update(AFFINE=affine,
+                          S_OFF=self.pool.add(u.scale) if affine else 0,
+                          O_OFF=self.pool.add(u.offset) if affine else 0,
+                          ACT=ACT_CODE[u.activation] if last else 0,
+                          MODE=MODE_CODE[self.opt.activation_mode])
+            tag = "add" if u.kind == "Add" else ("bn" if u.scale is not None else "act")
+            self.emit(pos, tag, "nnb::Elementwise", fields, ELEM_BLOCK, 0,
+                      elems // vec, ELEM_BLOCK)
+            first = False
+
+    def softmax(self, pos, u):
+        shape = u.output_shape
+        L = shape.dims[-1]
+        rows = shape.elements // L
+        per_thread = L <= 16
+        if L > 2048:
+            raise UnsupportedLayer(f"softmax rows longer than 2048 ({L})")
+        fields = dict(IN_OFF=self.arena_off(u.input_ids[0]), OUT_OFF=self.arena_off(u.output_id),
+                      ROWS=rows, L=L, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
+                      PER_THREAD=per_thread)
+        if per_thread:
+            self.emit(pos, "softmax", "nnb::SoftmaxRows", fields, 128, 0, rows, 128)
+        else:
+            self.emit(pos, "softmax", "nnb::SoftmaxRows", fields, 128, 0, rows, 4)
+
+    def upsample(self, pos, u):
+        H, W, C = u.input_shapes[0].dims
+        vec = 4 if C % 4 == 0 else 1
+        fields = dict(H=H, W=W, C=C, F=u.factor, VEC=vec,
+                      IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id))
+        self.emit(pos, "upsample", "nnb::Upsample", fields, ELEM_BLOCK, 0,
+                  H * W * u.factor * u.factor * (C // vec), ELEM_BLOCK)
+
+    def concat(self, pos, u):
+        shapes = u.input_shapes
+        if u.output_shape.rank == 1:
+            P, chans = 1, [s.dims[0] for s in shapes]
+        else:
+            P, chans = shapes[0].h * shapes[0].w, [s.c for s in shapes]
+        if len(shapes) > 4:
+            raise UnsupportedLayer("Concatenate of more than four tensors")
+        CT = sum(chans)
+        vec = 4 if all(c % 4 == 0 for c in chans) else 1
+        fields = dict(P=P, CT=CT, NIN=len(chans), VEC=vec,
+                      OUT_OFF=self.arena_off(u.output_id))
+        for k in range(4):
+            fields[f"C{k}"] = chans[k] if k < len(chans) else 0
+            fields[f"OFF{k}"] = self.arena_off(u.input_ids[k]) if k < len(chans) else 0
+        self.emit(pos, "concat", "nnb::Concat", fields, ELEM_BLOCK, 0, P * CT // vec, ELEM_BLOCK)
+
+    def pad(self, pos, u):
+        H, W, C = u.input_shapes[0].dims
+        HO, WO, _ = u.output_shape.dims
+        (t, _b), (l, _r) = u.pad
+        vec = 4 if C % 4 == 0 else 1
+        fields = dict(H=H, W=W, C=C, HO=HO, WO=WO, PT=t, PL=l, VEC=vec,
+                      IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id))
+        self.emit(pos, "zeropad", "nnb::Pad", fields, ELEM_BLOCK, 0, HO * WO * (C // vec),
+                  ELEM_BLOCK)
+
+    def run(self):
+        for pos, u in enumerate(self.plan.units):
+            if u.kind in ("Dense", "Conv2D"):
+                self.gemm(pos, u)
+            elif u.kind == "DepthwiseConv2D":
+                if u.residual_id is not None or u.pool_after or u.softmax_after:
+                    raise UnsupportedLayer("depthwise epilogue fusion")
+                self.depthwise(pos, u)
+            elif u.kind == "Pool":
+                self.pool_unit(pos, u)
+            elif u.kind in ("ElementwiseActivation", "Add"):
+                self.elementwise(pos, u)
+            elif u.kind == "Softmax":
+                self.softmax(pos, u)
+            elif u.kind == "Upsample":
+                self.upsample(pos, u)
+            elif u.kind == "Concat":
+                self.concat(pos, u)
+            elif u.kind == "Pad":
+                self.pad(pos, u)
+            else:
+                raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
+        src = ('#include "nnb_kernels.cuh"\n\n' + "\n\n".join(self.chunks) + "\n")
+        return Specialization(source=src, launches=self.launches,
+                              pool=bytes(self.pool.data), kernel_names=list(self.names))
+
+
+def specialize(plan, assignment, options, max_batch, capacity):
+    return Specializer(plan, assignment, options, max_batch, capacity).run()

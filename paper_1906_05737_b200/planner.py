@@ -1,0 +1,414 @@
+"""compile() front half: lower the graph to launch units and fuse them.
+
+Two groups of rewrites run in order:
+
+1. The reference fusions, restated from pkg/src/nnjit/optimizer.py so that
+   folded weights are bit-identical to the reference's:
+
+   * ``fuse_activation`` (:220-242) -- a standalone activation joins the
+     matvec unit immediately before it;
+   * ``fuse_batchnorm`` (:286-325) -- BatchNorm folds into the producer's
+     weights (case a), into the next Dense / 'valid' conv (case b, float64
+     bias correction), or becomes a post-activation affine (case c);
+   * both alternate to a fixpoint (``build_plan`` :328-341).
+
+   A fusion needs the intermediate tensor to have exactly one consumer and to
+   not be a network input/output (:189-193).
+
+2. B200 epilogue fusions (new; each removes one launch and one HBM round
+   trip of the intermediate tensor):
+
+   * ``fuse_pool``     -- MaxPool 2x2/2 into the producing Conv2D's epilogue;
+   * ``fuse_residual`` -- a binary Add into the epilogue of its later producer;
+   * ``fuse_softmax``  -- a softmax over <= 32 values per row into the
+     producing Dense / Conv2D epilogue.
+
+The result is a :class:`FusionPlan` whose units map one-to-one onto
+specialised sm_100a kernels (kernels.py).
+"""
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .errors import UnsupportedLayer
+from .graph import TensorShape
+from .model_format import layer_weights
+
+F32 = np.float32
+MATVEC_KINDS = ("Dense", "Conv2D", "DepthwiseConv2D")
+GEMM_KINDS = ("Dense", "Conv2D")
+SOFTMAX_FUSE_MAX = 32
+
+
+@dataclass
+class CompilationUnit:
+    uid: int
+    kind: str          # Dense Conv2D DepthwiseConv2D Pool ElementwiseActivation
+                       # Add Softmax Upsample Concat Copy Pad
+    name: str
+    input_ids: tuple
+    output_id: int
+    input_shapes: tuple
+    output_shape: object
+    kernel: object = None
+    bias: object = None
+    activation: str = "linear"
+    post_scale: object = None
+    post_offset: object = None
+    scale: object = None
+    offset: object = None
+    stride: int = 1
+    padding: str = "valid"
+    kernel_hw: tuple = None
+    pool_op: str = None
+    factor: int = 1
+    in_place_preference: int = None
+    # -- B200 additions --
+    pad: tuple = None               # Pad: ((top, bottom), (left, right))
+    pool_after: bool = False        # fused 2x2/2 max-pool epilogue
+    pre_pool_shape: object = None   # conv output shape before the fused pool
+    residual_id: int = None         # fused residual Add: tensor added last
+    softmax_after: bool = False     # fused row softmax epilogue
+
+    def describe(self):
+        bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
+        if self.kind in ("Conv2D", "DepthwiseConv2D", "Pool"):
+            kh, kw = self.kernel_hw
+            bits.append(f"{self.pool_op or ''}{kh}x{kw}/s{self.stride} {self.padding}")
+        if self.activation != "linear":
+            bits.append(f"act={self.activation}")
+        if self.post_scale is not None:
+            bits.append("post_bn")
+        if self.scale is not None:
+            bits.append("affine")
+        if self.pool_after:
+            bits.append("+maxpool2")
+        if self.residual_id is not None:
+            bits.append(f"+add(t{self.residual_id})")
+        if self.softmax_after:
+            bits.append("+softmax")
+        if self.in_place_preference is not None:
+            bits.append("in_place?")
+        return " ".join(bits)
+
+
+@dataclass
+class FusionPlan:
+    units: list
+    tensors: dict                  # tensor id -> TensorShape (per image)
+    input_ids: tuple
+    output_ids: tuple
+    node_units: dict = field(default_factory=dict)
+
+    def producer_positions(self):
+        return {u.output_id: p for p, u in enumerate(self.units)}
+
+    def consumer_count(self, tid):
+        return (sum(t == tid for u in self.units for t in self._reads(u))
+                + sum(t == tid for t in self.output_ids))
+
+    @staticmethod
+    def _reads(u):
+        return u.input_ids + ((u.residual_id,) if u.residual_id is not None else ())
+
+    def describe(self):
+        return "\n".join(f"  [{p:2d}] t{u.output_id:<3d} {u.describe()}"
+                         for p, u in enumerate(self.units))
+
+
+# ---------------------------------------------------------------------------
+# lowering
+
+def lower_to_units(graph):
+    """One unit per layer; Flatten is a relabel (NHWC row-major == flat)."""
+    alias = {}
+
+    def res(t):
+        while t in alias:
+            t = alias[t]
+        return t
+
+    units, tensors, node_units = [], {}, {}
+    next_tid = len(graph.nodes)
+
+    def add_unit(**kw):
+        u = CompilationUnit(uid=len(units), **kw)
+        units.append(u)
+        tensors[u.output_id] = u.output_shape
+        return u
+
+    for idx in graph.order:
+        node = graph.nodes[idx]
+        kind, cfg, shape = node.kind, node.config, node.output_shape
+        w = layer_weights(node.spec, graph.weights) if node.spec.weight_refs else {}
+        ins = tuple(res(i) for i in node.input_ids)
+        in_shapes = tuple(graph.nodes[i].output_shape for i in node.input_ids)
+        common = dict(name=node.name, input_ids=ins, output_id=idx,
+                      input_shapes=in_shapes, output_shape=shape)
+        if kind == "Input":
+            tensors[idx] = shape
+            node_units[idx] = None
+            continue
+        if kind == "Flatten":
+            alias[idx] = ins[0]
+            node_units[idx] = None
+            continue
+        zeros = lambda n: np.zeros(n, dtype=F32)
+        if kind == "Dense":
+            u = add_unit(kind="Dense", kernel=w["kernel"],
+                         bias=w.get("bias", zeros(cfg["units"])),
+                         activation=cfg["activation"], **common)
+        elif kind in ("Conv2D", "DepthwiseConv2D"):
+            nb = cfg["filters"] if kind == "Conv2D" else in_shapes[0].c
+            u = add_unit(kind=kind, kernel=w["kernel"], bias=w.get("bias", zeros(nb)),
+                         activation=cfg["activation"], stride=cfg["strides"],
+                         padding=cfg["padding"], kernel_hw=cfg["kernel_size"], **common)
+        elif kind == "SeparableConv2D":
+            x = in_shapes[0]
+            mid = TensorShape((shape.h, shape.w, x.c))
+            dw = add_unit(kind="DepthwiseConv2D", name=node.name + "/depthwise",
+                          input_ids=ins, output_id=next_tid, input_shapes=in_shapes,
+                          output_shape=mid, kernel=w["depthwise"], bias=zeros(x.c),
+                          stride=cfg["strides"], padding=cfg["padding"],
+                          kernel_hw=cfg["kernel_size"])
+            next_tid += 1
+            u = add_unit(kind="Conv2D", name=node.name + "/pointwise",
+                         input_ids=(dw.output_id,), output_id=idx, input_shapes=(mid,),
+                         output_shape=shape, kernel=w["pointwise"],
+                         bias=w.get("bias", zeros(cfg["filters"])),
+                         activation=cfg["activation"], kernel_hw=(1, 1))
+        elif kind in ("MaxPool2D", "AvgPool2D"):
+            u = add_unit(kind="Pool", pool_op="max" if kind == "MaxPool2D" else "avg",
+                         stride=cfg["strides"], padding=cfg["padding"],
+                         kernel_hw=cfg["pool_size"], **common)
+        elif kind == "GlobalAveragePooling2D":
+            x = in_shapes[0]
+            u = add_unit(kind="Pool", pool_op="avg", stride=1, padding="valid",
+                         kernel_hw=(x.h, x.w), **common)
+        elif kind == "ZeroPadding2D":
+            u = add_unit(kind="Pad", pad=cfg["padding"], **common)
+        elif kind == "BatchNorm":
+            u = add_unit(kind="ElementwiseActivation", scale=w["scale"],
+                         offset=w["offset"], in_place_preference=0, **common)
+        elif kind == "Activation":
+            u = add_unit(kind="ElementwiseActivation", activation=cfg["activation"],
+                         in_place_preference=0, **common)
+        elif kind == "Softmax":
+            u = add_unit(kind="Softmax", in_place_preference=0, **common)
+        elif kind == "UpSample2D":
+            u = add_unit(kind="Upsample", factor=cfg["factor"], **common)
+        elif kind == "Add":
+            u = add_unit(kind="Add", in_place_preference=0, **common)
+        elif kind == "Concatenate":
+            u = add_unit(kind="Concat", **common)
+        else:
+            raise UnsupportedLayer(f"cannot lower layer kind '{kind}'")
+        node_units[idx] = u.uid
+
+    return FusionPlan(units=units, tensors=tensors,
+                      input_ids=tuple(res(i) for i in graph.input_ids),
+                      output_ids=tuple(res(o) for o in graph.output_ids),
+                      node_units=node_units)
+
+
+# ---------------------------------------------------------------------------
+# reference fusions (pkg/src/nnjit/optimizer.py:189-341)
+
+def _private(plan, tid):
+    """Exactly one consumer and not network I/O."""
+    return (tid not in plan.input_ids and tid not in plan.output_ids
+            and plan.consumer_count(tid) == 1)
+
+
+def _absorb_forward(plan, pos, into):
+    """Delete units[pos]; ``into`` now produces the victim's output."""
+    victim = plan.units[pos]
+    plan.tensors.pop(into.output_id, None)
+    into.output_id = victim.output_id
+    _delete(plan, pos, into)
+
+
+def _absorb_backward(plan, pos, into):
+    """Delete units[pos]; ``into`` now reads the victim's input."""
+    victim = plan.units[pos]
+    into.input_ids = tuple(victim.input_ids[0] if t == victim.output_id else t
+                           for t in into.input_ids)
+    into.input_shapes = victim.input_shapes
+    plan.tensors.pop(victim.output_id, None)
+    _delete(plan, pos, into)
+
+
+def _delete(plan, pos, into):
+    victim = plan.units.pop(pos)
+    plan.node_units = {n: (into.uid if u == victim.uid else u)
+                       for n, u in plan.node_units.items()}
+
+
+def fuse_activation(plan):
+    progress = True
+    while progress:
+        progress = False
+        for pos in range(1, len(plan.units)):
+            u, p = plan.units[pos], plan.units[pos - 1]
+            if (u.kind == "ElementwiseActivation" and u.scale is None
+                    and p.kind in MATVEC_KINDS and p.output_id == u.input_ids[0]
+                    and p.activation == "linear" and p.post_scale is None
+                    and _private(plan, u.input_ids[0])):
+                p.activation = u.activation
+                _absorb_forward(plan, pos, p)
+                progress = True
+                break
+    return plan
+
+
+def _fold_after(u, s, o):
+    # output channels are the last axis of all three kernel layouts
+    u.kernel = np.multiply(u.kernel, s, dtype=F32)
+    u.bias = np.add(np.multiply(u.bias, s, dtype=F32), o, dtype=F32)
+
+
+def _fold_before(u, s, o):
+    k = u.kernel
+    if u.kind == "Dense":
+        if k.shape[0] != len(s):          # channelwise affine seen through Flatten
+            reps = k.shape[0] // len(s)
+            s, o = np.tile(s, reps), np.tile(o, reps)
+        extra = k.astype(np.float64).T @ o.astype(np.float64)
+        u.kernel = np.multiply(k, s[:, None], dtype=F32)
+    elif u.kind == "Conv2D":
+        extra = np.tensordot(k.astype(np.float64), o.astype(np.float64),
+                             axes=([2], [0])).sum((0, 1))
+        u.kernel = np.multiply(k, s[None, None, :, None], dtype=F32)
+    else:
+        extra = (k.astype(np.float64) * o.astype(np.float64)).sum((0, 1))
+        u.kernel = np.multiply(k, s, dtype=F32)
+    u.bias = (u.bias.astype(np.float64) + extra).astype(F32)
+
+
+def _post_affine(u, s, o):
+    if u.post_scale is None:
+        u.post_scale, u.post_offset = s.astype(F32), o.astype(F32)
+    else:
+        u.post_offset = np.add(np.multiply(u.post_offset, s, dtype=F32), o, dtype=F32)
+        u.post_scale = np.multiply(u.post_scale, s, dtype=F32)
+
+
+def fuse_batchnorm(plan):
+    progress = True
+    while progress:
+        progress = False
+        for pos, u in enumerate(plan.units):
+            if u.kind != "ElementwiseActivation" or u.scale is None:
+                continue
+            bn_in, bn_out = u.input_ids[0], u.output_id
+            if pos > 0:
+                p = plan.units[pos - 1]
+                if (p.kind in MATVEC_KINDS and p.output_id == bn_in
+                        and len(u.scale) == p.output_shape.dims[-1]
+                        and _private(plan, bn_in)):
+                    if p.activation == "linear" and p.post_scale is None:
+                        _fold_after(p, u.scale, u.offset)
+                    else:
+                        _post_affine(p, u.scale, u.offset)
+                    _absorb_forward(plan, pos, p)
+                    progress = True
+                    break
+            if pos + 1 < len(plan.units):
+                c = plan.units[pos + 1]
+                folds = c.kind == "Dense" or (c.kind in ("Conv2D", "DepthwiseConv2D")
+                                              and c.padding == "valid")
+                if folds and bn_out in c.input_ids and _private(plan, bn_out):
+                    _fold_before(c, u.scale, u.offset)
+                    _absorb_backward(plan, pos, c)
+                    progress = True
+                    break
+    return plan
+
+
+def build_reference_plan(graph):
+    """The reference's unit list (lowering + fusion fixpoint)."""
+    plan = lower_to_units(graph)
+    while True:
+        n = len(plan.units)
+        fuse_batchnorm(fuse_activation(plan))
+        if len(plan.units) == n:
+            return plan
+
+
+# ---------------------------------------------------------------------------
+# B200 epilogue fusions
+
+def _pool_fusable(p, u):
+    if not (u.kind == "Pool" and u.pool_op == "max" and u.kernel_hw == (2, 2)
+            and u.stride == 2):
+        return False
+    h, w = p.output_shape.h, p.output_shape.w
+    return u.padding == "valid" or (h % 2 == 0 and w % 2 == 0)
+
+
+def fuse_pool(plan):
+    pos = 1
+    while pos < len(plan.units):
+        u, p = plan.units[pos], plan.units[pos - 1]
+        if (p.kind == "Conv2D" and not p.pool_after and p.residual_id is None
+                and not p.softmax_after and p.output_id == u.input_ids[0]
+                and _pool_fusable(p, u) and _private(plan, p.output_id)):
+            p.pre_pool_shape = p.output_shape
+            p.output_shape = u.output_shape
+            p.pool_after = True
+            _absorb_forward(plan, pos, p)
+            continue
+        pos += 1
+    return plan
+
+
+def fuse_residual(plan):
+    pos = 0
+    while pos < len(plan.units):
+        u = plan.units[pos]
+        if u.kind == "Add" and len(u.input_ids) == 2 and u.input_ids[0] != u.input_ids[1]:
+            where = plan.producer_positions()
+            cand = [(where.get(t, -1), k) for k, t in enumerate(u.input_ids)]
+            ppos, k = max(cand)
+            if ppos >= 0:
+                p = plan.units[ppos]
+                tid = u.input_ids[k]
+                if (p.kind in GEMM_KINDS and not p.pool_after and p.residual_id is None
+                        and not p.softmax_after and _private(plan, tid)):
+                    p.residual_id = u.input_ids[1 - k]
+                    plan.tensors.pop(p.output_id, None)
+                    p.output_id = u.output_id
+                    _delete(plan, pos, p)
+                    continue
+        pos += 1
+    return plan
+
+
+def fuse_softmax(plan):
+    pos = 1
+    while pos < len(plan.units):
+        u, p = plan.units[pos], plan.units[pos - 1]
+        if (u.kind == "Softmax" and p.kind in GEMM_KINDS and p.output_id == u.input_ids[0]
+                and not p.pool_after and not p.softmax_after
+                and p.output_shape.dims[-1] <= SOFTMAX_FUSE_MAX
+                and _private(plan, p.output_id)):
+            p.softmax_after = True
+            _absorb_forward(plan, pos, p)
+            continue
+        pos += 1
+    return plan
+
+
+def build_plan(graph, gpu_fusion=True):
+    """Reference fusions to a fixpoint, then the B200 epilogue fusions."""
+    plan = build_reference_plan(graph)
+    if gpu_fusion:
+        fuse_pool(plan)
+        fuse_residual(plan)
+        fuse_softmax(plan)
+    return plan
+
+
+def describe_plan(plan):
+    return plan.describe()

@@ -1,0 +1,32 @@
+"""GPU parity: the five BASELINE configs through the C ABI vs the C oracle."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1906_05737_b200 import EXACT, ApproximationOptions, compile_model, zoo
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5          # BASELINE.json north_star FP32 tolerance
+
+
+@pytest.mark.parametrize("cfg,n", [(0, 1), (0, 37), (1, 1), (1, 20), (2, 1), (2, 9),
+                                   (3, 1), (3, 5), (4, 1), (4, 2)])
+def test_config_exact_vs_oracle(cfg, n):
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=n)
+    x = zoo.inputs(cfg, n)
+    got = net.run([x])[0].cpu().numpy()
+    want = oracle.run(m, w, [x], "exact")[0]
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_config_default_modes_vs_oracle_models(cfg):
+    opts = ApproximationOptions()
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, opts, batch=6)
+    x = zoo.inputs(cfg, 6)
+    got = net.run([x])[0].cpu().numpy()
+    want = oracle.run(m, w, [x], opts)[0]
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
