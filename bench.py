@@ -1,0 +1,363 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 CompiledNN path (contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nnb|reference]
+                    [--config C] [--batch B] [--no-extra]
+
+Workload: BASELINE.json configs[1] (the dense MLP, 1024 -> 512 tanh -> 256
+sigmoid -> 128 elu -> 10 softmax) at batch 65536 per GPU, FP32 in and out,
+exact (interpreter-grade) transcendentals.  A *step* is one ``apply()`` --
+one CUDA-graph replay of the whole network over the batch already resident
+in HBM.  Inputs (256 MiB per GPU) are larger than the 126 MB L2, so no flush
+is needed between steps.  N GPUs run N independent replicas (weak scaling,
+no collective on the data path); the time is the max over ranks.
+
+Keys beyond the base contract:
+  e2e          the same metric through ``CompiledNetwork.run_host`` (the C-ABI
+               host-buffer call): H2D of the step's inputs from pinned memory,
+               replay, D2H of the softmax outputs, every step.
+  roofline     dominant kernel: algorithmic FLOPs per launch / its CUDA-event
+               time, against the FP32 FFMA peak (SIMT kernels) or TF32 tensor
+               peak (tcgen05 kernels).
+  cpu_baseline the C oracle (oracle/nnoracle.c, the reference interpreter
+               restated) on all host threads over a bounded sample.
+  parity       max |GPU - oracle| over sampled images of the timed batch.
+  configs      all five BASELINE configs: batch-1 latency and large-batch
+               throughput (L2 flushed between timed replays), fraction of the
+               layerwise roofline of SURVEY.md 8(d).
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec per net (batch-1 latency + batched) at 1/2/4/8 B200; % roofline"
+BIG_BATCH = {0: 4096, 1: 65536, 2: 1024, 3: 256, 4: 64}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="nnb", choices=("nnb", "reference"))
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--batch", type=int, default=None)
+    p.add_argument("--no-extra", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler for the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.mhz, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.mhz.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.mhz:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.mhz)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.mhz)}
+
+
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, value, local):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference(cfg, batch, seconds, threads=None):
+    """Time the C oracle (reference interpreter restated) on host threads.
+    Returns (images/s, sample images, threads, seconds)."""
+    from oracle import oracle
+    from paper_1906_05737_b200 import zoo
+    threads = threads or os.cpu_count() or 1
+    m, w = zoo.build(cfg)
+    from paper_1906_05737_b200.graph import build_graph
+    g = build_graph(m, w)
+    probe = max(threads, 1)
+    x = zoo.inputs(cfg, probe, seed=7)
+    t0 = time.perf_counter()
+    oracle.run_graph(g, [x], "exact", threads)
+    dt = time.perf_counter() - t0
+    per_img = dt / probe
+    sample = int(min(batch, max(probe, seconds / max(per_img, 1e-9))))
+    sample = max(threads, sample // threads * threads)
+    x = zoo.inputs(cfg, sample, seed=7)
+    t0 = time.perf_counter()
+    oracle.run_graph(g, [x], "exact", threads)
+    dt = time.perf_counter() - t0
+    return sample / dt, sample, threads, dt
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    cfg = args.config
+    batch = args.batch or BIG_BATCH[cfg]
+    from paper_1906_05737_b200 import zoo  # noqa: F401
+    vals = []
+    sample = threads = None
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        v, sample, threads, _ = cpu_reference(cfg, batch, budget)
+        if i >= args.warmup:
+            vals.append(v)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sample / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.md section 2)",
+        "config": {"workload": zoo.CONFIGS[cfg]["name"], "global_batch": batch,
+                   "parallelism": "host threads", "sample_images_per_step": sample},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} images of {zoo.CONFIGS[cfg]['name']} per step "
+                                   "through oracle/nnoracle.c (reference interpreter "
+                                   "restated, float32 per-op rounding)"},
+        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def time_config(cfg, batch, device, torch, iters=20):
+    """(ms per replay with L2 flushed before each, net)."""
+    from paper_1906_05737_b200 import EXACT, compile_model, zoo
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=batch, device=device)
+    net.input_views[0].copy_(torch.from_numpy(zoo.inputs(cfg, batch)))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MiB > L2
+    for _ in range(3):
+        net.apply()
+    torch.cuda.synchronize(device)
+    times = []
+    s = torch.cuda.current_stream(device)
+    for _ in range(iters):
+        flush_l2(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        net.apply()
+        e1.record(s)
+        torch.cuda.synchronize(device)
+        times.append(e0.elapsed_time(e1))
+    return float(np.median(times)), net
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    import torch
+    from paper_1906_05737_b200 import EXACT, compile_model, roofline, zoo
+    from paper_1906_05737_b200.planner import build_reference_plan
+    from paper_1906_05737_b200.graph import build_graph
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    B = args.batch or BIG_BATCH[cfg]
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=B, device=local)
+    x = zoo.inputs(cfg, B, seed=1 + rank)
+    net.input_views[0].copy_(torch.from_numpy(x))
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        net.apply()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: K replays, inputs resident --------------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            net.apply()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    ms = max_over_ranks(world, e0.elapsed_time(e1), local)
+    ms_step = ms / args.steps
+    value = world * B * args.steps / (ms / 1e3)
+    n_launch = len(net.launches_for(B))
+
+    # ---------------- parity on sampled images of this batch ----------------
+    from oracle import oracle
+    idx = np.linspace(0, B - 1, 16).astype(int)
+    got = net.output_views[0][torch.as_tensor(idx, device=dev)].cpu().numpy()
+    want = oracle.run(m, w, [x[idx]], "exact")[0]
+    parity = {"images": len(idx), "max_abs": float(np.abs(got - want).max()),
+              "ok": bool(np.allclose(got, want, rtol=1e-4, atol=1e-5)),
+              "tolerance": "rtol 1e-4 / atol 1e-5 vs oracle/nnoracle.c (exact)"}
+
+    # ---------------- e2e through the C-ABI host-buffer call ----------------
+    from paper_1906_05737_b200 import pinned_empty
+    hx = pinned_empty(x.shape)
+    hx[...] = x
+    hy = pinned_empty((B,) + tuple(net.output_views[0].shape[1:]))
+    e2e_steps = max(3, min(args.steps, 10))
+    net.run_host([hx], [hy])
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        net.run_host([hx], [hy])
+    e2e_s = max_over_ranks(world, time.perf_counter() - t0, local)
+    e2e = {"value": world * B * e2e_steps / e2e_s, "unit": "images/s",
+           "h2d_bytes_per_step": int(hx.nbytes), "d2h_bytes_per_step": int(hy.nbytes),
+           "path": "CompiledNetwork.run_host -> nnb_run_host (pinned host buffers)"}
+
+    # ---------------- roofline of the dominant kernel -----------------------
+    peaks = roofline.measured_peaks()
+    lt = {i: net.time_launch(i, B, iters=5) for i in net.launches_for(B)}
+    dom = max(lt, key=lt.get)
+    L = net.artifact.launches[dom]
+    u = net.plan.units[L.unit]
+    f, io, wb = roofline.unit_work(u)
+    share = lt[dom] / sum(lt.values())
+    clocks = clk.summary()
+    peak_fp32 = roofline.fp32_peak_tflops()
+    achieved = B * f / (lt[dom] / 1e3) / 1e12
+    roof = {"bound": "fp32_ffma", "kernel": L.kernel, "unit": "TFLOP/s",
+            "achieved": achieved, "peak": peak_fp32, "frac": achieved / peak_fp32,
+            "peak_source": "derived 148 SM x 128 FFMA lanes x 2 x 1965 MHz (no tensor cores "
+                           "in this kernel)",
+            "algorithmic_per_launch": {"flops": B * f, "bytes": B * io + wb},
+            "kernel_ms": lt[dom], "share_of_step": share,
+            "hbm_frac_at_same_time": (B * io + wb) / (lt[dom] / 1e3) / 1e9 / peaks["hbm_gbs"],
+            "traffic": None}
+
+    # ---------------- per-config extras (rank 0, N == 1) ---------------------
+    extra = None
+    cpu = None
+    if rank == 0 and world == 1:
+        c_val, c_n, c_thr, c_dt = cpu_reference(cfg, B, args.cpu_seconds)
+        cpu = {"value": c_val, "unit": "images/s", "cores": c_thr, "kind": "port",
+               "sample": f"{c_n} images of {zoo.CONFIGS[cfg]['name']} through "
+                         f"oracle/nnoracle.c in {c_dt:.1f} s"}
+        if not args.no_extra:
+            extra = {}
+            for c in range(5):
+                try:
+                    big = BIG_BATCH[c]
+                    ms_b, netb = time_config(c, big, local, torch)
+                    ms_1, net1 = time_config(c, 1, local, torch, iters=50)
+                    g = build_graph(*zoo.build(c))
+                    rp = build_reference_plan(g)
+                    t_roof = roofline.layerwise_roof_s(rp, big, peaks["hbm_gbs"], peak_fp32)
+                    t_fused = roofline.fused_ideal_s(rp, big, peaks["hbm_gbs"], peak_fp32)
+                    extra[zoo.CONFIGS[c]["name"]] = {
+                        "batch": big, "ms": ms_b, "images_per_s": big / (ms_b / 1e3),
+                        "batch1_latency_us": ms_1 * 1e3,
+                        "launches": len(netb.launches_for(big)),
+                        "layerwise_roof_ms": t_roof * 1e3,
+                        "layerwise_roofline_frac": t_roof * 1e3 / ms_b,
+                        "fused_ideal_frac": t_fused * 1e3 / ms_b,
+                        "gflop_per_batch": big * roofline.total_flops(rp) / 1e9,
+                        "compile_ms": netb.compile_ms,
+                    }
+                    del netb, net1
+                except Exception as e:  # report, never hide
+                    extra[zoo.CONFIGS[c]["name"]] = {"error": repr(e)[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded weights/inputs, BASELINE.md section 2)",
+            "config": {"workload": zoo.CONFIGS[cfg]["name"], "global_batch": world * B,
+                       "per_gpu_batch": B, "parallelism": f"replicas x{world}",
+                       "l2": "inputs larger than L2 (no flush)" if x.nbytes > 126e6
+                       else "inputs smaller than L2",
+                       "transcendentals": "exact (float64 tanh/exp, rounded once)"},
+            "e2e": e2e, "gpu_launches": n_launch * args.steps, "clocks": clocks,
+            "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "compile_ms": net.compile_ms, "configs": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,11 @@ nnb_status nnb_sync(nnb_net *net, void *stream);
  * nnb_time_apply replays `iters` times between two events. */
 nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms);
 
+/* Mean milliseconds of launch `index` of the schedule run alone `iters`
+ * times (no graph) -- per-kernel roofline evidence for bench.py. */
+nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters, void *stream,
+                           double *ms);
+
 nnb_status nnb_host_alloc(uint64_t bytes, void **ptr);
 void nnb_host_free(void *ptr);
 void nnb_free(void *ptr);

@@ -501,6 +501,32 @@ nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, 
   return NNB_OK;
 }
 
+nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters, void *stream,
+                           double *ms) {
+  if (!net || iters < 1 || !ms || index < 0 || index >= (int32_t)net->launches.size())
+    return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  if (n < 1 || n > net->max_batch)
+    return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
+  Cu *C = cu();
+  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  const nnb_launch &l = net->launches[index];
+  uint64_t gx = ((uint64_t)n * l.items_per_image + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
+  CUdeviceptr pool = net->pool, arena = net->arena;
+  int nn = n;
+  void *args[] = {&pool, &arena, &nn};
+  CU_CHECK(C->p_cuEventRecord(net->ev0, s));
+  for (int i = 0; i < iters; ++i)
+    CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
+                                 l.smem_bytes, s, args, nullptr));
+  CU_CHECK(C->p_cuEventRecord(net->ev1, s));
+  CU_CHECK(C->p_cuEventSynchronize(net->ev1));
+  float f = 0;
+  CU_CHECK(C->p_cuEventElapsedTime(&f, net->ev0, net->ev1));
+  *ms = f / iters;
+  return NNB_OK;
+}
+
 nnb_status nnb_host_alloc(uint64_t bytes, void **ptr) {
   Cu *C = cu();
   if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());

@@ -220,6 +220,19 @@ class CompiledNetwork:
                                                    ctypes.byref(ms)))
         return ms.value
 
+    def time_launch(self, index, n=None, iters=10):
+        """Mean milliseconds of one schedule launch run alone (CUDA events)."""
+        n = self.max_batch if n is None else n
+        ms = ctypes.c_double()
+        _native.check(_native.lib().nnb_time_launch(self._h.ptr, index, n, iters, self._stream(),
+                                                    ctypes.byref(ms)))
+        return ms.value
+
+    def launches_for(self, n=None):
+        """Indices of the launches a replay over ``n`` images runs."""
+        n = self.max_batch if n is None else n
+        return [i for i, l in enumerate(self.artifact.launches) if l.n_min <= n <= l.n_max]
+
     def describe(self):
         lines = [f"units ({len(self.plan.units)}):"]
         for pos, u in enumerate(self.plan.units):
