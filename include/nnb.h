@@ -68,11 +68,14 @@ typedef struct {
 
 typedef struct {
   int32_t device;
-  /* kernels: CUDA C++ translation unit + the extern "C" kernel names */
-  const char *source;
+  /* kernels: CUDA C++ translation units (compiled by NVRTC in parallel, one
+   * module each) and the extern "C" kernel names with their source index */
+  const char *const *sources;
+  int32_t n_sources;
   const char *include_dir;   /* directory of the kernel headers               */
   const char *cache_dir;     /* cubin cache directory, NULL = no cache        */
   const char *const *kernel_names;
+  const int32_t *kernel_source;
   int32_t n_kernels;
   /* schedule */
   const nnb_launch *launches;

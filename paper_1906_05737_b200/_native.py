@@ -36,9 +36,11 @@ class IO(ctypes.Structure):
 
 
 class NetDesc(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int32), ("source", ctypes.c_char_p),
+    _fields_ = [("device", ctypes.c_int32), ("sources", ctypes.POINTER(ctypes.c_char_p)),
+                ("n_sources", ctypes.c_int32),
                 ("include_dir", ctypes.c_char_p), ("cache_dir", ctypes.c_char_p),
-                ("kernel_names", ctypes.POINTER(ctypes.c_char_p)), ("n_kernels", ctypes.c_int32),
+                ("kernel_names", ctypes.POINTER(ctypes.c_char_p)),
+                ("kernel_source", ctypes.POINTER(ctypes.c_int32)), ("n_kernels", ctypes.c_int32),
                 ("launches", ctypes.POINTER(Launch)), ("n_launches", ctypes.c_int32),
                 ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_uint64),
                 ("arena_bytes", ctypes.c_uint64), ("max_batch", ctypes.c_int32),

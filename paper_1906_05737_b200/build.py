@@ -7,9 +7,10 @@
   specialisations of BASELINE config 0, written to build/kcheck.cubin.  At run
   time the same headers are compiled by NVRTC inside libnnb.so with the
   shapes of the network being compiled.
-* ``oracle/libnnoracle.so`` -- the CPU checker (test infrastructure).
+The CPU checker under oracle/ (test infrastructure) is built by
+__graft_entry__.build(), not by the package.
 
-``python -m paper_1906_05737_b200.build`` runs all three.
+``python -m paper_1906_05737_b200.build`` runs both.
 """
 
 import pathlib
@@ -58,15 +59,8 @@ def kernel_check():
     return out
 
 
-def build_oracle():
-    sys.path.insert(0, str(ROOT))
-    from oracle import oracle
-    return oracle.build(force=True)
-
-
 def main():
     print("runtime:", build_runtime())
-    print("oracle :", build_oracle())
     print("kernels:", kernel_check())
 
 

@@ -22,6 +22,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -32,6 +33,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -194,7 +196,7 @@ std::string headers_digest(const char *dir) {
 const char *kArchOpt = "--gpu-architecture=sm_100a";
 
 nnb_status compile_cubin(const char *source, const char *include_dir, const char *cache_dir,
-                         std::string *cubin, double *ms, bool *hit) {
+                         const std::string &digest, std::string *cubin, double *ms, bool *hit) {
   auto t0 = std::chrono::steady_clock::now();
   *hit = false;
   Nvrtc *N = nv();
@@ -204,7 +206,7 @@ nnb_status compile_cubin(const char *source, const char *include_dir, const char
   std::string inc = std::string("--include-path=") + (include_dir ? include_dir : ".");
   std::vector<std::string> opts = {kArchOpt, "--std=c++17", inc, "--generate-line-info",
                                    "-DNNB_NVRTC=1"};
-  std::string key_src = std::string(source) + "\x1f" + headers_digest(include_dir ? include_dir : ".");
+  std::string key_src = std::string(source) + "\x1f" + digest;
   for (auto &o : opts) key_src += "\x1f" + o;
   key_src += "\x1f" + std::to_string(vmaj) + "." + std::to_string(vmin);
   char key[40];
@@ -244,7 +246,8 @@ nnb_status compile_cubin(const char *source, const char *include_dir, const char
   N->p_nvrtcDestroyProgram(&prog);
   if (!cpath.empty()) {
     mkdir(cache_dir, 0755);
-    std::string tmp = cpath + ".tmp." + std::to_string(getpid());
+    std::string tmp = cpath + ".tmp." + std::to_string(getpid()) + "." +
+                      std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
     {
       std::ofstream f(tmp, std::ios::binary);
       f.write(cubin->data(), (std::streamsize)cubin->size());
@@ -277,7 +280,7 @@ nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
 struct nnb_net {
   int device = 0;
   CUcontext ctx = nullptr;
-  CUmodule mod = nullptr;
+  std::vector<CUmodule> mods;
   std::vector<CUfunction> fns;
   std::vector<nnb_launch> launches;
   CUdeviceptr arena = 0, pool = 0;
@@ -365,7 +368,8 @@ nnb_status nnb_compile(const char *source, const char *include_dir, const char *
   std::string cubin;
   double ms = 0;
   bool hit = false;
-  nnb_status st = compile_cubin(source, include_dir, cache_dir, &cubin, &ms, &hit);
+  std::string digest = headers_digest(include_dir ? include_dir : ".");
+  nnb_status st = compile_cubin(source, include_dir, cache_dir, digest, &cubin, &ms, &hit);
   if (st != NNB_OK) return st;
   if (cubin_bytes) *cubin_bytes = cubin.size();
   if (compile_ms) *compile_ms = ms;
@@ -381,7 +385,8 @@ nnb_status nnb_compile(const char *source, const char *include_dir, const char *
 void nnb_free(void *p) { free(p); }
 
 nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
-  if (!d || !out || !d->source || d->n_kernels < 0 || d->n_launches < 0 || d->max_batch < 1)
+  if (!d || !out || !d->sources || d->n_sources < 1 || d->n_kernels < 0 || d->n_launches < 0 ||
+      d->max_batch < 1)
     return fail(NNB_ERR_ARGUMENT, "invalid nnb_net_desc");
   for (int i = 0; i < d->n_launches; ++i) {
     const nnb_launch &l = d->launches[i];
@@ -397,15 +402,45 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   nnb_status st = device_ctx(d->device, &net->ctx, &dev);
   if (st != NNB_OK) { delete net; return st; }
 
-  std::string cubin;
-  st = compile_cubin(d->source, d->include_dir, d->cache_dir, &cubin, &net->compile_ms, &net->cache_hit);
-  if (st != NNB_OK) { delete net; return st; }
+  // one NVRTC program per source, compiled in parallel, one module each
+  struct Job { std::string cubin, err; nnb_status st = NNB_OK; double ms = 0; bool hit = false; };
+  std::vector<Job> jobs(d->n_sources);
+  std::string digest = headers_digest(d->include_dir ? d->include_dir : ".");
+  {
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    unsigned nthreads = std::min<unsigned>(hw, (unsigned)d->n_sources);
+    std::vector<std::thread> pool;
+    std::atomic<int> next{0};
+    auto auto_t0 = std::chrono::steady_clock::now();
+    for (unsigned t = 0; t < std::max(1u, nthreads); ++t)
+      pool.emplace_back([&] {
+        for (int i = next++; i < d->n_sources; i = next++) {
+          Job &j = jobs[i];
+          j.st = compile_cubin(d->sources[i], d->include_dir, d->cache_dir, digest, &j.cubin,
+                              &j.ms, &j.hit);
+          if (j.st != NNB_OK) j.err = g_err;
+        }
+      });
+    for (auto &th : pool) th.join();
+    net->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - auto_t0).count();
+  }
+  net->cache_hit = true;
+  for (auto &j : jobs) {
+    if (j.st != NNB_OK) { g_err = j.err; nnb_status s2 = j.st; delete net; return s2; }
+    net->cache_hit = net->cache_hit && j.hit;
+  }
   auto bail = [&](nnb_status s) { nnb_destroy(net); return s; };
-  CUresult r = C->p_cuModuleLoadData(&net->mod, cubin.data());
-  if (r != CUDA_SUCCESS) { g_err = "cuModuleLoadData failed (" + std::to_string((int)r) + ")"; return bail(NNB_ERR_CUDA); }
+  net->mods.resize(d->n_sources, nullptr);
+  CUresult r;
+  for (int i = 0; i < d->n_sources; ++i) {
+    r = C->p_cuModuleLoadData(&net->mods[i], jobs[i].cubin.data());
+    if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "cuModuleLoadData failed (%d)", (int)r); return bail(NNB_ERR_CUDA); }
+  }
   net->fns.resize(d->n_kernels);
   for (int i = 0; i < d->n_kernels; ++i) {
-    r = C->p_cuModuleGetFunction(&net->fns[i], net->mod, d->kernel_names[i]);
+    int src = d->kernel_source ? d->kernel_source[i] : 0;
+    if (src < 0 || src >= d->n_sources) { fail(NNB_ERR_ARGUMENT, "kernel %d has no source", i); return bail(NNB_ERR_ARGUMENT); }
+    r = C->p_cuModuleGetFunction(&net->fns[i], net->mods[src], d->kernel_names[i]);
     if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "kernel %s not in module", d->kernel_names[i]); return bail(NNB_ERR_CUDA); }
   }
   net->launches.assign(d->launches, d->launches + d->n_launches);
@@ -560,7 +595,8 @@ void nnb_destroy(nnb_net *net) {
     if (net->capture_stream) C->p_cuStreamDestroy(net->capture_stream);
     if (net->arena) C->p_cuMemFree(net->arena);
     if (net->pool) C->p_cuMemFree(net->pool);
-    if (net->mod) C->p_cuModuleUnload(net->mod);
+    for (CUmodule m : net->mods)
+      if (m) C->p_cuModuleUnload(m);
   }
   delete net;
 }

@@ -75,10 +75,12 @@ class DevicePool:
 
 @dataclass
 class Specialization:
-    source: str
+    source: str                 # all units in one translation unit (inspection)
     launches: list
     pool: bytes
     kernel_names: list
+    sources: list = field(default_factory=list)      # one TU per kernel (NVRTC jobs)
+    kernel_source: list = field(default_factory=list)
     notes: dict = field(default_factory=dict)
 
 
@@ -393,9 +395,18 @@ class Specializer:
                 self.pad(pos, u)
             else:
                 raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
-        src = ('#include "nnb_kernels.cuh"\n\n' + "\n\n".join(self.chunks) + "\n")
-        return Specialization(source=src, launches=self.launches,
-                              pool=bytes(self.pool.data), kernel_names=list(self.names))
+        head = '#include "nnb_kernels.cuh"\n\n'
+        src = head + "\n\n".join(self.chunks) + "\n"
+        sources, index, ks = [], {}, []
+        for chunk in self.chunks:
+            tu = head + chunk
+            if tu not in index:
+                index[tu] = len(sources)
+                sources.append(tu)
+            ks.append(index[tu])
+        return Specialization(source=src, launches=self.launches, pool=bytes(self.pool.data),
+                              kernel_names=list(self.names), sources=sources,
+                              kernel_source=ks)
 
 
 def specialize(plan, assignment, options, max_batch, capacity):

@@ -1,0 +1,78 @@
+"""Data-parallel replicas over the GPUs of one node.
+
+Images are independent, so batched inference shards the batch into
+contiguous slices, one per process/GPU, each running its own compiled
+network (own arena, own CUDA graph).  There is no collective on the data
+path; ``torch.distributed`` is only used around it -- a barrier before the
+timed region, a MAX reduction of the per-rank device time, and an optional
+gather of the outputs for the caller (outside any timed region).
+"""
+
+import os
+
+import numpy as np
+
+
+def shard(global_batch, world, rank):
+    """Contiguous slice of ``global_batch`` for ``rank``: (start, count);
+    the first ``global_batch % world`` ranks take one extra image."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(global_batch, world)
+    count = base + (1 if rank < extra else 0)
+    start = rank * base + min(rank, extra)
+    return start, count
+
+
+class ReplicaGroup:
+    """One replica of a compiled network per rank.
+
+    ``engine_factory(count)`` builds the per-rank engine; by default it is
+    ``CompiledNetwork(manifest, weights, options, batch=count,
+    device=LOCAL_RANK)``.  The engine must offer ``run(inputs) -> outputs``.
+    """
+
+    def __init__(self, global_batch, engine_factory, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.global_batch = global_batch
+        self.start, self.count = shard(global_batch, self.world, self.rank)
+        self.engine = engine_factory(self.count)
+
+    @classmethod
+    def compiled(cls, manifest, weights, global_batch, options=None, group=None, **kw):
+        from .runtime import compile_model
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        return cls(global_batch, lambda c: compile_model(manifest, weights, options, batch=c,
+                                                         device=local, **kw), group)
+
+    def local_inputs(self, global_inputs):
+        return [x[self.start:self.start + self.count] for x in global_inputs]
+
+    def run(self, global_inputs):
+        """Run this rank's shard; returns the local outputs."""
+        return self.engine.run(self.local_inputs(global_inputs))
+
+    def gather(self, local_outputs):
+        """All shards' outputs concatenated in rank order (every rank gets
+        them; host-side, outside the hot path)."""
+        if self.world == 1:
+            return [np.asarray(o) for o in local_outputs]
+        arrs = [np.asarray(o.cpu() if hasattr(o, "cpu") else o) for o in local_outputs]
+        got = [None] * self.world
+        self.dist.all_gather_object(got, arrs, group=self.group)
+        return [np.concatenate([g[i] for g in got]) for i in range(len(arrs))]
+
+    def max_time(self, seconds):
+        """MAX over ranks of a per-rank duration (the job's time)."""
+        if self.world == 1:
+            return seconds
+        import torch
+        t = torch.tensor([float(seconds)], dtype=torch.float64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())

@@ -106,6 +106,8 @@ class CompiledNetwork:
         L = _native.lib()
         names = (ctypes.c_char_p * max(len(spec.kernel_names), 1))(
             *[n.encode() for n in spec.kernel_names])
+        srcs = (ctypes.c_char_p * len(spec.sources))(*[s.encode() for s in spec.sources])
+        ksrc = (ctypes.c_int32 * max(len(spec.kernel_source), 1))(*spec.kernel_source)
         launches = (_native.Launch * max(len(spec.launches), 1))()
         index = {n: i for i, n in enumerate(spec.kernel_names)}
         for i, l in enumerate(spec.launches):
@@ -117,8 +119,8 @@ class CompiledNetwork:
         pool_buf = ctypes.create_string_buffer(spec.pool, max(len(spec.pool), 1))
         cache = cache_dir if cache_dir is not None else _native.default_cache_dir()
         desc = _native.NetDesc(
-            device, spec.source.encode(), str(_native.KERNEL_DIR).encode(),
-            cache.encode() if cache else None, names, len(spec.kernel_names),
+            device, srcs, len(spec.sources), str(_native.KERNEL_DIR).encode(),
+            cache.encode() if cache else None, names, ksrc, len(spec.kernel_names),
             launches, len(spec.launches), ctypes.cast(pool_buf, ctypes.c_void_p),
             len(spec.pool), arena_bytes, self.max_batch, in_arr, len(ins), out_arr, len(outs))
         ptr = ctypes.c_void_p()

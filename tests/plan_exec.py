@@ -1,0 +1,68 @@
+"""CPU executor of a FusionPlan, built on the oracle's per-layer primitives.
+
+Test infrastructure in the spirit of the reference's ``run_plan``
+(pkg/tests/test_optimizer.py:26-72): it evaluates the *fused* units with the
+epilogue semantics the sm_100a kernels implement (activation, post-affine,
+residual Add, 2x2 max-pool, row softmax), so planner rewrites can be checked
+against the unfused graph without a GPU.
+"""
+import numpy as np
+
+from oracle import oracle
+
+F32 = np.float32
+ACT_MODE = 2
+
+
+def _post(y, u):
+    y = oracle.activation(y, u.activation, ACT_MODE)
+    if u.post_scale is not None:
+        y = (y * u.post_scale).astype(F32) + u.post_offset
+    return y.astype(F32)
+
+
+def run_plan(plan, inputs):
+    vals = {t: np.asarray(x, F32) for t, x in zip(plan.input_ids, inputs)}
+    for u in plan.units:
+        x = vals[u.input_ids[0]]
+        n = x.shape[0]
+        if u.kind == "Dense":
+            y = _post(oracle.dense(x.reshape(n, -1), u.kernel, u.bias, 1), u)
+        elif u.kind in ("Conv2D", "DepthwiseConv2D"):
+            dw = u.kind == "DepthwiseConv2D"
+            y = oracle.conv(x.reshape((n,) + u.input_shapes[0].dims), u.kernel, u.bias,
+                            u.stride, u.padding, dw, 1)
+            y = _post(y, u)
+        elif u.kind == "Pool":
+            ph, pw = u.kernel_hw
+            y = oracle.pool(x.reshape((n,) + u.input_shapes[0].dims), ph, pw, u.stride,
+                            u.padding, u.pool_op == "avg")
+        elif u.kind in ("ElementwiseActivation", "Add"):
+            y = x.copy()
+            for t in u.input_ids[1:]:
+                y = (y + vals[t]).astype(F32)
+            if u.scale is not None:
+                y = ((y.reshape(n, -1, len(u.scale)) * u.scale).astype(F32) + u.offset)
+                y = y.astype(F32).reshape(x.shape)
+            y = oracle.activation(y, u.activation, ACT_MODE)
+        elif u.kind == "Softmax":
+            y = oracle.softmax(x.reshape((n,) + u.output_shape.dims))
+        elif u.kind == "Upsample":
+            f = u.factor
+            y = np.repeat(np.repeat(x.reshape((n,) + u.input_shapes[0].dims), f, 1), f, 2)
+        elif u.kind == "Concat":
+            parts = [vals[t].reshape((n,) + s.dims) for t, s in zip(u.input_ids, u.input_shapes)]
+            y = np.concatenate(parts, axis=-1)
+        elif u.kind == "Pad":
+            (t, b), (l, r) = u.pad
+            y = np.pad(x.reshape((n,) + u.input_shapes[0].dims), ((0, 0), (t, b), (l, r), (0, 0)))
+        else:
+            raise AssertionError(u.kind)
+        if getattr(u, "residual_id", None) is not None:
+            y = (y.reshape(vals[u.residual_id].shape) + vals[u.residual_id]).astype(F32)
+        if getattr(u, "pool_after", False):
+            y = oracle.pool(y, 2, 2, 2, "valid", False)
+        if getattr(u, "softmax_after", False):
+            y = oracle.softmax(y)
+        vals[u.output_id] = y.reshape((n,) + u.output_shape.dims)
+    return [vals[t] for t in plan.output_ids]

@@ -1,0 +1,158 @@
+"""Fusion planner: reference fusions (bit-identical folded weights) and the
+B200 epilogue fusions (numerically sound, checked with a CPU plan executor)."""
+import numpy as np
+import pytest
+
+from builders import bn_params, conv_net, he, random_network
+from golden_util import load, names, sha
+from oracle import oracle
+from plan_exec import run_plan
+from paper_1906_05737_b200 import build_graph, build_plan, build_reference_plan, zoo
+from paper_1906_05737_b200.planner import lower_to_units
+from paper_1906_05737_b200.zoo import NetBuilder
+
+F32 = np.float32
+TOL = dict(rtol=1e-4, atol=1e-5)
+
+
+def kinds(plan):
+    return [u.kind for u in plan.units]
+
+
+def test_lowering_kinds_and_flatten_alias():
+    m, w = zoo.build(0)
+    g = build_graph(m, w)
+    p = lower_to_units(g)
+    assert kinds(p).count("Conv2D") == 3 and kinds(p).count("Pool") == 3
+    assert "Flatten" not in kinds(p)
+    dense = [u for u in p.units if u.kind == "Dense"][0]
+    pool = [u for u in p.units if u.kind == "Pool"][-1]
+    assert dense.input_ids == (pool.output_id,)      # Flatten relabelled
+
+
+@pytest.mark.parametrize("name", names())
+def test_reference_plan_bit_identical_to_reference_optimizer(name):
+    """Unit kinds, activations and every folded array match the reference
+    planner's (hashes recorded by tests/golden/make_golden.py)."""
+    m, w, x, rec = load(name)
+    plan = build_reference_plan(build_graph(m, w))
+    want = sorted({int(k.split(":")[1]) for k in rec if k.startswith("plan:")})
+    assert len(plan.units) == len(want)
+    for i, u in enumerate(plan.units):
+        assert bytes(rec[f"plan:{i}:{u.kind}:act"]).decode() == u.activation
+        for fld in ("kernel", "bias", "post_scale", "post_offset", "scale", "offset"):
+            v = getattr(u, fld)
+            key = f"plan:{i}:{u.kind}:{fld}"
+            assert (v is None) == (key not in rec), key
+            if v is not None:
+                assert sha(v) == bytes(rec[key]), key
+
+
+def _net(build):
+    b = NetBuilder(seed=0)
+    out = build(b, np.random.default_rng(0))
+    return build_graph(*b.build([out]))
+
+
+def test_conv_bn_act_single_unit_and_bn_before_dense():
+    def f(b, rng):
+        x = b.input((6, 6, 2))
+        c = b.layer("Conv2D", [x], {"filters": 3, "kernel_size": 3, "padding": "same"},
+                    [("kernel", he(rng, (3, 3, 2, 3), 18)), ("bias", np.zeros(3, F32))])
+        bn = b.layer("BatchNorm", [c], None, bn_params(rng, 3))
+        a = b.layer("Activation", [bn], {"activation": "relu6"})
+        fl = b.layer("Flatten", [a])
+        bn2 = b.layer("BatchNorm", [fl], None, bn_params(rng, 108))
+        return b.layer("Dense", [bn2], {"units": 4},
+                       [("kernel", he(rng, (108, 4), 108)), ("bias", np.zeros(4, F32))])
+    p = build_reference_plan(_net(f))
+    assert kinds(p) == ["Conv2D", "Dense"]
+    assert p.units[0].activation == "relu6" and p.units[0].post_scale is None
+
+
+def test_case_c_post_affine_and_double_bn_composes():
+    def f(b, rng):
+        x = b.input((5, 5, 2))
+        c = b.layer("Conv2D", [x], {"filters": 2, "kernel_size": 1, "activation": "elu"},
+                    [("kernel", he(rng, (1, 1, 2, 2), 2)), ("bias", np.zeros(2, F32))])
+        b1 = b.layer("BatchNorm", [c], None, bn_params(rng, 2))
+        return b.layer("BatchNorm", [b1], None, bn_params(rng, 2))
+    g = _net(f)
+    p = build_reference_plan(g)
+    assert kinds(p) == ["Conv2D"] and p.units[0].post_scale is not None
+    x = np.random.default_rng(1).normal(size=(3, 5, 5, 2)).astype(F32)
+    np.testing.assert_allclose(run_plan(p, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
+
+
+@pytest.mark.parametrize("pad,folds", [("same", False), ("valid", True)])
+def test_bn_before_conv_folds_only_when_valid(pad, folds):
+    def f(b, rng):
+        x = b.input((6, 6, 3))
+        bn = b.layer("BatchNorm", [x], None, bn_params(rng, 3))
+        return b.layer("Conv2D", [bn], {"filters": 2, "kernel_size": 3, "padding": pad},
+                       [("kernel", he(rng, (3, 3, 3, 2), 27)), ("bias", np.zeros(2, F32))])
+    # case (b): BN folds forward into the conv only under 'valid' padding
+    # (the folded bias would otherwise also apply to the zero padding)
+    g = _net(f)
+    p = build_reference_plan(g)
+    assert sum(1 for u in p.units if u.scale is not None) == (0 if folds else 1)
+    x = np.random.default_rng(5).normal(size=(2, 6, 6, 3)).astype(F32)
+    np.testing.assert_allclose(run_plan(p, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
+
+
+def test_fanout_and_output_block_fusion():
+    def f(b, rng):
+        x = b.input((4, 4, 2))
+        c = b.layer("Conv2D", [x], {"filters": 2, "kernel_size": 1},
+                    [("kernel", he(rng, (1, 1, 2, 2), 2)), ("bias", np.zeros(2, F32))])
+        a = b.layer("Activation", [c], {"activation": "relu"})
+        t = b.layer("Activation", [c], {"activation": "tanh"})
+        return b.layer("Add", [a, t])
+    p = build_plan(_net(f))
+    assert kinds(p).count("ElementwiseActivation") == 2     # c has two consumers
+    m, w = conv_net(np.random.default_rng(0), 4, 4, 2, 2, act="linear")
+    p = build_plan(build_graph(m, w))
+    assert kinds(p) == ["Conv2D"]
+
+
+def test_gpu_fusions_on_zoo():
+    p0 = build_plan(build_graph(*zoo.build(0)))
+    assert [u.pool_after for u in p0.units if u.kind == "Conv2D"] == [True, True, True]
+    assert p0.units[-1].softmax_after and kinds(p0) == ["Conv2D"] * 3 + ["Dense"] * 2
+    p2 = build_plan(build_graph(*zoo.build(2)))
+    assert sum(u.residual_id is not None for u in p2.units) == 1 and "Add" not in kinds(p2)
+    p4 = build_plan(build_graph(*zoo.build(4)))
+    convs = [u for u in p4.units if u.kind == "Conv2D"]
+    # encoder convs 2 and 3 feed a skip connection: their pools stay separate
+    assert [c.pool_after for c in convs[:3]] == [True, False, False]
+    assert convs[-1].softmax_after
+
+
+@pytest.mark.parametrize("cfg", range(5))
+def test_gpu_plan_numerically_sound_on_zoo(cfg):
+    m, w = zoo.build(cfg)
+    g = build_graph(m, w)
+    x = zoo.inputs(cfg, 2)
+    np.testing.assert_allclose(run_plan(build_plan(g), [x])[0], oracle.run_graph(g, [x])[0],
+                               **TOL)
+
+
+def test_build_plan_idempotent_and_deterministic():
+    m, w = zoo.build(3)
+    a, b = build_plan(build_graph(m, w)), build_plan(build_graph(m, w))
+    assert [u.describe() for u in a.units] == [u.describe() for u in b.units]
+    for u, v in zip(a.units, b.units):
+        if u.kernel is not None:
+            assert sha(u.kernel) == sha(v.kernel) and sha(u.bias) == sha(v.bias)
+
+
+def test_random_networks_fusion_soundness():
+    """A4-style sweep: fused plan == unfused graph on random DAGs."""
+    rng = np.random.default_rng(2024)
+    for trial in range(120):
+        m, w, shape = random_network(rng)
+        g = build_graph(m, w)
+        x = rng.uniform(-2, 2, (2,) + shape).astype(F32)
+        want = oracle.run_graph(g, [x])[0]
+        got = run_plan(build_plan(g), [x])[0]
+        np.testing.assert_allclose(got, want, rtol=2e-4, atol=2e-5, err_msg=f"trial {trial}")
