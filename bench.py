@@ -193,6 +193,36 @@ def reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+_TF32 = {}
+
+
+def measure_tf32_peak(torch, dev):
+    """cuBLAS TF32 dense throughput on this GPU (the roofline denominator for
+    the 3xTF32 tcgen05 kernels)."""
+    if dev in _TF32:
+        return _TF32[dev]
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(2):
+            a @ b
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1))
+        _TF32[dev] = 2 * n ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return _TF32[dev]
+
+
 def flush_l2(buf):
     buf.zero_()
 
@@ -295,15 +325,30 @@ def main():
     share = lt[dom] / sum(lt.values())
     clocks = clk.summary()
     peak_fp32 = roofline.fp32_peak_tflops()
-    achieved = B * f / (lt[dom] / 1e3) / 1e12
-    roof = {"bound": "fp32_ffma", "kernel": L.kernel, "unit": "TFLOP/s",
-            "achieved": achieved, "peak": peak_fp32, "frac": achieved / peak_fp32,
-            "peak_source": "derived 148 SM x 128 FFMA lanes x 2 x 1965 MHz (no tensor cores "
-                           "in this kernel)",
-            "algorithmic_per_launch": {"flops": B * f, "bytes": B * io + wb},
-            "kernel_ms": lt[dom], "share_of_step": share,
-            "hbm_frac_at_same_time": (B * io + wb) / (lt[dom] / 1e3) / 1e9 / peaks["hbm_gbs"],
-            "traffic": None}
+    fp32_equiv = B * f / (lt[dom] / 1e3) / 1e12
+    if "_tc_" in L.kernel:
+        # 3xTF32: the tensor pipe executes three TF32 products per FP32 MAC
+        tf32 = measure_tf32_peak(torch, dev)
+        achieved = 3 * fp32_equiv
+        roof = {"bound": "tensor", "kernel": L.kernel, "unit": "TFLOP/s",
+                "achieved": achieved, "peak": tf32, "frac": achieved / tf32,
+                "peak_source": "TF32 dense, cuBLAS fp32 matmul with allow_tf32 on this GPU "
+                               "(8192^3, best of 5; MEASURED_PEAKS.json has bf16 only: "
+                               f"{peaks['bf16_tflops']} TF/s)",
+                "achieved_counts": "3 x 2MNK tensor flops (3xTF32 split) per launch",
+                "fp32_equivalent_tflops": fp32_equiv,
+                "fp32_ffma_peak_tflops": peak_fp32}
+    else:
+        achieved = fp32_equiv
+        roof = {"bound": "fp32_ffma", "kernel": L.kernel, "unit": "TFLOP/s",
+                "achieved": achieved, "peak": peak_fp32, "frac": achieved / peak_fp32,
+                "peak_source": "derived 148 SM x 128 FFMA lanes x 2 x 1965 MHz (no tensor "
+                               "cores in this kernel)"}
+    roof.update({"algorithmic_per_launch": {"flops": B * f, "bytes": B * io + wb},
+                 "kernel_ms": lt[dom], "share_of_step": share,
+                 "hbm_frac_at_same_time": (B * io + wb) / (lt[dom] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                 "launch_ms": {net.artifact.launches[i].kernel: v for i, v in lt.items()},
+                 "traffic": None})
 
     # ---------------- per-config extras (rank 0, N == 1) ---------------------
     extra = None

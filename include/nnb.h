@@ -45,11 +45,24 @@ typedef enum {
   NNB_ERR_BATCH = 8         /* batch outside [1, max_batch]                -> InputShapeMismatch */
 } nnb_status;
 
+/* A 2-D float32 TMA descriptor the runtime encodes (cuTensorMapEncodeTiled)
+ * once the arena and pool addresses are known. */
+typedef struct {
+  uint32_t space;            /* 1 = arena, 2 = weight pool                    */
+  uint32_t swizzle;          /* 0 none, 3 = 128-byte swizzle                  */
+  uint64_t offset;           /* byte offset inside the space                 */
+  uint64_t inner;            /* elements along the contiguous dimension      */
+  uint64_t outer;            /* rows                                          */
+  uint64_t row_bytes;        /* stride between rows (multiple of 16)          */
+  uint32_t box_inner, box_outer;
+} nnb_tmap;
+
 /* One kernel launch of the schedule.  The grid is
- *   grid.x = ceil(n * items_per_image / items_per_block) * grid_mult
- * for a replay over n images; the launch is part of the replay only when
- * n_min <= n <= n_max.  Every kernel has the signature
- *   void k(const float *pool, float *arena, int n). */
+ *   grid.x = min(ceil(n * items_per_image / items_per_block) * grid_mult, grid_cap)
+ * for a replay over n images (grid_cap 0 = no cap); the launch is part of the
+ * replay only when n_min <= n <= n_max.  Every kernel has the signature
+ *   void k(const float *pool, float *arena, int n [, TmaDesc tm0, tm1, tm2])
+ * with the three tensor maps present iff n_tmaps > 0. */
 typedef struct {
   int32_t kernel;            /* index into the kernel-name list             */
   uint32_t block;            /* threads per block                           */
@@ -58,6 +71,9 @@ typedef struct {
   uint64_t items_per_image;
   uint64_t items_per_block;
   int32_t n_min, n_max;
+  uint32_t grid_cap;
+  uint32_t n_tmaps;
+  nnb_tmap tmaps[3];
 } nnb_launch;
 
 /* A network I/O tensor: byte offset in the arena and bytes per image. */

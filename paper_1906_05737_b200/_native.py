@@ -24,11 +24,20 @@ EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "n
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
 
+class TMap(ctypes.Structure):
+    _fields_ = [("space", ctypes.c_uint32), ("swizzle", ctypes.c_uint32),
+                ("offset", ctypes.c_uint64), ("inner", ctypes.c_uint64),
+                ("outer", ctypes.c_uint64), ("row_bytes", ctypes.c_uint64),
+                ("box_inner", ctypes.c_uint32), ("box_outer", ctypes.c_uint32)]
+
+
 class Launch(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("block", ctypes.c_uint32),
                 ("smem_bytes", ctypes.c_uint32), ("grid_mult", ctypes.c_uint32),
                 ("items_per_image", ctypes.c_uint64), ("items_per_block", ctypes.c_uint64),
-                ("n_min", ctypes.c_int32), ("n_max", ctypes.c_int32)]
+                ("n_min", ctypes.c_int32), ("n_max", ctypes.c_int32),
+                ("grid_cap", ctypes.c_uint32), ("n_tmaps", ctypes.c_uint32),
+                ("tmaps", TMap * 3)]
 
 
 class IO(ctypes.Structure):

@@ -5,3 +5,4 @@
 #include "nnb_softmax.cuh"
 #include "nnb_small.cuh"
 #include "nnb_gemm_simt.cuh"
+#include "nnb_gemm_tc.cuh"

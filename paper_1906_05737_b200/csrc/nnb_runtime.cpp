@@ -69,7 +69,7 @@ struct Cu {
   CU_FN(cuGraphInstantiateWithFlags) CU_FN(cuGraphLaunch) CU_FN(cuGraphDestroy)
   CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
   CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
-  CU_FN(cuGetErrorString)
+  CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled)
 #undef CU_FN
   void load() {
     const char *names[] = {"libcuda.so.1", "libcuda.so"};
@@ -91,7 +91,7 @@ struct Cu {
     CU_LOAD(cuStreamEndCapture) CU_LOAD(cuGraphInstantiateWithFlags) CU_LOAD(cuGraphLaunch)
     CU_LOAD(cuGraphDestroy) CU_LOAD(cuGraphExecDestroy) CU_LOAD(cuEventCreate)
     CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
-    CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString)
+    CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString) CU_LOAD(cuTensorMapEncodeTiled)
 #undef CU_LOAD
     CUresult r = p_cuInit(0);
     if (r != CUDA_SUCCESS) {
@@ -279,6 +279,7 @@ nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
 
 struct nnb_net {
   int device = 0;
+  std::vector<std::vector<CUtensorMap>> maps;   // per launch
   CUcontext ctx = nullptr;
   std::vector<CUmodule> mods;
   std::vector<CUfunction> fns;
@@ -302,11 +303,14 @@ nnb_status enqueue(nnb_net *net, int n, CUstream s) {
     if (n < l.n_min || n > l.n_max) continue;
     uint64_t items = (uint64_t)n * l.items_per_image;
     uint64_t gx = (items + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
+    if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
     if (gx == 0) continue;
     if (gx > 0x7fffffffull) return fail(NNB_ERR_ARGUMENT, "grid too large (%llu)", (unsigned long long)gx);
     CUdeviceptr pool = net->pool, arena = net->arena;
     int nn = n;
-    void *args[] = {&pool, &arena, &nn};
+    size_t li = &l - net->launches.data();
+    void *args[6] = {&pool, &arena, &nn, nullptr, nullptr, nullptr};
+    for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
     CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
                                  l.smem_bytes, s, args, nullptr));
   }
@@ -463,6 +467,33 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   if (r != CUDA_SUCCESS) { fail(NNB_ERR_OOM, "arena alloc %llu bytes failed", (unsigned long long)d->arena_bytes); return bail(NNB_ERR_OOM); }
   r = C->p_cuMemsetD8(net->arena, 0, std::max<uint64_t>(d->arena_bytes, 256));
   if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "arena memset failed (%d)", (int)r); return bail(NNB_ERR_CUDA); }
+  net->maps.resize(net->launches.size());
+  for (size_t i = 0; i < net->launches.size(); ++i) {
+    const nnb_launch &l = net->launches[i];
+    if (l.n_tmaps > 3) { fail(NNB_ERR_ARGUMENT, "launch %zu: too many tensor maps", i); return bail(NNB_ERR_ARGUMENT); }
+    net->maps[i].resize(l.n_tmaps);
+    for (uint32_t k = 0; k < l.n_tmaps; ++k) {
+      const nnb_tmap &t = l.tmaps[k];
+      CUdeviceptr base = t.space == 1 ? net->arena : net->pool;
+      uint64_t limit = t.space == 1 ? net->arena_bytes : net->pool_bytes;
+      if ((t.space != 1 && t.space != 2) || t.offset + (t.outer - 1) * t.row_bytes + 4 * t.inner > limit ||
+          t.row_bytes % 16 || t.offset % 16) {
+        fail(NNB_ERR_ARGUMENT, "launch %zu: tensor map %u out of range", i, k);
+        return bail(NNB_ERR_ARGUMENT);
+      }
+      cuuint64_t dims[2] = {t.inner, t.outer};
+      cuuint64_t strides[1] = {t.row_bytes};
+      cuuint32_t box[2] = {t.box_inner, t.box_outer};
+      cuuint32_t estr[2] = {1, 1};
+      r = C->p_cuTensorMapEncodeTiled(&net->maps[i][k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      reinterpret_cast<void *>(base + t.offset), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      t.swizzle == 3 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for launch %zu map %u", (int)r, i, k); return bail(NNB_ERR_CUDA); }
+    }
+  }
   net->inputs.assign(d->inputs, d->inputs + d->n_inputs);
   net->outputs.assign(d->outputs, d->outputs + d->n_outputs);
   r = C->p_cuStreamCreate(&net->capture_stream, CU_STREAM_NON_BLOCKING);
@@ -547,9 +578,11 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
   CUstream s = reinterpret_cast<CUstream>(stream);
   const nnb_launch &l = net->launches[index];
   uint64_t gx = ((uint64_t)n * l.items_per_image + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
+  if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
   CUdeviceptr pool = net->pool, arena = net->arena;
   int nn = n;
-  void *args[] = {&pool, &arena, &nn};
+  void *args[6] = {&pool, &arena, &nn, nullptr, nullptr, nullptr};
+  for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[index][k];
   CU_CHECK(C->p_cuEventRecord(net->ev0, s));
   for (int i = 0; i < iters; ++i)
     CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,

@@ -32,6 +32,9 @@ MODE_CODE = {"rational": 0, "fast": 1, "exact": 2}
 SMEXP_CODE = {"fast": 0, "precise": 1, "exact": 2}
 
 SMALL_M = 8           # Dense rows at or below this use the split-K GEMV kernel
+TC_MIN_K = 32         # tensor-core GEMM eligibility (contraction and output width)
+TC_MIN_N = 32
+TC_MIN_ROWS = 2048    # GEMM rows per launch from which the tcgen05 kernel is used
 ELEM_BLOCK = 256
 
 
@@ -49,6 +52,8 @@ class Launch:
     n_max: int = 1 << 30
     unit: int = -1
     note: str = ""
+    grid_cap: int = 0                 # persistent kernels: at most this many CTAs
+    tmaps: list = field(default_factory=list)   # TMA descriptors (see nnb_tmap)
 
 
 class DevicePool:
@@ -99,7 +104,10 @@ def _pad4(x):
 
 
 class Specializer:
-    def __init__(self, plan, assignment, options, max_batch, capacity):
+    def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
+                 sm_count=148):
+        self.use_tc = use_tc
+        self.sm_count = sm_count
         self.plan = plan
         self.asg = assignment
         self.opt = options
@@ -118,10 +126,23 @@ class Specializer:
         return 4 * self.plan.tensors[tid].elements
 
     def emit(self, unit_pos, tag, template, fields, block, smem, ipi, ipb,
-             grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note=""):
+             grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note="",
+             tmaps=(), grid_cap=0):
         kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
         cfg = f"Cfg_{len(self.names)}"
         body = _cfg_struct(cfg, fields)
+        if tmaps:
+            body += (f"\nextern \"C\" __global__ void __launch_bounds__({block}, 1) {kname}("
+                     f"const float* __restrict__ pool, float* __restrict__ arena, int n, "
+                     f"const __grid_constant__ nnb::TmaDesc tm0, "
+                     f"const __grid_constant__ nnb::TmaDesc tm1, "
+                     f"const __grid_constant__ nnb::TmaDesc tm2) {{\n"
+                     f"  {template}<{cfg}>::run(pool, arena, n, &tm0, &tm1, &tm2);\n}}\n")
+            self.chunks.append(body)
+            self.names.append(kname)
+            self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min, n_max,
+                                        unit_pos, note, grid_cap, list(tmaps)))
+            return
         if dynamic_smem:
             call = (f"  extern __shared__ __align__(16) unsigned char nnb_smem[];\n"
                     f"  {template}<{cfg}>::run(pool, arena, n, "
@@ -187,6 +208,18 @@ class Specializer:
         else:
             n_min = 1
 
+        # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
+        n_max = 1 << 30
+        tc_ok = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
+                 and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
+        if tc_ok:
+            n_tc = max(n_min, -(-TC_MIN_ROWS // rows))
+            if n_tc <= self.max_batch:
+                self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc)
+                n_max = n_tc - 1
+                if n_max < n_min:
+                    return
+
         # tile shape
         if softmax:
             TN = _pad4(CO)
@@ -234,8 +267,37 @@ class Specializer:
         fields.update(self.epilogue_fields(u, CO))
         tag = "dense" if u.kind == "Dense" else f"conv{KH}x{KW}"
         self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
-                  grid_mult=ntile_n, n_min=n_min, dynamic_smem=True,
+                  grid_mult=ntile_n, n_min=n_min, n_max=n_max, dynamic_smem=True,
                   note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
+
+    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min):
+        """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min."""
+        BN = min(256, -(-CO // 16) * 16)
+        NPAD = -(-CO // BN) * BN
+        KPAD = -(-K // 32) * 32
+        stage = 2 * 128 * 32 * 4 + 2 * BN * 32 * 4
+        NS = max(2, min(4, (200 * 1024) // stage))
+        wt = np.zeros((NPAD, KPAD), F32)
+        wt[:CO, :K] = np.asarray(wmat, F32).T
+        hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
+        lo = (wt - hi).astype(F32)
+        hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
+        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows,
+                      OUT_OFF=self.arena_off(u.output_id), B_OFF=self.pool.add(u.bias),
+                      RES=u.residual_id is not None,
+                      RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
+        fields.update(self.epilogue_fields(u, CO))
+        tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]), inner=K,
+                    outer=self.cap * rows, row_bytes=4 * K, box_inner=32, box_outer=128)
+        tm_b = dict(space=2, offset=hi_off, inner=KPAD, outer=NPAD, row_bytes=4 * KPAD,
+                    box_inner=32, box_outer=BN)
+        tm_bl = dict(tm_b, offset=lo_off)
+        smem = NS * stage + 1024 + 256
+        ntn = NPAD // BN
+        tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
+        self.emit(pos, tag, "nnb::GemmTc", fields, 256, smem, rows, 128, grid_mult=ntn,
+                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl], grid_cap=self.sm_count,
+                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}")
 
     def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max):
         MB = n_max
@@ -409,5 +471,5 @@ class Specializer:
                               kernel_source=ks)
 
 
-def specialize(plan, assignment, options, max_batch, capacity):
-    return Specializer(plan, assignment, options, max_batch, capacity).run()
+def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148):
+    return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count).run()

@@ -79,7 +79,7 @@ class _Handle:
 
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
-                 gpu_fusion=True, cache_dir=None):
+                 gpu_fusion=True, cache_dir=None, use_tc=True):
         import torch
 
         t0 = time.perf_counter()
@@ -90,12 +90,13 @@ class CompiledNetwork:
         self.max_batch = int(batch) if batch is not None else 1
         if self.max_batch < 1:
             raise ValueError("batch must be >= 1")
-        _native.device_check(device)
+        _, _, sm_count = _native.device_check(device)
         self.graph = build_graph(manifest, weights)
         self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion)
         self.assignment = plan_buffers(self.plan)
         cap = _capacity(self.max_batch)
-        spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap)
+        spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
+                          use_tc=use_tc, sm_count=sm_count)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):
@@ -111,9 +112,14 @@ class CompiledNetwork:
         launches = (_native.Launch * max(len(spec.launches), 1))()
         index = {n: i for i, n in enumerate(spec.kernel_names)}
         for i, l in enumerate(spec.launches):
+            tm = (_native.TMap * 3)()
+            for k, t in enumerate(l.tmaps):
+                tm[k] = _native.TMap(t["space"], t.get("swizzle", 3), t["offset"], t["inner"],
+                                     t["outer"], t["row_bytes"], t["box_inner"], t["box_outer"])
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,
                                          l.items_per_image, l.items_per_block,
-                                         l.n_min, min(l.n_max, 1 << 30))
+                                         l.n_min, min(l.n_max, 1 << 30), l.grid_cap,
+                                         len(l.tmaps), tm)
         in_arr = (_native.IO * max(len(ins), 1))(*[_native.IO(o, b) for o, b in ins])
         out_arr = (_native.IO * max(len(outs), 1))(*[_native.IO(o, b) for o, b in outs])
         pool_buf = ctypes.create_string_buffer(spec.pool, max(len(spec.pool), 1))

@@ -30,3 +30,16 @@ def test_config_default_modes_vs_oracle_models(cfg):
     got = net.run([x])[0].cpu().numpy()
     want = oracle.run(m, w, [x], opts)[0]
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 2048), (1, 3001), (2, 40), (3, 33)])
+def test_tensor_core_path_vs_oracle(cfg, n):
+    """Batches large enough for the tcgen05 3xTF32 GEMM (Dense, 1x1 conv)."""
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=n)
+    assert any("_tc_" in l.kernel for l in net.artifact.launches
+               if l.n_min <= n <= l.n_max), "tensor-core kernel not selected"
+    x = zoo.inputs(cfg, n)
+    got = net.run([x])[0].cpu().numpy()
+    want = oracle.run(m, w, [x], "exact")[0]
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
