@@ -14,15 +14,17 @@
 // shared memory by two converter warps while the tensor core works on the
 // previous stage.
 //
-// Warp roles (256 threads, one CTA per SM, persistent over output tiles):
+// Warp roles (384 threads, one CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: A tile [128 x 32] and B_hi/B_lo tiles [BN x 32],
 //               128B-swizzled, into an NS-stage ring (mbarrier full/empty)
 //   warp 1      TMEM allocator + single-thread MMA issuer:
 //               tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8
 //   warps 2-3   converter: A -> (A_hi in place, A_lo) in the same swizzled
 //               layout (elementwise, so the layout is preserved)
-//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 16 columns, bias, activation,
-//               post-affine, residual, float4 stores; the accumulator is
+//   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (the hardware's
+//               lane-quarter rule) and half of the tile's columns;
+//               tcgen05.ld 32 lanes x 16 columns, bias, activation,
+//               post-affine, residual, float4 stores.  The accumulator is
 //               double-buffered in TMEM so the epilogue of tile t overlaps the
 //               MMAs of tile t+1.
 #pragma once
@@ -128,7 +130,10 @@ struct GemmTc {
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)(BM >> 4) << 24);
   static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(C::BN % 16 == 0 && C::BN >= 16 && C::BN <= 256, "UMMA N");
+  static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int THREADS = 128 + EPI_THREADS;
+  static constexpr int EPI_COLS = C::BN / (EPI_WARPS / 4);   // columns per epilogue warp
+  static_assert(C::BN % 32 == 0 && C::BN >= 32 && C::BN <= 256, "UMMA N / epilogue split");
   static_assert(STAGE % 1024 == 0, "stage alignment");
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
@@ -157,7 +162,7 @@ struct GemmTc {
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 128);
+        mbar_init(&tempty[a], EPI_THREADS);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -249,6 +254,7 @@ struct GemmTc {
       // ---------------- epilogue ----------------
       const int q = warp & 3;                    // TMEM lane quarter of this warp
       const int r = q * 32 + lane;               // row within the tile
+      const int cbeg = ((warp - 4) >> 2) * EPI_COLS;
       const float* bias = at<float>(pool, C::B_OFF);
       const float* ps = at<float>(pool, C::PS_OFF);
       const float* po = at<float>(pool, C::PO_OFF);
@@ -264,7 +270,7 @@ struct GemmTc {
         float* dst = out + m * C::N;
         const float* res = at<float>(arena, C::RES_OFF) + m * C::N;
 #pragma unroll 1
-        for (int c0 = 0; c0 < C::BN; c0 += 16) {
+        for (int c0 = cbeg; c0 < cbeg + EPI_COLS; c0 += 16) {
           float v[16];
           tmem_ld16(tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c0, v);
           const int col0 = nb * C::BN + c0;

@@ -29,7 +29,7 @@ __device__ __forceinline__ void softmax_row_regs(float (&v)[TN]) {
     double e[L];
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < L; ++j) { e[j] = exp((double)v[j] - (double)m); s += e[j]; }
+    for (int j = 0; j < L; ++j) { e[j] = d_exp((double)v[j] - (double)m); s += e[j]; }
 #pragma unroll
     for (int j = 0; j < L; ++j) v[j] = (float)(e[j] / s);
   } else {
@@ -49,7 +49,7 @@ __device__ __forceinline__ float softmax_warp_row(float v, bool live) {
   const float ninf = -__int_as_float(0x7f800000);
   float m = warp_max(live ? v : ninf);
   if (SMEXP == SMEXP_EXACT) {
-    double e = live ? exp((double)v - (double)m) : 0.0;
+    double e = live ? d_exp((double)v - (double)m) : 0.0;
     double s = warp_sum(e);
     return (float)(e / s);
   }
@@ -98,7 +98,7 @@ struct SoftmaxRows {
 #pragma unroll
       for (int t = 0; t < PER; ++t) {
         int j = lane + 32 * t;
-        e[t] = j < C::L ? exp((double)v[t] - (double)m) : 0.0;
+        e[t] = j < C::L ? d_exp((double)v[t] - (double)m) : 0.0;
         s += e[t];
       }
       s = warp_sum(s);

@@ -272,7 +272,7 @@ class Specializer:
 
     def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min."""
-        BN = min(256, -(-CO // 16) * 16)
+        BN = min(256, -(-CO // 32) * 32)
         NPAD = -(-CO // BN) * BN
         KPAD = -(-K // 32) * 32
         stage = 2 * 128 * 32 * 4 + 2 * BN * 32 * 4
@@ -295,7 +295,7 @@ class Specializer:
         smem = NS * stage + 1024 + 256
         ntn = NPAD // BN
         tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 256, smem, rows, 128, grid_mult=ntn,
+        self.emit(pos, tag, "nnb::GemmTc", fields, 384, smem, rows, 128, grid_mult=ntn,
                   n_min=n_min, tmaps=[tm_a, tm_b, tm_bl], grid_cap=self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}")
 
