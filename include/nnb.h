@@ -45,16 +45,18 @@ typedef enum {
   NNB_ERR_BATCH = 8         /* batch outside [1, max_batch]                -> InputShapeMismatch */
 } nnb_status;
 
-/* A 2-D float32 TMA descriptor the runtime encodes (cuTensorMapEncodeTiled)
- * once the arena and pool addresses are known. */
+/* A float32 TMA descriptor (rank 2..4) that the runtime encodes with
+ * cuTensorMapEncodeTiled once the arena and pool addresses are known.
+ * Coordinates outside the tensor are zero-filled by the hardware, which is
+ * how the convolution kernels get TF 'same' padding for free. */
 typedef struct {
   uint32_t space;            /* 1 = arena, 2 = weight pool                    */
   uint32_t swizzle;          /* 0 none, 3 = 128-byte swizzle                  */
   uint64_t offset;           /* byte offset inside the space                 */
-  uint64_t inner;            /* elements along the contiguous dimension      */
-  uint64_t outer;            /* rows                                          */
-  uint64_t row_bytes;        /* stride between rows (multiple of 16)          */
-  uint32_t box_inner, box_outer;
+  uint32_t rank;             /* 2..4                                          */
+  uint32_t box[4];           /* box extent per dimension (innermost first)    */
+  uint64_t dims[4];          /* elements per dimension (innermost first)      */
+  uint64_t strides[3];       /* bytes between consecutive indices of dims 1.. */
 } nnb_tmap;
 
 /* One kernel launch of the schedule.  The grid is

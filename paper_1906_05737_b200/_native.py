@@ -26,9 +26,18 @@ EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "n
 
 class TMap(ctypes.Structure):
     _fields_ = [("space", ctypes.c_uint32), ("swizzle", ctypes.c_uint32),
-                ("offset", ctypes.c_uint64), ("inner", ctypes.c_uint64),
-                ("outer", ctypes.c_uint64), ("row_bytes", ctypes.c_uint64),
-                ("box_inner", ctypes.c_uint32), ("box_outer", ctypes.c_uint32)]
+                ("offset", ctypes.c_uint64), ("rank", ctypes.c_uint32),
+                ("box", ctypes.c_uint32 * 4), ("dims", ctypes.c_uint64 * 4),
+                ("strides", ctypes.c_uint64 * 3)]
+
+
+def make_tmap(t):
+    """TMap from the dict the specialiser emits: space, offset, dims, strides, box."""
+    r = len(t["dims"])
+    box = (ctypes.c_uint32 * 4)(*(list(t["box"]) + [1] * (4 - r)))
+    dims = (ctypes.c_uint64 * 4)(*(list(t["dims"]) + [1] * (4 - r)))
+    strides = (ctypes.c_uint64 * 3)(*(list(t["strides"]) + [0] * (3 - len(t["strides"]))))
+    return TMap(t["space"], t.get("swizzle", 3), t["offset"], r, box, dims, strides)
 
 
 class Launch(ctypes.Structure):

@@ -70,6 +70,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const TmaDesc* map, u64* 
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const TmaDesc* map, u64* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -124,7 +133,13 @@ struct GemmTc {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int KB = (C::K + BK - 1) / BK;
   static constexpr int NTN = C::NPAD / C::BN;
-  static constexpr int ACC_COLS = C::BN;                  // fp32 accumulator columns
+  // One accumulator buffer = main (a_hi*b_hi) + correction (a_hi*b_lo + a_lo*b_hi)
+  // columns.  Tensor-core accumulation truncates once per MMA instruction, so the
+  // error grows with the number of accumulate steps into a large running sum;
+  // keeping the two small correction products out of the main sum cuts the
+  // truncations on it by 3x, and the two are added in FP32 (round-to-nearest)
+  // in the epilogue.
+  static constexpr int ACC_COLS = 2 * C::BN;              // fp32 columns per buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
                                  : 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
@@ -132,8 +147,16 @@ struct GemmTc {
   static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   static constexpr int THREADS = 128 + EPI_THREADS;
-  static constexpr int EPI_COLS = C::BN / (EPI_WARPS / 4);   // columns per epilogue warp
-  static_assert(C::BN % 32 == 0 && C::BN >= 32 && C::BN <= 256, "UMMA N / epilogue split");
+  static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
+  static constexpr int CHUNK_KB = 8;                 // k-blocks (K = 256) per TMEM chunk
+  static constexpr int NCHUNK = (KB + CHUNK_KB - 1) / CHUNK_KB;
+  static_assert(C::BN % 16 == 0 && C::BN >= 16 && C::BN <= 128, "UMMA N / TMEM budget");
+  // spatial (implicit-GEMM convolution) tiling: 8 x 16 output pixels per tile
+  static constexpr int TH = 8, TW = 16;
+  static constexpr int TX = C::CONV ? (C::WO + TW - 1) / TW : 1;
+  static constexpr int TPI = C::CONV ? ((C::HO + TH - 1) / TH) * TX : 1;
+  static constexpr int CB = C::CONV ? C::CI / BK : 1;       // channel blocks per tap
+  static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % 32 == 0");
   static_assert(STAGE % 1024 == 0, "stage alignment");
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
@@ -151,7 +174,7 @@ struct GemmTc {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
-    const int mtiles = (int)((rows + BM - 1) / BM);
+    const int mtiles = C::CONV ? n * TPI : (int)((rows + BM - 1) / BM);
     const int tiles = mtiles * NTN;
 
     if (threadIdx.x == 0) {
@@ -188,7 +211,16 @@ struct GemmTc {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
             mbar_expect_tx(&full[s], A_BYTES + 2 * B_BYTES);
-            tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
+            if (C::CONV) {
+              // tap (ky, kx) and channel block cb of an 8x16 output-pixel tile;
+              // out-of-image coordinates are zero-filled = 'same' padding
+              const int img = mb / TPI, tt = mb % TPI;
+              const int tap = kb / CB, cb = kb % CB;
+              tma_load_4d(st, tmA, &full[s], cb * BK, (tt % TX) * TW + tap % C::KW - C::PL,
+                          (tt / TX) * TH + tap / C::KW - C::PT, img);
+            } else {
+              tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
+            }
             tma_load_2d(st + 2 * A_BYTES, tmB, &full[s], kb * BK, nb * C::BN);
             tma_load_2d(st + 2 * A_BYTES + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
             if (++s == C::NS) { s = 0; ph ^= 1; }
@@ -197,13 +229,19 @@ struct GemmTc {
       }
     } else if (warp == 1) {
       // ---------------- MMA issuer ----------------
+      // K is consumed in chunks of CHUNK_KB k-blocks; every chunk starts a fresh
+      // (main, correction) accumulator pair in the next TMEM buffer and is
+      // reduced in FP32 by the epilogue warps (split-K inside the CTA).
       int s = 0, acc = 0;
       u32 ph = 0, aph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
-        tc_fence_after();
-        const u32 d = tmem + acc * ACC_COLS;
         for (int kb = 0; kb < KB; ++kb) {
+          const int kc = kb % CHUNK_KB;
+          if (kc == 0) {
+            mbar_wait(&tempty[acc], aph ^ 1);
+            tc_fence_after();
+          }
+          const u32 d = tmem + acc * ACC_COLS;
           mbar_wait(&lo_ready[s], ph);
           tc_fence_after();
           if (lane == 0) {
@@ -213,17 +251,20 @@ struct GemmTc {
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
-              mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_hi + o), IDESC, (kb | k) != 0);
-              mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_lo + o), IDESC, 1);
-              mma_tf32(d, sw128_desc(a_lo + o), sw128_desc(b_hi + o), IDESC, 1);
+              const u32 accum = (kc | k) != 0;
+              mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_hi + o), IDESC, accum);
+              mma_tf32(d + C::BN, sw128_desc(a_hi + o), sw128_desc(b_lo + o), IDESC, accum);
+              mma_tf32(d + C::BN, sw128_desc(a_lo + o), sw128_desc(b_hi + o), IDESC, 1);
             }
             mma_commit(&empty[s]);
-            if (kb == KB - 1) mma_commit(&tfull[acc]);
+            if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
           }
           __syncwarp();
           if (++s == C::NS) { s = 0; ph ^= 1; }
+          if (kc == CHUNK_KB - 1 || kb == KB - 1) {
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+          }
         }
-        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     } else if (warp < 4) {
       // ---------------- converter: A -> (hi, lo) ----------------
@@ -263,28 +304,66 @@ struct GemmTc {
       u32 aph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int mb = t / NTN, nb = t % NTN;
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        const long long m = (long long)mb * BM + r;
-        const bool live = m < rows;
-        float* dst = out + m * C::N;
-        const float* res = at<float>(arena, C::RES_OFF) + m * C::N;
-#pragma unroll 1
-        for (int c0 = cbeg; c0 < cbeg + EPI_COLS; c0 += 16) {
-          float v[16];
-          tmem_ld16(tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c0, v);
-          const int col0 = nb * C::BN + c0;
-          if (live && col0 < C::N) {
+        // FP32 (round-to-nearest) reduction of the per-chunk tensor-core sums
+        float run[EPI_COLS];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int col = col0 + i;
-              if (C::N % 16 == 0 || col < C::N) {
-                float y = v[i] + __ldg(bias + col);
-                y = finish<C::ACT, C::MODE, C::POST>(y, ps, po, col);
-                if (C::RES) y = add(y, __ldg(res + col));
-                v[i] = y;
-              }
+        for (int i = 0; i < EPI_COLS; ++i) run[i] = 0.f;
+        for (int ch = 0; ch < NCHUNK; ++ch) {
+          mbar_wait(&tfull[acc], aph);
+          tc_fence_after();
+#pragma unroll
+          for (int g = 0; g < EPI_COLS / 16; ++g) {
+            if (cbeg + g * 16 < C::BN) {             // warp-uniform
+              float v[16], cr[16];
+              const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + cbeg + g * 16;
+              tmem_ld16(ta, v);
+              tmem_ld16(ta + C::BN, cr);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) run[g * 16 + i] += v[i] + cr[i];
             }
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+        // output position of this thread's row
+        long long obase;            // element offset of the row's first channel
+        bool live;
+        if (C::CONV) {
+          const int img = mb / TPI, tt = mb % TPI;
+          const int oy = (tt / TX) * TH + r / TW, ox = (tt % TX) * TW + r % TW;
+          live = img < n && oy < C::HO && ox < C::WO;
+          obase = (long long)img * (C::OUT_IMG / 4) + ((long long)oy * C::WO + ox) * C::N;
+          if (C::POOL) {      // pooled row index of the 2x2 window this lane leads
+            const int py = (tt / TX) * (TH / 2) + (r / TW) / 2, px = (tt % TX) * (TW / 2) + (r % TW) / 2;
+            live = img < n && py < C::PHO && px < C::PWO && (lane & 17) == 0;
+            obase = (long long)img * (C::OUT_IMG / 4) + ((long long)py * C::PWO + px) * C::N;
+          }
+        } else {
+          const long long m = (long long)mb * BM + r;
+          live = m < rows;
+          obase = m * C::N;
+        }
+        float* dst = out + obase;
+        const float* res = at<float>(arena, C::RES_OFF) + obase;
+#pragma unroll
+        for (int g = 0; g < EPI_COLS / 16; ++g) {
+          const int col0 = nb * C::BN + cbeg + g * 16;
+          if (cbeg + g * 16 >= C::BN || col0 >= C::N) continue;   // warp-uniform
+          float* v = run + g * 16;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = col0 + i < C::N ? col0 + i : C::N - 1;
+            float y = v[i] + __ldg(bias + col);
+            y = finish<C::ACT, C::MODE, C::POST>(y, ps, po, col);
+            if (C::RES && live) y = add(y, __ldg(res + col));
+            if (C::POOL) {     // lanes w, w^1 (same image row), w^16 (next row)
+              y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
+              y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 16));
+            }
+            v[i] = y;
+          }
+          if (live) {
             if (C::N % 16 == 0) {
 #pragma unroll
               for (int i = 0; i < 16; i += 4)
@@ -297,9 +376,6 @@ struct GemmTc {
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
     tc_fence_before();

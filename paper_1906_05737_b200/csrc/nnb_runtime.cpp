@@ -476,16 +476,21 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
       const nnb_tmap &t = l.tmaps[k];
       CUdeviceptr base = t.space == 1 ? net->arena : net->pool;
       uint64_t limit = t.space == 1 ? net->arena_bytes : net->pool_bytes;
-      if ((t.space != 1 && t.space != 2) || t.offset + (t.outer - 1) * t.row_bytes + 4 * t.inner > limit ||
-          t.row_bytes % 16 || t.offset % 16) {
-        fail(NNB_ERR_ARGUMENT, "launch %zu: tensor map %u out of range", i, k);
+      bool bad = (t.space != 1 && t.space != 2) || t.rank < 2 || t.rank > 4 || t.offset % 16;
+      uint64_t last = t.offset + 4 * t.dims[0];
+      for (uint32_t d = 1; d < t.rank && !bad; ++d) {
+        bad = t.strides[d - 1] % 16 != 0 || t.box[d] == 0 || t.box[d] > 256;
+        last += (t.dims[d] - 1) * t.strides[d - 1];
+      }
+      if (bad || last > limit || t.box[0] * 4 > 128) {
+        fail(NNB_ERR_ARGUMENT, "launch %zu: tensor map %u malformed or out of range", i, k);
         return bail(NNB_ERR_ARGUMENT);
       }
-      cuuint64_t dims[2] = {t.inner, t.outer};
-      cuuint64_t strides[1] = {t.row_bytes};
-      cuuint32_t box[2] = {t.box_inner, t.box_outer};
-      cuuint32_t estr[2] = {1, 1};
-      r = C->p_cuTensorMapEncodeTiled(&net->maps[i][k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      cuuint64_t dims[4], strides[3];
+      cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+      for (uint32_t d = 0; d < t.rank; ++d) { dims[d] = t.dims[d]; box[d] = t.box[d]; }
+      for (uint32_t d = 0; d + 1 < t.rank; ++d) strides[d] = t.strides[d];
+      r = C->p_cuTensorMapEncodeTiled(&net->maps[i][k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, t.rank,
                                       reinterpret_cast<void *>(base + t.offset), dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE,
                                       t.swizzle == 3 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,

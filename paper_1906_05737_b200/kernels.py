@@ -105,8 +105,9 @@ def _pad4(x):
 
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
-                 sm_count=148):
+                 sm_count=148, tc_min_rows=TC_MIN_ROWS):
         self.use_tc = use_tc
+        self.tc_min_rows = tc_min_rows
         self.sm_count = sm_count
         self.plan = plan
         self.asg = assignment
@@ -210,12 +211,18 @@ class Specializer:
 
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
         n_max = 1 << 30
-        tc_ok = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
-                 and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
-        if tc_ok:
-            n_tc = max(n_min, -(-TC_MIN_ROWS // rows))
+        tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
+                   and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
+        tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
+                   and S == 1 and CI % 32 == 0 and CO >= 16)
+        if tc_rows or tc_conv:
+            n_tc = max(n_min, -(-self.tc_min_rows // rows))
             if n_tc <= self.max_batch:
-                self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc)
+                conv = None
+                if tc_conv:
+                    conv = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, KW=KW, PT=PT, PL=PL,
+                                POOL=pool_fused, PHO=PHO, PWO=PWO)
+                self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv)
                 n_max = n_tc - 1
                 if n_max < n_min:
                     return
@@ -270,9 +277,11 @@ class Specializer:
                   grid_mult=ntile_n, n_min=n_min, n_max=n_max, dynamic_smem=True,
                   note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
 
-    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min):
-        """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min."""
-        BN = min(256, -(-CO // 32) * 32)
+    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None):
+        """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
+        ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
+        stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
+        BN = min(128, -(-CO // 16) * 16) if CO < 32 else min(128, -(-CO // 32) * 32)
         NPAD = -(-CO // BN) * BN
         KPAD = -(-K // 32) * 32
         stage = 2 * 128 * 32 * 4 + 2 * BN * 32 * 4
@@ -282,20 +291,36 @@ class Specializer:
         hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
         lo = (wt - hi).astype(F32)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
-        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows,
+        geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1)
+        if conv:
+            geo.update(conv, CONV=1)
+        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows, **geo,
+                      OUT_IMG=self.img_bytes(u.output_id),
                       OUT_OFF=self.arena_off(u.output_id), B_OFF=self.pool.add(u.bias),
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO))
-        tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]), inner=K,
-                    outer=self.cap * rows, row_bytes=4 * K, box_inner=32, box_outer=128)
-        tm_b = dict(space=2, offset=hi_off, inner=KPAD, outer=NPAD, row_bytes=4 * KPAD,
-                    box_inner=32, box_outer=BN)
+        if conv:
+            H, W, CI = conv["H"], conv["W"], conv["CI"]
+            tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
+                        dims=(CI, W, H, self.cap), box=(32, 16, 8, 1),
+                        strides=(4 * CI, 4 * CI * W, 4 * CI * W * H))
+        else:
+            tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
+                        dims=(K, self.cap * rows), strides=(4 * K,), box=(32, 128))
+        tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
+                    box=(32, BN))
         tm_bl = dict(tm_b, offset=lo_off)
         smem = NS * stage + 1024 + 256
         ntn = NPAD // BN
-        tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 384, smem, rows, 128, grid_mult=ntn,
+        if conv:
+            tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // 16)
+            ipi, ipb = tpi, 1
+            tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
+        else:
+            ipi, ipb = rows, 128
+            tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
+        self.emit(pos, tag, "nnb::GemmTc", fields, 384, smem, ipi, ipb, grid_mult=ntn,
                   n_min=n_min, tmaps=[tm_a, tm_b, tm_bl], grid_cap=self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}")
 
@@ -471,5 +496,7 @@ class Specializer:
                               kernel_source=ks)
 
 
-def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148):
-    return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count).run()
+def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
+               tc_min_rows=TC_MIN_ROWS):
+    return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
+                       tc_min_rows).run()

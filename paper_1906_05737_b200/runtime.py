@@ -79,7 +79,7 @@ class _Handle:
 
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
-                 gpu_fusion=True, cache_dir=None, use_tc=True):
+                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None):
         import torch
 
         t0 = time.perf_counter()
@@ -95,8 +95,10 @@ class CompiledNetwork:
         self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion)
         self.assignment = plan_buffers(self.plan)
         cap = _capacity(self.max_batch)
+        from .kernels import TC_MIN_ROWS
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
-                          use_tc=use_tc, sm_count=sm_count)
+                          use_tc=use_tc, sm_count=sm_count,
+                          tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):
@@ -114,8 +116,7 @@ class CompiledNetwork:
         for i, l in enumerate(spec.launches):
             tm = (_native.TMap * 3)()
             for k, t in enumerate(l.tmaps):
-                tm[k] = _native.TMap(t["space"], t.get("swizzle", 3), t["offset"], t["inner"],
-                                     t["outer"], t["row_bytes"], t["box_inner"], t["box_outer"])
+                tm[k] = _native.make_tmap(t)
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,
                                          l.items_per_image, l.items_per_block,
                                          l.n_min, min(l.n_max, 1 << 30), l.grid_cap,
@@ -172,7 +173,9 @@ class CompiledNetwork:
     # -- execution ------------------------------------------------------------
     def apply(self, n=None):
         """Replay the compiled schedule (one CUDA graph) over the first ``n``
-        images (default: all ``batch``) on the current torch stream."""
+        images (default: all ``batch``) on the current torch stream.  Only the
+        first ``n`` rows of the output views are defined afterwards (the arena
+        space of rows ``>= n`` is shared with intermediate tensors)."""
         n = self.max_batch if n is None else int(n)
         _native.check(_native.lib().nnb_apply(self._h.ptr, n, self._stream()), "apply")
 

@@ -1,0 +1,244 @@
+"""GPU kernel sweeps through the public API vs the C oracle (cf. the reference's
+pkg/tests/test_emitters.py): irregular shapes, ragged channel vectors, clipped
+windows, every fused epilogue, the tcgen05 paths, bit-exact kinds, the
+approximation modes, and the runtime API contract."""
+import numpy as np
+import pytest
+
+from builders import bn_params, conv_net, dense_net, he, random_network
+from golden_util import GOLDEN, load, names
+from oracle import oracle
+from paper_1906_05737_b200 import (EXACT, ApproximationOptions, InputShapeMismatch,
+                                   build_graph, compile_model, zoo)
+from paper_1906_05737_b200.zoo import NetBuilder
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+TOL = dict(rtol=1e-4, atol=1e-5)
+
+
+def gpu(m, w, x, opts=EXACT, **kw):
+    net = compile_model(m, w, opts, batch=len(x), **kw)
+    return net.run([x])[0].cpu().numpy(), net
+
+
+def ref(m, w, x, opts="exact"):
+    return oracle.run(m, w, [x], opts)[0]
+
+
+@pytest.mark.parametrize("h,w,ci,co,k,s,pad,act", [
+    (7, 9, 3, 5, 3, 1, "same", "relu"), (8, 6, 4, 8, 3, 2, "same", "tanh"),
+    (5, 5, 2, 3, 2, 1, "valid", "sigmoid"), (9, 7, 1, 4, 3, 2, "valid", "linear"),
+    (6, 6, 5, 7, 1, 1, "valid", "relu6"), (10, 12, 8, 16, 3, 1, "same", "elu"),
+    (11, 13, 16, 33, 5, 2, "same", "relu"), (4, 4, 64, 64, 1, 1, "valid", "tanh")])
+@pytest.mark.parametrize("n", [1, 5])
+def test_conv_sweep(h, w, ci, co, k, s, pad, act, n):
+    rng = np.random.default_rng(h * 100 + co)
+    m, wt = conv_net(rng, h, w, ci, co, k=k, stride=s, padding=pad, act=act)
+    x = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
+    got, _ = gpu(m, wt, x)
+    np.testing.assert_allclose(got, ref(m, wt, x), **TOL)
+
+
+@pytest.mark.parametrize("h,w,ci,co,pad,pool,n", [
+    (10, 18, 32, 16, "same", False, 3), (17, 23, 32, 48, "same", True, 2),
+    (12, 40, 64, 32, "valid", True, 2), (9, 16, 32, 40, "same", False, 1),
+    (60, 80, 32, 64, "same", True, 2)])
+def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
+    """Implicit-GEMM tcgen05 conv (4-D TMA boxes, zero-filled borders), with
+    and without the fused 2x2 max-pool epilogue, ragged 8x16 tiles."""
+    rng = np.random.default_rng(ci + co + h)
+    b = NetBuilder()
+    x = b.input((h, w, ci))
+    y = b.layer("Conv2D", [x], {"filters": co, "kernel_size": 3, "padding": pad,
+                                "activation": "relu"},
+                [("kernel", he(rng, (3, 3, ci, co), 9 * ci)),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    if pool:
+        y = b.layer("MaxPool2D", [y], {"pool_size": 2, "strides": 2})
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
+    got, net = gpu(m, wt, xin, tc_min_rows=1)
+    assert any("_tc_" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+
+
+@pytest.mark.parametrize("k,units,act,n", [
+    (1, 1, "linear", 1), (3, 5, "relu", 7), (17, 9, "tanh", 3), (130, 7, "sigmoid", 12),
+    (64, 64, "elu", 2100), (256, 96, "relu6", 2048), (100, 40, "linear", 2500),
+    (1024, 512, "tanh", 2049)])
+def test_dense_sweep(k, units, act, n):
+    rng = np.random.default_rng(k + units)
+    m, w = dense_net(rng, k, units, act)
+    x = rng.uniform(-2, 2, (n, k)).astype(F32)
+    got, _ = gpu(m, w, x)
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+    if n > 8 and k % 4 == 0 and k >= 32 and units >= 32:     # force the tcgen05 path
+        got, net = gpu(m, w, x, tc_min_rows=1)
+        assert any("_tc_" in l.kernel for l in net.artifact.launches)
+        np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+
+
+def _single(kind, shape, config=None, weights=()):
+    b = NetBuilder()
+    x = b.input(shape)
+    y = b.layer(kind, [x], config, weights)
+    return b.build([y])
+
+
+@pytest.mark.parametrize("case", [
+    ("DepthwiseConv2D", (7, 9, 3), {"kernel_size": 3, "padding": "same", "activation": "relu"}),
+    ("DepthwiseConv2D", (8, 8, 8), {"kernel_size": 3, "strides": 2, "padding": "same"}),
+    ("DepthwiseConv2D", (6, 5, 5), {"kernel_size": [2, 3], "padding": "valid"}),
+    ("MaxPool2D", (7, 9, 3), {"pool_size": 2, "strides": 2, "padding": "same"}),
+    ("AvgPool2D", (7, 9, 3), {"pool_size": 3, "strides": 2, "padding": "same"}),
+    ("AvgPool2D", (6, 6, 4), {"pool_size": [2, 1], "strides": 1}),
+    ("MaxPool2D", (5, 7, 8), {"pool_size": 3, "strides": 1, "padding": "same"}),
+    ("GlobalAveragePooling2D", (8, 10, 12), None),
+    ("UpSample2D", (3, 4, 5), {"factor": 3}), ("UpSample2D", (3, 4, 8), {"factor": 2}),
+    ("ZeroPadding2D", (3, 4, 5), {"padding": [[1, 2], [0, 3]]}),
+    ("Activation", (37,), {"activation": "relu"}), ("Activation", (5, 5, 4), {"activation": "relu6"}),
+])
+def test_bit_exact_kinds(case):
+    kind, shape, cfg = case
+    rng = np.random.default_rng(len(shape) + shape[-1])
+    wts = ()
+    if kind == "DepthwiseConv2D":
+        kh, kw = (cfg["kernel_size"],) * 2 if isinstance(cfg["kernel_size"], int) else cfg["kernel_size"]
+        wts = [("kernel", he(rng, (kh, kw, shape[-1]), kh * kw)),
+               ("bias", (rng.standard_normal(shape[-1]) * 0.1).astype(F32))]
+    m, w = _single(kind, shape, cfg, wts)
+    x = rng.uniform(-2, 2, (4,) + shape).astype(F32)
+    got, _ = gpu(m, w, x)
+    np.testing.assert_array_equal(got, ref(m, w, x))
+
+
+@pytest.mark.parametrize("shape", [(5,), (4, 5, 6), (3, 3, 3)])
+def test_batchnorm_and_add_concat_bit_exact(shape):
+    rng = np.random.default_rng(11)
+    b = NetBuilder()
+    x = b.input(shape)
+    bn = b.layer("BatchNorm", [x], None, bn_params(rng, shape[-1]))
+    r = b.layer("Activation", [x], {"activation": "relu"})
+    t = b.layer("Activation", [x], {"activation": "relu6"})
+    a = b.layer("Add", [bn, r, t])
+    c = b.layer("Concatenate", [a, x, bn])
+    m, w = b.build([c])
+    xin = rng.uniform(-3, 3, (3,) + shape).astype(F32)
+    got, _ = gpu(m, w, xin)
+    np.testing.assert_array_equal(got, ref(m, w, xin))
+
+
+@pytest.mark.parametrize("n", [1, 2, 33])
+@pytest.mark.parametrize("smexp", ["fast", "precise", "exact"])
+def test_softmax_rows_and_pixels(n, smexp):
+    rng = np.random.default_rng(n)
+    opts = ApproximationOptions(activation_mode="exact", softmax_exp=smexp)
+    for shape in ((1000,), (33,), (2,), (6, 7, 3), (4, 4, 40)):
+        m, w = _single("Softmax", shape)
+        x = rng.normal(0, 4, (n,) + shape).astype(F32)
+        got, _ = gpu(m, w, x, opts)
+        np.testing.assert_allclose(got, ref(m, w, x, opts), rtol=1e-5, atol=1e-7)
+        np.testing.assert_allclose(got.sum(-1), 1.0, rtol=1e-5)
+
+
+@pytest.mark.parametrize("mode", ["rational", "fast"])
+@pytest.mark.parametrize("tag", ["tanh", "sigmoid"])
+def test_activation_kernels_bit_exact_vs_reference_models(mode, tag):
+    """The device approximations equal the reference's numpy models bit for bit
+    (tests/golden/approx.npz, pkg/src/nnjit/codegen/approx.py:72-128)."""
+    g = dict(np.load(GOLDEN / "approx.npz"))
+    xs = g["x"].astype(F32)
+    m, w = _single("Activation", (len(xs),), {"activation": tag})
+    got, _ = gpu(m, w, xs[None, :], ApproximationOptions(activation_mode=mode))
+    np.testing.assert_array_equal(got[0].view(np.uint32),
+                                  g[f"{tag}_{mode}"].astype(F32).view(np.uint32))
+
+
+def test_exact_transcendentals_match_float64_rounding():
+    """activation_mode='exact' reproduces the interpreter's float64 tanh /
+    sigmoid / expm1 rounded to float32 on a dense grid."""
+    xs = np.concatenate([np.linspace(-30, 30, 200001), [0.0, -0.0, 1e-30, -1e-30]]).astype(F32)
+    for tag in ("tanh", "sigmoid", "elu"):
+        m, w = _single("Activation", (len(xs),), {"activation": tag})
+        got, _ = gpu(m, w, xs[None, :])
+        want = oracle.activation(xs, tag)
+        mismatch = np.count_nonzero(got[0] != want)
+        assert mismatch <= 2, (tag, mismatch)
+
+
+@pytest.mark.parametrize("name", names())
+def test_golden_nets_vs_reference(name):
+    """Against the REAL reference's recorded outputs: interpreter (exact mode)
+    and compiled x86 path (its default and precise options)."""
+    m, w, x, rec = load(name)
+    got, _ = gpu(m, w, x)
+    np.testing.assert_allclose(got, rec["interp"], **TOL)
+    got, _ = gpu(m, w, x, ApproximationOptions())
+    np.testing.assert_allclose(got, rec["compiled_default"], **TOL)
+    got, _ = gpu(m, w, x, ApproximationOptions(softmax_exp="precise"))
+    np.testing.assert_allclose(got, rec["compiled_precise"], **TOL)
+
+
+def test_random_networks():
+    rng = np.random.default_rng(99)
+    for trial in range(12):
+        m, w, shape = random_network(rng)
+        x = rng.uniform(-2, 2, (3,) + shape).astype(F32)
+        got, _ = gpu(m, w, x)
+        np.testing.assert_allclose(got, ref(m, w, x), rtol=2e-4, atol=2e-5,
+                                   err_msg=f"trial {trial}")
+
+
+# -- runtime API contract ----------------------------------------------------------
+
+def test_views_stable_apply_idempotent_and_partial_batch():
+    m, w = zoo.build(2)
+    net = compile_model(m, w, EXACT, batch=6)
+    x = zoo.inputs(2, 6)
+    out1 = net.run([x])
+    first = out1[0].clone()
+    assert out1[0] is net.output_views[0] and net.run([x])[0] is out1[0]
+    net.apply()                                  # inputs are pinned: same result
+    np.testing.assert_array_equal(net.output_views[0].cpu().numpy(), first.cpu().numpy())
+    want = ref(m, w, x)
+    np.testing.assert_allclose(first.cpu().numpy(), want, **TOL)
+    net.output_views[0].zero_()
+    net.run([x[:2]])                             # apply over the first 2 images only
+    got = net.output_views[0].cpu().numpy()      # rows >= 2 are undefined after apply(2)
+    np.testing.assert_allclose(got[:2], want[:2], **TOL)
+    host = net.run_host([x])[0]
+    np.testing.assert_allclose(host, want, **TOL)
+
+
+def test_unbatched_views_have_reference_shapes():
+    m, w = zoo.build(0)
+    net = compile_model(m, w, EXACT)
+    assert tuple(net.input_views[0].shape) == (32, 32, 1)
+    assert tuple(net.output_views[0].shape) == (2,)
+    x = zoo.inputs(0, 1)[0]
+    net.input_views[0].copy_(__import__("torch").from_numpy(x))
+    net.apply()
+    np.testing.assert_allclose(net.output_views[0].cpu().numpy(), ref(m, w, x[None])[0], **TOL)
+    assert "units" in net.describe() and net.compile_ms > 0
+
+
+def test_errors():
+    m, w = zoo.build(1)
+    net = compile_model(m, w, EXACT, batch=4)
+    with pytest.raises(InputShapeMismatch):
+        net.run([np.zeros((4, 1000), F32)])
+    with pytest.raises(InputShapeMismatch):
+        net.run([np.zeros((5, 1024), F32)])
+    with pytest.raises(InputShapeMismatch):
+        net.run([])
+    with pytest.raises(InputShapeMismatch):
+        net.apply(5)
+
+
+def test_deterministic_outputs_across_compiles():
+    m, w = zoo.build(3)
+    x = zoo.inputs(3, 3)
+    a, _ = gpu(m, w, x)
+    b, _ = gpu(m, w, x)
+    np.testing.assert_array_equal(a, b)
