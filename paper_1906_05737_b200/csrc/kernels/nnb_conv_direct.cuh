@@ -1,0 +1,136 @@
+// nnb_conv_direct.cuh -- direct FFMA convolution for narrow inputs (CI <= 16,
+// CO <= 32): the network stems and the small encoder layers.
+//
+// At K = KH*KW*CI <= 144 an implicit GEMM spends its time on tile staging and
+// index arithmetic, not on FMAs.  Here every thread owns PY x PX output pixels
+// and all CO output channels in registers, walks the taps in the interpreter's
+// (ky, kx, ci) order (accumulators start at the bias; pkg/src/nnjit/
+// interpreter.py:52-62) with float4 loads along the channels when CI % 4 == 0,
+// and reads the (kh, kw, ci, co) weights as warp-uniform broadcasts from
+// shared memory.  The epilogue fuses activation, post-BN, residual Add and the
+// 2x2/2 max-pool (a thread owns a whole pool window when POOL).
+#pragma once
+#include "nnb_common.cuh"
+
+namespace nnb {
+
+template <class C>
+struct ConvDirect {
+  static constexpr int PY = C::POOL ? 2 : 1;
+  static constexpr int PX = C::POOL ? 2 : C::PXT;
+  static constexpr int NP = PY * PX;
+  static constexpr int CV = (C::CI % 4 == 0) ? 4 : 1;        // channels per load
+  static constexpr int WN = C::KH * C::KW * C::CI * C::CO;   // weight floats
+  static constexpr int CELLS_Y = C::POOL ? C::PHO : C::HO;
+  static constexpr int CELLS_X = C::POOL ? C::PWO : (C::WO + PX - 1) / PX;
+
+  struct Smem { alignas(16) float w[WN]; float b[C::CO]; };
+
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
+                             Smem& sm) {
+    const float* wg = at<float>(pool, C::W_OFF);
+    for (int i = threadIdx.x; i < WN; i += blockDim.x) sm.w[i] = __ldg(wg + i);
+    for (int i = threadIdx.x; i < C::CO; i += blockDim.x) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
+    __syncthreads();
+
+    const i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= (i64)n * CELLS_Y * CELLS_X) return;
+    const int cx = (int)(cell % CELLS_X);
+    const int cy = (int)((cell / CELLS_X) % CELLS_Y);
+    const i64 img = cell / ((i64)CELLS_X * CELLS_Y);
+    const int oy0 = cy * PY, ox0 = cx * PX;
+    const float* in = at<float>(arena, C::IN_OFF + img * C::IN_IMG);
+
+    float acc[NP][C::CO];
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int o = 0; o < C::CO; ++o) acc[p][o] = sm.b[o];
+
+#pragma unroll 1
+    for (int ky = 0; ky < C::KH; ++ky) {
+#pragma unroll
+      for (int kx = 0; kx < C::KW; ++kx) {
+#pragma unroll
+        for (int c0 = 0; c0 < C::CI; c0 += CV) {
+          float xv[NP][CV];
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const int iy = (oy0 + p / PX) * C::S - C::PT + ky;
+            const int ix = (ox0 + p % PX) * C::S - C::PL + kx;
+            const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
+            const float* src = in + ((i64)iy * C::W + ix) * C::CI + c0;
+            if (CV == 4) {
+              float4 v = ok ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+              xv[p][0] = v.x; xv[p][CV > 1 ? 1 : 0] = v.y; xv[p][CV > 2 ? 2 : 0] = v.z; xv[p][CV > 3 ? 3 : 0] = v.w;
+            } else {
+              xv[p][0] = ok ? __ldg(src) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CV; ++c) {
+            const float* wr = sm.w + ((ky * C::KW + kx) * C::CI + c0 + c) * C::CO;
+            if (C::CO % 4 == 0) {             // one LDS.128 broadcast feeds 4*NP FMAs
+#pragma unroll
+              for (int o = 0; o < C::CO; o += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wr + o);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                  acc[p][o] = fmaf(xv[p][c], w4.x, acc[p][o]);
+                  acc[p][o + 1] = fmaf(xv[p][c], w4.y, acc[p][o + 1]);
+                  acc[p][o + 2] = fmaf(xv[p][c], w4.z, acc[p][o + 2]);
+                  acc[p][o + 3] = fmaf(xv[p][c], w4.w, acc[p][o + 3]);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int o = 0; o < C::CO; ++o) {
+                const float wv = wr[o];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) acc[p][o] = fmaf(xv[p][c], wv, acc[p][o]);
+              }
+            }
+          }
+        }
+      }
+    }
+
+    const float* ps = at<float>(pool, C::PS_OFF);
+    const float* po = at<float>(pool, C::PO_OFF);
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int o = 0; o < C::CO; ++o) acc[p][o] = finish<C::ACT, C::MODE, C::POST>(acc[p][o], ps, po, o);
+
+    float* out = at<float>(arena, C::OUT_OFF + img * C::OUT_IMG);
+    if (C::POOL) {
+      float* dst = out + ((i64)cy * C::PWO + cx) * C::CO;
+#pragma unroll
+      for (int o = 0; o < C::CO; ++o)
+        dst[o] = fmaxf(fmaxf(acc[0][o], acc[1][o]), fmaxf(acc[2][o], acc[3][o]));
+      return;
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int oy = oy0 + p / PX, ox = ox0 + p % PX;
+      if (ox >= C::WO) continue;
+      const i64 pix = (i64)oy * C::WO + ox;
+      float* dst = out + pix * C::CO;
+      if (C::RES) {
+        const float* res = at<float>(arena, C::RES_OFF + img * C::OUT_IMG) + pix * C::CO;
+#pragma unroll
+        for (int o = 0; o < C::CO; ++o) acc[p][o] = add(acc[p][o], __ldg(res + o));
+      }
+      if (C::CO % 4 == 0) {
+#pragma unroll
+        for (int o = 0; o < C::CO; o += 4)
+          *reinterpret_cast<float4*>(dst + o) = make_float4(acc[p][o], acc[p][o + 1], acc[p][o + 2], acc[p][o + 3]);
+      } else {
+#pragma unroll
+        for (int o = 0; o < C::CO; ++o) dst[o] = acc[p][o];
+      }
+    }
+  }
+};
+
+}  // namespace nnb

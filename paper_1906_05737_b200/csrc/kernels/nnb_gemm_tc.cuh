@@ -103,6 +103,30 @@ __device__ __forceinline__ void mma_tf32(u32 tmem_d, u64 adesc, u64 bdesc, u32 i
       : "memory");
 }
 
+// A operand from tensor memory (lane = row, one tf32 per 32-bit column)
+__device__ __forceinline__ void mma_tf32_ts(u32 tmem_d, u32 tmem_a, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(u32 taddr, const u32 (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -130,7 +154,12 @@ struct GemmTc {
   static constexpr int BM = 128, BK = 32;
   static constexpr int A_BYTES = BM * BK * 4;            // 16 KiB
   static constexpr int B_BYTES = C::BN * BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  // TMEM_A: the split A operand lives in tensor memory (MMA "ts" form), so the
+  // tensor core reads only B from shared memory -- for narrow N the A re-reads
+  // (three products per k-step) otherwise saturate shared-memory bandwidth.
+  static constexpr bool TA = C::TMEM_A != 0;
+  static constexpr int A_SMEM = TA ? A_BYTES : 2 * A_BYTES;     // A (+ A_lo) in smem
+  static constexpr int STAGE = A_SMEM + 2 * B_BYTES;
   static constexpr int KB = (C::K + BK - 1) / BK;
   static constexpr int NTN = C::NPAD / C::BN;
   // One accumulator buffer = main (a_hi*b_hi) + correction (a_hi*b_lo + a_lo*b_hi)
@@ -140,13 +169,18 @@ struct GemmTc {
   // truncations on it by 3x, and the two are added in FP32 (round-to-nearest)
   // in the epilogue.
   static constexpr int ACC_COLS = 2 * C::BN;              // fp32 columns per buffer
-  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
-                                 : 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int A_TCOL = 2 * ACC_COLS;                    // first A column (TA)
+  static constexpr int TMEM_NEED = TA ? 2 * ACC_COLS + C::NS * 2 * BK : 2 * ACC_COLS;
+  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64
+                                 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static_assert(TMEM_NEED <= 512, "TMEM budget");
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)(BM >> 4) << 24);
   static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
-  static constexpr int THREADS = 128 + EPI_THREADS;
+  static constexpr int CONV_WARPS = TA ? 4 : 2;                   // A splitters
+  static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
+  static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
   static constexpr int CHUNK_KB = 8;                 // k-blocks (K = 256) per TMEM chunk
   static constexpr int NCHUNK = (KB + CHUNK_KB - 1) / CHUNK_KB;
@@ -180,7 +214,7 @@ struct GemmTc {
     if (threadIdx.x == 0) {
       for (int s = 0; s < C::NS; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&lo_ready[s], 64);
+        mbar_init(&lo_ready[s], 32 * CONV_WARPS);
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
@@ -221,8 +255,8 @@ struct GemmTc {
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
             }
-            tma_load_2d(st + 2 * A_BYTES, tmB, &full[s], kb * BK, nb * C::BN);
-            tma_load_2d(st + 2 * A_BYTES + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
+            tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, nb * C::BN);
+            tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
             if (++s == C::NS) { s = 0; ph ^= 1; }
           }
         }
@@ -247,14 +281,21 @@ struct GemmTc {
           if (lane == 0) {
             const u32 base = smem_u32(smem + s * STAGE);
             const u32 a_hi = base, a_lo = base + A_BYTES;
-            const u32 b_hi = base + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+            const u32 b_hi = base + A_SMEM, b_lo = b_hi + B_BYTES;
+            const u32 ta = tmem + A_TCOL + s * 2 * BK;                // TMEM A slot
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
               const u32 accum = (kc | k) != 0;
-              mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_hi + o), IDESC, accum);
-              mma_tf32(d + C::BN, sw128_desc(a_hi + o), sw128_desc(b_lo + o), IDESC, accum);
-              mma_tf32(d + C::BN, sw128_desc(a_lo + o), sw128_desc(b_hi + o), IDESC, 1);
+              if (TA) {
+                mma_tf32_ts(d, ta + 8 * k, sw128_desc(b_hi + o), IDESC, accum);
+                mma_tf32_ts(d + C::BN, ta + 8 * k, sw128_desc(b_lo + o), IDESC, accum);
+                mma_tf32_ts(d + C::BN, ta + BK + 8 * k, sw128_desc(b_hi + o), IDESC, 1);
+              } else {
+                mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_hi + o), IDESC, accum);
+                mma_tf32(d + C::BN, sw128_desc(a_hi + o), sw128_desc(b_lo + o), IDESC, accum);
+                mma_tf32(d + C::BN, sw128_desc(a_lo + o), sw128_desc(b_hi + o), IDESC, 1);
+              }
             }
             mma_commit(&empty[s]);
             if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
@@ -266,7 +307,37 @@ struct GemmTc {
           }
         }
       }
-    } else if (warp < 4) {
+    } else if (warp < EPI_W0 && TA) {
+      // ---------------- converter: A row -> (hi, lo) columns in TMEM ----------------
+      const int q = warp & 3, r = q * 32 + lane;      // this thread's tile row = TMEM lane
+      int s = 0;
+      u32 ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[s], ph);
+          const unsigned char* row = smem + s * STAGE + r * 128;
+          u32 hi[BK], lo[BK];
+#pragma unroll
+          for (int j = 0; j < BK / 4; ++j) {          // 16-byte chunk j of the swizzled row
+            const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (r & 7)) << 4));
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const u32 h = __float_as_uint(e[i]) & 0xFFFFE000u;
+              hi[4 * j + i] = h;
+              lo[4 * j + i] = __float_as_uint(e[i] - __uint_as_float(h));
+            }
+          }
+          const u32 ta = tmem + ((u32)(q * 32) << 16) + A_TCOL + s * 2 * BK;
+          tmem_st32(ta, hi);
+          tmem_st32(ta + BK, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&lo_ready[s]);
+          if (++s == C::NS) { s = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp < EPI_W0) {
       // ---------------- converter: A -> (hi, lo) ----------------
       const int ct = threadIdx.x - 64;   // 0..63
       int s = 0;
@@ -295,7 +366,7 @@ struct GemmTc {
       // ---------------- epilogue ----------------
       const int q = warp & 3;                    // TMEM lane quarter of this warp
       const int r = q * 32 + lane;               // row within the tile
-      const int cbeg = ((warp - 4) >> 2) * EPI_COLS;
+      const int cbeg = ((warp - EPI_W0) >> 2) * EPI_COLS;
       const float* bias = at<float>(pool, C::B_OFF);
       const float* ps = at<float>(pool, C::PS_OFF);
       const float* po = at<float>(pool, C::PO_OFF);

@@ -6,3 +6,4 @@
 #include "nnb_small.cuh"
 #include "nnb_gemm_simt.cuh"
 #include "nnb_gemm_tc.cuh"
+#include "nnb_conv_direct.cuh"

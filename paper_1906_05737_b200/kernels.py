@@ -105,8 +105,9 @@ def _pad4(x):
 
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
-                 sm_count=148, tc_min_rows=TC_MIN_ROWS):
+                 sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True):
         self.use_tc = use_tc
+        self.tmem_a = tmem_a
         self.tc_min_rows = tc_min_rows
         self.sm_count = sm_count
         self.plan = plan
@@ -209,6 +210,13 @@ class Specializer:
         else:
             n_min = 1
 
+        # narrow inputs: direct FFMA convolution (all batch sizes)
+        if (u.kind == "Conv2D" and not softmax and CO <= 32
+                and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
+            self._conv_direct(pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL,
+                              pool_fused, PHO, PWO)
+            return
+
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
         n_max = 1 << 30
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
@@ -284,8 +292,12 @@ class Specializer:
         BN = min(128, -(-CO // 16) * 16) if CO < 32 else min(128, -(-CO // 32) * 32)
         NPAD = -(-CO // BN) * BN
         KPAD = -(-K // 32) * 32
-        stage = 2 * 128 * 32 * 4 + 2 * BN * 32 * 4
-        NS = max(2, min(4, (200 * 1024) // stage))
+        tmem_a = BN <= 64 and self.tmem_a
+        stage = (1 if tmem_a else 2) * 128 * 32 * 4 + 2 * BN * 32 * 4
+        # deep rings hide the TMA/L2 latency when a stage carries little MMA work
+        NS = max(2, min(8, (200 * 1024) // stage))
+        if tmem_a:
+            NS = min(NS, (512 - 4 * BN) // 64)
         wt = np.zeros((NPAD, KPAD), F32)
         wt[:CO, :K] = np.asarray(wmat, F32).T
         hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
@@ -294,7 +306,7 @@ class Specializer:
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1)
         if conv:
             geo.update(conv, CONV=1)
-        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows, **geo,
+        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows, TMEM_A=tmem_a, **geo,
                       OUT_IMG=self.img_bytes(u.output_id),
                       OUT_OFF=self.arena_off(u.output_id), B_OFF=self.pool.add(u.bias),
                       RES=u.residual_id is not None,
@@ -320,9 +332,29 @@ class Specializer:
         else:
             ipi, ipb = rows, 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 384, smem, ipi, ipb, grid_mult=ntn,
+        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if tmem_a else 384, smem, ipi, ipb,
+                  grid_mult=ntn,
                   n_min=n_min, tmaps=[tm_a, tm_b, tm_bl], grid_cap=self.sm_count,
-                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}")
+                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}"
+                       f"{' A in TMEM' if tmem_a else ''}")
+
+    def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
+                     PHO, PWO):
+        pxt = 4 if CO <= 8 else 2 if CO <= 16 else 1
+        fields = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
+                      POOL=pool_fused, PHO=PHO, PWO=PWO, PXT=pxt,
+                      IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                      W_OFF=self.pool.add(wmat), B_OFF=self.pool.add(u.bias),
+                      RES=u.residual_id is not None,
+                      RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
+        fields.update(self.epilogue_fields(u, CO))
+        cells = PHO * PWO if pool_fused else HO * -(-WO // pxt)
+        smem = 4 * (KH * KW * CI * CO + CO)
+        self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, cells, 128,
+                  dynamic_smem=True,
+                  note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
+                       f"{4 if pool_fused else pxt}")
 
     def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max):
         MB = n_max
@@ -497,6 +529,6 @@ class Specializer:
 
 
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
-               tc_min_rows=TC_MIN_ROWS):
+               tc_min_rows=TC_MIN_ROWS, tmem_a=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
-                       tc_min_rows).run()
+                       tc_min_rows, tmem_a).run()

@@ -79,7 +79,7 @@ class _Handle:
 
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
-                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None):
+                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True):
         import torch
 
         t0 = time.perf_counter()
@@ -98,7 +98,8 @@ class CompiledNetwork:
         from .kernels import TC_MIN_ROWS
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
                           use_tc=use_tc, sm_count=sm_count,
-                          tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows)
+                          tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
+                          tmem_a=tmem_a)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):
