@@ -69,7 +69,7 @@ struct Cu {
   CU_FN(cuGraphInstantiateWithFlags) CU_FN(cuGraphLaunch) CU_FN(cuGraphDestroy)
   CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
   CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
-  CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled)
+  CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled) CU_FN(cuLaunchKernelEx)
 #undef CU_FN
   void load() {
     const char *names[] = {"libcuda.so.1", "libcuda.so"};
@@ -92,6 +92,7 @@ struct Cu {
     CU_LOAD(cuGraphDestroy) CU_LOAD(cuGraphExecDestroy) CU_LOAD(cuEventCreate)
     CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
     CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString) CU_LOAD(cuTensorMapEncodeTiled)
+    CU_LOAD(cuLaunchKernelEx)
 #undef CU_LOAD
     CUresult r = p_cuInit(0);
     if (r != CUDA_SUCCESS) {
@@ -279,6 +280,7 @@ nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
 
 struct nnb_net {
   int device = 0;
+  bool pdl = false;   // NNB_PDL=1 enables programmatic dependent launch (measured: no gain)
   std::vector<std::vector<CUtensorMap>> maps;   // per launch
   CUcontext ctx = nullptr;
   std::vector<CUmodule> mods;
@@ -311,8 +313,24 @@ nnb_status enqueue(nnb_net *net, int n, CUstream s) {
     size_t li = &l - net->launches.data();
     void *args[6] = {&pool, &arena, &nn, nullptr, nullptr, nullptr};
     for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
-    CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
-                                 l.smem_bytes, s, args, nullptr));
+    if (net->pdl) {
+      // programmatic dependent launch: the next kernel's CTAs are scheduled while
+      // this one drains; each kernel starts with griddepcontrol.wait.
+      CUlaunchAttribute attr[1];
+      attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      attr[0].value.programmaticStreamSerializationAllowed = 1;
+      CUlaunchConfig cfg = {};
+      cfg.gridDimX = (unsigned)gx; cfg.gridDimY = 1; cfg.gridDimZ = 1;
+      cfg.blockDimX = l.block; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+      cfg.sharedMemBytes = l.smem_bytes;
+      cfg.hStream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CU_CHECK(C->p_cuLaunchKernelEx(&cfg, net->fns[l.kernel], args, nullptr));
+    } else {
+      CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
+                                   l.smem_bytes, s, args, nullptr));
+    }
   }
   return NNB_OK;
 }
@@ -402,6 +420,7 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   nnb_net *net = new nnb_net();
   net->device = d->device;
   net->max_batch = d->max_batch;
+  if (const char *e = getenv("NNB_PDL")) net->pdl = atoi(e) != 0;
   CUdevice dev;
   nnb_status st = device_ctx(d->device, &net->ctx, &dev);
   if (st != NNB_OK) { delete net; return st; }

@@ -139,6 +139,7 @@ class Specializer:
                      f"const __grid_constant__ nnb::TmaDesc tm0, "
                      f"const __grid_constant__ nnb::TmaDesc tm1, "
                      f"const __grid_constant__ nnb::TmaDesc tm2) {{\n"
+                     f"  NNB_PDL_PROLOGUE\n"
                      f"  {template}<{cfg}>::run(pool, arena, n, &tm0, &tm1, &tm2);\n}}\n")
             self.chunks.append(body)
             self.names.append(kname)
@@ -153,7 +154,7 @@ class Specializer:
             call = f"  {template}<{cfg}>::run(pool, arena, n);\n"
         body += (f"\nextern \"C\" __global__ void __launch_bounds__({block}) {kname}("
                  f"const float* __restrict__ pool, float* __restrict__ arena, int n) {{\n"
-                 + call + "}\n")
+                 f"  NNB_PDL_PROLOGUE\n" + call + "}\n")
         self.chunks.append(body)
         self.names.append(kname)
         self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min,
