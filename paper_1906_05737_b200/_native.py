@@ -46,7 +46,7 @@ class Launch(ctypes.Structure):
                 ("items_per_image", ctypes.c_uint64), ("items_per_block", ctypes.c_uint64),
                 ("n_min", ctypes.c_int32), ("n_max", ctypes.c_int32),
                 ("grid_cap", ctypes.c_uint32), ("n_tmaps", ctypes.c_uint32),
-                ("tmaps", TMap * 3)]
+                ("tmaps", TMap * 4)]
 
 
 class IO(ctypes.Structure):

@@ -115,19 +115,23 @@ struct ConvDirect {
       const int oy = oy0 + p / PX, ox = ox0 + p % PX;
       if (ox >= C::WO) continue;
       const i64 pix = (i64)oy * C::WO + ox;
-      float* dst = out + pix * C::CO;
+      float* dst = out + (C::UPF > 1 ? ((i64)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) : pix) * C::CO;
       if (C::RES) {
         const float* res = at<float>(arena, C::RES_OFF + img * C::OUT_IMG) + pix * C::CO;
 #pragma unroll
         for (int o = 0; o < C::CO; ++o) acc[p][o] = add(acc[p][o], __ldg(res + o));
       }
-      if (C::CO % 4 == 0) {
 #pragma unroll
-        for (int o = 0; o < C::CO; o += 4)
-          *reinterpret_cast<float4*>(dst + o) = make_float4(acc[p][o], acc[p][o + 1], acc[p][o + 2], acc[p][o + 3]);
-      } else {
+      for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
+        float* d = dst + ((i64)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO;
+        if (C::CO % 4 == 0) {
 #pragma unroll
-        for (int o = 0; o < C::CO; ++o) dst[o] = acc[p][o];
+          for (int o = 0; o < C::CO; o += 4)
+            *reinterpret_cast<float4*>(d + o) = make_float4(acc[p][o], acc[p][o + 1], acc[p][o + 2], acc[p][o + 3]);
+        } else {
+#pragma unroll
+          for (int o = 0; o < C::CO; ++o) d[o] = acc[p][o];
+        }
       }
     }
   }

@@ -74,8 +74,9 @@ struct GemmSimt {
     // ---- per-thread A-load rows (fixed across the K loop) ----
     constexpr int KQ = C::BK / AKV;          // load slots per row
     int a_mi[A_LOADS], a_kq[A_LOADS];
-    const float* a_base[A_LOADS];
+    const float* a_base[A_LOADS];          // image base of source 0 (or the only source)
     int a_iy[A_LOADS], a_ix[A_LOADS];
+    i64 a_img[A_LOADS];
 #pragma unroll
     for (int l = 0; l < A_LOADS; ++l) {
       int e = tid + l * NT;
@@ -88,11 +89,13 @@ struct GemmSimt {
         int oy, ox;
         row_pixel(r, oy, ox);
         a_base[l] = in + img * (C::IN_IMG / 4);
+        a_img[l] = img;
         a_iy[l] = oy * C::S - C::PT;
         a_ix[l] = ox * C::S - C::PL;
       } else {
         a_base[l] = nullptr;
         a_iy[l] = a_ix[l] = 0;
+        a_img[l] = 0;
       }
     }
 
@@ -109,12 +112,17 @@ struct GemmSimt {
         int ci = k % C::CI;
         int iy = a_iy[l] + ky, ix = a_ix[l] + kx;
         ok = ok && iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
+        // channel-concat loader: channels [0, C0) from source 0, the rest from source 1
+        const float* src = a_base[l] + (iy * C::W + ix) * C::C0 + ci;
+        if (C::CONCAT && ci >= C::C0)
+          src = at<float>(arena, C::IN1_OFF) + a_img[l] * (C::IN1_IMG / 4) +
+                (iy * C::W + ix) * (C::CI - C::C0) + (ci - C::C0);
         if (AVEC) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ok) v = __ldg(reinterpret_cast<const float4*>(a_base[l] + (iy * C::W + ix) * C::CI + ci));
+          if (ok) v = __ldg(reinterpret_cast<const float4*>(src));
           ra[l][0] = v.x; if (AKV > 1) { ra[l][1 % AKV] = v.y; ra[l][2 % AKV] = v.z; ra[l][3 % AKV] = v.w; }
         } else {
-          ra[l][0] = ok ? __ldg(a_base[l] + (iy * C::W + ix) * C::CI + ci) : 0.f;
+          ra[l][0] = ok ? __ldg(src) : 0.f;
         }
       }
     };
@@ -234,6 +242,10 @@ struct GemmSimt {
       i64 img = m / C::ROWS;
       int r = (int)(m - img * C::ROWS);
       float* dst = out + img * (C::OUT_IMG / 4) + (i64)r * C::CO;
+      if (C::UPF > 1) {       // fused nearest upsampling: the pixel's first replica
+        const int oy = r / C::WO, ox = r % C::WO;
+        dst = out + img * (C::OUT_IMG / 4) + ((i64)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::CO;
+      }
       if (C::RES) {
         const float* res = at<float>(arena, C::RES_OFF) + img * (C::OUT_IMG / 4) + (i64)r * C::CO;
 #pragma unroll
@@ -247,19 +259,23 @@ struct GemmSimt {
         // the thread owns the whole row (planner guarantees TN >= CO, NTX == 1)
         softmax_row_regs<C::TN, C::CO, C::SMEXP>(acc[i]);
       }
-      if (BVEC && C::TN % 4 == 0 && C::CO % 4 == 0) {
 #pragma unroll
-        for (int j = 0; j < C::TN; j += 4) {
-          int col = n0 + tx * C::TN + j;
-          if (col < C::CO)
-            *reinterpret_cast<float4*>(dst + col) =
-                make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
-        }
-      } else {
+      for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
+        float* d = dst + ((i64)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO;
+        if (BVEC && C::TN % 4 == 0 && C::CO % 4 == 0) {
 #pragma unroll
-        for (int j = 0; j < C::TN; ++j) {
-          int col = n0 + tx * C::TN + j;
-          if (col < C::CO) dst[col] = acc[i][j];
+          for (int j = 0; j < C::TN; j += 4) {
+            int col = n0 + tx * C::TN + j;
+            if (col < C::CO)
+              *reinterpret_cast<float4*>(d + col) =
+                  make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < C::TN; ++j) {
+            int col = n0 + tx * C::TN + j;
+            if (col < C::CO) d[col] = acc[i][j];
+          }
         }
       }
     }

@@ -190,11 +190,13 @@ struct GemmTc {
   static constexpr int TX = C::CONV ? (C::WO + TW - 1) / TW : 1;
   static constexpr int TPI = C::CONV ? ((C::HO + TH - 1) / TH) * TX : 1;
   static constexpr int CB = C::CONV ? C::CI / BK : 1;       // channel blocks per tap
+  static constexpr int CB0 = C::CONV ? C::C0 / BK : 1;      // ... from source 0
   static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % 32 == 0");
   static_assert(STAGE % 1024 == 0, "stage alignment");
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
-                             const TmaDesc* tmA, const TmaDesc* tmB, const TmaDesc* tmBlo) {
+                             const TmaDesc* tmA, const TmaDesc* tmB, const TmaDesc* tmBlo,
+                             const TmaDesc* tmA1) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + 1023) & ~(u64)1023);
@@ -248,9 +250,12 @@ struct GemmTc {
             if (C::CONV) {
               // tap (ky, kx) and channel block cb of an 8x16 output-pixel tile;
               // out-of-image coordinates are zero-filled = 'same' padding
+              // with CONCAT, channel blocks >= C0/32 come from the second source
               const int img = mb / TPI, tt = mb % TPI;
               const int tap = kb / CB, cb = kb % CB;
-              tma_load_4d(st, tmA, &full[s], cb * BK, (tt % TX) * TW + tap % C::KW - C::PL,
+              const bool second = C::CONCAT && cb >= CB0;
+              tma_load_4d(st, second ? tmA1 : tmA, &full[s], (second ? cb - CB0 : cb) * BK,
+                          (tt % TX) * TW + tap % C::KW - C::PL,
                           (tt / TX) * TH + tap / C::KW - C::PT, img);
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
@@ -405,6 +410,9 @@ struct GemmTc {
           const int oy = (tt / TX) * TH + r / TW, ox = (tt % TX) * TW + r % TW;
           live = img < n && oy < C::HO && ox < C::WO;
           obase = (long long)img * (C::OUT_IMG / 4) + ((long long)oy * C::WO + ox) * C::N;
+          if (C::UPF > 1)     // fused nearest upsampling: first replica of the pixel
+            obase = (long long)img * (C::OUT_IMG / 4) +
+                    ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
           if (C::POOL) {      // pooled row index of the 2x2 window this lane leads
             const int py = (tt / TX) * (TH / 2) + (r / TW) / 2, px = (tt % TX) * (TW / 2) + (r % TW) / 2;
             live = img < n && py < C::PHO && px < C::PWO && (lane & 17) == 0;
@@ -414,6 +422,12 @@ struct GemmTc {
           const long long m = (long long)mb * BM + r;
           live = m < rows;
           obase = m * C::N;
+          if (C::UPF > 1) {   // 1x1 conv rows: pixel (oy, ox) of image m / ROWS
+            const long long img = m / C::ROWS;
+            const int rr = (int)(m - img * C::ROWS), oy = rr / C::WO, ox = rr % C::WO;
+            obase = img * (C::OUT_IMG / 4) +
+                    ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
+          }
         }
         float* dst = out + obase;
         const float* res = at<float>(arena, C::RES_OFF) + obase;
@@ -435,15 +449,19 @@ struct GemmTc {
             v[i] = y;
           }
           if (live) {
-            if (C::N % 16 == 0) {
 #pragma unroll
-              for (int i = 0; i < 16; i += 4)
-                *reinterpret_cast<float4*>(dst + col0 + i) =
-                    make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            } else {
+            for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
+              float* d = dst + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::N;
+              if (C::N % 16 == 0) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (col0 + i < C::N) dst[col0 + i] = v[i];
+                for (int i = 0; i < 16; i += 4)
+                  *reinterpret_cast<float4*>(d + col0 + i) =
+                      make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (col0 + i < C::N) d[col0 + i] = v[i];
+              }
             }
           }
         }

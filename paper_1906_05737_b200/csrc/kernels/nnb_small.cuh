@@ -167,7 +167,14 @@ struct Pool {
 #pragma unroll
       for (int l = 0; l < V; ++l) set_lane(acc, l, dvd(lane(acc, l), cf));
     }
-    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[p % ((i64)C::HO * C::WO) * CG + cg] = acc;
+    T* out = at<T>(arena, C::OUT_OFF + img * C::OUT_IMG);
+    if (C::UPF > 1) {             // fused nearest upsampling of the pooled map
+#pragma unroll
+      for (int rep = 0; rep < C::UPF * C::UPF; ++rep)
+        out[((i64)(oy * C::UPF + rep / C::UPF) * C::WO * C::UPF + ox * C::UPF + rep % C::UPF) * CG + cg] = acc;
+      return;
+    }
+    out[p % ((i64)C::HO * C::WO) * CG + cg] = acc;
   }
 };
 

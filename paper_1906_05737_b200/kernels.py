@@ -138,9 +138,10 @@ class Specializer:
                      f"const float* __restrict__ pool, float* __restrict__ arena, int n, "
                      f"const __grid_constant__ nnb::TmaDesc tm0, "
                      f"const __grid_constant__ nnb::TmaDesc tm1, "
-                     f"const __grid_constant__ nnb::TmaDesc tm2) {{\n"
+                     f"const __grid_constant__ nnb::TmaDesc tm2, "
+                     f"const __grid_constant__ nnb::TmaDesc tm3) {{\n"
                      f"  NNB_PDL_PROLOGUE\n"
-                     f"  {template}<{cfg}>::run(pool, arena, n, &tm0, &tm1, &tm2);\n}}\n")
+                     f"  {template}<{cfg}>::run(pool, arena, n, &tm0, &tm1, &tm2, &tm3);\n}}\n")
             self.chunks.append(body)
             self.names.append(kname)
             self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min, n_max,
@@ -181,10 +182,12 @@ class Specializer:
             HO = WO = 1
             wmat = np.asarray(u.kernel, F32)
         else:
-            H, W, CI = x.dims
+            H, W = x.h, x.w
+            CI = sum(sh.c for sh in u.input_shapes)      # concat loader: both sources
             KH, KW = u.kernel_hw
             S = u.stride
-            conv_out = u.pre_pool_shape if u.pool_after else u.output_shape
+            conv_out = (u.pre_pool_shape if u.pool_after else
+                        u.pre_up_shape if u.upsample_after > 1 else u.output_shape)
             HO, WO, CO = conv_out.dims
             if u.padding == "same":
                 PT, PL = same_padding(H, KH, S)[0], same_padding(W, KW, S)[0]
@@ -193,6 +196,12 @@ class Specializer:
             wmat = np.asarray(u.kernel, F32).reshape(KH * KW * CI, CO)
         K = KH * KW * CI
         pool_fused = bool(u.pool_after)
+        UPF = u.upsample_after
+        concat = bool(u.concat_in)
+        C0 = u.input_shapes[0].c if concat else CI
+        src1 = dict(CONCAT=concat, C0=C0, UPF=UPF,
+                    IN1_OFF=self.arena_off(u.input_ids[1]) if concat else 0,
+                    IN1_IMG=self.img_bytes(u.input_ids[1]) if concat else 0)
         if pool_fused:
             PHO, PWO = u.output_shape.h, u.output_shape.w
             rows = PHO * PWO * 4
@@ -214,8 +223,9 @@ class Specializer:
         # narrow inputs: direct FFMA convolution (all batch sizes)
         if (u.kind == "Conv2D" and not softmax and CO <= 32
                 and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
+            assert not concat
             self._conv_direct(pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL,
-                              pool_fused, PHO, PWO)
+                              pool_fused, PHO, PWO, UPF)
             return
 
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
@@ -223,15 +233,17 @@ class Specializer:
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
                    and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
-                   and S == 1 and CI % 32 == 0 and CO >= 16)
+                   and S == 1 and CI % 32 == 0 and C0 % 32 == 0 and CO >= 16)
         if tc_rows or tc_conv:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
             if n_tc <= self.max_batch:
                 conv = None
                 if tc_conv:
                     conv = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, KW=KW, PT=PT, PL=PL,
-                                POOL=pool_fused, PHO=PHO, PWO=PWO)
-                self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv)
+                                POOL=pool_fused, PHO=PHO, PWO=PWO, C0=C0,
+                                CONCAT=concat, UPF=UPF)
+                self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
+                              rows_geo=dict(HO=HO, WO=WO, UPF=UPF))
                 n_max = n_tc - 1
                 if n_max < n_min:
                     return
@@ -260,7 +272,7 @@ class Specializer:
             BK = _pad4(K)
         else:
             BK = 8 if BM >= 256 else 16
-        avec = CI % 4 == 0 and BK % 4 == 0
+        avec = CI % 4 == 0 and C0 % 4 == 0 and BK % 4 == 0
         akv = 4 if avec else 1
         while (BM * BK) % (akv * NT):
             BK += 4 if avec else 1
@@ -279,14 +291,14 @@ class Specializer:
             RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
             RES_FIRST=False,
             SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
-            BM=BM, BN=BN, BK=BK, TM=TM, TN=TN)
+            BM=BM, BN=BN, BK=BK, TM=TM, TN=TN, **src1)
         fields.update(self.epilogue_fields(u, CO))
         tag = "dense" if u.kind == "Dense" else f"conv{KH}x{KW}"
         self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
                   grid_mult=ntile_n, n_min=n_min, n_max=n_max, dynamic_smem=True,
                   note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
 
-    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None):
+    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
@@ -304,9 +316,12 @@ class Specializer:
         hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
         lo = (wt - hi).astype(F32)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
-        geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1)
+        geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
+                   C0=1, CONCAT=0, UPF=1)
         if conv:
             geo.update(conv, CONV=1)
+        elif rows_geo:
+            geo.update(rows_geo)
         fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows, TMEM_A=tmem_a, **geo,
                       OUT_IMG=self.img_bytes(u.output_id),
                       OUT_OFF=self.arena_off(u.output_id), B_OFF=self.pool.add(u.bias),
@@ -314,13 +329,18 @@ class Specializer:
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO))
         if conv:
-            H, W, CI = conv["H"], conv["W"], conv["CI"]
-            tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
-                        dims=(CI, W, H, self.cap), box=(32, 16, 8, 1),
-                        strides=(4 * CI, 4 * CI * W, 4 * CI * W * H))
+            H, W = conv["H"], conv["W"]
+
+            def act_map(tid, ch):
+                return dict(space=1, offset=self.arena_off(tid), dims=(ch, W, H, self.cap),
+                            box=(32, 16, 8, 1), strides=(4 * ch, 4 * ch * W, 4 * ch * W * H))
+            tm_a = act_map(u.input_ids[0], conv["C0"])
+            tm_a1 = (act_map(u.input_ids[1], conv["CI"] - conv["C0"]) if conv["CONCAT"]
+                     else tm_a)
         else:
             tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
                         dims=(K, self.cap * rows), strides=(4 * K,), box=(32, 128))
+            tm_a1 = tm_a
         tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
                     box=(32, BN))
         tm_bl = dict(tm_b, offset=lo_off)
@@ -335,15 +355,15 @@ class Specializer:
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if tmem_a else 384, smem, ipi, ipb,
                   grid_mult=ntn,
-                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl], grid_cap=self.sm_count,
+                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1], grid_cap=self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}"
                        f"{' A in TMEM' if tmem_a else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
-                     PHO, PWO):
+                     PHO, PWO, UPF=1):
         pxt = 4 if CO <= 8 else 2 if CO <= 16 else 1
         fields = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
-                      POOL=pool_fused, PHO=PHO, PWO=PWO, PXT=pxt,
+                      POOL=pool_fused, PHO=PHO, PWO=PWO, PXT=pxt, UPF=UPF,
                       IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
                       OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
                       W_OFF=self.pool.add(wmat), B_OFF=self.pool.add(u.bias),
@@ -396,15 +416,16 @@ class Specializer:
         H, W, C = u.input_shapes[0].dims
         PH, PW = u.kernel_hw
         S = u.stride
-        if u.output_shape.rank == 1:
+        out_shape = u.pre_up_shape if u.upsample_after > 1 else u.output_shape
+        if out_shape.rank == 1:
             HO = WO = 1
         else:
-            HO, WO = u.output_shape.h, u.output_shape.w
+            HO, WO = out_shape.h, out_shape.w
         PT = same_padding(H, PH, S)[0] if u.padding == "same" else 0
         PL = same_padding(W, PW, S)[0] if u.padding == "same" else 0
         vec = 4 if C % 4 == 0 else 1
         fields = dict(H=H, W=W, C=C, HO=HO, WO=WO, PH=PH, PW=PW, S=S, PT=PT, PL=PL,
-                      AVG=u.pool_op == "avg", VEC=vec,
+                      AVG=u.pool_op == "avg", VEC=vec, UPF=u.upsample_after,
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),
                       OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id))

@@ -70,6 +70,9 @@ class CompilationUnit:
     pre_pool_shape: object = None   # conv output shape before the fused pool
     residual_id: int = None         # fused residual Add: tensor added last
     softmax_after: bool = False     # fused row softmax epilogue
+    upsample_after: int = 1         # fused nearest upsampling of the output
+    pre_up_shape: object = None     # output shape before the fused upsampling
+    concat_in: bool = False         # conv reads the channel concat of input_ids
 
     def describe(self):
         bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
@@ -88,6 +91,10 @@ class CompilationUnit:
             bits.append(f"+add(t{self.residual_id})")
         if self.softmax_after:
             bits.append("+softmax")
+        if self.upsample_after > 1:
+            bits.append(f"+upsample{self.upsample_after}")
+        if self.concat_in:
+            bits.append("concat-loader")
         if self.in_place_preference is not None:
             bits.append("in_place?")
         return " ".join(bits)
@@ -400,6 +407,56 @@ def fuse_softmax(plan):
     return plan
 
 
+def fuse_upsample(plan):
+    """Nearest UpSample2D into the epilogue of its producer (Conv2D / Pool):
+    each computed pixel is stored to its f x f replicas."""
+    pos = 0
+    while pos < len(plan.units):
+        u = plan.units[pos]
+        if u.kind == "Upsample":
+            where = plan.producer_positions()
+            ppos = where.get(u.input_ids[0], -1)
+            if ppos >= 0:
+                p = plan.units[ppos]
+                if (p.kind in ("Conv2D", "Pool") and p.upsample_after == 1 and not p.pool_after
+                        and not p.softmax_after and p.residual_id is None
+                        and p.output_shape.rank == 3 and _private(plan, p.output_id)):
+                    p.pre_up_shape = p.output_shape
+                    p.output_shape = u.output_shape
+                    p.upsample_after = u.factor
+                    plan.tensors.pop(p.output_id, None)
+                    p.output_id = u.output_id
+                    _delete(plan, pos, p)
+                    continue
+        pos += 1
+    return plan
+
+
+def fuse_concat(plan):
+    """A two-way channel Concatenate feeding only a stride-1 Conv2D becomes a
+    two-source operand loader of that conv (no concatenated tensor)."""
+    pos = 0
+    while pos < len(plan.units):
+        u = plan.units[pos]
+        if (u.kind == "Concat" and len(u.input_ids) == 2 and u.output_shape.rank == 3
+                and u.input_ids[0] != u.input_ids[1] and _private(plan, u.output_id)):
+            cons = [c for c in plan.units if u.output_id in FusionPlan._reads(c)]
+            c0 = u.input_shapes[0].c
+            ctot = u.output_shape.c
+            if (len(cons) == 1 and cons[0].kind == "Conv2D" and cons[0].stride == 1
+                    and not cons[0].concat_in and cons[0].input_ids == (u.output_id,)
+                    and c0 % 4 == 0 and ctot > 8):
+                c = cons[0]
+                c.input_ids = u.input_ids
+                c.input_shapes = u.input_shapes
+                c.concat_in = True
+                plan.tensors.pop(u.output_id, None)
+                _delete(plan, pos, c)
+                continue
+        pos += 1
+    return plan
+
+
 def build_plan(graph, gpu_fusion=True):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions."""
     plan = build_reference_plan(graph)
@@ -407,6 +464,8 @@ def build_plan(graph, gpu_fusion=True):
         fuse_pool(plan)
         fuse_residual(plan)
         fuse_softmax(plan)
+        fuse_upsample(plan)
+        fuse_concat(plan)
     return plan
 
 

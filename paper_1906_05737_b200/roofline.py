@@ -57,7 +57,8 @@ def unit_work(u, plan=None):
         f = 2 * kin * units
     elif k == "Conv2D":
         kh, kw, ci, co = u.kernel.shape
-        conv_out = u.pre_pool_shape if getattr(u, "pool_after", False) else u.output_shape
+        conv_out = (u.pre_pool_shape if getattr(u, "pool_after", False) else
+                    u.pre_up_shape if getattr(u, "upsample_after", 1) > 1 else u.output_shape)
         f = 2 * conv_out.h * conv_out.w * kh * kw * ci * co
     elif k == "DepthwiseConv2D":
         kh, kw, c = u.kernel.shape

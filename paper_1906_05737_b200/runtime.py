@@ -115,7 +115,7 @@ class CompiledNetwork:
         launches = (_native.Launch * max(len(spec.launches), 1))()
         index = {n: i for i, n in enumerate(spec.kernel_names)}
         for i, l in enumerate(spec.launches):
-            tm = (_native.TMap * 3)()
+            tm = (_native.TMap * 4)()
             for k, t in enumerate(l.tmaps):
                 tm[k] = _native.make_tmap(t)
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,

@@ -30,8 +30,11 @@ def run_plan(plan, inputs):
             y = _post(oracle.dense(x.reshape(n, -1), u.kernel, u.bias, 1), u)
         elif u.kind in ("Conv2D", "DepthwiseConv2D"):
             dw = u.kind == "DepthwiseConv2D"
-            y = oracle.conv(x.reshape((n,) + u.input_shapes[0].dims), u.kernel, u.bias,
-                            u.stride, u.padding, dw, 1)
+            if getattr(u, "concat_in", False):
+                x = np.concatenate([vals[t].reshape((n,) + sh.dims)
+                                    for t, sh in zip(u.input_ids, u.input_shapes)], axis=-1)
+            y = oracle.conv(x.reshape((n,) + tuple(u.input_shapes[0].dims[:2]) + (-1,)),
+                            u.kernel, u.bias, u.stride, u.padding, dw, 1)
             y = _post(y, u)
         elif u.kind == "Pool":
             ph, pw = u.kernel_hw
@@ -64,5 +67,8 @@ def run_plan(plan, inputs):
             y = oracle.pool(y, 2, 2, 2, "valid", False)
         if getattr(u, "softmax_after", False):
             y = oracle.softmax(y)
+        f = getattr(u, "upsample_after", 1)
+        if f > 1:
+            y = np.repeat(np.repeat(y.reshape((n,) + u.pre_up_shape.dims), f, 1), f, 2)
         vals[u.output_id] = y.reshape((n,) + u.output_shape.dims)
     return [vals[t] for t in plan.output_ids]

@@ -63,6 +63,44 @@ def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
 
+@pytest.mark.parametrize("c0,c1,co,up_src,tc", [
+    (64, 64, 32, "pool", True), (32, 32, 16, "conv", True), (8, 12, 16, "conv", False),
+    (4, 8, 8, "pool", False), (32, 64, 48, "conv", False)])
+def test_decoder_fusions(c0, c1, co, up_src, tc):
+    """UpSample2D fused into its producer's epilogue (pool / direct / FFMA /
+    tcgen05 conv) and Concatenate fused into the consumer conv's loader."""
+    rng = np.random.default_rng(c0 + c1 + co)
+    h, w = 6, 10
+    b = NetBuilder()
+    x = b.input((2 * h, 2 * w, c1))
+    if up_src == "pool":
+        lo = b.layer("MaxPool2D", [x], {"pool_size": 2, "strides": 2})
+        lo = b.layer("Conv2D", [lo], {"filters": c0, "kernel_size": 1, "activation": "relu"},
+                     [("kernel", he(rng, (1, 1, c1, c0), c1)), ("bias", np.zeros(c0, F32))])
+        lo = b.layer("MaxPool2D", [b.layer("UpSample2D", [lo], {"factor": 2})],
+                     {"pool_size": 1, "strides": 1})
+        up = b.layer("UpSample2D", [b.layer("MaxPool2D", [lo], {"pool_size": 2, "strides": 2})],
+                     {"factor": 2})
+    else:
+        lo = b.layer("AvgPool2D", [x], {"pool_size": 2, "strides": 2})
+        lo = b.layer("Conv2D", [lo], {"filters": c0, "kernel_size": 3, "padding": "same",
+                                      "activation": "tanh"},
+                     [("kernel", he(rng, (3, 3, c1, c0), 9 * c1)), ("bias", np.zeros(c0, F32))])
+        up = b.layer("UpSample2D", [lo], {"factor": 2})
+    cat = b.layer("Concatenate", [up, x])
+    y = b.layer("Conv2D", [cat], {"filters": co, "kernel_size": 3, "padding": "same",
+                                  "activation": "relu"},
+                [("kernel", he(rng, (3, 3, c0 + c1, co), 9 * (c0 + c1))),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (3, 2 * h, 2 * w, c1)).astype(F32)
+    got, net = gpu(m, wt, xin, tc_min_rows=1 if tc else 1 << 30)
+    kinds = [u.kind for u in net.plan.units]
+    assert "Concat" not in kinds and "Upsample" not in kinds, net.plan.describe()
+    assert any("_tc_" in l.kernel for l in net.artifact.launches) == tc
+    np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+
+
 @pytest.mark.parametrize("k,units,act,n", [
     (1, 1, "linear", 1), (3, 5, "relu", 7), (17, 9, "tanh", 3), (130, 7, "sigmoid", 12),
     (64, 64, "elu", 2100), (256, 96, "relu6", 2048), (100, 40, "linear", 2500),

@@ -126,6 +126,10 @@ def test_gpu_fusions_on_zoo():
     # encoder convs 2 and 3 feed a skip connection: their pools stay separate
     assert [c.pool_after for c in convs[:3]] == [True, False, False]
     assert convs[-1].softmax_after
+    # decoder: pool->upsample and conv->upsample epilogues, concat as operand loader
+    assert "Upsample" not in kinds(p4) and "Concat" not in kinds(p4)
+    assert sum(u.upsample_after == 2 for u in p4.units) == 2
+    assert sum(u.concat_in for u in p4.units) == 2
 
 
 @pytest.mark.parametrize("cfg", range(5))
