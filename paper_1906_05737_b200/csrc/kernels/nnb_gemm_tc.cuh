@@ -30,6 +30,17 @@
 #pragma once
 #include "nnb_common.cuh"
 
+#ifndef NNB_TC_DBG
+#define NNB_TC_DBG 0
+#endif
+// The tensor core reads FP32 operands of kind::tf32 with the 13 low mantissa
+// bits ignored (verified on B200 by scripts/tc_hi.py: bit-identical results
+// with and without writing hi = a & 0xffffe000 back), so only lo = a - hi is
+// materialised; the raw tile serves as the hi operand.
+#ifndef NNB_HI_INPLACE
+#define NNB_HI_INPLACE 0
+#endif
+
 namespace nnb {
 
 struct __align__(64) TmaDesc { unsigned long long opaque[16]; };
@@ -86,11 +97,16 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// K-major operand, 128-byte swizzle, rows of 128 B, 8-row atoms 1024 B apart.
-__device__ __forceinline__ u64 sw128_desc(u32 saddr) {
-  return (u64)((saddr >> 4) & 0x3FFF) | ((u64)1 << 16) | ((u64)(1024 >> 4) << 32) |
-         ((u64)1 << 46) | ((u64)2 << 61);
+// K-major operand descriptor.  ROWB = bytes per row = BK*4: 128 -> 128-byte
+// swizzle (layout type 2), 8-row atoms 1024 B apart; 64 -> 64-byte swizzle
+// (layout type 4), atoms 512 B apart.
+template <int ROWB>
+__device__ __forceinline__ u64 kmajor_desc(u32 saddr) {
+  constexpr u64 layout = ROWB == 128 ? 2 : 4;
+  return (u64)((saddr >> 4) & 0x3FFF) | ((u64)1 << 16) | ((u64)(8 * ROWB >> 4) << 32) |
+         ((u64)1 << 46) | (layout << 61);
 }
+__device__ __forceinline__ u64 sw128_desc(u32 saddr) { return kmajor_desc<128>(saddr); }
 
 __device__ __forceinline__ void mma_tf32(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
   asm volatile(
@@ -127,6 +143,21 @@ __device__ __forceinline__ void tmem_st32(u32 taddr, const u32 (&v)[32]) {
       : "memory");
 }
 
+template <int N>
+__device__ __forceinline__ void tmem_st(u32 taddr, const u32 (&v)[N]) {
+  if constexpr (N == 32) {
+    tmem_st32(taddr, v);
+  } else {
+    static_assert(N == 16, "tmem_st width");
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void mma_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -147,12 +178,31 @@ __device__ __forceinline__ void tmem_ld16(u32 taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <int N>
+__device__ __forceinline__ void tmem_ld(u32 taddr, float (&v)[N]) {
+  if constexpr (N == 16) {
+    tmem_ld16(taddr, v);
+  } else {
+    static_assert(N == 8, "tmem_ld width");
+    u32 r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  }
+}
+
 // C: K, N, NPAD (multiple of BN), BN (32..256, multiple of 16), NS (stages),
 //    ROWS (GEMM rows per image), IN/OUT offsets, B_OFF (bias), epilogue fields.
 template <class C>
 struct GemmTc {
-  static constexpr int BM = 128, BK = 32;
-  static constexpr int A_BYTES = BM * BK * 4;            // 16 KiB
+  static constexpr int BM = 128, BK = C::BK;                // 32 (SW128) or 16 (SW64)
+  static constexpr int ROWB = BK * 4;
+  static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = C::BN * BK * 4;
   // TMEM_A: the split A operand lives in tensor memory (MMA "ts" form), so the
   // tensor core reads only B from shared memory -- for narrow N the A re-reads
@@ -168,7 +218,11 @@ struct GemmTc {
   // keeping the two small correction products out of the main sum cuts the
   // truncations on it by 3x, and the two are added in FP32 (round-to-nearest)
   // in the epilogue.
-  static constexpr int ACC_COLS = 2 * C::BN;              // fp32 columns per buffer
+  // NACC independent (main, correction) chains per buffer: consecutive k-steps
+  // rotate over them so dependent tcgen05.mma instructions overlap (for narrow
+  // N a single accumulator chain is bound by MMA latency, not throughput).
+  static constexpr int NACC = C::NACC;
+  static constexpr int ACC_COLS = NACC * 2 * C::BN;       // fp32 columns per buffer
   static constexpr int A_TCOL = 2 * ACC_COLS;                    // first A column (TA)
   static constexpr int TMEM_NEED = TA ? 2 * ACC_COLS + C::NS * 2 * BK : 2 * ACC_COLS;
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64
@@ -178,7 +232,12 @@ struct GemmTc {
                                ((u32)(BM >> 4) << 24);
   static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
-  static constexpr int CONV_WARPS = TA ? 4 : 2;                   // A splitters
+  // ALDG: the A operand is gathered by the four loader/converter warps with
+  // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
+  // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
+  static constexpr bool AL = C::ALDG != 0;
+  static_assert(!(AL && TA), "A via LDGSTS lives in shared memory");
+  static constexpr int CONV_WARPS = (TA || AL) ? 4 : 2;           // A splitters
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
@@ -187,11 +246,20 @@ struct GemmTc {
   static_assert(C::BN % 16 == 0 && C::BN >= 16 && C::BN <= 128, "UMMA N / TMEM budget");
   // spatial (implicit-GEMM convolution) tiling: 8 x 16 output pixels per tile
   static constexpr int TH = 8, TW = 16;
-  static constexpr int TX = C::CONV ? (C::WO + TW - 1) / TW : 1;
+  // KPACK: the KW horizontal taps are packed into N (N = KW*CO, K = KH*CI): a
+  // tile computes per-input-column partial sums D'[pixel][kx][co] and the
+  // epilogue combines out(x) = sum_kx D'(x + kx)[kx] with warp shuffles, so a
+  // tile of 16 input columns yields OW = 16 - (KW - 1) output columns.
+  static constexpr bool KP = C::KPACK != 0;
+  static constexpr int OW = KP ? TW - (C::KW - 1) : TW;
+  static constexpr int TX = C::CONV ? (C::WO + OW - 1) / OW : 1;
   static constexpr int TPI = C::CONV ? ((C::HO + TH - 1) / TH) * TX : 1;
   static constexpr int CB = C::CONV ? C::CI / BK : 1;       // channel blocks per tap
   static constexpr int CB0 = C::CONV ? C::C0 / BK : 1;      // ... from source 0
-  static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % 32 == 0");
+  static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % BK == 0");
+  static_assert(BK == 32 || BK == 16, "K block");
+  static_assert(!KP || (C::CONV && !C::POOL && !C::RES && C::CO % 16 == 0 &&
+                        C::KW * C::CO == C::N), "KPACK geometry");
   static_assert(STAGE % 1024 == 0, "stage alignment");
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
@@ -246,22 +314,28 @@ struct GemmTc {
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
-            mbar_expect_tx(&full[s], A_BYTES + 2 * B_BYTES);
-            if (C::CONV) {
+            mbar_expect_tx(&full[s], NNB_TC_DBG == 2 ? 0 : (AL ? 0 : A_BYTES) + 2 * B_BYTES);
+            if (NNB_TC_DBG == 2) {
+              // diagnostic: no operand traffic
+            } else if (AL) {
+              // A is gathered by the loader warps
+            } else if (C::CONV) {
               // tap (ky, kx) and channel block cb of an 8x16 output-pixel tile;
               // out-of-image coordinates are zero-filled = 'same' padding
               // with CONCAT, channel blocks >= C0/32 come from the second source
               const int img = mb / TPI, tt = mb % TPI;
-              const int tap = kb / CB, cb = kb % CB;
+              const int tap = kb / CB, cb = kb % CB;     // KPACK: tap = ky only
               const bool second = C::CONCAT && cb >= CB0;
+              const int kx = KP ? 0 : tap % C::KW, ky = KP ? tap : tap / C::KW;
               tma_load_4d(st, second ? tmA1 : tmA, &full[s], (second ? cb - CB0 : cb) * BK,
-                          (tt % TX) * TW + tap % C::KW - C::PL,
-                          (tt / TX) * TH + tap / C::KW - C::PT, img);
+                          (tt % TX) * OW + kx - C::PL, (tt / TX) * TH + ky - C::PT, img);
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
             }
-            tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, nb * C::BN);
-            tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
+            if (NNB_TC_DBG != 2) {
+              tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, nb * C::BN);
+              tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
+            }
             if (++s == C::NS) { s = 0; ph ^= 1; }
           }
         }
@@ -280,7 +354,8 @@ struct GemmTc {
             mbar_wait(&tempty[acc], aph ^ 1);
             tc_fence_after();
           }
-          const u32 d = tmem + acc * ACC_COLS;
+          const u32 dbuf = tmem + acc * ACC_COLS;
+          if (AL) mbar_wait(&full[s], ph);           // B (TMA); A comes via lo_ready
           mbar_wait(&lo_ready[s], ph);
           tc_fence_after();
           if (lane == 0) {
@@ -289,17 +364,20 @@ struct GemmTc {
             const u32 b_hi = base + A_SMEM, b_lo = b_hi + B_BYTES;
             const u32 ta = tmem + A_TCOL + s * 2 * BK;                // TMEM A slot
 #pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
+            for (int k = 0; k < (NNB_TC_DBG == 1 ? 0 : BK / 8); ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
-              const u32 accum = (kc | k) != 0;
+              const int ks = kc * (BK / 8) + k;                  // k-step within the chunk
+              const u32 d = dbuf + (ks % NACC) * 2 * C::BN;      // this step's chain
+              const u32 accum = ks >= NACC;
               if (TA) {
-                mma_tf32_ts(d, ta + 8 * k, sw128_desc(b_hi + o), IDESC, accum);
-                mma_tf32_ts(d + C::BN, ta + 8 * k, sw128_desc(b_lo + o), IDESC, accum);
-                mma_tf32_ts(d + C::BN, ta + BK + 8 * k, sw128_desc(b_hi + o), IDESC, 1);
+                mma_tf32_ts(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_tf32_ts(d + C::BN, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, accum);
+                mma_tf32_ts(d + C::BN, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               } else {
-                mma_tf32(d, sw128_desc(a_hi + o), sw128_desc(b_hi + o), IDESC, accum);
-                mma_tf32(d + C::BN, sw128_desc(a_hi + o), sw128_desc(b_lo + o), IDESC, accum);
-                mma_tf32(d + C::BN, sw128_desc(a_lo + o), sw128_desc(b_hi + o), IDESC, 1);
+                mma_tf32(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_tf32(d + C::BN, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC,
+                         accum);
+                mma_tf32(d + C::BN, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               }
             }
             mma_commit(&empty[s]);
@@ -320,11 +398,13 @@ struct GemmTc {
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
-          const unsigned char* row = smem + s * STAGE + r * 128;
+          const unsigned char* row = smem + s * STAGE + r * ROWB;
           u32 hi[BK], lo[BK];
 #pragma unroll
           for (int j = 0; j < BK / 4; ++j) {          // 16-byte chunk j of the swizzled row
-            const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (r & 7)) << 4));
+            // SW128: chunk ^= row & 7; SW64: chunk ^= (row >> 1) & 3
+            const int pj = ROWB == 128 ? (j ^ (r & 7)) : (j ^ ((r >> 1) & 3));
+            const float4 v = *reinterpret_cast<const float4*>(row + (pj << 4));
             const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -334,13 +414,89 @@ struct GemmTc {
             }
           }
           const u32 ta = tmem + ((u32)(q * 32) << 16) + A_TCOL + s * 2 * BK;
-          tmem_st32(ta, hi);
-          tmem_st32(ta + BK, lo);
+          tmem_st<BK>(ta, hi);
+          tmem_st<BK>(ta + BK, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           mbar_arrive(&lo_ready[s]);
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
+      }
+    } else if (warp < EPI_W0 && AL) {
+      // ---------------- loader: cp.async gather of A, then split in place ----------------
+      constexpr int CH = BK / 4;                       // 16-byte chunks per row
+      constexpr int PER = BM * CH / 128;               // chunks per loader thread
+      constexpr int D = C::NS - 1;                     // k-blocks in flight
+      const int lt = threadIdx.x - 64;                 // 0..127
+      const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+      const int total = my_tiles * KB;
+      const float* a0 = at<float>(arena, C::IN_OFF);
+      const float* a1 = at<float>(arena, C::IN1_OFF);
+      auto issue = [&](int it) {
+        const int t = blockIdx.x + (it / KB) * gridDim.x, kb = it % KB, mb = t / NTN;
+        const int stg = it % C::NS;
+        mbar_wait(&empty[stg], ((it / C::NS) & 1) ^ 1);
+        const u32 sbase = smem_u32(smem + stg * STAGE);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int e = j * 128 + lt, row = e / CH, ch = e % CH;
+          const float* src = a0;
+          bool ok;
+          if (C::CONV) {
+            const int img = mb / TPI, tt = mb % TPI;
+            const int tap = kb / CB, cb = kb % CB;
+            const int kx = KP ? 0 : tap % C::KW, ky = KP ? tap : tap / C::KW;
+            const int iy = (tt / TX) * TH + row / TW + ky - C::PT;
+            const int ix = (tt % TX) * OW + row % TW + kx - C::PL;
+            ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
+            const bool second = C::CONCAT && cb >= CB0;
+            const int cis = second ? C::CI - C::C0 : C::C0;
+            const long long off = (long long)img * ((second ? C::IN1_IMG : C::IN_IMG) / 4) +
+                                  ((long long)iy * C::W + ix) * cis +
+                                  (second ? cb - CB0 : cb) * BK + ch * 4;
+            if (ok) src = (second ? a1 : a0) + off;
+          } else {
+            const long long m = (long long)mb * BM + row;
+            const int k = kb * BK + ch * 4;
+            ok = m < rows && k < C::K;
+            if (ok) src = a0 + m * C::K + k;
+          }
+          const u32 pj = ROWB == 128 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3));
+          const u32 dst = sbase + row * ROWB + (pj << 4);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                       "r"(ok ? 16 : 0) : "memory");
+        }
+      };
+      // prologue: D k-blocks in flight; afterwards convert k-block `it`, hand it
+      // to the MMA, then refill the stage of `it-1` (free once MMA(it-1) is done,
+      // while MMA(it) already runs).  Exactly one commit group per k-block.
+      for (int it = 0; it < D; ++it) {
+        if (it < total) issue(it);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      for (int it = 0; it < total; ++it) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        // this thread's own chunks of k-block `it` have landed: split in place
+        const int stg = it % C::NS;
+        unsigned char* sb = smem + stg * STAGE;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int e = j * 128 + lt, row = e / CH, ch = e % CH;
+          const int pj = ROWB == 128 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3));
+          float4* pa = reinterpret_cast<float4*>(sb + row * ROWB + (pj << 4));
+          float4* pl = reinterpret_cast<float4*>(sb + A_BYTES + row * ROWB + (pj << 4));
+          float4 v = *pa, h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+          if (NNB_HI_INPLACE) *pa = h;
+          *pl = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&lo_ready[stg]);
+        if (it + D < total) issue(it + D);
+        asm volatile("cp.async.commit_group;" ::: "memory");
       }
     } else if (warp < EPI_W0) {
       // ---------------- converter: A -> (hi, lo) ----------------
@@ -359,7 +515,7 @@ struct GemmTc {
             h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
             h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
             h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
-            a[i] = h;
+            if (NNB_HI_INPLACE) a[i] = h;
             lo[i] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -380,6 +536,63 @@ struct GemmTc {
       u32 aph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int mb = t / NTN, nb = t % NTN;
+        if constexpr (KP) {
+          // ---- packed horizontal taps: reduce chunks, combine across lanes ----
+          constexpr int GCO = C::CO / 2;                 // output channels per warp group
+          const int g = (warp - EPI_W0) >> 2;
+          float run[C::KW][GCO];
+#pragma unroll
+          for (int kx = 0; kx < C::KW; ++kx)
+#pragma unroll
+            for (int i = 0; i < GCO; ++i) run[kx][i] = 0.f;
+          for (int ch = 0; ch < NCHUNK; ++ch) {
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * (BK / 8);
+#pragma unroll
+            for (int c = 0; c < NACC; ++c) {
+              if (c >= ksteps) break;
+#pragma unroll
+              for (int kx = 0; kx < C::KW; ++kx) {
+                float v[GCO], cr[GCO];
+                const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * 2 * C::BN +
+                               kx * C::CO + g * GCO;
+                tmem_ld<GCO>(ta, v);
+                tmem_ld<GCO>(ta + C::BN, cr);
+#pragma unroll
+                for (int i = 0; i < GCO; ++i) run[kx][i] += v[i] + cr[i];
+              }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+          }
+          const int img = mb / TPI, tt = mb % TPI;
+          const int w = r % TW;
+          const int oy = (tt / TX) * TH + r / TW, ox = (tt % TX) * OW + w;
+          const bool live = img < n && w < OW && oy < C::HO && ox < C::WO;
+          float y[GCO];
+#pragma unroll
+          for (int i = 0; i < GCO; ++i) {
+            float sacc = run[0][i];
+#pragma unroll
+            for (int kx = 1; kx < C::KW; ++kx) sacc += __shfl_down_sync(0xffffffffu, run[kx][i], kx);
+            const int col = g * GCO + i;
+            y[i] = finish<C::ACT, C::MODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
+          }
+          if (live) {
+            const long long ob = (long long)img * (C::OUT_IMG / 4) +
+                ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::CO + g * GCO;
+#pragma unroll
+            for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
+              float* d = out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO;
+#pragma unroll
+              for (int i = 0; i < GCO; i += 4)
+                *reinterpret_cast<float4*>(d + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+            }
+          }
+          continue;
+        }
         // FP32 (round-to-nearest) reduction of the per-chunk tensor-core sums
         float run[EPI_COLS];
 #pragma unroll
@@ -387,15 +600,22 @@ struct GemmTc {
         for (int ch = 0; ch < NCHUNK; ++ch) {
           mbar_wait(&tfull[acc], aph);
           tc_fence_after();
+          // chains written in this chunk (a short last chunk may not reach all)
+          const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * (BK / 8);
 #pragma unroll
           for (int g = 0; g < EPI_COLS / 16; ++g) {
             if (cbeg + g * 16 < C::BN) {             // warp-uniform
-              float v[16], cr[16];
-              const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + cbeg + g * 16;
-              tmem_ld16(ta, v);
-              tmem_ld16(ta + C::BN, cr);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) run[g * 16 + i] += v[i] + cr[i];
+              for (int c = 0; c < NACC; ++c) {
+                if (c >= ksteps) break;
+                float v[16], cr[16];
+                const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * 2 * C::BN +
+                               cbeg + g * 16;
+                tmem_ld16(ta, v);
+                tmem_ld16(ta + C::BN, cr);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) run[g * 16 + i] += v[i] + cr[i];
+              }
             }
           }
           tc_fence_before();

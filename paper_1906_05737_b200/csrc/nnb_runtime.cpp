@@ -512,7 +512,10 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
       r = C->p_cuTensorMapEncodeTiled(&net->maps[i][k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, t.rank,
                                       reinterpret_cast<void *>(base + t.offset), dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                      t.swizzle == 3 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      t.swizzle == 3 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                      : t.swizzle == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                      : t.swizzle == 1 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for launch %zu map %u", (int)r, i, k); return bail(NNB_ERR_CUDA); }

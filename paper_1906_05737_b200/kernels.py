@@ -105,8 +105,12 @@ def _pad4(x):
 
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
-                 sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True):
+                 sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
+                 kpack=True):
         self.use_tc = use_tc
+        self.aldg = aldg
+        self.kpack = kpack
+        self.nacc = nacc
         self.tmem_a = tmem_a
         self.tc_min_rows = tc_min_rows
         self.sm_count = sm_count
@@ -233,7 +237,7 @@ class Specializer:
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
                    and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
-                   and S == 1 and CI % 32 == 0 and C0 % 32 == 0 and CO >= 16)
+                   and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16)
         if tc_rows or tc_conv:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
             if n_tc <= self.max_batch:
@@ -302,15 +306,33 @@ class Specializer:
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
+        # narrow outputs: pack the horizontal taps into N (3x fewer MMAs)
+        kw = u.kernel_hw[1] if conv else 1
+        kpack = bool(conv and self.kpack and CO % 16 == 0 and kw * CO <= 128 and kw > 1
+                     and not conv["POOL"] and u.residual_id is None)
+        CO_real = CO
+        if kpack:
+            kh = u.kernel_hw[0]
+            ci = conv["CI"]
+            wmat = (np.asarray(wmat, F32).reshape(kh, kw, ci, CO).transpose(0, 2, 1, 3)
+                    .reshape(kh * ci, kw * CO))           # [ky*CI+ci][kx*CO+co]
+            K, CO = kh * ci, kw * CO
         BN = min(128, -(-CO // 16) * 16) if CO < 32 else min(128, -(-CO // 32) * 32)
+        if kpack:
+            BN = CO
         NPAD = -(-CO // BN) * BN
-        KPAD = -(-K // 32) * 32
-        tmem_a = BN <= 64 and self.tmem_a
-        stage = (1 if tmem_a else 2) * 128 * 32 * 4 + 2 * BN * 32 * 4
+        KPAD = -(-K // 32) * 32 if not conv or conv["CI"] % 32 == 0 else -(-K // 16) * 16
+        BK = 32 if (not conv or (conv["CI"] % 32 == 0 and conv["C0"] % 32 == 0)) else 16
+        sw = 3 if BK == 32 else 2                  # TMA swizzle: 128 B or 64 B rows
+        # independent accumulator chains fill TMEM (2 buffers x NACC x (main, corr))
+        NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
+        aldg = self.aldg
+        tmem_a = self.tmem_a and NACC == 1 and BN <= 64 and not aldg
+        stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * BN * BK * 4
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
         NS = max(2, min(8, (200 * 1024) // stage))
         if tmem_a:
-            NS = min(NS, (512 - 4 * BN) // 64)
+            NS = min(NS, (512 - 4 * BN) // (2 * BK))
         wt = np.zeros((NPAD, KPAD), F32)
         wt[:CO, :K] = np.asarray(wmat, F32).T
         hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
@@ -322,18 +344,26 @@ class Specializer:
             geo.update(conv, CONV=1)
         elif rows_geo:
             geo.update(rows_geo)
-        fields = dict(K=K, N=CO, NPAD=NPAD, BN=BN, NS=NS, ROWS=rows, TMEM_A=tmem_a, **geo,
+        fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
+                      ROWS=rows, TMEM_A=tmem_a,
+                      NACC=NACC, ALDG=aldg,
+                      IN_OFF=self.arena_off(u.input_ids[0]),
+                      IN_IMG=self.img_bytes(u.input_ids[0]),
+                      IN1_OFF=(self.arena_off(u.input_ids[1]) if conv and conv["CONCAT"] else 0),
+                      IN1_IMG=(self.img_bytes(u.input_ids[1]) if conv and conv["CONCAT"] else 0),
+                      **geo,
                       OUT_IMG=self.img_bytes(u.output_id),
                       OUT_OFF=self.arena_off(u.output_id), B_OFF=self.pool.add(u.bias),
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
-        fields.update(self.epilogue_fields(u, CO))
+        fields.update(self.epilogue_fields(u, CO_real))
         if conv:
             H, W = conv["H"], conv["W"]
 
             def act_map(tid, ch):
                 return dict(space=1, offset=self.arena_off(tid), dims=(ch, W, H, self.cap),
-                            box=(32, 16, 8, 1), strides=(4 * ch, 4 * ch * W, 4 * ch * W * H))
+                            box=(BK, 16, 8, 1), strides=(4 * ch, 4 * ch * W, 4 * ch * W * H),
+                            swizzle=sw)
             tm_a = act_map(u.input_ids[0], conv["C0"])
             tm_a1 = (act_map(u.input_ids[1], conv["CI"] - conv["C0"]) if conv["CONCAT"]
                      else tm_a)
@@ -342,21 +372,25 @@ class Specializer:
                         dims=(K, self.cap * rows), strides=(4 * K,), box=(32, 128))
             tm_a1 = tm_a
         tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
-                    box=(32, BN))
+                    box=(BK, BN), swizzle=sw)
         tm_bl = dict(tm_b, offset=lo_off)
         smem = NS * stage + 1024 + 256
         ntn = NPAD // BN
         if conv:
-            tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // 16)
+            ow = 16 - (kw - 1) if kpack else 16
+            tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // ow)
             ipi, ipb = tpi, 1
             tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
         else:
             ipi, ipb = rows, 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if tmem_a else 384, smem, ipi, ipb,
+        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg) else 384, smem,
+                  ipi, ipb,
                   grid_mult=ntn,
                   n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1], grid_cap=self.sm_count,
-                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x32 stages {NS}"
+                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x{BK} stages {NS}"
+                       f" chains {NACC}{' A via cp.async' if aldg else ''}"
+                       f"{' taps packed in N' if kpack else ''}"
                        f"{' A in TMEM' if tmem_a else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
@@ -551,6 +585,6 @@ class Specializer:
 
 
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
-               tc_min_rows=TC_MIN_ROWS, tmem_a=True):
+               tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
-                       tc_min_rows, tmem_a).run()
+                       tc_min_rows, tmem_a, nacc, aldg, kpack).run()

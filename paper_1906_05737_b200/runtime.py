@@ -79,7 +79,8 @@ class _Handle:
 
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
-                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True):
+                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
+                 nacc=None, aldg=False, kpack=True):
         import torch
 
         t0 = time.perf_counter()
@@ -99,7 +100,7 @@ class CompiledNetwork:
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
                           use_tc=use_tc, sm_count=sm_count,
                           tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
-                          tmem_a=tmem_a)
+                          tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):

@@ -16,10 +16,14 @@ p.add_argument("--mode", default="exact")
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--no-tc", action="store_true")
 p.add_argument("--no-tmem-a", action="store_true")
+p.add_argument("--nacc", type=int, default=None)
+p.add_argument("--aldg", action="store_true")
+p.add_argument("--no-kpack", action="store_true")
 a = p.parse_args()
 opts = EXACT if a.mode == "exact" else ApproximationOptions()
 m, w = zoo.build(a.config)
-net = compile_model(m, w, opts, batch=a.batch, use_tc=not a.no_tc, tmem_a=not a.no_tmem_a)
+net = compile_model(m, w, opts, batch=a.batch, use_tc=not a.no_tc, tmem_a=not a.no_tmem_a, nacc=a.nacc,
+                    aldg=a.aldg, kpack=not a.no_kpack)
 net.input_views[0].copy_(torch.from_numpy(zoo.inputs(a.config, a.batch)))
 for _ in range(a.reps):
     net.apply()

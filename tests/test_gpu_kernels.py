@@ -43,7 +43,8 @@ def test_conv_sweep(h, w, ci, co, k, s, pad, act, n):
 @pytest.mark.parametrize("h,w,ci,co,pad,pool,n", [
     (10, 18, 32, 16, "same", False, 3), (17, 23, 32, 48, "same", True, 2),
     (12, 40, 64, 32, "valid", True, 2), (9, 16, 32, 40, "same", False, 1),
-    (60, 80, 32, 64, "same", True, 2)])
+    (60, 80, 32, 64, "same", True, 2), (14, 20, 16, 32, "same", False, 2),
+    (11, 30, 16, 16, "same", True, 2), (9, 12, 48, 32, "valid", False, 2)])
 def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
     """Implicit-GEMM tcgen05 conv (4-D TMA boxes, zero-filled borders), with
     and without the fused 2x2 max-pool epilogue, ragged 8x16 tiles."""
@@ -65,7 +66,7 @@ def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
 
 @pytest.mark.parametrize("c0,c1,co,up_src,tc", [
     (64, 64, 32, "pool", True), (32, 32, 16, "conv", True), (8, 12, 16, "conv", False),
-    (4, 8, 8, "pool", False), (32, 64, 48, "conv", False)])
+    (4, 8, 8, "pool", False), (32, 64, 48, "conv", False), (16, 16, 32, "conv", True)])
 def test_decoder_fusions(c0, c1, co, up_src, tc):
     """UpSample2D fused into its producer's epilogue (pool / direct / FFMA /
     tcgen05 conv) and Concatenate fused into the consumer conv's loader."""
