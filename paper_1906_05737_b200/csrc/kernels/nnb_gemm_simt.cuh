@@ -58,6 +58,35 @@ struct GemmSimt {
     }
   }
 
+  // depthwise output at pixel (oy, ox) of its output map, channels c..c+3:
+  // bias, taps (ky, kx) as FMAs, then its own activation / post-BN
+  __device__ static __forceinline__ float4 dw_point(const float* __restrict__ pool,
+                                                    const float* img, int oy, int ox, int c) {
+    const float* wk = at<float>(pool, C::DW_W_OFF);
+    float4 acc = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::DW_B_OFF) + c));
+#pragma unroll
+    for (int ky = 0; ky < C::DW_KH; ++ky) {
+      const int y = oy * C::DW_S - C::DW_PT + ky;
+      if (y < 0 || y >= C::DW_H) continue;
+#pragma unroll
+      for (int kx = 0; kx < C::DW_KW; ++kx) {
+        const int x = ox * C::DW_S - C::DW_PL + kx;
+        if (x < 0 || x >= C::DW_W) continue;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(img + ((i64)y * C::DW_W + x) * C::CI + c));
+        const float4 w = __ldg(reinterpret_cast<const float4*>(wk + (ky * C::DW_KW + kx) * C::CI + c));
+        acc.x = fmaf(v.x, w.x, acc.x); acc.y = fmaf(v.y, w.y, acc.y);
+        acc.z = fmaf(v.z, w.z, acc.z); acc.w = fmaf(v.w, w.w, acc.w);
+      }
+    }
+    const float* ps = at<float>(pool, C::DW_PS_OFF);
+    const float* po = at<float>(pool, C::DW_PO_OFF);
+    acc.x = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.x, ps, po, c);
+    acc.y = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.y, ps, po, c + 1);
+    acc.z = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.z, ps, po, c + 2);
+    acc.w = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.w, ps, po, c + 3);
+    return acc;
+  }
+
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena,
                              int n, Smem& sm) {
     const int tid = threadIdx.x;
@@ -112,6 +141,13 @@ struct GemmSimt {
         int ci = k % C::CI;
         int iy = a_iy[l] + ky, ix = a_ix[l] + kx;
         ok = ok && iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
+        if (C::DW) {
+          // fused depthwise producer: A[pixel, ci..ci+3] = dw(x)(iy, ix, ci..ci+3)
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok) v = dw_point(pool, a_base[l], iy, ix, ci);
+          ra[l][0] = v.x; if (AKV > 1) { ra[l][1 % AKV] = v.y; ra[l][2 % AKV] = v.z; ra[l][3 % AKV] = v.w; }
+          continue;
+        }
         // channel-concat loader: channels [0, C0) from source 0, the rest from source 1
         const float* src = a_base[l] + (iy * C::W + ix) * C::C0 + ci;
         if (C::CONCAT && ci >= C::C0)

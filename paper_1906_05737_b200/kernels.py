@@ -185,6 +185,14 @@ class Specializer:
             CO = u.kernel.shape[1]
             HO = WO = 1
             wmat = np.asarray(u.kernel, F32)
+        elif u.dw is not None:
+            # fused depthwise loader: the GEMM's input map is the dw output
+            H, W, CI = u.dw.output_shape.dims
+            KH = KW = S = 1
+            PT = PL = 0
+            HO, WO, CO = u.output_shape.dims
+            conv_out = u.output_shape
+            wmat = np.asarray(u.kernel, F32).reshape(CI, CO)
         else:
             H, W = x.h, x.w
             CI = sum(sh.c for sh in u.input_shapes)      # concat loader: both sources
@@ -206,6 +214,7 @@ class Specializer:
         src1 = dict(CONCAT=concat, C0=C0, UPF=UPF,
                     IN1_OFF=self.arena_off(u.input_ids[1]) if concat else 0,
                     IN1_IMG=self.img_bytes(u.input_ids[1]) if concat else 0)
+        src1.update(self._dw_fields(u))
         if pool_fused:
             PHO, PWO = u.output_shape.h, u.output_shape.w
             rows = PHO * PWO * 4
@@ -225,7 +234,7 @@ class Specializer:
             n_min = 1
 
         # narrow inputs: direct FFMA convolution (all batch sizes)
-        if (u.kind == "Conv2D" and not softmax and CO <= 32
+        if (u.kind == "Conv2D" and not softmax and CO <= 32 and u.dw is None
                 and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
             assert not concat
             self._conv_direct(pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL,
@@ -235,6 +244,7 @@ class Specializer:
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
         n_max = 1 << 30
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
+                   and u.dw is None
                    and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
                    and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16)
@@ -301,6 +311,22 @@ class Specializer:
         self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
                   grid_mult=ntile_n, n_min=n_min, n_max=n_max, dynamic_smem=True,
                   note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
+
+    def _dw_fields(self, u):
+        """Fields of a fused depthwise producer (GemmSimt DW loader)."""
+        d = u.dw
+        if d is None:
+            return dict(DW=0, DW_H=1, DW_W=1, DW_S=1, DW_PT=0, DW_PL=0, DW_KH=1, DW_KW=1,
+                        DW_W_OFF=0, DW_B_OFF=0, DW_ACT=0, DW_POST=0, DW_PS_OFF=0, DW_PO_OFF=0)
+        h, w, c = d.input_shapes[0].dims
+        kh, kw = d.kernel_hw
+        pt = same_padding(h, kh, d.stride)[0] if d.padding == "same" else 0
+        pl = same_padding(w, kw, d.stride)[0] if d.padding == "same" else 0
+        ep = self.epilogue_fields(d, c)
+        return dict(DW=1, DW_H=h, DW_W=w, DW_S=d.stride, DW_PT=pt, DW_PL=pl, DW_KH=kh, DW_KW=kw,
+                    DW_W_OFF=self.pool.add(d.kernel), DW_B_OFF=self.pool.add(d.bias),
+                    DW_ACT=ep["ACT"], DW_POST=ep["POST"], DW_PS_OFF=ep["PS_OFF"],
+                    DW_PO_OFF=ep["PO_OFF"])
 
     def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.

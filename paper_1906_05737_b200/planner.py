@@ -73,6 +73,7 @@ class CompilationUnit:
     upsample_after: int = 1         # fused nearest upsampling of the output
     pre_up_shape: object = None     # output shape before the fused upsampling
     concat_in: bool = False         # conv reads the channel concat of input_ids
+    dw: object = None               # fused depthwise producer (a CompilationUnit)
 
     def describe(self):
         bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
@@ -95,6 +96,10 @@ class CompilationUnit:
             bits.append(f"+upsample{self.upsample_after}")
         if self.concat_in:
             bits.append("concat-loader")
+        if self.dw is not None:
+            kh, kw = self.dw.kernel_hw
+            bits.append(f"dw{kh}x{kw}/s{self.dw.stride}-loader"
+                        + (f"(act={self.dw.activation})" if self.dw.activation != "linear" else ""))
         if self.in_place_preference is not None:
             bits.append("in_place?")
         return " ".join(bits)
@@ -457,8 +462,33 @@ def fuse_concat(plan):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True):
-    """Reference fusions to a fixpoint, then the B200 epilogue fusions."""
+def fuse_dw_pw(plan):
+    """DepthwiseConv2D feeding only a pointwise (1x1, stride 1) Conv2D becomes
+    that conv's operand loader: the depthwise output is computed on the fly
+    and never written to memory (separable-conv blocks of cfg2/cfg3)."""
+    pos = 1
+    while pos < len(plan.units):
+        u, d = plan.units[pos], plan.units[pos - 1]
+        if (u.kind == "Conv2D" and d.kind == "DepthwiseConv2D" and u.kernel_hw == (1, 1)
+                and u.stride == 1 and u.input_ids == (d.output_id,) and u.dw is None
+                and not u.concat_in and d.residual_id is None and not d.pool_after
+                and d.upsample_after == 1 and d.input_shapes[0].c % 4 == 0
+                and _private(plan, d.output_id)):
+            u.dw = d
+            u.input_ids = d.input_ids
+            u.input_shapes = d.input_shapes
+            plan.tensors.pop(d.output_id, None)
+            _delete(plan, pos - 1, u)
+            continue
+        pos += 1
+    return plan
+
+
+def build_plan(graph, gpu_fusion=True, dw_fusion=False):
+    """Reference fusions to a fixpoint, then the B200 epilogue fusions.
+    ``dw_fusion`` (off by default: measured slower than a depthwise kernel
+    followed by the tcgen05 pointwise GEMM) folds depthwise convs into the
+    pointwise conv's FFMA loader."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
         fuse_pool(plan)
@@ -466,6 +496,8 @@ def build_plan(graph, gpu_fusion=True):
         fuse_softmax(plan)
         fuse_upsample(plan)
         fuse_concat(plan)
+        if dw_fusion:
+            fuse_dw_pw(plan)
     return plan
 
 

@@ -70,6 +70,11 @@ def unit_work(u, plan=None):
         f = u.output_shape.elements * max(1, len(u.input_ids))
     else:
         f = 0
+    d = getattr(u, "dw", None)
+    if d is not None:              # fused depthwise producer
+        df, _, dwb = unit_work(d)
+        f += df
+        wb += dwb
     return f, ins + out, wb
 
 

@@ -80,7 +80,7 @@ class _Handle:
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
-                 nacc=None, aldg=False, kpack=True):
+                 nacc=None, aldg=False, kpack=True, dw_fusion=False):
         import torch
 
         t0 = time.perf_counter()
@@ -93,7 +93,7 @@ class CompiledNetwork:
             raise ValueError("batch must be >= 1")
         _, _, sm_count = _native.device_check(device)
         self.graph = build_graph(manifest, weights)
-        self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion)
+        self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion, dw_fusion=dw_fusion)
         self.assignment = plan_buffers(self.plan)
         cap = _capacity(self.max_batch)
         from .kernels import TC_MIN_ROWS

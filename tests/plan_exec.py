@@ -30,11 +30,18 @@ def run_plan(plan, inputs):
             y = _post(oracle.dense(x.reshape(n, -1), u.kernel, u.bias, 1), u)
         elif u.kind in ("Conv2D", "DepthwiseConv2D"):
             dw = u.kind == "DepthwiseConv2D"
+            if getattr(u, "dw", None) is not None:
+                d = u.dw
+                x = oracle.conv(x.reshape((n,) + d.input_shapes[0].dims), d.kernel, d.bias,
+                                d.stride, d.padding, True, 1)
+                x = _post(x, d)
             if getattr(u, "concat_in", False):
                 x = np.concatenate([vals[t].reshape((n,) + sh.dims)
                                     for t, sh in zip(u.input_ids, u.input_shapes)], axis=-1)
-            y = oracle.conv(x.reshape((n,) + tuple(u.input_shapes[0].dims[:2]) + (-1,)),
-                            u.kernel, u.bias, u.stride, u.padding, dw, 1)
+            in_hw = (tuple(u.dw.output_shape.dims[:2]) if getattr(u, "dw", None) is not None
+                     else tuple(u.input_shapes[0].dims[:2]))
+            y = oracle.conv(x.reshape((n,) + in_hw + (-1,)), u.kernel, u.bias, u.stride,
+                            u.padding, dw, 1)
             y = _post(y, u)
         elif u.kind == "Pool":
             ph, pw = u.kernel_hw

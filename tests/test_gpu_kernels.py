@@ -102,6 +102,30 @@ def test_decoder_fusions(c0, c1, co, up_src, tc):
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
 
+@pytest.mark.parametrize("h,w,c,co,s,act,bn,n", [
+    (9, 13, 8, 16, 1, "relu6", True, 3), (16, 16, 16, 32, 2, "relu", False, 2),
+    (7, 10, 64, 128, 2, "elu", True, 2), (8, 8, 128, 96, 1, "linear", False, 5)])
+def test_depthwise_pointwise_fusion(h, w, c, co, s, act, bn, n):
+    """DepthwiseConv2D (+BN+act) computed inside the pointwise conv's loader."""
+    rng = np.random.default_rng(h * w + c)
+    b = NetBuilder()
+    x = b.input((h, w, c))
+    d = b.layer("DepthwiseConv2D", [x], {"kernel_size": 3, "strides": s, "padding": "same",
+                                         "use_bias": False},
+                [("kernel", he(rng, (3, 3, c), 9))])
+    if bn:
+        d = b.layer("BatchNorm", [d], None, bn_params(rng, c))
+    d = b.layer("Activation", [d], {"activation": act}) if act != "linear" else d
+    y = b.layer("Conv2D", [d], {"filters": co, "kernel_size": 1, "activation": "relu"},
+                [("kernel", he(rng, (1, 1, c, co), c)),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (n, h, w, c)).astype(F32)
+    got, net = gpu(m, wt, xin, dw_fusion=True)
+    assert [u.kind for u in net.plan.units] == ["Conv2D"] and net.plan.units[0].dw is not None
+    np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+
+
 @pytest.mark.parametrize("k,units,act,n", [
     (1, 1, "linear", 1), (3, 5, "relu", 7), (17, 9, "tanh", 3), (130, 7, "sigmoid", 12),
     (64, 64, "elu", 2100), (256, 96, "relu6", 2048), (100, 40, "linear", 2500),

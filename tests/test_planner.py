@@ -133,12 +133,15 @@ def test_gpu_fusions_on_zoo():
 
 
 @pytest.mark.parametrize("cfg", range(5))
-def test_gpu_plan_numerically_sound_on_zoo(cfg):
+@pytest.mark.parametrize("dw_fusion", [False, True])
+def test_gpu_plan_numerically_sound_on_zoo(cfg, dw_fusion):
     m, w = zoo.build(cfg)
     g = build_graph(m, w)
     x = zoo.inputs(cfg, 2)
-    np.testing.assert_allclose(run_plan(build_plan(g), [x])[0], oracle.run_graph(g, [x])[0],
-                               **TOL)
+    plan = build_plan(g, dw_fusion=dw_fusion)
+    if dw_fusion and cfg in (2, 3):
+        assert "DepthwiseConv2D" not in kinds(plan)
+    np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
 
 
 def test_build_plan_idempotent_and_deterministic():
