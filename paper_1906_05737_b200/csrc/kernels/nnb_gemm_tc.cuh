@@ -223,8 +223,12 @@ struct GemmTc {
   // N a single accumulator chain is bound by MMA latency, not throughput).
   static constexpr int NACC = C::NACC;
   static constexpr int ACC_COLS = NACC * 2 * C::BN;       // fp32 columns per buffer
-  static constexpr int A_TCOL = 2 * ACC_COLS;                    // first A column (TA)
-  static constexpr int TMEM_NEED = TA ? 2 * ACC_COLS + C::NS * 2 * BK : 2 * ACC_COLS;
+  // ABUF accumulator buffers: 2 lets the epilogue drain one while the MMA fills
+  // the other; 1 frees TMEM for the A operand at BN = 128 (the MMA then waits
+  // only for the short per-chunk drain).
+  static constexpr int ABUF = C::ABUF;
+  static constexpr int A_TCOL = ABUF * ACC_COLS;                 // first A column (TA)
+  static constexpr int TMEM_NEED = TA ? ABUF * ACC_COLS + C::NS * 2 * BK : ABUF * ACC_COLS;
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64
                                  : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
@@ -272,9 +276,9 @@ struct GemmTc {
     u64* full = bars;                 // [NS]  TMA landed
     u64* lo_ready = bars + C::NS;     // [NS]  A split done (64 converter arrivals)
     u64* empty = bars + 2 * C::NS;    // [NS]  MMA finished reading the stage
-    u64* tfull = bars + 3 * C::NS;    // [2]   accumulator ready
-    u64* tempty = tfull + 2;          // [2]   accumulator drained (128 arrivals)
-    u32* tmem_slot = reinterpret_cast<u32*>(tempty + 2);
+    u64* tfull = bars + 3 * C::NS;    // [ABUF] accumulator ready
+    u64* tempty = tfull + ABUF;       // [ABUF] accumulator drained (epilogue arrivals)
+    u32* tmem_slot = reinterpret_cast<u32*>(tempty + ABUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
@@ -287,7 +291,7 @@ struct GemmTc {
         mbar_init(&lo_ready[s], 32 * CONV_WARPS);
         mbar_init(&empty[s], 1);
       }
-      for (int a = 0; a < 2; ++a) {
+      for (int a = 0; a < ABUF; ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], EPI_THREADS);
       }
@@ -386,7 +390,7 @@ struct GemmTc {
           __syncwarp();
           if (++s == C::NS) { s = 0; ph ^= 1; }
           if (kc == CHUNK_KB - 1 || kb == KB - 1) {
-            if (++acc == 2) { acc = 0; aph ^= 1; }
+            if (++acc == ABUF) { acc = 0; aph ^= 1; }
           }
         }
       }
@@ -565,7 +569,7 @@ struct GemmTc {
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
-            if (++acc == 2) { acc = 0; aph ^= 1; }
+            if (++acc == ABUF) { acc = 0; aph ^= 1; }
           }
           const int img = mb / TPI, tt = mb % TPI;
           const int w = r % TW;
@@ -620,7 +624,7 @@ struct GemmTc {
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
-          if (++acc == 2) { acc = 0; aph ^= 1; }
+          if (++acc == ABUF) { acc = 0; aph ^= 1; }
         }
         // output position of this thread's row
         long long obase;            // element offset of the row's first channel

@@ -353,12 +353,13 @@ class Specializer:
         # independent accumulator chains fill TMEM (2 buffers x NACC x (main, corr))
         NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
         aldg = self.aldg
-        tmem_a = self.tmem_a and NACC == 1 and BN <= 64 and not aldg
+        tmem_a = self.tmem_a and NACC == 1 and not aldg and (BN <= 64 or BN == 128)
+        ABUF = 1 if (tmem_a and BN > 64) else 2
         stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * BN * BK * 4
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
         NS = max(2, min(8, (200 * 1024) // stage))
         if tmem_a:
-            NS = min(NS, (512 - 4 * BN) // (2 * BK))
+            NS = min(NS, (512 - ABUF * 2 * NACC * BN) // (2 * BK))
         wt = np.zeros((NPAD, KPAD), F32)
         wt[:CO, :K] = np.asarray(wmat, F32).T
         hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
@@ -372,7 +373,7 @@ class Specializer:
             geo.update(rows_geo)
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
-                      NACC=NACC, ALDG=aldg,
+                      NACC=NACC, ALDG=aldg, ABUF=ABUF,
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),
                       IN1_OFF=(self.arena_off(u.input_ids[1]) if conv and conv["CONCAT"] else 0),
