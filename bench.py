@@ -110,15 +110,26 @@ class ClockSampler:
 
 
 def dist_setup(gpus):
+    """One process per GPU (torchrun).  The data path has no collective; the
+    process group only carries the barrier and the MAX of per-rank device
+    time, so it runs over NCCL when every rank owns a GPU and over gloo
+    otherwise (e.g. a functional check with several ranks on one device)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ndev = max(torch.cuda.device_count(), 1) if torch.cuda.is_available() else 1
+        own = ndev >= int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        local = local % ndev
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        if own and torch.cuda.is_available():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -133,7 +144,8 @@ def max_over_ranks(world, value, local):
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
