@@ -4,7 +4,7 @@
   libcuda and libnvrtc are dlopen'ed at run time.
 * ahead-of-time check of the kernel headers with nvcc for sm_100a
   (``-gencode arch=compute_100a,code=sm_100a -lineinfo``) on the
-  specialisations of BASELINE config 0, written to build/kcheck.cubin.  At run
+  specialisations of every BASELINE config, written to build/kcheck_cfg*.cubin.  At run
   time the same headers are compiled by NVRTC inside libnnb.so with the
   shapes of the network being compiled.
 The CPU checker under oracle/ (test infrastructure) is built by
@@ -32,8 +32,10 @@ def build_runtime():
     return out
 
 
-def kernel_check():
-    """nvcc-compile the kernel templates for sm_100a with real instantiations."""
+def kernel_check(configs=range(5), batch=4096):
+    """nvcc-compile the kernel templates for sm_100a with real instantiations:
+    every unit of each zoo config at ``batch`` (SIMT, direct and tcgen05
+    variants), one translation unit per config, compiled in parallel."""
     sys.path.insert(0, str(ROOT))
     from paper_1906_05737_b200 import zoo
     from paper_1906_05737_b200.buffers import plan_buffers
@@ -42,21 +44,28 @@ def kernel_check():
     from paper_1906_05737_b200.options import ApproximationOptions
     from paper_1906_05737_b200.planner import build_plan
 
-    m, w = zoo.build(0)
-    plan = build_plan(build_graph(m, w))
-    spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), 64, 64)
     bdir = ROOT / "build"
     bdir.mkdir(exist_ok=True)
-    cu = bdir / "kcheck.cu"
-    cu.write_text(spec.source)
-    out = bdir / "kcheck.cubin"
-    cmd = [str(CUDA / "bin" / "nvcc"), *NVCC_ARCH, "-lineinfo", "-O3", "-std=c++17", "-cubin",
-           f"-I{PKG / 'csrc' / 'kernels'}", "-Xptxas", "-v", str(cu), "-o", str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc kernel check failed:\n" + r.stderr[-4000:])
-    (bdir / "kcheck.ptxas.txt").write_text(r.stderr)
-    return out
+    jobs = []
+    for c in configs:
+        m, w = zoo.build(c)
+        plan = build_plan(build_graph(m, w))
+        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch)
+        cu = bdir / f"kcheck_cfg{c}.cu"
+        cu.write_text(spec.source)
+        out = bdir / f"kcheck_cfg{c}.cubin"
+        cmd = [str(CUDA / "bin" / "nvcc"), *NVCC_ARCH, "-lineinfo", "-O3", "-std=c++17", "-cubin",
+               f"-I{PKG / 'csrc' / 'kernels'}", "-Xptxas", "-v", str(cu), "-o", str(out)]
+        jobs.append((c, out, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                              stderr=subprocess.PIPE, text=True)))
+    outs = []
+    for c, out, p in jobs:
+        _, err = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError(f"nvcc kernel check (config {c}) failed:\n" + err[-4000:])
+        (bdir / f"kcheck_cfg{c}.ptxas.txt").write_text(err)
+        outs.append(out)
+    return outs
 
 
 def main():

@@ -24,7 +24,8 @@
 //   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (the hardware's
 //               lane-quarter rule) and half of the tile's columns;
 //               tcgen05.ld 32 lanes x 16 columns, bias, activation,
-//               post-affine, residual, float4 stores.  The accumulator is
+//               post-affine, then a shared-memory transpose so residual
+//               loads and stores are row-coalesced float4s.  The accumulator is
 //               double-buffered in TMEM so the epilogue of tile t overlaps the
 //               MMAs of tile t+1.
 #pragma once
@@ -196,6 +197,27 @@ __device__ __forceinline__ void tmem_ld(u32 taddr, float (&v)[N]) {
   }
 }
 
+// Epilogue transpose through shared memory.  After the TMEM read every lane
+// owns one output row; storing (or residual-loading) NC columns per lane
+// touches 32 rows = 32 cache lines per warp instruction.  stage_rows writes
+// the warp's 32 x NC block into a per-warp staging area (16-byte chunks
+// XOR-swizzled so both phases are bank-conflict free); staged_chunk then
+// hands lane l the chunk (l % CPR) of row p*(32/CPR) + l/CPR in pass p, so a
+// warp instruction covers 32/CPR whole row segments.
+template <int NC>
+__device__ __forceinline__ int stage_slot(int row, int c) {
+  constexpr int CPR = NC / 4, RPW = 8 / CPR;
+  return row * CPR + (c ^ ((row / RPW) & (CPR - 1)));
+}
+template <int NC>
+__device__ __forceinline__ void stage_rows(float4* st, const float* v, int lane) {
+  static_assert(NC == 4 || NC == 8 || NC == 16, "staged columns");
+#pragma unroll
+  for (int j = 0; j < NC / 4; ++j)
+    st[stage_slot<NC>(lane, j)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+}
+
 // C: K, N, NPAD (multiple of BN), BN (32..256, multiple of 16), NS (stages),
 //    ROWS (GEMM rows per image), IN/OUT offsets, B_OFF (bias), epilogue fields.
 template <class C>
@@ -234,8 +256,9 @@ struct GemmTc {
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)(BM >> 4) << 24);
-  static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int EPI_STAGE = EPI_WARPS * 32 * 16 * 4;   // per-warp 32 x 16 staging
+  static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
   // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
@@ -279,6 +302,7 @@ struct GemmTc {
     u64* tfull = bars + 3 * C::NS;    // [ABUF] accumulator ready
     u64* tempty = tfull + ABUF;       // [ABUF] accumulator drained (epilogue arrivals)
     u32* tmem_slot = reinterpret_cast<u32*>(tempty + ABUF);
+    float4* epi_stage = reinterpret_cast<float4*>(smem + C::NS * STAGE + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
@@ -543,6 +567,7 @@ struct GemmTc {
         if constexpr (KP) {
           // ---- packed horizontal taps: reduce chunks, combine across lanes ----
           constexpr int GCO = C::CO / 2;                 // output channels per warp group
+          static_assert(GCO == 8 || GCO % 16 == 0, "KPACK staged store width");
           const int g = (warp - EPI_W0) >> 2;
           float run[C::KW][GCO];
 #pragma unroll
@@ -572,9 +597,14 @@ struct GemmTc {
             if (++acc == ABUF) { acc = 0; aph ^= 1; }
           }
           const int img = mb / TPI, tt = mb % TPI;
-          const int w = r % TW;
-          const int oy = (tt / TX) * TH + r / TW, ox = (tt % TX) * OW + w;
-          const bool live = img < n && w < OW && oy < C::HO && ox < C::WO;
+          // output pixel of tile row rr (16 input columns per tile row)
+          auto pix = [&](int rr, long long& ob) {
+            const int w = rr % TW;
+            const int oy = (tt / TX) * TH + rr / TW, ox = (tt % TX) * OW + w;
+            ob = (long long)img * (C::OUT_IMG / 4) +
+                 ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::CO + g * GCO;
+            return img < n && w < OW && oy < C::HO && ox < C::WO;
+          };
           float y[GCO];
 #pragma unroll
           for (int i = 0; i < GCO; ++i) {
@@ -584,16 +614,26 @@ struct GemmTc {
             const int col = g * GCO + i;
             y[i] = finish<C::ACT, C::MODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
           }
-          if (live) {
-            const long long ob = (long long)img * (C::OUT_IMG / 4) +
-                ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::CO + g * GCO;
 #pragma unroll
-            for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
-              float* d = out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO;
+          for (int h = 0; h < (GCO + 15) / 16; ++h) {
+            constexpr int NC = GCO < 16 ? GCO : 16;
+            constexpr int CPR = NC / 4;
+            float4* st = epi_stage + (warp - EPI_W0) * 128;
+            stage_rows<NC>(st, y + h * 16, lane);
 #pragma unroll
-              for (int i = 0; i < GCO; i += 4)
-                *reinterpret_cast<float4*>(d + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+            for (int p = 0; p < CPR; ++p) {
+              const int row = p * (32 / CPR) + lane / CPR, c = lane % CPR;
+              long long ob;
+              if (pix(q * 32 + row, ob)) {
+                const float4 x = st[stage_slot<NC>(row, c)];
+#pragma unroll
+                for (int rep = 0; rep < C::UPF * C::UPF; ++rep)
+                  *reinterpret_cast<float4*>(
+                      out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO +
+                      h * 16 + 4 * c) = x;
+              }
             }
+            __syncwarp();
           }
           continue;
         }
@@ -626,35 +666,37 @@ struct GemmTc {
           mbar_arrive(&tempty[acc]);
           if (++acc == ABUF) { acc = 0; aph ^= 1; }
         }
-        // output position of this thread's row
-        long long obase;            // element offset of the row's first channel
-        bool live;
-        if (C::CONV) {
-          const int img = mb / TPI, tt = mb % TPI;
-          const int oy = (tt / TX) * TH + r / TW, ox = (tt % TX) * TW + r % TW;
-          live = img < n && oy < C::HO && ox < C::WO;
-          obase = (long long)img * (C::OUT_IMG / 4) + ((long long)oy * C::WO + ox) * C::N;
-          if (C::UPF > 1)     // fused nearest upsampling: first replica of the pixel
-            obase = (long long)img * (C::OUT_IMG / 4) +
-                    ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
-          if (C::POOL) {      // pooled row index of the 2x2 window this lane leads
-            const int py = (tt / TX) * (TH / 2) + (r / TW) / 2, px = (tt % TX) * (TW / 2) + (r % TW) / 2;
-            live = img < n && py < C::PHO && px < C::PWO && (lane & 17) == 0;
-            obase = (long long)img * (C::OUT_IMG / 4) + ((long long)py * C::PWO + px) * C::N;
+        // output position of tile row rr: element offset of its first channel
+        auto rowpos = [&](int rr, long long& obase) {
+          bool live;
+          if (C::CONV) {
+            const int img = mb / TPI, tt = mb % TPI;
+            const int oy = (tt / TX) * TH + rr / TW, ox = (tt % TX) * TW + rr % TW;
+            live = img < n && oy < C::HO && ox < C::WO;
+            obase = (long long)img * (C::OUT_IMG / 4) + ((long long)oy * C::WO + ox) * C::N;
+            if (C::UPF > 1)     // fused nearest upsampling: first replica of the pixel
+              obase = (long long)img * (C::OUT_IMG / 4) +
+                      ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
+            if (C::POOL) {      // pooled row index of the 2x2 window this row leads
+              const int py = (tt / TX) * (TH / 2) + (rr / TW) / 2,
+                        px = (tt % TX) * (TW / 2) + (rr % TW) / 2;
+              live = img < n && py < C::PHO && px < C::PWO && (rr & 17) == 0;
+              obase = (long long)img * (C::OUT_IMG / 4) + ((long long)py * C::PWO + px) * C::N;
+            }
+          } else {
+            const long long m = (long long)mb * BM + rr;
+            live = m < rows;
+            obase = m * C::N;
+            if (C::UPF > 1) {   // 1x1 conv rows: pixel (oy, ox) of image m / ROWS
+              const long long img = m / C::ROWS;
+              const int ri = (int)(m - img * C::ROWS), oy = ri / C::WO, ox = ri % C::WO;
+              obase = img * (C::OUT_IMG / 4) +
+                      ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
+            }
           }
-        } else {
-          const long long m = (long long)mb * BM + r;
-          live = m < rows;
-          obase = m * C::N;
-          if (C::UPF > 1) {   // 1x1 conv rows: pixel (oy, ox) of image m / ROWS
-            const long long img = m / C::ROWS;
-            const int rr = (int)(m - img * C::ROWS), oy = rr / C::WO, ox = rr % C::WO;
-            obase = img * (C::OUT_IMG / 4) +
-                    ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::N;
-          }
-        }
-        float* dst = out + obase;
-        const float* res = at<float>(arena, C::RES_OFF) + obase;
+          return live;
+        };
+        const float* res = at<float>(arena, C::RES_OFF);
 #pragma unroll
         for (int g = 0; g < EPI_COLS / 16; ++g) {
           const int col0 = nb * C::BN + cbeg + g * 16;
@@ -665,26 +707,56 @@ struct GemmTc {
             const int col = col0 + i < C::N ? col0 + i : C::N - 1;
             float y = v[i] + __ldg(bias + col);
             y = finish<C::ACT, C::MODE, C::POST>(y, ps, po, col);
-            if (C::RES && live) y = add(y, __ldg(res + col));
             if (C::POOL) {     // lanes w, w^1 (same image row), w^16 (next row)
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 16));
             }
             v[i] = y;
           }
-          if (live) {
+          if constexpr (C::N % 16 == 0 && C::EPI_ST) {
+            // coalesced: 8 lanes per row segment of 16 columns (residual too)
+            float4* st = epi_stage + (warp - EPI_W0) * 128;
+            stage_rows<16>(st, v, lane);
 #pragma unroll
-            for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
-              float* d = dst + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::N;
-              if (C::N % 16 == 0) {
+            for (int p = 0; p < 4; ++p) {
+              const int row = p * 8 + (lane >> 2), c = lane & 3;
+              long long ob;
+              if (rowpos(q * 32 + row, ob)) {
+                float4 x = st[stage_slot<16>(row, c)];
+                if (C::RES) {
+                  const float4 rv = __ldg(reinterpret_cast<const float4*>(res + ob + col0 + 4 * c));
+                  x.x = add(x.x, rv.x); x.y = add(x.y, rv.y);
+                  x.z = add(x.z, rv.z); x.w = add(x.w, rv.w);
+                }
 #pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                  *reinterpret_cast<float4*>(d + col0 + i) =
-                      make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-              } else {
+                for (int rep = 0; rep < C::UPF * C::UPF; ++rep)
+                  *reinterpret_cast<float4*>(
+                      out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::N +
+                      col0 + 4 * c) = x;
+              }
+            }
+            __syncwarp();
+          } else {
+            long long ob;
+            const bool live = rowpos(r, ob);
+            if (live) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                  if (col0 + i < C::N) d[col0 + i] = v[i];
+              for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {
+                float* d = out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::N;
+                if (C::RES) {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i)
+                    if (col0 + i < C::N) v[i] = add(v[i], __ldg(res + ob + col0 + i));
+                }
+                if (C::N % 16 == 0) {
+#pragma unroll
+                  for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4*>(d + col0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i)
+                    if (col0 + i < C::N) d[col0 + i] = v[i];
+                }
               }
             }
           }

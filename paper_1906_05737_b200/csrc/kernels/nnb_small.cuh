@@ -85,43 +85,76 @@ struct DenseSmallM {
 
 // ---------------------------------------------------------------------------
 // DepthwiseConv2D: acc = bias; taps (ky, kx) in order; mul then add.
+// A thread owns PX horizontally adjacent output pixels of one channel vector:
+// the (PX-1)*S + KW input columns of each kernel row are loaded once into
+// registers and shared by the PX outputs (PX=4, 3x3 stride 1: 18 loads for 4
+// pixels instead of 36).  Out-of-image taps are skipped, not zero-multiplied,
+// as in the reference.  IDX32: the launch's index space fits in 32 bits.
 template <class C>
 struct Depthwise {
-  static constexpr int V = C::VEC;
+  static constexpr int V = C::VEC, PX = C::PX;
   typedef typename Vec<V>::T T;
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
-    constexpr int CG = C::C / V;
+    constexpr int CG = C::C / V, XG = (C::WO + PX - 1) / PX;
+    constexpr int NCOL = (PX - 1) * C::S + C::KW;
     const i64 t = gtid();
-    if (t >= (i64)n * C::HO * C::WO * CG) return;
-    const int cg = (int)(t % CG);
-    const i64 p = t / CG;
-    const int ox = (int)(p % C::WO);
-    const int oy = (int)((p / C::WO) % C::HO);
-    const i64 img = p / ((i64)C::HO * C::WO);
+    if (t >= (i64)n * C::HO * XG * CG) return;
+    int cg, xg, oy;
+    i64 img;
+    if (C::IDX32) {
+      unsigned q = (unsigned)t;
+      cg = (int)(q % CG); q /= CG;
+      xg = (int)(q % XG); q /= XG;
+      oy = (int)(q % C::HO); img = q / C::HO;
+    } else {
+      i64 q = t;
+      cg = (int)(q % CG); q /= CG;
+      xg = (int)(q % XG); q /= XG;
+      oy = (int)(q % C::HO); img = q / C::HO;
+    }
     const T* in = at<T>(arena, C::IN_OFF + img * C::IN_IMG);
     const T* wk = at<T>(pool, C::W_OFF);
-    T acc = at<T>(pool, C::B_OFF)[cg];
-    const int iy0 = oy * C::S - C::PT, ix0 = ox * C::S - C::PL;
+    const T b = at<T>(pool, C::B_OFF)[cg];
+    T acc[PX];
+#pragma unroll
+    for (int p = 0; p < PX; ++p) acc[p] = b;
+    const int ox0 = xg * PX;
+    const int iy0 = oy * C::S - C::PT, ix0 = ox0 * C::S - C::PL;
 #pragma unroll
     for (int ky = 0; ky < C::KH; ++ky) {
       const int iy = iy0 + ky;
       if (iy < 0 || iy >= C::H) continue;
+      const T* row = in + (i64)iy * C::W * CG + cg;
+      T xv[NCOL];
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) {
+        const int ix = ix0 + j;
+        xv[j] = (ix >= 0 && ix < C::W) ? __ldg(row + ix * CG) : vzero<V>();
+      }
 #pragma unroll
       for (int kx = 0; kx < C::KW; ++kx) {
-        const int ix = ix0 + kx;
-        if (ix < 0 || ix >= C::W) continue;
-        T xv = __ldg(in + ((i64)iy * C::W + ix) * CG + cg);
-        T wv = __ldg(wk + (ky * C::KW + kx) * CG + cg);
+        const T wv = __ldg(wk + (ky * C::KW + kx) * CG + cg);
 #pragma unroll
-        for (int l = 0; l < V; ++l) set_lane(acc, l, add(lane(acc, l), mul(lane(xv, l), lane(wv, l))));
+        for (int p = 0; p < PX; ++p) {
+          const int ix = ix0 + p * C::S + kx;
+          if (ix < 0 || ix >= C::W) continue;
+#pragma unroll
+          for (int l = 0; l < V; ++l)
+            set_lane(acc[p], l, add(lane(acc[p], l), mul(lane(xv[p * C::S + kx], l), lane(wv, l))));
+        }
       }
     }
     const float* ps = at<float>(pool, C::PS_OFF);
     const float* po = at<float>(pool, C::PO_OFF);
+    T* out = at<T>(arena, C::OUT_OFF + img * C::OUT_IMG) + ((i64)oy * C::WO + ox0) * CG + cg;
 #pragma unroll
-    for (int l = 0; l < V; ++l)
-      set_lane(acc, l, finish<C::ACT, C::MODE, C::POST>(lane(acc, l), ps, po, cg * V + l));
-    at<T>(arena, C::OUT_OFF + img * C::OUT_IMG)[p % ((i64)C::HO * C::WO) * CG + cg] = acc;
+    for (int p = 0; p < PX; ++p) {
+      if (ox0 + p >= C::WO) break;
+#pragma unroll
+      for (int l = 0; l < V; ++l)
+        set_lane(acc[p], l, finish<C::ACT, C::MODE, C::POST>(lane(acc[p], l), ps, po, cg * V + l));
+      out[p * CG] = acc[p];
+    }
   }
 };
 

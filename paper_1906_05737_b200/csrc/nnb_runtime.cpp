@@ -280,7 +280,12 @@ nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
 
 struct nnb_net {
   int device = 0;
-  bool pdl = false;   // NNB_PDL=1 enables programmatic dependent launch (measured: no gain)
+  // Programmatic dependent launch: the next kernel's launch and prologue
+  // overlap the previous kernel's tail; griddepcontrol.wait (no early
+  // trigger) keeps full-completion ordering.  Measured: -3% batch-1 replay
+  // on cfg3, neutral elsewhere; an early trigger was 3-10% slower.
+  // NNB_PDL=0 disables it.
+  bool pdl = true;
   std::vector<std::vector<CUtensorMap>> maps;   // per launch
   CUcontext ctx = nullptr;
   std::vector<CUmodule> mods;

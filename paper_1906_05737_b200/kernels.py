@@ -335,6 +335,7 @@ class Specializer:
         # narrow outputs: pack the horizontal taps into N (3x fewer MMAs)
         kw = u.kernel_hw[1] if conv else 1
         kpack = bool(conv and self.kpack and CO % 16 == 0 and kw * CO <= 128 and kw > 1
+                     and (CO == 16 or CO % 32 == 0)
                      and not conv["POOL"] and u.residual_id is None)
         CO_real = CO
         if kpack:
@@ -374,6 +375,11 @@ class Specializer:
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF,
+                      # shared-memory transposed epilogue (coalesced residual
+                      # loads / stores); long-K tiles keep direct row stores --
+                      # their mainloop is shared-memory bound and the extra
+                      # staging traffic cost 9% at K=1024 (equal at K=512)
+                      EPI_ST=int(u.residual_id is not None or K < 512),
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),
                       IN1_OFF=(self.arena_off(u.input_ids[1]) if conv and conv["CONCAT"] else 0),
@@ -401,7 +407,7 @@ class Specializer:
         tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
                     box=(BK, BN), swizzle=sw)
         tm_bl = dict(tm_b, offset=lo_off)
-        smem = NS * stage + 1024 + 256
+        smem = NS * stage + 1024 + 256 + 8 * 32 * 16 * 4   # + epilogue staging
         ntn = NPAD // BN
         if conv:
             ow = 16 - (kw - 1) if kpack else 16
@@ -464,14 +470,33 @@ class Specializer:
         PT = same_padding(H, KH, S)[0] if u.padding == "same" else 0
         PL = same_padding(W, KW, S)[0] if u.padding == "same" else 0
         vec = 4 if C % 4 == 0 else 1
-        fields = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
-                      VEC=vec, IN_OFF=self.arena_off(u.input_ids[0]),
-                      IN_IMG=self.img_bytes(u.input_ids[0]),
-                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
-                      W_OFF=self.pool.add(u.kernel), B_OFF=self.pool.add(u.bias))
-        fields.update(self.epilogue_fields(u, C))
-        self.emit(pos, f"dw{KH}x{KW}", "nnb::Depthwise", fields, ELEM_BLOCK, 0,
-                  HO * WO * (C // vec), ELEM_BLOCK)
+        base = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
+                    VEC=vec, IN_OFF=self.arena_off(u.input_ids[0]),
+                    IN_IMG=self.img_bytes(u.input_ids[0]),
+                    OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                    W_OFF=self.pool.add(u.kernel), B_OFF=self.pool.add(u.bias))
+        base.update(self.epilogue_fields(u, C))
+
+        def variant(px, n_min, n_max):
+            per_img = HO * -(-WO // px) * (C // vec)
+            self.emit(pos, f"dw{KH}x{KW}", "nnb::Depthwise",
+                      dict(base, PX=px, IDX32=int(self.cap * per_img < 2 ** 31)),
+                      ELEM_BLOCK, 0, per_img, ELEM_BLOCK, n_min=n_min, n_max=n_max,
+                      note=f"{px} px/thread")
+        # several output pixels per thread share input columns in registers
+        # (measured: 1.4-1.7x at C >= 16); narrow channel vectors keep one
+        # pixel per thread (the x-strided warp touches 4x the cache lines),
+        # and so do batches too small to fill the GPU with the wide variant
+        wide = 1 if C // vec < 4 else min(4 if S == 1 else 2, WO)
+        if wide == 1:
+            variant(1, 1, 1 << 30)
+            return
+        per_wide = HO * -(-WO // wide) * (C // vec)
+        n_small = (self.sm_count * 512 - 1) // per_wide
+        if n_small >= 1:
+            variant(1, 1, n_small)
+        if n_small < self.max_batch:
+            variant(wide, n_small + 1, 1 << 30)
 
     def pool_unit(self, pos, u):
         H, W, C = u.input_shapes[0].dims

@@ -1,7 +1,5 @@
-python -c "import __graft_entry__ as g; g.build()" > /dev/null
-timeout 900 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -4
-for c in 0 4 3; do
-  case $c in 0) B=4096;; 2) B=1024;; 3) B=256;; 4) B=64;; esac
-  python scripts/prof_net.py --config $c --batch $B 2>&1 | grep -E "replay|direct"
-  python scripts/prof_net.py --config $c --batch 1 2>&1 | grep -E "replay"
-done
+#!/bin/bash
+# GPU tests + per-launch profile of the given "cfg batch" pairs
+python -c "import __graft_entry__ as g; g.build()" >/dev/null || exit 1
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+for c in "$@"; do set -- $c; echo "== cfg$1 b$2"; timeout 300 python scripts/prof_net.py --config $1 --batch $2; done
