@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define NNB_ABI_VERSION 1
+#define NNB_ABI_VERSION 2
+#define NNB_MAX_TMAPS 6
 
 typedef enum {
   NNB_OK = 0,
@@ -63,8 +64,9 @@ typedef struct {
  *   grid.x = min(ceil(n * items_per_image / items_per_block) * grid_mult, grid_cap)
  * for a replay over n images (grid_cap 0 = no cap); the launch is part of the
  * replay only when n_min <= n <= n_max.  Every kernel has the signature
- *   void k(const float *pool, float *arena, int n [, TmaDesc tm0, tm1, tm2, tm3])
- * with the four tensor maps present iff n_tmaps > 0. */
+ *   void k(const float *pool, float *arena, int n [, TmaDesc tm0, ..., tm5])
+ * with the NNB_MAX_TMAPS tensor maps present iff n_tmaps > 0 (unused trailing
+ * maps are passed zeroed). */
 typedef struct {
   int32_t kernel;            /* index into the kernel-name list             */
   uint32_t block;            /* threads per block                           */
@@ -75,7 +77,7 @@ typedef struct {
   int32_t n_min, n_max;
   uint32_t grid_cap;
   uint32_t n_tmaps;
-  nnb_tmap tmaps[4];
+  nnb_tmap tmaps[NNB_MAX_TMAPS];
 } nnb_launch;
 
 /* A network I/O tensor: byte offset in the arena and bytes per image. */

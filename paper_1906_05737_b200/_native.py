@@ -24,6 +24,9 @@ EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "n
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
 
+MAX_TMAPS = 6          # NNB_MAX_TMAPS
+
+
 class TMap(ctypes.Structure):
     _fields_ = [("space", ctypes.c_uint32), ("swizzle", ctypes.c_uint32),
                 ("offset", ctypes.c_uint64), ("rank", ctypes.c_uint32),
@@ -46,7 +49,7 @@ class Launch(ctypes.Structure):
                 ("items_per_image", ctypes.c_uint64), ("items_per_block", ctypes.c_uint64),
                 ("n_min", ctypes.c_int32), ("n_max", ctypes.c_int32),
                 ("grid_cap", ctypes.c_uint32), ("n_tmaps", ctypes.c_uint32),
-                ("tmaps", TMap * 4)]
+                ("tmaps", TMap * MAX_TMAPS)]
 
 
 class IO(ctypes.Structure):

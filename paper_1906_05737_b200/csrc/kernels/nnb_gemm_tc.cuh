@@ -31,6 +31,9 @@
 #pragma once
 #include "nnb_common.cuh"
 
+// NNB_TC_DBG (diagnostics only, results are garbage): bit 0 skips the MMAs,
+// bit 1 the TMA operand loads, bit 2 the A split, bit 3 the epilogue's TMEM
+// reads and math.
 #ifndef NNB_TC_DBG
 #define NNB_TC_DBG 0
 #endif
@@ -38,6 +41,14 @@
 // bits ignored (verified on B200 by scripts/tc_hi.py: bit-identical results
 // with and without writing hi = a & 0xffffe000 back), so only lo = a - hi is
 // materialised; the raw tile serves as the hi operand.
+// Split rule for A in TMEM: hi = A rounded to the nearest TF32 (exactly
+// representable, so the tensor core uses it as is) and lo = A - hi, exact and
+// of either sign -- the tensor core's truncation of lo then errs in both
+// directions instead of always toward zero.  (A read from shared memory is
+// the raw FP32 tile, which the hardware truncates: there hi = trunc(A).)
+#ifndef NNB_SPLIT_RN
+#define NNB_SPLIT_RN 1
+#endif
 #ifndef NNB_HI_INPLACE
 #define NNB_HI_INPLACE 0
 #endif
@@ -45,6 +56,11 @@
 namespace nnb {
 
 struct __align__(64) TmaDesc { unsigned long long opaque[16]; };
+
+__device__ __forceinline__ u32 split_hi(float a) {
+  const u32 u = __float_as_uint(a);
+  return ((NNB_SPLIT_RN ? u + 0x1000u : u) & 0xFFFFE000u);
+}
 
 __device__ __forceinline__ u32 smem_u32(const void* p) {
   return (u32)__cvta_generic_to_shared(p);
@@ -90,6 +106,28 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const TmaDesc* map, u64* 
       "l"(reinterpret_cast<u64>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+
+// TMA tensor stores (bulk-group completion, per issuing thread)
+__device__ __forceinline__ void tma_store_2d(const TmaDesc* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<u64>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const TmaDesc* map, const void* src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<u64>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -179,6 +217,26 @@ __device__ __forceinline__ void tmem_ld16(u32 taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Batched TMEM reads: several tcgen05.ld in flight, one wait.  tmem_pin
+// re-defines the destination registers after the wait so no use of them
+// can be scheduled above it.
+__device__ __forceinline__ void tmem_ld16_async(u32 taddr, u32 (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_pin(u32 (&r)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 template <int N>
 __device__ __forceinline__ void tmem_ld(u32 taddr, float (&v)[N]) {
   if constexpr (N == 16) {
@@ -244,7 +302,14 @@ struct GemmTc {
   // rotate over them so dependent tcgen05.mma instructions overlap (for narrow
   // N a single accumulator chain is bound by MMA latency, not throughput).
   static constexpr int NACC = C::NACC;
-  static constexpr int ACC_COLS = NACC * 2 * C::BN;       // fp32 columns per buffer
+  // CSPLIT = 0 accumulates the correction products into the main chain (half
+  // the TMEM columns, so BN = 128 keeps two accumulator buffers next to a
+  // TMEM-resident A); the chunk length CHUNK then bounds the truncation error.
+  static constexpr bool CS = C::CSPLIT != 0;
+  // exact-mode activations in FP32 (no FP64: it issues on the MMA's pipe)
+  static constexpr int EMODE = C::MODE == MODE_EXACT ? MODE_EXACT_F32 : C::MODE;
+  static constexpr int CW = (CS ? 2 : 1) * C::BN;         // columns per chain
+  static constexpr int ACC_COLS = NACC * CW;              // fp32 columns per buffer
   // ABUF accumulator buffers: 2 lets the epilogue drain one while the MMA fills
   // the other; 1 frees TMEM for the A operand at BN = 128 (the MMA then waits
   // only for the short per-chunk drain).
@@ -257,8 +322,6 @@ struct GemmTc {
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)(BM >> 4) << 24);
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
-  static constexpr int EPI_STAGE = EPI_WARPS * 32 * 16 * 4;   // per-warp 32 x 16 staging
-  static constexpr int SMEM = C::NS * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
   // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
@@ -268,7 +331,7 @@ struct GemmTc {
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
-  static constexpr int CHUNK_KB = 8;                 // k-blocks (K = 256) per TMEM chunk
+  static constexpr int CHUNK_KB = C::CHUNK;          // k-blocks per TMEM chunk
   static constexpr int NCHUNK = (KB + CHUNK_KB - 1) / CHUNK_KB;
   static_assert(C::BN % 16 == 0 && C::BN >= 16 && C::BN <= 128, "UMMA N / TMEM budget");
   // spatial (implicit-GEMM convolution) tiling: 8 x 16 output pixels per tile
@@ -288,21 +351,33 @@ struct GemmTc {
   static_assert(!KP || (C::CONV && !C::POOL && !C::RES && C::CO % 16 == 0 &&
                         C::KW * C::CO == C::N), "KPACK geometry");
   static_assert(STAGE % 1024 == 0, "stage alignment");
+  // EPI_TMA: the epilogue writes the tile into 64B-swizzled shared-memory
+  // boxes of 32 rows x 16 columns (the layout a lane = row thread writes
+  // without bank conflicts) and stores them with TMA; a residual operand is
+  // prefetched into the same boxes by TMA before the accumulator is ready.
+  static constexpr bool ET = C::EPI_TMA != 0;
+  static constexpr int EGRP = EPI_COLS / 16;                       // 16-column groups per warp
+  static constexpr int NBUF = ET ? (C::RES ? EGRP : (EGRP < 2 ? EGRP : 2)) : 1;
+  static_assert(!ET || !(C::POOL || C::UPF > 1 || KP), "TMA epilogue: plain row tiles only");
+  static_assert(!(C::RES && C::UPF > 1), "residual fusion excludes upsampling (planner)");
+  static constexpr int EPI_STAGE = EPI_WARPS * NBUF * 2048;       // 32 x 16 fp32 per buffer
+  static constexpr int SMEM = C::NS * STAGE + EPI_STAGE + 1024 /*align*/ + 512 /*barriers*/;
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
                              const TmaDesc* tmA, const TmaDesc* tmB, const TmaDesc* tmBlo,
-                             const TmaDesc* tmA1) {
+                             const TmaDesc* tmA1, const TmaDesc* tmO, const TmaDesc* tmR) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + 1023) & ~(u64)1023);
-    u64* bars = reinterpret_cast<u64*>(smem + C::NS * STAGE);
+    float4* epi_stage = reinterpret_cast<float4*>(smem + C::NS * STAGE);
+    u64* bars = reinterpret_cast<u64*>(smem + C::NS * STAGE + EPI_STAGE);
     u64* full = bars;                 // [NS]  TMA landed
     u64* lo_ready = bars + C::NS;     // [NS]  A split done (64 converter arrivals)
     u64* empty = bars + 2 * C::NS;    // [NS]  MMA finished reading the stage
     u64* tfull = bars + 3 * C::NS;    // [ABUF] accumulator ready
     u64* tempty = tfull + ABUF;       // [ABUF] accumulator drained (epilogue arrivals)
-    u32* tmem_slot = reinterpret_cast<u32*>(tempty + ABUF);
-    float4* epi_stage = reinterpret_cast<float4*>(smem + C::NS * STAGE + 256);
+    u64* rbar = tempty + ABUF;        // [EPI_WARPS] residual boxes landed (EPI_TMA)
+    u32* tmem_slot = reinterpret_cast<u32*>(rbar + EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
@@ -319,6 +394,7 @@ struct GemmTc {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], EPI_THREADS);
       }
+      for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -342,8 +418,8 @@ struct GemmTc {
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
-            mbar_expect_tx(&full[s], NNB_TC_DBG == 2 ? 0 : (AL ? 0 : A_BYTES) + 2 * B_BYTES);
-            if (NNB_TC_DBG == 2) {
+            mbar_expect_tx(&full[s], (NNB_TC_DBG & 2) ? 0 : (AL ? 0 : A_BYTES) + 2 * B_BYTES);
+            if (NNB_TC_DBG & 2) {
               // diagnostic: no operand traffic
             } else if (AL) {
               // A is gathered by the loader warps
@@ -360,7 +436,7 @@ struct GemmTc {
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
             }
-            if (NNB_TC_DBG != 2) {
+            if (!(NNB_TC_DBG & 2)) {
               tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, nb * C::BN);
               tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
             }
@@ -392,20 +468,21 @@ struct GemmTc {
             const u32 b_hi = base + A_SMEM, b_lo = b_hi + B_BYTES;
             const u32 ta = tmem + A_TCOL + s * 2 * BK;                // TMEM A slot
 #pragma unroll
-            for (int k = 0; k < (NNB_TC_DBG == 1 ? 0 : BK / 8); ++k) {
+            for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
               const int ks = kc * (BK / 8) + k;                  // k-step within the chunk
-              const u32 d = dbuf + (ks % NACC) * 2 * C::BN;      // this step's chain
+              const u32 d = dbuf + (ks % NACC) * CW;             // this step's chain
+              const u32 dc = CS ? d + C::BN : d;                 // its correction columns
               const u32 accum = ks >= NACC;
+              const u32 acc_c = CS ? accum : 1u;
               if (TA) {
                 mma_tf32_ts(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
-                mma_tf32_ts(d + C::BN, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, accum);
-                mma_tf32_ts(d + C::BN, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+                mma_tf32_ts(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
+                mma_tf32_ts(dc, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               } else {
                 mma_tf32(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
-                mma_tf32(d + C::BN, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC,
-                         accum);
-                mma_tf32(d + C::BN, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+                mma_tf32(dc, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
+                mma_tf32(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               }
             }
             mma_commit(&empty[s]);
@@ -426,24 +503,33 @@ struct GemmTc {
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
-          const unsigned char* row = smem + s * STAGE + r * ROWB;
-          u32 hi[BK], lo[BK];
-#pragma unroll
-          for (int j = 0; j < BK / 4; ++j) {          // 16-byte chunk j of the swizzled row
-            // SW128: chunk ^= row & 7; SW64: chunk ^= (row >> 1) & 3
-            const int pj = ROWB == 128 ? (j ^ (r & 7)) : (j ^ ((r >> 1) & 3));
-            const float4 v = *reinterpret_cast<const float4*>(row + (pj << 4));
-            const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const u32 h = __float_as_uint(e[i]) & 0xFFFFE000u;
-              hi[4 * j + i] = h;
-              lo[4 * j + i] = __float_as_uint(e[i] - __uint_as_float(h));
-            }
+          if (NNB_TC_DBG & 4) {
+            mbar_arrive(&lo_ready[s]);
+            if (++s == C::NS) { s = 0; ph ^= 1; }
+            continue;
           }
+          const unsigned char* row = smem + s * STAGE + r * ROWB;
           const u32 ta = tmem + ((u32)(q * 32) << 16) + A_TCOL + s * 2 * BK;
-          tmem_st<BK>(ta, hi);
-          tmem_st<BK>(ta + BK, lo);
+#pragma unroll
+          for (int hh = 0; hh < BK / 16; ++hh) {      // 16 columns at a time (registers)
+            u32 hi[16], lo[16];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {          // 16-byte chunk j of the swizzled row
+              const int j = hh * 4 + jj;
+              // SW128: chunk ^= row & 7; SW64: chunk ^= (row >> 1) & 3
+              const int pj = ROWB == 128 ? (j ^ (r & 7)) : (j ^ ((r >> 1) & 3));
+              const float4 v = *reinterpret_cast<const float4*>(row + (pj << 4));
+              const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const u32 h = split_hi(e[i]);
+                hi[4 * jj + i] = h;
+                lo[4 * jj + i] = __float_as_uint(e[i] - __uint_as_float(h));
+              }
+            }
+            tmem_st<16>(ta + hh * 16, hi);
+            tmem_st<16>(ta + BK + hh * 16, lo);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           mbar_arrive(&lo_ready[s]);
@@ -560,10 +646,36 @@ struct GemmTc {
       const float* ps = at<float>(pool, C::PS_OFF);
       const float* po = at<float>(pool, C::PO_OFF);
       float* out = at<float>(arena, C::OUT_OFF);
+      const int ew = warp - EPI_W0;
+      float4* ebuf = epi_stage + ew * NBUF * 128;      // this warp's 2 KB boxes
       int acc = 0;
-      u32 aph = 0;
+      u32 aph = 0, rph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int mb = t / NTN, nb = t % NTN;
+        // TMA box (32 rows of this warp x 16 columns from `col`) load / store
+        auto box_io = [&](bool load, float4* b, int col) {
+          if (C::CONV) {       // rows = 2 image rows x 16 pixels of the 8 x 16 tile
+            const int img = mb / TPI, tt = mb % TPI;
+            const int x = (tt % TX) * TW, y = (tt / TX) * TH + 2 * q;
+            if (load) tma_load_4d(b, tmR, &rbar[ew], col, x, y, img);
+            else tma_store_4d(tmO, b, col, x, y, img);
+          } else {
+            if (load) tma_load_2d(b, tmR, &rbar[ew], col, mb * BM + q * 32);
+            else tma_store_2d(tmO, b, col, mb * BM + q * 32);
+          }
+        };
+        int ngrp = 0;                                   // live 16-column groups (warp-uniform)
+#pragma unroll
+        for (int g = 0; g < EGRP; ++g)
+          ngrp += (cbeg + g * 16 < C::BN && nb * C::BN + cbeg + g * 16 < C::N) ? 1 : 0;
+        if constexpr (ET && C::RES) {
+          // prefetch the residual boxes; they land while the MMAs run
+          if (lane == 0 && ngrp > 0) {
+            bulk_wait_read<0>();                        // last tile's stores have read them
+            mbar_expect_tx(&rbar[ew], ngrp * 2048);
+            for (int g = 0; g < ngrp; ++g) box_io(true, ebuf + g * 128, nb * C::BN + cbeg + g * 16);
+          }
+        }
         if constexpr (KP) {
           // ---- packed horizontal taps: reduce chunks, combine across lanes ----
           constexpr int GCO = C::CO / 2;                 // output channels per warp group
@@ -584,10 +696,12 @@ struct GemmTc {
 #pragma unroll
               for (int kx = 0; kx < C::KW; ++kx) {
                 float v[GCO], cr[GCO];
-                const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * 2 * C::BN +
+                const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * CW +
                                kx * C::CO + g * GCO;
                 tmem_ld<GCO>(ta, v);
-                tmem_ld<GCO>(ta + C::BN, cr);
+#pragma unroll
+                for (int i = 0; i < GCO; ++i) cr[i] = 0.f;
+                if (CS) tmem_ld<GCO>(ta + C::BN, cr);
 #pragma unroll
                 for (int i = 0; i < GCO; ++i) run[kx][i] += v[i] + cr[i];
               }
@@ -612,7 +726,7 @@ struct GemmTc {
 #pragma unroll
             for (int kx = 1; kx < C::KW; ++kx) sacc += __shfl_down_sync(0xffffffffu, run[kx][i], kx);
             const int col = g * GCO + i;
-            y[i] = finish<C::ACT, C::MODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
+            y[i] = finish<C::ACT, EMODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
           }
 #pragma unroll
           for (int h = 0; h < (GCO + 15) / 16; ++h) {
@@ -646,19 +760,34 @@ struct GemmTc {
           tc_fence_after();
           // chains written in this chunk (a short last chunk may not reach all)
           const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * (BK / 8);
+          // batches of GB 16-column groups: all their loads in flight, one wait
+          // (32 loaded registers per batch: the 64-column running sums stay in
+          // registers next to them)
+          constexpr int GB = (EPI_COLS / 16 >= 2 && !CS) ? 2 : 1;
 #pragma unroll
-          for (int g = 0; g < EPI_COLS / 16; ++g) {
-            if (cbeg + g * 16 < C::BN) {             // warp-uniform
+          for (int g0 = 0; g0 < ((NNB_TC_DBG & 8) ? 0 : EPI_COLS / 16); g0 += GB) {
+            if (cbeg + g0 * 16 < C::BN) {            // warp-uniform (whole batch valid)
 #pragma unroll
               for (int c = 0; c < NACC; ++c) {
                 if (c >= ksteps) break;
-                float v[16], cr[16];
-                const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * 2 * C::BN +
-                               cbeg + g * 16;
-                tmem_ld16(ta, v);
-                tmem_ld16(ta + C::BN, cr);
+                u32 rv[GB][16], rc[GB][16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) run[g * 16 + i] += v[i] + cr[i];
+                for (int b = 0; b < GB; ++b) {
+                  const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * CW +
+                                 cbeg + (g0 + b) * 16;
+                  tmem_ld16_async(ta, rv[b]);
+                  if (CS) tmem_ld16_async(ta + C::BN, rc[b]);
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int b = 0; b < GB; ++b) {
+                  tmem_pin(rv[b]);
+                  if (CS) tmem_pin(rc[b]);
+#pragma unroll
+                  for (int i = 0; i < 16; ++i)
+                    run[(g0 + b) * 16 + i] += CS ? __uint_as_float(rv[b][i]) + __uint_as_float(rc[b][i])
+                                                 : __uint_as_float(rv[b][i]);
+                }
               }
             }
           }
@@ -666,6 +795,7 @@ struct GemmTc {
           mbar_arrive(&tempty[acc]);
           if (++acc == ABUF) { acc = 0; aph ^= 1; }
         }
+        if (NNB_TC_DBG & 16) continue;
         // output position of tile row rr: element offset of its first channel
         auto rowpos = [&](int rr, long long& obase) {
           bool live;
@@ -706,14 +836,39 @@ struct GemmTc {
           for (int i = 0; i < 16; ++i) {
             const int col = col0 + i < C::N ? col0 + i : C::N - 1;
             float y = v[i] + __ldg(bias + col);
-            y = finish<C::ACT, C::MODE, C::POST>(y, ps, po, col);
+            y = finish<C::ACT, EMODE, C::POST>(y, ps, po, col);
             if (C::POOL) {     // lanes w, w^1 (same image row), w^16 (next row)
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 16));
             }
             v[i] = y;
           }
-          if constexpr (C::N % 16 == 0 && C::EPI_ST) {
+          if constexpr (ET) {
+            float4* b = ebuf + (g % NBUF) * 128;
+            if (C::RES) {
+              if (g == 0) mbar_wait(&rbar[ew], rph);
+            } else {
+              if (lane == 0) bulk_wait_read<NBUF - 1>();  // the box's previous store has read it
+              __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int sl = stage_slot<16>(lane, j);
+              float4 x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              if (C::RES) {
+                const float4 rv = b[sl];
+                x.x = add(x.x, rv.x); x.y = add(x.y, rv.y);
+                x.z = add(x.z, rv.z); x.w = add(x.w, rv.w);
+              }
+              b[sl] = x;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              box_io(false, b, col0);
+              bulk_commit();
+            }
+          } else if constexpr (C::N % 16 == 0 && C::EPI_ST) {
             // coalesced: 8 lanes per row segment of 16 columns (residual too)
             float4* st = epi_stage + (warp - EPI_W0) * 128;
             stage_rows<16>(st, v, lane);
@@ -761,7 +916,9 @@ struct GemmTc {
             }
           }
         }
+        if (C::RES && ngrp > 0) rph ^= 1;
       }
+      if (ET && lane == 0) bulk_wait_all();        // boxes stay valid until stored
     }
     tc_fence_before();
     __syncthreads();

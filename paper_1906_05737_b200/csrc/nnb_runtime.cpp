@@ -316,7 +316,7 @@ nnb_status enqueue(nnb_net *net, int n, CUstream s) {
     CUdeviceptr pool = net->pool, arena = net->arena;
     int nn = n;
     size_t li = &l - net->launches.data();
-    void *args[7] = {&pool, &arena, &nn, nullptr, nullptr, nullptr, nullptr};
+    void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
     for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
     if (net->pdl) {
       // programmatic dependent launch: the next kernel's CTAs are scheduled while
@@ -494,7 +494,7 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   net->maps.resize(net->launches.size());
   for (size_t i = 0; i < net->launches.size(); ++i) {
     const nnb_launch &l = net->launches[i];
-    if (l.n_tmaps > 4) { fail(NNB_ERR_ARGUMENT, "launch %zu: too many tensor maps", i); return bail(NNB_ERR_ARGUMENT); }
+    if (l.n_tmaps != 0 && l.n_tmaps != NNB_MAX_TMAPS) { fail(NNB_ERR_ARGUMENT, "launch %zu: n_tmaps must be 0 or %d", i, NNB_MAX_TMAPS); return bail(NNB_ERR_ARGUMENT); }
     net->maps[i].resize(l.n_tmaps);
     for (uint32_t k = 0; k < l.n_tmaps; ++k) {
       const nnb_tmap &t = l.tmaps[k];
@@ -613,7 +613,7 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
   if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
   CUdeviceptr pool = net->pool, arena = net->arena;
   int nn = n;
-  void *args[7] = {&pool, &arena, &nn, nullptr, nullptr, nullptr, nullptr};
+  void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
   for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[index][k];
   CU_CHECK(C->p_cuEventRecord(net->ev0, s));
   for (int i = 0; i < iters; ++i)

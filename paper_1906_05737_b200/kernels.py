@@ -35,6 +35,8 @@ SMALL_M = 8           # Dense rows at or below this use the split-K GEMV kernel
 TC_MIN_K = 32         # tensor-core GEMM eligibility (contraction and output width)
 TC_MIN_N = 32
 TC_MIN_ROWS = 2048    # GEMM rows per launch from which the tcgen05 kernel is used
+SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
+MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS)
 ELEM_BLOCK = 256
 
 
@@ -106,10 +108,14 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True):
+                 kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
+        self.epi_tma = epi_tma
+        self.csplit = csplit
+        self.split_rn = split_rn
+        self.chunk = chunk
         self.nacc = nacc
         self.tmem_a = tmem_a
         self.tc_min_rows = tc_min_rows
@@ -140,12 +146,12 @@ class Specializer:
         if tmaps:
             body += (f"\nextern \"C\" __global__ void __launch_bounds__({block}, 1) {kname}("
                      f"const float* __restrict__ pool, float* __restrict__ arena, int n, "
-                     f"const __grid_constant__ nnb::TmaDesc tm0, "
-                     f"const __grid_constant__ nnb::TmaDesc tm1, "
-                     f"const __grid_constant__ nnb::TmaDesc tm2, "
-                     f"const __grid_constant__ nnb::TmaDesc tm3) {{\n"
+                     + ", ".join(f"const __grid_constant__ nnb::TmaDesc tm{k}"
+                                 for k in range(MAX_TMAPS)) + ") {\n"
                      f"  NNB_PDL_PROLOGUE\n"
-                     f"  {template}<{cfg}>::run(pool, arena, n, &tm0, &tm1, &tm2, &tm3);\n}}\n")
+                     f"  {template}<{cfg}>::run(pool, arena, n, "
+                     + ", ".join(f"&tm{k}" for k in range(MAX_TMAPS)) + ");\n}\n")
+            tmaps = list(tmaps) + [tmaps[0]] * (MAX_TMAPS - len(tmaps))
             self.chunks.append(body)
             self.names.append(kname)
             self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min, n_max,
@@ -281,36 +287,51 @@ class Specializer:
             TM = 4
         NT = 128
         BN = TN * NTX
-        BM = TM * (NT // NTX)
-        if K <= 16:
-            BK = _pad4(K)
-        else:
-            BK = 8 if BM >= 256 else 16
-        avec = CI % 4 == 0 and C0 % 4 == 0 and BK % 4 == 0
-        akv = 4 if avec else 1
-        while (BM * BK) % (akv * NT):
-            BK += 4 if avec else 1
         ntile_n = (CO + BN - 1) // BN
-        smem = 4 * (2 * BK * (BM + 4) + 2 * BK * (BN + 4))
-
         wo = self.pool.add(wmat)
         bo = self.pool.add(u.bias)
-        fields = dict(
-            H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
-            K=K, ROWS=rows, POOL=pool_fused, PHO=PHO, PWO=PWO,
-            IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
-            OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
-            W_OFF=wo, B_OFF=bo,
-            RES=u.residual_id is not None,
-            RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
-            RES_FIRST=False,
-            SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
-            BM=BM, BN=BN, BK=BK, TM=TM, TN=TN, **src1)
-        fields.update(self.epilogue_fields(u, CO))
-        tag = "dense" if u.kind == "Dense" else f"conv{KH}x{KW}"
-        self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
-                  grid_mult=ntile_n, n_min=n_min, n_max=n_max, dynamic_smem=True,
-                  note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
+
+        def simt(TM, lo, hi):
+            BM = TM * (NT // NTX)
+            if K <= 16:
+                BK = _pad4(K)
+            else:
+                BK = 8 if BM >= 256 else 16
+            avec = CI % 4 == 0 and C0 % 4 == 0 and BK % 4 == 0
+            akv = 4 if avec else 1
+            while (BM * BK) % (akv * NT):
+                BK += 4 if avec else 1
+            smem = 4 * (2 * BK * (BM + 4) + 2 * BK * (BN + 4))
+            fields = dict(
+                H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
+                K=K, ROWS=rows, POOL=pool_fused, PHO=PHO, PWO=PWO,
+                IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                W_OFF=wo, B_OFF=bo,
+                RES=u.residual_id is not None,
+                RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
+                RES_FIRST=False,
+                SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp],
+                BM=BM, BN=BN, BK=BK, TM=TM, TN=TN, **src1)
+            fields.update(self.epilogue_fields(u, CO))
+            tag = "dense" if u.kind == "Dense" else f"conv{KH}x{KW}"
+            self.emit(pos, tag, "nnb::GemmSimt", fields, NT, smem, rows, BM,
+                      grid_mult=ntile_n, n_min=lo, n_max=hi, dynamic_smem=True,
+                      note=f"gemm M=n*{rows} N={CO} K={K} tile {BM}x{BN}x{BK}")
+
+        # batches whose grid would not fill two waves of SMs with this tile get
+        # a short-tile variant (TM = 1, or 4 under a fused pool): more CTAs
+        TM_small = 4 if pool_fused else 1
+        target = 2 * self.sm_count
+        bm_big = TM * (NT // NTX)
+        n_split = -(-target * bm_big // (rows * ntile_n))    # first n with >= target CTAs
+        hi = min(n_max, self.max_batch)
+        if TM > TM_small and n_split > n_min:
+            simt(TM_small, n_min, min(n_split - 1, n_max))
+            if n_split <= hi:
+                simt(TM, n_split, n_max)
+        else:
+            simt(TM, n_min, n_max)
 
     def _dw_fields(self, u):
         """Fields of a fused depthwise producer (GemmSimt DW loader)."""
@@ -355,15 +376,35 @@ class Specializer:
         NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
         aldg = self.aldg
         tmem_a = self.tmem_a and NACC == 1 and not aldg and (BN <= 64 or BN == 128)
-        ABUF = 1 if (tmem_a and BN > 64) else 2
+        csplit = self.csplit
+        # k-blocks (of 32) per TMEM accumulator chunk: every chunk ends in a
+        # drain the MMAs wait for (one accumulator buffer at BN = 128), so
+        # long chunks are faster; the tensor core truncates once per MMA, so
+        # short chunks are more accurate.  Measured (scripts/tc_error.py,
+        # max |d| / (atol + rtol |ref|)): K=1024: 0.39 / 0.50 / 0.80 at 8 / 16
+        # / 32; K=4096: 0.77 / 0.83 / 0.89.  dense 1024->512: 0.40 / 0.34 /
+        # 0.32 ms at 65536 rows.
+        chunk = self.chunk or (16 if K <= 1024 else 8)
+        cw = (2 if csplit else 1) * BN                # TMEM columns per accumulator chain
+        ABUF = 1 if (tmem_a and BN > 64 and csplit) else 2
         stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * BN * BK * 4
+        # epilogue through TMA stores (and a TMA-prefetched residual) for plain
+        # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
+        res = u.residual_id is not None
+        egrp = max(1, (BN // 2 if BN >= 32 else 16) // 16)
+        epi_tma = bool(self.epi_tma and not kpack and CO % 4 == 0 and (not res or egrp <= 2)
+                       and not (conv and conv["POOL"])
+                       and (conv or not rows_geo or rows_geo.get("UPF", 1) == 1)
+                       and (not conv or conv.get("UPF", 1) == 1))
+        nbuf = (egrp if res else min(egrp, 2)) if epi_tma else 1
+        epi_bytes = 8 * nbuf * 2048
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
-        NS = max(2, min(8, (200 * 1024) // stage))
+        NS = max(2, min(8, (SMEM_MAX - 1024 - 512 - epi_bytes) // stage))
         if tmem_a:
-            NS = min(NS, (512 - ABUF * 2 * NACC * BN) // (2 * BK))
+            NS = min(NS, (512 - ABUF * NACC * cw) // (2 * BK))
         wt = np.zeros((NPAD, KPAD), F32)
         wt[:CO, :K] = np.asarray(wmat, F32).T
-        hi = (wt.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32)
+        hi = tf32_split_hi(wt, self.split_rn)
         lo = (wt - hi).astype(F32)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
@@ -374,12 +415,13 @@ class Specializer:
             geo.update(rows_geo)
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
-                      NACC=NACC, ALDG=aldg, ABUF=ABUF,
+                      NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
                       # their mainloop is shared-memory bound and the extra
                       # staging traffic cost 9% at K=1024 (equal at K=512)
-                      EPI_ST=int(u.residual_id is not None or K < 512),
+                      EPI_ST=int(u.residual_id is not None or K < 512 or self.epi_tma == "staged"),
+                      EPI_TMA=int(epi_tma),
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),
                       IN1_OFF=(self.arena_off(u.input_ids[1]) if conv and conv["CONCAT"] else 0),
@@ -400,14 +442,25 @@ class Specializer:
             tm_a = act_map(u.input_ids[0], conv["C0"])
             tm_a1 = (act_map(u.input_ids[1], conv["CI"] - conv["C0"]) if conv["CONCAT"]
                      else tm_a)
+
+            def out_map(tid):      # epilogue boxes: 16 channels x 16 px x 2 rows
+                return dict(space=1, offset=self.arena_off(tid), dims=(CO, conv["WO"], conv["HO"], self.cap),
+                            box=(16, 16, 2, 1), strides=(4 * CO, 4 * CO * conv["WO"],
+                                                         self.img_bytes(tid)), swizzle=2)
         else:
             tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
                         dims=(K, self.cap * rows), strides=(4 * K,), box=(32, 128))
             tm_a1 = tm_a
+
+            def out_map(tid):      # epilogue boxes: 16 columns x 32 rows
+                return dict(space=1, offset=self.arena_off(tid), dims=(CO, self.cap * rows),
+                            strides=(4 * CO,), box=(16, 32), swizzle=2)
         tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
                     box=(BK, BN), swizzle=sw)
         tm_bl = dict(tm_b, offset=lo_off)
-        smem = NS * stage + 1024 + 256 + 8 * 32 * 16 * 4   # + epilogue staging
+        tm_o = out_map(u.output_id) if epi_tma else tm_a
+        tm_r = out_map(u.residual_id) if (epi_tma and res) else tm_o
+        smem = NS * stage + epi_bytes + 1024 + 512
         ntn = NPAD // BN
         if conv:
             ow = 16 - (kw - 1) if kpack else 16
@@ -420,11 +473,12 @@ class Specializer:
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn,
-                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1], grid_cap=self.sm_count,
+                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], grid_cap=self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x{BK} stages {NS}"
-                       f" chains {NACC}{' A via cp.async' if aldg else ''}"
+                       f" chains {NACC} bufs {ABUF}{'' if csplit else ' merged-corr'}"
+                       f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
-                       f"{' A in TMEM' if tmem_a else ''}")
+                       f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
                      PHO, PWO, UPF=1):
@@ -636,7 +690,21 @@ class Specializer:
                               kernel_source=ks)
 
 
+def tf32_split_hi(w, rn=True):
+    """TF32 'hi' part of a float32 array: rounded to the nearest TF32 (11
+    significant bits) when ``rn``, else truncated; ``w - hi`` is exact."""
+    u = np.ascontiguousarray(w, F32).view(np.uint32)
+    t = u & np.uint32(0xFFFFE000)
+    if rn:
+        r = (u + np.uint32(0x1000)) & np.uint32(0xFFFFE000)
+        ok = np.isfinite(r.view(F32))
+        t = np.where(ok, r, t)
+    return t.view(F32)
+
+
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
-               tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True):
+               tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
+               epi_tma=True, csplit=True, chunk=None, split_rn=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
-                       tc_min_rows, tmem_a, nacc, aldg, kpack).run()
+                       tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
+                       split_rn).run()

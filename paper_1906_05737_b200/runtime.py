@@ -80,7 +80,8 @@ class _Handle:
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
-                 nacc=None, aldg=False, kpack=True, dw_fusion=False):
+                 nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
+                 split_rn=True):
         import torch
 
         t0 = time.perf_counter()
@@ -100,7 +101,8 @@ class CompiledNetwork:
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
                           use_tc=use_tc, sm_count=sm_count,
                           tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
-                          tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack)
+                          tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack, epi_tma=epi_tma,
+                          csplit=csplit, chunk=chunk, split_rn=split_rn)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):
@@ -116,7 +118,7 @@ class CompiledNetwork:
         launches = (_native.Launch * max(len(spec.launches), 1))()
         index = {n: i for i, n in enumerate(spec.kernel_names)}
         for i, l in enumerate(spec.launches):
-            tm = (_native.TMap * 4)()
+            tm = (_native.TMap * _native.MAX_TMAPS)()
             for k, t in enumerate(l.tmaps):
                 tm[k] = _native.make_tmap(t)
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,
