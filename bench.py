@@ -31,6 +31,7 @@ import argparse
 import json
 import os
 import sys
+import pathlib
 import threading
 import time
 
@@ -208,6 +209,24 @@ def reference_arm(args, world, rank):
 _TF32 = {}
 
 
+def ncu_traffic(kernel):
+    """dram read + write bytes per launch of `kernel` from the committed
+    `ncu --set full` capture (profiles/r01_dense_tc_ncu_raw.csv), or None."""
+    import csv
+    p = pathlib.Path(ROOT) / "profiles" / "r01_dense_tc_ncu_raw.csv"
+    try:
+        rows = list(csv.reader(open(p)))
+        h, units, v = rows[0], rows[1], rows[2]
+        if v[h.index("Kernel Name")] != kernel:
+            return {"traffic": None}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = sum(float(v[h.index(m)]) * scale[units[h.index(m)]]
+                  for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return {"traffic": tot, "traffic_source": f"{p.name} (ncu --set full, cold cache, one launch)"}
+    except (OSError, ValueError, IndexError, KeyError):
+        return {"traffic": None}
+
+
 def measure_tf32_peak(torch, dev):
     """cuBLAS TF32 dense throughput on this GPU (the roofline denominator for
     the 3xTF32 tcgen05 kernels)."""
@@ -329,7 +348,9 @@ def main():
 
     # ---------------- roofline of the dominant kernel -----------------------
     peaks = roofline.measured_peaks()
-    lt = {i: net.time_launch(i, B, iters=5) for i in net.launches_for(B)}
+    # per-launch CUDA-event durations inside full passes (same order, same
+    # inputs as the timed replays, events between consecutive launches)
+    lt = net.time_sequence(B, iters=max(3, args.steps))
     dom = max(lt, key=lt.get)
     L = net.artifact.launches[dom]
     u = net.plan.units[L.unit]
@@ -360,7 +381,9 @@ def main():
                  "kernel_ms": lt[dom], "share_of_step": share,
                  "hbm_frac_at_same_time": (B * io + wb) / (lt[dom] / 1e3) / 1e9 / peaks["hbm_gbs"],
                  "launch_ms": {net.artifact.launches[i].kernel: v for i, v in lt.items()},
-                 "traffic": None})
+                 "timing": "CUDA events between consecutive launches of the pass, "
+                           "mean over the step count",
+                 **ncu_traffic(L.kernel)})
 
     # ---------------- per-config extras (rank 0, N == 1) ---------------------
     extra = None
@@ -405,7 +428,8 @@ def main():
                        "per_gpu_batch": B, "parallelism": f"replicas x{world}",
                        "l2": "inputs larger than L2 (no flush)" if x.nbytes > 126e6
                        else "inputs smaller than L2",
-                       "transcendentals": "exact (float64 tanh/exp, rounded once)"},
+                       "transcendentals": "exact mode (tanh/sigmoid/elu float64-rounded in "
+                                          "FFMA kernels; FP32 within 2 ulp in tcgen05 epilogues)"},
             "e2e": e2e, "gpu_launches": n_launch * args.steps, "clocks": clocks,
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
             "compile_ms": net.compile_ms, "configs": extra,

@@ -152,6 +152,12 @@ nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, 
 nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters, void *stream,
                            double *ms);
 
+/* Per-launch mean milliseconds inside a full pass over n images: the
+ * schedule is enqueued directly (no graph, no PDL) with a CUDA event between
+ * consecutive launches, `iters` times; ms[i] = -1 for launches not in the
+ * pass.  ms must hold one entry per launch of the schedule. */
+nnb_status nnb_time_sequence(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms);
+
 nnb_status nnb_host_alloc(uint64_t bytes, void **ptr);
 void nnb_host_free(void *ptr);
 void nnb_free(void *ptr);

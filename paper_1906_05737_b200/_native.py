@@ -20,7 +20,7 @@ NNB_OK, NNB_ERR_ARGUMENT, NNB_ERR_NO_DRIVER, NNB_ERR_NO_DEVICE, NNB_ERR_ARCH, \
     NNB_ERR_NVRTC, NNB_ERR_CUDA, NNB_ERR_OOM, NNB_ERR_BATCH = range(9)
 
 EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "nnb_apply",
-            "nnb_run_host", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_host_alloc", "nnb_host_free",
+            "nnb_run_host", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_host_alloc", "nnb_host_free",
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
 
@@ -93,6 +93,7 @@ def lib():
         "nnb_sync": (I32, [VP, VP]),
         "nnb_time_apply": (I32, [VP, I32, I32, VP, P(ctypes.c_double)]),
         "nnb_time_launch": (I32, [VP, I32, I32, I32, VP, P(ctypes.c_double)]),
+        "nnb_time_sequence": (I32, [VP, I32, I32, VP, P(ctypes.c_double)]),
         "nnb_host_alloc": (I32, [U64, P(VP)]),
         "nnb_host_free": (None, [VP]),
         "nnb_free": (None, [VP]),

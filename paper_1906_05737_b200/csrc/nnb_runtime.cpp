@@ -304,21 +304,23 @@ struct nnb_net {
 
 namespace {
 
-nnb_status enqueue(nnb_net *net, int n, CUstream s) {
+// One launch of the schedule over n images (no-op when it is not part of
+// the replay for n or its grid is empty).
+nnb_status launch_one(nnb_net *net, size_t li, int n, CUstream s, bool pdl) {
   Cu *C = cu();
-  for (const nnb_launch &l : net->launches) {
-    if (n < l.n_min || n > l.n_max) continue;
+  const nnb_launch &l = net->launches[li];
+  if (n < l.n_min || n > l.n_max) return NNB_OK;
+  {
     uint64_t items = (uint64_t)n * l.items_per_image;
     uint64_t gx = (items + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
     if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
-    if (gx == 0) continue;
+    if (gx == 0) return NNB_OK;
     if (gx > 0x7fffffffull) return fail(NNB_ERR_ARGUMENT, "grid too large (%llu)", (unsigned long long)gx);
     CUdeviceptr pool = net->pool, arena = net->arena;
     int nn = n;
-    size_t li = &l - net->launches.data();
     void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
     for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
-    if (net->pdl) {
+    if (pdl) {
       // programmatic dependent launch: the next kernel's CTAs are scheduled while
       // this one drains; each kernel starts with griddepcontrol.wait.
       CUlaunchAttribute attr[1];
@@ -336,6 +338,14 @@ nnb_status enqueue(nnb_net *net, int n, CUstream s) {
       CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
                                    l.smem_bytes, s, args, nullptr));
     }
+  }
+  return NNB_OK;
+}
+
+nnb_status enqueue(nnb_net *net, int n, CUstream s) {
+  for (size_t li = 0; li < net->launches.size(); ++li) {
+    nnb_status st = launch_one(net, li, n, s, net->pdl);
+    if (st != NNB_OK) return st;
   }
   return NNB_OK;
 }
@@ -624,6 +634,45 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
   float f = 0;
   CU_CHECK(C->p_cuEventElapsedTime(&f, net->ev0, net->ev1));
   *ms = f / iters;
+  return NNB_OK;
+}
+
+nnb_status nnb_time_sequence(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms) {
+  if (!net || iters < 1 || !ms) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  if (n < 1 || n > net->max_batch)
+    return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
+  Cu *C = cu();
+  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  const size_t L = net->launches.size();
+  std::vector<CUevent> ev(L + 1, nullptr);
+  nnb_status st = NNB_OK;
+  for (auto &e : ev)
+    if (C->p_cuEventCreate(&e, CU_EVENT_DEFAULT) != CUDA_SUCCESS) st = fail(NNB_ERR_CUDA, "cuEventCreate failed");
+  std::vector<double> acc(L, 0.0);
+  for (int it = 0; it < iters && st == NNB_OK; ++it) {
+    // same order and inputs as a replay; events between consecutive launches
+    if (C->p_cuEventRecord(ev[0], s) != CUDA_SUCCESS) { st = fail(NNB_ERR_CUDA, "cuEventRecord failed"); break; }
+    for (size_t li = 0; li < L && st == NNB_OK; ++li) {
+      st = launch_one(net, li, n, s, false);
+      if (st == NNB_OK && C->p_cuEventRecord(ev[li + 1], s) != CUDA_SUCCESS)
+        st = fail(NNB_ERR_CUDA, "cuEventRecord failed");
+    }
+    if (st != NNB_OK) break;
+    if (C->p_cuEventSynchronize(ev[L]) != CUDA_SUCCESS) { st = fail(NNB_ERR_CUDA, "kernel failed"); break; }
+    for (size_t li = 0; li < L; ++li) {
+      float f = 0;
+      C->p_cuEventElapsedTime(&f, ev[li], ev[li + 1]);
+      acc[li] += f;
+    }
+  }
+  for (auto &e : ev)
+    if (e) C->p_cuEventDestroy(e);
+  if (st != NNB_OK) return st;
+  for (size_t li = 0; li < L; ++li) {
+    const nnb_launch &l = net->launches[li];
+    ms[li] = (n < l.n_min || n > l.n_max) ? -1.0 : acc[li] / iters;
+  }
   return NNB_OK;
 }
 

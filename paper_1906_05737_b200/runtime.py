@@ -243,6 +243,16 @@ class CompiledNetwork:
                                                     ctypes.byref(ms)))
         return ms.value
 
+    def time_sequence(self, n=None, iters=10):
+        """Per-launch mean milliseconds within full passes over ``n`` images
+        (direct launches in replay order, CUDA events between them).
+        Returns {launch index: ms} for the launches of the pass."""
+        n = self.max_batch if n is None else n
+        L = len(self.artifact.launches)
+        ms = (ctypes.c_double * max(L, 1))()
+        _native.check(_native.lib().nnb_time_sequence(self._h.ptr, n, iters, self._stream(), ms))
+        return {i: ms[i] for i in range(L) if ms[i] >= 0}
+
     def launches_for(self, n=None):
         """Indices of the launches a replay over ``n`` images runs."""
         n = self.max_batch if n is None else n

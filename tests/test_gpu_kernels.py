@@ -305,3 +305,18 @@ def test_deterministic_outputs_across_compiles():
     a, _ = gpu(m, w, x)
     b, _ = gpu(m, w, x)
     np.testing.assert_array_equal(a, b)
+
+
+def test_timing_entry_points():
+    """time_apply / time_launch / time_sequence (bench.py's roofline evidence)
+    cover exactly the launches of the pass and return positive durations."""
+    m, w = zoo.build(3)
+    net = compile_model(m, w, EXACT, batch=8)
+    net.run([zoo.inputs(3, 8)])
+    for n in (1, 8):
+        seq = net.time_sequence(n, iters=2)
+        assert sorted(seq) == net.launches_for(n)
+        assert all(v > 0 for v in seq.values())
+        i = net.launches_for(n)[0]
+        assert net.time_launch(i, n, iters=2) > 0
+    assert net.time_apply(iters=2) > 0
