@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define NNB_ABI_VERSION 2
+#define NNB_ABI_VERSION 3
 #define NNB_MAX_TMAPS 6
 
 typedef enum {
@@ -78,6 +78,8 @@ typedef struct {
   uint32_t grid_cap;
   uint32_t n_tmaps;
   nnb_tmap tmaps[NNB_MAX_TMAPS];
+  uint32_t cluster;          /* thread-block cluster size along x (0/1: none);
+                              * the grid is rounded down to a multiple of it */
 } nnb_launch;
 
 /* A network I/O tensor: byte offset in the arena and bytes per image. */

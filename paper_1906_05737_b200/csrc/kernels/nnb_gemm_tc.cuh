@@ -197,6 +197,43 @@ __device__ __forceinline__ void tmem_st(u32 taddr, const u32 (&v)[N]) {
   }
 }
 
+// CTA-pair (cta_group::2) forms: the leader CTA issues M=256 MMAs whose rows
+// 128..255 (and B columns BN/2..BN-1) live in the peer CTA's TMEM / shared
+// memory at the same addresses; commits arrive on the barrier in both CTAs.
+__device__ __forceinline__ void mma_tf32_ts_pair(u32 tmem_d, u32 tmem_a, u64 bdesc, u32 idesc,
+                                                 u32 acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(u64* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ u32 cluster_rank() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same offset in the leader CTA (rank 0)
+__device__ __forceinline__ void mbar_arrive_leader(u64* bar) {
+  u32 r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -283,7 +320,15 @@ struct GemmTc {
   static constexpr int BM = 128, BK = C::BK;                // 32 (SW128) or 16 (SW64)
   static constexpr int ROWB = BK * 4;
   static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = C::BN * BK * 4;
+  // PAIR: CTA pairs (cluster of 2, tcgen05 cta_group::2).  The pair computes a
+  // 256 x BN tile: each CTA loads its own 128 rows of A and HALF of B (BN/2
+  // rows of W^T), the leader issues M=256 MMAs that read both CTAs' operands,
+  // each CTA's TMEM receives its own 128 accumulator rows.  Per SM this halves
+  // the B traffic (TMA writes and tensor-core reads of shared memory), which
+  // is what bounds the single-CTA kernel at BN=128.
+  static constexpr bool PAIR = C::PAIR != 0;
+  static constexpr int B_ROWS = PAIR ? C::BN / 2 : C::BN;   // B rows held per CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 4;
   // TMEM_A: the split A operand lives in tensor memory (MMA "ts" form), so the
   // tensor core reads only B from shared memory -- for narrow N the A re-reads
   // (three products per k-step) otherwise saturate shared-memory bandwidth.
@@ -320,13 +365,14 @@ struct GemmTc {
                                  : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
-                               ((u32)(BM >> 4) << 24);
+                               ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
   // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
   static constexpr bool AL = C::ALDG != 0;
   static_assert(!(AL && TA), "A via LDGSTS lives in shared memory");
+  static_assert(!PAIR || (TA && !C::CONV && C::BN % 32 == 0), "CTA pairs: rows mode, A in TMEM");
   static constexpr int CONV_WARPS = (TA || AL) ? 4 : 2;           // A splitters
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
@@ -382,29 +428,53 @@ struct GemmTc {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
     const int mtiles = C::CONV ? n * TPI : (int)((rows + BM - 1) / BM);
-    const int tiles = mtiles * NTN;
+    // pairs walk 256-row tile pairs: CTA `rank` of the pair takes 128 of them
+    const int rank = PAIR ? (int)cluster_rank() : 0;
+    const int tiles = (PAIR ? (mtiles + 1) / 2 : mtiles) * NTN;
+    const int t0 = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int tstep = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    auto mb_of = [&](int t) { return PAIR ? (t / NTN) * 2 + rank : t / NTN; };
+    // consumer-side arrivals that the (leader's) MMA warp waits for: pairs
+    // count one per warp of both CTAs, single CTAs one per thread
+    auto arrive_mma = [&](u64* bar) {
+      if (PAIR) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive_leader(bar);
+      } else {
+        mbar_arrive(bar);
+      }
+    };
 
     if (threadIdx.x == 0) {
       for (int s = 0; s < C::NS; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&lo_ready[s], 32 * CONV_WARPS);
+        // pairs: one arrival per split warp of both CTAs, on the leader's barrier
+        mbar_init(&lo_ready[s], PAIR ? 2 * CONV_WARPS : 32 * CONV_WARPS);
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < ABUF; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], EPI_THREADS);
+        mbar_init(&tempty[a], PAIR ? 2 * EPI_WARPS : EPI_THREADS);
       }
       for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "r"(TMEM_COLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      if (PAIR) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+      } else {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      }
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();          // the peer's barriers exist before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const u32 tmem = *tmem_slot;
 
@@ -413,8 +483,8 @@ struct GemmTc {
       if (lane == 0) {
         int s = 0;
         u32 ph = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-          const int mb = t / NTN, nb = t % NTN;
+        for (int t = t0; t < tiles; t += tstep) {
+          const int mb = mb_of(t), nb = t % NTN;
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
@@ -437,21 +507,25 @@ struct GemmTc {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
             }
             if (!(NNB_TC_DBG & 2)) {
-              tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, nb * C::BN);
-              tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, nb * C::BN);
+              const int brow = nb * C::BN + rank * B_ROWS;         // this CTA's B rows
+              tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, brow);
+              tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, brow);
             }
             if (++s == C::NS) { s = 0; ph ^= 1; }
           }
         }
       }
     } else if (warp == 1) {
-      // ---------------- MMA issuer ----------------
+      // ---------------- MMA issuer (the leader CTA of a pair) ----------------
+      if (PAIR && rank != 0) {
+        // the peer's MMA warp only owns the TMEM allocation
+      } else {
       // K is consumed in chunks of CHUNK_KB k-blocks; every chunk starts a fresh
       // (main, correction) accumulator pair in the next TMEM buffer and is
       // reduced in FP32 by the epilogue warps (split-K inside the CTA).
       int s = 0, acc = 0;
       u32 ph = 0, aph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t0; t < tiles; t += tstep) {
         for (int kb = 0; kb < KB; ++kb) {
           const int kc = kb % CHUNK_KB;
           if (kc == 0) {
@@ -475,7 +549,11 @@ struct GemmTc {
               const u32 dc = CS ? d + C::BN : d;                 // its correction columns
               const u32 accum = ks >= NACC;
               const u32 acc_c = CS ? accum : 1u;
-              if (TA) {
+              if (PAIR) {
+                mma_tf32_ts_pair(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_tf32_ts_pair(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
+                mma_tf32_ts_pair(dc, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+              } else if (TA) {
                 mma_tf32_ts(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
                 mma_tf32_ts(dc, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
@@ -485,8 +563,13 @@ struct GemmTc {
                 mma_tf32(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               }
             }
-            mma_commit(&empty[s]);
-            if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
+            if (PAIR) {
+              mma_commit_pair(&empty[s]);
+              if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit_pair(&tfull[acc]);
+            } else {
+              mma_commit(&empty[s]);
+              if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
+            }
           }
           __syncwarp();
           if (++s == C::NS) { s = 0; ph ^= 1; }
@@ -495,16 +578,17 @@ struct GemmTc {
           }
         }
       }
+      }
     } else if (warp < EPI_W0 && TA) {
       // ---------------- converter: A row -> (hi, lo) columns in TMEM ----------------
       const int q = warp & 3, r = q * 32 + lane;      // this thread's tile row = TMEM lane
       int s = 0;
       u32 ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t0; t < tiles; t += tstep) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
           if (NNB_TC_DBG & 4) {
-            mbar_arrive(&lo_ready[s]);
+            arrive_mma(&lo_ready[s]);
             if (++s == C::NS) { s = 0; ph ^= 1; }
             continue;
           }
@@ -532,7 +616,7 @@ struct GemmTc {
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
-          mbar_arrive(&lo_ready[s]);
+          arrive_mma(&lo_ready[s]);
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
       }
@@ -617,7 +701,7 @@ struct GemmTc {
       const int ct = threadIdx.x - 64;   // 0..63
       int s = 0;
       u32 ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t0; t < tiles; t += tstep) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
           float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
@@ -650,8 +734,8 @@ struct GemmTc {
       float4* ebuf = epi_stage + ew * NBUF * 128;      // this warp's 2 KB boxes
       int acc = 0;
       u32 aph = 0, rph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mb = t / NTN, nb = t % NTN;
+      for (int t = t0; t < tiles; t += tstep) {
+        const int mb = mb_of(t), nb = t % NTN;
         // TMA box (32 rows of this warp x 16 columns from `col`) load / store
         auto box_io = [&](bool load, float4* b, int col) {
           if (C::CONV) {       // rows = 2 image rows x 16 pixels of the 8 x 16 tile
@@ -707,7 +791,7 @@ struct GemmTc {
               }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            arrive_mma(&tempty[acc]);
             if (++acc == ABUF) { acc = 0; aph ^= 1; }
           }
           const int img = mb / TPI, tt = mb % TPI;
@@ -792,7 +876,7 @@ struct GemmTc {
             }
           }
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          arrive_mma(&tempty[acc]);
           if (++acc == ABUF) { acc = 0; aph ^= 1; }
         }
         if (NNB_TC_DBG & 16) continue;
@@ -921,11 +1005,16 @@ struct GemmTc {
       if (ET && lane == 0) bulk_wait_all();        // boxes stay valid until stored
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();          // neither CTA leaves while its peer may still use it
+    else __syncthreads();
     if (warp == 1) {
       tc_fence_after();
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                   "r"(TMEM_COLS));
+      if (PAIR)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+      else
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
     }
   }
 };

@@ -314,25 +314,39 @@ nnb_status launch_one(nnb_net *net, size_t li, int n, CUstream s, bool pdl) {
     uint64_t items = (uint64_t)n * l.items_per_image;
     uint64_t gx = (items + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
     if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
+    const uint32_t cl = l.cluster > 1 ? l.cluster : 1;
+    if (cl > 1) gx = std::max<uint64_t>(cl, gx / cl * cl);   // whole clusters
     if (gx == 0) return NNB_OK;
     if (gx > 0x7fffffffull) return fail(NNB_ERR_ARGUMENT, "grid too large (%llu)", (unsigned long long)gx);
     CUdeviceptr pool = net->pool, arena = net->arena;
     int nn = n;
     void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
     for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
-    if (pdl) {
+    if (pdl || cl > 1) {
       // programmatic dependent launch: the next kernel's CTAs are scheduled while
       // this one drains; each kernel starts with griddepcontrol.wait.
-      CUlaunchAttribute attr[1];
-      attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
-      attr[0].value.programmaticStreamSerializationAllowed = 1;
+      // Clusters: CTA pairs for the tcgen05 cta_group::2 GEMM.
+      CUlaunchAttribute attr[2];
+      unsigned na = 0;
+      if (pdl) {
+        attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+        attr[na].value.programmaticStreamSerializationAllowed = 1;
+        ++na;
+      }
+      if (cl > 1) {
+        attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attr[na].value.clusterDim.x = cl;
+        attr[na].value.clusterDim.y = 1;
+        attr[na].value.clusterDim.z = 1;
+        ++na;
+      }
       CUlaunchConfig cfg = {};
       cfg.gridDimX = (unsigned)gx; cfg.gridDimY = 1; cfg.gridDimZ = 1;
       cfg.blockDimX = l.block; cfg.blockDimY = 1; cfg.blockDimZ = 1;
       cfg.sharedMemBytes = l.smem_bytes;
       cfg.hStream = s;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = na;
       CU_CHECK(C->p_cuLaunchKernelEx(&cfg, net->fns[l.kernel], args, nullptr));
     } else {
       CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
@@ -618,17 +632,11 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
   Cu *C = cu();
   CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
   CUstream s = reinterpret_cast<CUstream>(stream);
-  const nnb_launch &l = net->launches[index];
-  uint64_t gx = ((uint64_t)n * l.items_per_image + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
-  if (l.grid_cap && gx > l.grid_cap) gx = l.grid_cap;
-  CUdeviceptr pool = net->pool, arena = net->arena;
-  int nn = n;
-  void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
-  for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[index][k];
   CU_CHECK(C->p_cuEventRecord(net->ev0, s));
-  for (int i = 0; i < iters; ++i)
-    CU_CHECK(C->p_cuLaunchKernel(net->fns[l.kernel], (unsigned)gx, 1, 1, l.block, 1, 1,
-                                 l.smem_bytes, s, args, nullptr));
+  for (int i = 0; i < iters; ++i) {
+    nnb_status st = launch_one(net, (size_t)index, n, s, false);
+    if (st != NNB_OK) return st;
+  }
   CU_CHECK(C->p_cuEventRecord(net->ev1, s));
   CU_CHECK(C->p_cuEventSynchronize(net->ev1));
   float f = 0;

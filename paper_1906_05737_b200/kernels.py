@@ -56,6 +56,7 @@ class Launch:
     note: str = ""
     grid_cap: int = 0                 # persistent kernels: at most this many CTAs
     tmaps: list = field(default_factory=list)   # TMA descriptors (see nnb_tmap)
+    cluster: int = 1                  # thread-block cluster size along x (CTA pairs: 2)
 
 
 class DevicePool:
@@ -108,13 +109,15 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True):
+                 kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 pair=True):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
         self.epi_tma = epi_tma
         self.csplit = csplit
         self.split_rn = split_rn
+        self.pair = pair
         self.chunk = chunk
         self.nacc = nacc
         self.tmem_a = tmem_a
@@ -139,7 +142,7 @@ class Specializer:
 
     def emit(self, unit_pos, tag, template, fields, block, smem, ipi, ipb,
              grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note="",
-             tmaps=(), grid_cap=0):
+             tmaps=(), grid_cap=0, cluster=1):
         kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
         cfg = f"Cfg_{len(self.names)}"
         body = _cfg_struct(cfg, fields)
@@ -155,7 +158,7 @@ class Specializer:
             self.chunks.append(body)
             self.names.append(kname)
             self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min, n_max,
-                                        unit_pos, note, grid_cap, list(tmaps)))
+                                        unit_pos, note, grid_cap, list(tmaps), cluster))
             return
         if dynamic_smem:
             call = (f"  extern __shared__ __align__(16) unsigned char nnb_smem[];\n"
@@ -387,7 +390,11 @@ class Specializer:
         chunk = self.chunk or (16 if K <= 1024 else 8)
         cw = (2 if csplit else 1) * BN                # TMEM columns per accumulator chain
         ABUF = 1 if (tmem_a and BN > 64 and csplit) else 2
-        stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * BN * BK * 4
+        # CTA pairs (cta_group::2, 256-row tiles, each CTA holds half of B):
+        # the BN = 128 row GEMMs, whose single-CTA form is bound by
+        # shared-memory bandwidth (B is re-read by every product)
+        pair = bool(self.pair and not conv and tmem_a and BN == 128 and K >= 256)
+        stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * (BN // 2 if pair else BN) * BK * 4
         # epilogue through TMA stores (and a TMA-prefetched residual) for plain
         # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
         res = u.residual_id is not None
@@ -416,6 +423,7 @@ class Specializer:
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
+                      PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
                       # their mainloop is shared-memory bound and the extra
@@ -456,7 +464,7 @@ class Specializer:
                 return dict(space=1, offset=self.arena_off(tid), dims=(CO, self.cap * rows),
                             strides=(4 * CO,), box=(16, 32), swizzle=2)
         tm_b = dict(space=2, offset=hi_off, dims=(KPAD, NPAD), strides=(4 * KPAD,),
-                    box=(BK, BN), swizzle=sw)
+                    box=(BK, BN // 2 if pair else BN), swizzle=sw)
         tm_bl = dict(tm_b, offset=lo_off)
         tm_o = out_map(u.output_id) if epi_tma else tm_a
         tm_r = out_map(u.residual_id) if (epi_tma and res) else tm_o
@@ -468,13 +476,15 @@ class Specializer:
             ipi, ipb = tpi, 1
             tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
         else:
-            ipi, ipb = rows, 128
+            ipi, ipb = rows, 256 if pair else 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg) else 384, smem,
                   ipi, ipb,
-                  grid_mult=ntn,
-                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], grid_cap=self.sm_count,
-                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile 128x{BN}x{BK} stages {NS}"
+                  grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
+                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r],
+                  grid_cap=self.sm_count - self.sm_count % 2 if pair else self.sm_count,
+                  note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile {256 if pair else 128}x{BN}x{BK}"
+                       f"{' CTA pair' if pair else ''} stages {NS}"
                        f" chains {NACC} bufs {ABUF}{'' if csplit else ' merged-corr'}"
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
@@ -704,7 +714,7 @@ def tf32_split_hi(w, rn=True):
 
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
-               epi_tma=True, csplit=True, chunk=None, split_rn=True):
+               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn).run()
+                       split_rn, pair).run()

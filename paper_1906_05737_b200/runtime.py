@@ -81,7 +81,7 @@ class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
                  nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
-                 split_rn=True):
+                 split_rn=True, pair=True):
         import torch
 
         t0 = time.perf_counter()
@@ -102,7 +102,8 @@ class CompiledNetwork:
                           use_tc=use_tc, sm_count=sm_count,
                           tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
                           tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack, epi_tma=epi_tma,
-                          csplit=csplit, chunk=chunk, split_rn=split_rn)
+                          csplit=csplit, chunk=chunk, split_rn=split_rn,
+                          pair=pair)
         arena_bytes = self.assignment.arena_size * cap
 
         def io(tids):
@@ -124,7 +125,7 @@ class CompiledNetwork:
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,
                                          l.items_per_image, l.items_per_block,
                                          l.n_min, min(l.n_max, 1 << 30), l.grid_cap,
-                                         len(l.tmaps), tm)
+                                         len(l.tmaps), tm, l.cluster)
         in_arr = (_native.IO * max(len(ins), 1))(*[_native.IO(o, b) for o, b in ins])
         out_arr = (_native.IO * max(len(outs), 1))(*[_native.IO(o, b) for o, b in outs])
         pool_buf = ctypes.create_string_buffer(spec.pool, max(len(spec.pool), 1))

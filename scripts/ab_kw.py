@@ -34,4 +34,4 @@ for variant in sys.argv[3:]:
     print(f"[{variant}] replay {net.time_apply(iters=20):.4f} ms{same}")
     for i in net.launches_for():
         l = net.artifact.launches[i]
-        print(f"   {l.kernel:32s} {net.time_launch(i, iters=10):8.4f} ms  {l.note[-40:]}")
+        print(f"   {l.kernel:32s} {net.time_launch(i, iters=10):8.4f} ms  {l.note[-70:]}")

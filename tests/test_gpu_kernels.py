@@ -320,3 +320,32 @@ def test_timing_entry_points():
         i = net.launches_for(n)[0]
         assert net.time_launch(i, n, iters=2) > 0
     assert net.time_apply(iters=2) > 0
+
+
+def test_integration_md_binding_stub_runs():
+    """The reference-side ctypes stub in INTEGRATION.md section 3 drives a
+    network end to end (kept honest against the ABI)."""
+    import pathlib
+    import torch
+    from paper_1906_05737_b200 import build_graph, build_plan, plan_buffers
+    from paper_1906_05737_b200.kernels import specialize
+    from paper_1906_05737_b200.runtime import _DeviceArray
+    md = (pathlib.Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    code = md.split("## 3.")[1].split("```python")[1].split("```")[0]
+    ns = {}
+    exec(code, ns)
+    m, w = zoo.build(0)
+    plan = build_plan(build_graph(m, w))
+    asg = plan_buffers(plan)
+    cap, n = 16, 4
+    ex = ns["DeviceExecutable"](specialize(plan, asg, EXACT, n, cap), asg.arena_size * cap, max_batch=n)
+    tin, tout = plan.input_ids[0], plan.output_ids[0]
+    view = lambda t: torch.as_tensor(_DeviceArray(ex, ex.arena_address(asg.offsets[t][0] * cap),
+                                                  (cap,) + tuple(plan.tensors[t].dims)), device="cuda")
+    x = zoo.inputs(0, n)
+    view(tin)[:n].copy_(torch.from_numpy(x))
+    ex(n)
+    torch.cuda.synchronize()
+    got = view(tout)[:n].cpu().numpy()
+    ex.close()
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
