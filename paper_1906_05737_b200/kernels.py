@@ -110,7 +110,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True):
+                 pair=True, tc_tile_use=0.75):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -118,6 +118,7 @@ class Specializer:
         self.csplit = csplit
         self.split_rn = split_rn
         self.pair = pair
+        self.tc_tile_use = tc_tile_use
         self.chunk = chunk
         self.nacc = nacc
         self.tmem_a = tmem_a
@@ -255,8 +256,13 @@ class Specializer:
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
                    and u.dw is None
                    and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
+        # implicit-GEMM tiles are 8 x 16 output pixels of one image: small images
+        # waste most of a tile (cfg0's 8x8 conv: 0.103 ms on tensor cores vs
+        # 0.046 ms as an FFMA GEMM), so require tc_tile_use (75%) useful pixels
+        tile_use = (HO * WO) / ((-(-HO // 8) * 8) * (-(-WO // 16) * 16))
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
-                   and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16)
+                   and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16
+                   and tile_use >= self.tc_tile_use)
         if tc_rows or tc_conv:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
             if n_tc <= self.max_batch:
@@ -714,7 +720,7 @@ def tf32_split_hi(w, rn=True):
 
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
-               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True):
+               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair).run()
+                       split_rn, pair, tc_tile_use).run()

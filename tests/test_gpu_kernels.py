@@ -59,7 +59,7 @@ def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
         y = b.layer("MaxPool2D", [y], {"pool_size": 2, "strides": 2})
     m, wt = b.build([y])
     xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
-    got, net = gpu(m, wt, xin, tc_min_rows=1)
+    got, net = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0)
     assert any("_tc_" in l.kernel for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
@@ -95,7 +95,7 @@ def test_decoder_fusions(c0, c1, co, up_src, tc):
                  ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
     m, wt = b.build([y])
     xin = rng.uniform(-2, 2, (3, 2 * h, 2 * w, c1)).astype(F32)
-    got, net = gpu(m, wt, xin, tc_min_rows=1 if tc else 1 << 30)
+    got, net = gpu(m, wt, xin, tc_min_rows=1 if tc else 1 << 30, tc_tile_use=0)
     kinds = [u.kind for u in net.plan.units]
     assert "Concat" not in kinds and "Upsample" not in kinds, net.plan.describe()
     assert any("_tc_" in l.kernel for l in net.artifact.launches) == tc
