@@ -32,8 +32,10 @@ template <> __device__ __forceinline__ float4 vzero<4>() { return make_float4(0.
 __device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + threadIdx.x; }
 
 // ---------------------------------------------------------------------------
-// Dense for a handful of rows (batch-1 latency path): 32 output columns per
-// block, KS warps split K, partial sums reduced in a fixed order.
+// Dense / 1x1 convolution for a handful of rows (batch-1 latency path): MB
+// rows and 32 output columns per block, KS warps split K, partial sums
+// reduced in a fixed order.  Row m is pixel m % ROWS of image m / ROWS
+// (ROWS = 1 for Dense).
 template <class C>
 struct DenseSmallM {
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
@@ -45,19 +47,26 @@ struct DenseSmallM {
     const int j = jb * 32 + lane_;
     const float* x = at<float>(arena, C::IN_OFF);
     const float* w = at<float>(pool, C::W_OFF);
+    const i64 nrows = (i64)n * C::ROWS;
+    auto in_row = [](i64 m) { return (m / C::ROWS) * (C::IN_IMG / 4) + (m % C::ROWS) * C::K; };
+    auto out_row = [](i64 m) { return (m / C::ROWS) * (C::OUT_IMG / 4) + (m % C::ROWS) * C::CO; };
     constexpr int KPER = (C::K + C::KS - 1) / C::KS;
     const int k0 = ks * KPER;
     const int k1 = k0 + KPER < C::K ? k0 + KPER : C::K;
     float acc[C::MB];
+    const float* xr[C::MB];
 #pragma unroll
-    for (int r = 0; r < C::MB; ++r) acc[r] = 0.f;
+    for (int r = 0; r < C::MB; ++r) {
+      acc[r] = 0.f;
+      xr[r] = x + (row0 + r < nrows ? in_row(row0 + r) : 0);
+    }
     if (j < C::CO) {
 #pragma unroll 4
       for (int k = k0; k < k1; ++k) {
         float wv = __ldg(w + (i64)k * C::CO + j);
 #pragma unroll
         for (int r = 0; r < C::MB; ++r)
-          if (row0 + r < n) acc[r] = fmaf(__ldg(x + (i64)(row0 + r) * (C::IN_IMG / 4) + k), wv, acc[r]);
+          if (row0 + r < nrows) acc[r] = fmaf(__ldg(xr[r] + k), wv, acc[r]);
       }
     }
 #pragma unroll
@@ -71,14 +80,14 @@ struct DenseSmallM {
     const float b = live ? __ldg(at<float>(pool, C::B_OFF) + j) : 0.f;
 #pragma unroll
     for (int r = 0; r < C::MB; ++r) {
-      if (row0 + r >= n) break;
+      if (row0 + r >= nrows) break;
       float s = b;
       for (int q = 0; q < C::KS; ++q) s = s + red[q][r][lane_];
       float v = finish<C::ACT, C::MODE, C::POST>(s, ps, po, live ? j : 0);
       if (C::RES && live)
-        v = add(v, __ldg(at<float>(arena, C::RES_OFF) + (i64)(row0 + r) * (C::OUT_IMG / 4) + j));
+        v = add(v, __ldg(at<float>(arena, C::RES_OFF) + out_row(row0 + r) + j));
       if (C::SOFTMAX) v = softmax_warp_row<C::SMEXP>(v, live);   // CO <= 32
-      if (live) out[(i64)(row0 + r) * (C::OUT_IMG / 4) + j] = v;
+      if (live) out[out_row(row0 + r) + j] = v;
     }
   }
 };

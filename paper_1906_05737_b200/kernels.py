@@ -248,7 +248,7 @@ class Specializer:
                 and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
             assert not concat
             self._conv_direct(pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL,
-                              pool_fused, PHO, PWO, UPF)
+                              pool_fused, PHO, PWO, UPF, n_min=n_min)
             return
 
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
@@ -497,7 +497,7 @@ class Specializer:
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
-                     PHO, PWO, UPF=1):
+                     PHO, PWO, UPF=1, n_min=1):
         pxt = 4 if CO <= 8 else 2 if CO <= 16 else 1
         fields = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, CO=CO, KH=KH, KW=KW, S=S, PT=PT, PL=PL,
                       POOL=pool_fused, PHO=PHO, PWO=PWO, PXT=pxt, UPF=UPF,
@@ -510,14 +510,17 @@ class Specializer:
         cells = PHO * PWO if pool_fused else HO * -(-WO // pxt)
         smem = 4 * (KH * KW * CI * CO + CO)
         self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, cells, 128,
-                  dynamic_smem=True,
+                  dynamic_smem=True, n_min=n_min,
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
                        f"{4 if pool_fused else pxt}")
 
-    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max):
-        MB = n_max
+    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None):
+        """Split-K GEMV/GEMM for few rows: Dense at n <= n_max (MB = n_max
+        rows per block), or a 1x1 conv whose n*rows pixels are the rows (MB
+        = ``mb`` per block)."""
+        MB = mb or n_max
         KS = max(1, min(32, K // 32))
-        fields = dict(K=K, CO=CO, MB=MB, KS=KS,
+        fields = dict(K=K, CO=CO, MB=MB, KS=KS, ROWS=rows,
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),
                       OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
@@ -529,8 +532,9 @@ class Specializer:
         if softmax and CO > 32:
             raise UnsupportedLayer("fused softmax needs <= 32 units")
         nj = (CO + 31) // 32
-        self.emit(pos, "gemv", "nnb::DenseSmallM", fields, 32 * KS, 0, 1, MB,
-                  grid_mult=nj, n_max=n_max, note=f"gemv K={K} N={CO} ks={KS}")
+        self.emit(pos, "gemv" if rows == 1 else "conv1x1_rows", "nnb::DenseSmallM", fields,
+                  32 * KS, 0, rows, MB, grid_mult=nj, n_max=n_max,
+                  note=f"split-K rows K={K} N={CO} ks={KS} rows/block {MB}")
 
     def depthwise(self, pos, u):
         H, W, C = u.input_shapes[0].dims
