@@ -76,3 +76,71 @@ class ReplicaGroup:
             t = t.cuda()
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
+
+
+class MultiDeviceNetwork:
+    """One host process driving one replica per device (SURVEY.md 8(e)'s
+    single-thread alternative to one process per GPU): the global batch is
+    sharded into contiguous slices (``shard``), replica ``r`` is a
+    ``CompiledNetwork`` on ``devices[r]`` with its own arena, weights and
+    CUDA graph, and ``apply()`` enqueues every replica's graph on its
+    device's current stream before anything waits -- the devices run
+    concurrently, with no collective and no peer traffic on the data path.
+
+    ``devices`` may repeat an id (several replicas on one GPU), which is how
+    the single-GPU tests exercise this class.
+    """
+
+    def __init__(self, manifest, weights, options=None, *, batch, devices, **kw):
+        from .runtime import CompiledNetwork
+        if not devices:
+            raise ValueError("devices must name at least one GPU")
+        self.devices = list(devices)
+        self.batch = int(batch)
+        self.slices = [shard(self.batch, len(self.devices), r) for r in range(len(self.devices))]
+        if any(c == 0 for _, c in self.slices):
+            raise ValueError(f"batch {batch} is smaller than the {len(devices)} replicas")
+        self.replicas = [CompiledNetwork(manifest, weights, options, batch=c, device=d, **kw)
+                         for (_, c), d in zip(self.slices, self.devices)]
+
+    @property
+    def input_views(self):
+        """Per replica: its input views (torch tensors on its device)."""
+        return [r.input_views for r in self.replicas]
+
+    @property
+    def output_views(self):
+        return [r.output_views for r in self.replicas]
+
+    def apply(self):
+        """Enqueue every replica's replay (asynchronous across devices)."""
+        for r in self.replicas:
+            r.apply()
+
+    def synchronize(self):
+        for r in self.replicas:
+            r.synchronize()
+
+    def run(self, inputs, gather_device=None):
+        """Scatter ``inputs`` (arrays with the global batch leading), replay
+        all replicas, and return the outputs concatenated in batch order: torch
+        tensors on ``gather_device`` (default: the first device) -- the copies
+        are the only cross-device traffic and happen after the replays."""
+        import torch
+        xs = [x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, np.float32))
+              for x in inputs]
+        for (start, count), rep in zip(self.slices, self.replicas):
+            for view, x in zip(rep.input_views, xs):
+                if tuple(x.shape[1:]) != tuple(view.shape[1:]) or x.shape[0] != self.batch:
+                    from .errors import InputShapeMismatch
+                    raise InputShapeMismatch(f"input shape {tuple(x.shape)} does not match "
+                                             f"({self.batch},) + {tuple(view.shape[1:])}")
+                view.copy_(x[start:start + count], non_blocking=True)
+        self.apply()
+        dev = torch.device("cuda", self.devices[0] if gather_device is None else gather_device)
+        outs = []
+        for i in range(len(self.replicas[0].output_views)):
+            parts = [rep.output_views[i].to(dev, non_blocking=True) for rep in self.replicas]
+            outs.append(torch.cat(parts))
+        torch.cuda.synchronize(dev)
+        return outs

@@ -304,10 +304,16 @@ class _PinnedArray(np.ndarray):
     pass
 
 
-def compile_model(manifest, weights, options=None, **kw):
+def compile_model(manifest, weights, options=None, devices=None, **kw):
+    """pkg/src/nnjit/runtime.py:101-104.  ``devices=[...]`` (additive) shards
+    ``batch`` over one replica per listed GPU (``replicas.MultiDeviceNetwork``)."""
+    if devices is not None:
+        from .replicas import MultiDeviceNetwork
+        return MultiDeviceNetwork(manifest, weights, options, devices=devices, **kw)
     return CompiledNetwork(manifest, weights, options, **kw)
 
 
-def compile_file(manifest_path, blob_path=None, options=None, **kw):
+def compile_file(manifest_path, blob_path=None, options=None, devices=None, **kw):
+    """pkg/src/nnjit/runtime.py:105-107 (same ``devices`` extension)."""
     manifest, weights = load_model(manifest_path, blob_path)
-    return CompiledNetwork(manifest, weights, options, **kw)
+    return compile_model(manifest, weights, options, devices=devices, **kw)
