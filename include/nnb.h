@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define NNB_ABI_VERSION 3
+#define NNB_ABI_VERSION 4
 #define NNB_MAX_TMAPS 6
 
 typedef enum {
@@ -80,6 +80,9 @@ typedef struct {
   nnb_tmap tmaps[NNB_MAX_TMAPS];
   uint32_t cluster;          /* thread-block cluster size along x (0/1: none);
                               * the grid is rounded down to a multiple of it */
+  uint32_t cooperative;      /* 1: co-resident grid (cooperative launch)      */
+  int64_t zero_offset;       /* >= 0: arena byte offset of a uint32 set to 0
+                              * (stream-ordered) right before the launch      */
 } nnb_launch;
 
 /* A network I/O tensor: byte offset in the arena and bytes per image. */

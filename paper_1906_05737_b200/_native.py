@@ -49,7 +49,8 @@ class Launch(ctypes.Structure):
                 ("items_per_image", ctypes.c_uint64), ("items_per_block", ctypes.c_uint64),
                 ("n_min", ctypes.c_int32), ("n_max", ctypes.c_int32),
                 ("grid_cap", ctypes.c_uint32), ("n_tmaps", ctypes.c_uint32),
-                ("tmaps", TMap * MAX_TMAPS), ("cluster", ctypes.c_uint32)]
+                ("tmaps", TMap * MAX_TMAPS), ("cluster", ctypes.c_uint32),
+                ("cooperative", ctypes.c_uint32), ("zero_offset", ctypes.c_int64)]
 
 
 class IO(ctypes.Structure):

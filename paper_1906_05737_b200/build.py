@@ -50,20 +50,24 @@ def kernel_check(configs=range(5), batch=4096):
     for c in configs:
         m, w = zoo.build(c)
         plan = build_plan(build_graph(m, w))
-        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch)
-        cu = bdir / f"kcheck_cfg{c}.cu"
-        cu.write_text(spec.source)
-        out = bdir / f"kcheck_cfg{c}.cubin"
-        cmd = [str(CUDA / "bin" / "nvcc"), *NVCC_ARCH, "-lineinfo", "-O3", "-std=c++17", "-cubin",
-               f"-I{PKG / 'csrc' / 'kernels'}", "-Xptxas", "-v", str(cu), "-o", str(out)]
-        jobs.append((c, out, subprocess.Popen(cmd, stdout=subprocess.PIPE,
-                                              stderr=subprocess.PIPE, text=True)))
+        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch, mega=True)
+        tus = [(f"cfg{c}", spec.source)]
+        if spec.mega_source:                      # the batch-1 persistent kernel's own TU
+            tus.append((f"cfg{c}_mega", spec.mega_source))
+        for tag, text in tus:
+            cu = bdir / f"kcheck_{tag}.cu"
+            cu.write_text(text)
+            out = bdir / f"kcheck_{tag}.cubin"
+            cmd = [str(CUDA / "bin" / "nvcc"), *NVCC_ARCH, "-lineinfo", "-O3", "-std=c++17",
+                   "-cubin", f"-I{PKG / 'csrc' / 'kernels'}", "-Xptxas", "-v", str(cu), "-o", str(out)]
+            jobs.append((tag, out, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                    stderr=subprocess.PIPE, text=True)))
     outs = []
-    for c, out, p in jobs:
+    for tag, out, p in jobs:
         _, err = p.communicate()
         if p.returncode != 0:
-            raise RuntimeError(f"nvcc kernel check (config {c}) failed:\n" + err[-4000:])
-        (bdir / f"kcheck_cfg{c}.ptxas.txt").write_text(err)
+            raise RuntimeError(f"nvcc kernel check ({tag}) failed:\n" + err[-4000:])
+        (bdir / f"kcheck_{tag}.ptxas.txt").write_text(err)
         outs.append(out)
     return outs
 

@@ -29,11 +29,11 @@ struct ConvDirect {
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
                              Smem& sm) {
     const float* wg = at<float>(pool, C::W_OFF);
-    for (int i = threadIdx.x; i < WN; i += blockDim.x) sm.w[i] = __ldg(wg + i);
-    for (int i = threadIdx.x; i < C::CO; i += blockDim.x) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
-    __syncthreads();
+    for (int i = threadIdx.x; i < WN; i += nnb_bdim()) sm.w[i] = __ldg(wg + i);
+    for (int i = threadIdx.x; i < C::CO; i += nnb_bdim()) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
+    nnb_sync();
 
-    const i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 cell = nnb_bid() * nnb_bdim() + threadIdx.x;
     if (cell >= (i64)n * CELLS_Y * CELLS_X) return;
     const int cx = (int)(cell % CELLS_X);
     const int cy = (int)((cell / CELLS_X) % CELLS_Y);
@@ -61,10 +61,10 @@ struct ConvDirect {
             const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
             const float* src = in + ((i64)iy * C::W + ix) * C::CI + c0;
             if (CV == 4) {
-              float4 v = ok ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+              float4 v = ok ? lda(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
               xv[p][0] = v.x; xv[p][CV > 1 ? 1 : 0] = v.y; xv[p][CV > 2 ? 2 : 0] = v.z; xv[p][CV > 3 ? 3 : 0] = v.w;
             } else {
-              xv[p][0] = ok ? __ldg(src) : 0.f;
+              xv[p][0] = ok ? lda(src) : 0.f;
             }
           }
 #pragma unroll
@@ -119,7 +119,7 @@ struct ConvDirect {
       if (C::RES) {
         const float* res = at<float>(arena, C::RES_OFF + img * C::OUT_IMG) + pix * C::CO;
 #pragma unroll
-        for (int o = 0; o < C::CO; ++o) acc[p][o] = add(acc[p][o], __ldg(res + o));
+        for (int o = 0; o < C::CO; ++o) acc[p][o] = add(acc[p][o], lda(res + o));
       }
 #pragma unroll
       for (int rep = 0; rep < C::UPF * C::UPF; ++rep) {

@@ -72,7 +72,7 @@ struct GemmSimt {
       for (int kx = 0; kx < C::DW_KW; ++kx) {
         const int x = ox * C::DW_S - C::DW_PL + kx;
         if (x < 0 || x >= C::DW_W) continue;
-        const float4 v = __ldg(reinterpret_cast<const float4*>(img + ((i64)y * C::DW_W + x) * C::CI + c));
+        const float4 v = lda(reinterpret_cast<const float4*>(img + ((i64)y * C::DW_W + x) * C::CI + c));
         const float4 w = __ldg(reinterpret_cast<const float4*>(wk + (ky * C::DW_KW + kx) * C::CI + c));
         acc.x = fmaf(v.x, w.x, acc.x); acc.y = fmaf(v.y, w.y, acc.y);
         acc.z = fmaf(v.z, w.z, acc.z); acc.w = fmaf(v.w, w.w, acc.w);
@@ -93,8 +93,8 @@ struct GemmSimt {
     const int tx = tid % NTX, ty = tid / NTX;
     const i64 mtotal = (i64)n * C::ROWS;
     const int ntile_n = (C::CO + C::BN - 1) / C::BN;
-    const i64 m0 = (i64)(blockIdx.x / ntile_n) * C::BM;
-    const int n0 = (blockIdx.x % ntile_n) * C::BN;
+    const i64 m0 = (i64)(nnb_bid() / ntile_n) * C::BM;
+    const int n0 = (int)(nnb_bid() % ntile_n) * C::BN;
     if (m0 >= mtotal) return;
 
     const float* __restrict__ in = at<float>(arena, C::IN_OFF);
@@ -155,10 +155,10 @@ struct GemmSimt {
                 (iy * C::W + ix) * (C::CI - C::C0) + (ci - C::C0);
         if (AVEC) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ok) v = __ldg(reinterpret_cast<const float4*>(src));
+          if (ok) v = lda(reinterpret_cast<const float4*>(src));
           ra[l][0] = v.x; if (AKV > 1) { ra[l][1 % AKV] = v.y; ra[l][2 % AKV] = v.z; ra[l][3 % AKV] = v.w; }
         } else {
-          ra[l][0] = ok ? __ldg(src) : 0.f;
+          ra[l][0] = ok ? lda(src) : 0.f;
         }
       }
     };
@@ -213,7 +213,7 @@ struct GemmSimt {
     load_b(0);
     store_a(0);
     store_b(0);
-    __syncthreads();
+    nnb_sync();
     for (int kc = 0; kc < KCH; ++kc) {
       const int buf = kc & 1;
       if (kc + 1 < KCH) {
@@ -236,7 +236,7 @@ struct GemmSimt {
         store_a(buf ^ 1);
         store_b(buf ^ 1);
       }
-      __syncthreads();
+      nnb_sync();
     }
 
     // ---- epilogue ----
@@ -287,8 +287,8 @@ struct GemmSimt {
 #pragma unroll
         for (int j = 0; j < C::TN; ++j) {
           int col = n0 + tx * C::TN + j;
-          if (col < C::CO) acc[i][j] = C::RES_FIRST ? add(__ldg(res + col), acc[i][j])
-                                                     : add(acc[i][j], __ldg(res + col));
+          if (col < C::CO) acc[i][j] = C::RES_FIRST ? add(lda(res + col), acc[i][j])
+                                                     : add(acc[i][j], lda(res + col));
         }
       }
       if (C::SOFTMAX) {

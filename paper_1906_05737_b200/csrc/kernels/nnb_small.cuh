@@ -29,7 +29,7 @@ template <int V> __device__ __forceinline__ typename Vec<V>::T vzero();
 template <> __device__ __forceinline__ float vzero<1>() { return 0.f; }
 template <> __device__ __forceinline__ float4 vzero<4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-__device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ i64 gtid() { return nnb_bid() * nnb_bdim() + threadIdx.x; }
 
 // ---------------------------------------------------------------------------
 // Dense / 1x1 convolution for a handful of rows (batch-1 latency path): MB
@@ -39,11 +39,16 @@ __device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + th
 template <class C>
 struct DenseSmallM {
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+#if NNB_MEGA
+    extern __shared__ __align__(16) unsigned char nnb_dyn_smem[];
+    float (*red)[C::MB][32] = reinterpret_cast<float (*)[C::MB][32]>(nnb_dyn_smem);
+#else
     __shared__ float red[C::KS][C::MB][32];
+#endif
     const int lane_ = threadIdx.x & 31, ks = threadIdx.x >> 5;
     constexpr int NJ = (C::CO + 31) / 32;
-    const int jb = blockIdx.x % NJ;
-    const int row0 = (blockIdx.x / NJ) * C::MB;
+    const int jb = (int)(nnb_bid() % NJ);
+    const int row0 = (int)(nnb_bid() / NJ) * C::MB;
     const int j = jb * 32 + lane_;
     const float* x = at<float>(arena, C::IN_OFF);
     const float* w = at<float>(pool, C::W_OFF);
@@ -66,12 +71,12 @@ struct DenseSmallM {
         float wv = __ldg(w + (i64)k * C::CO + j);
 #pragma unroll
         for (int r = 0; r < C::MB; ++r)
-          if (row0 + r < nrows) acc[r] = fmaf(__ldg(xr[r] + k), wv, acc[r]);
+          if (row0 + r < nrows) acc[r] = fmaf(lda(xr[r] + k), wv, acc[r]);
       }
     }
 #pragma unroll
     for (int r = 0; r < C::MB; ++r) red[ks][r][lane_] = acc[r];
-    __syncthreads();
+    nnb_sync();
     if (ks != 0) return;                       // warp 0 finishes all rows
     const bool live = j < C::CO;
     const float* ps = at<float>(pool, C::PS_OFF);
@@ -85,7 +90,7 @@ struct DenseSmallM {
       for (int q = 0; q < C::KS; ++q) s = s + red[q][r][lane_];
       float v = finish<C::ACT, C::MODE, C::POST>(s, ps, po, live ? j : 0);
       if (C::RES && live)
-        v = add(v, __ldg(at<float>(arena, C::RES_OFF) + out_row(row0 + r) + j));
+        v = add(v, lda(at<float>(arena, C::RES_OFF) + out_row(row0 + r) + j));
       if (C::SOFTMAX) v = softmax_warp_row<C::SMEXP>(v, live);   // CO <= 32
       if (live) out[out_row(row0 + r) + j] = v;
     }
@@ -138,7 +143,7 @@ struct Depthwise {
 #pragma unroll
       for (int j = 0; j < NCOL; ++j) {
         const int ix = ix0 + j;
-        xv[j] = (ix >= 0 && ix < C::W) ? __ldg(row + ix * CG) : vzero<V>();
+        xv[j] = (ix >= 0 && ix < C::W) ? lda(row + ix * CG) : vzero<V>();
       }
 #pragma unroll
       for (int kx = 0; kx < C::KW; ++kx) {
@@ -197,7 +202,7 @@ struct Pool {
       for (int kx = 0; kx < C::PW; ++kx) {
         const int ix = ix0 + kx;
         if (ix < 0 || ix >= C::W) continue;
-        T xv = __ldg(in + ((i64)iy * C::W + ix) * CG + cg);
+        T xv = lda(in + ((i64)iy * C::W + ix) * CG + cg);
         ++count;
 #pragma unroll
         for (int l = 0; l < V; ++l)

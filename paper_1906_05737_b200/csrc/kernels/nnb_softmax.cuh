@@ -67,7 +67,7 @@ struct SoftmaxRows {
     float* out = at<float>(arena, C::OUT_OFF);
     const i64 rows = (i64)n * C::ROWS;
     if (C::PER_THREAD) {
-      i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+      i64 r = nnb_bid() * nnb_bdim() + threadIdx.x;
       if (r >= rows) return;
       float v[C::L];
 #pragma unroll
@@ -78,7 +78,7 @@ struct SoftmaxRows {
       return;
     }
     const int lane = threadIdx.x & 31;
-    i64 r = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    i64 r = (nnb_bid() * nnb_bdim() + threadIdx.x) >> 5;
     if (r >= rows) return;
     const float* x = in + r * C::L;
     float* y = out + r * C::L;

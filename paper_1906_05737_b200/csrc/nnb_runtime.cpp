@@ -70,6 +70,7 @@ struct Cu {
   CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
   CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
   CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled) CU_FN(cuLaunchKernelEx)
+  CU_FN(cuMemsetD32Async)
 #undef CU_FN
   void load() {
     const char *names[] = {"libcuda.so.1", "libcuda.so"};
@@ -92,7 +93,7 @@ struct Cu {
     CU_LOAD(cuGraphDestroy) CU_LOAD(cuGraphExecDestroy) CU_LOAD(cuEventCreate)
     CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
     CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString) CU_LOAD(cuTensorMapEncodeTiled)
-    CU_LOAD(cuLaunchKernelEx)
+    CU_LOAD(cuLaunchKernelEx) CU_LOAD(cuMemsetD32Async)
 #undef CU_LOAD
     CUresult r = p_cuInit(0);
     if (r != CUDA_SUCCESS) {
@@ -322,12 +323,19 @@ nnb_status launch_one(nnb_net *net, size_t li, int n, CUstream s, bool pdl) {
     int nn = n;
     void *args[3 + NNB_MAX_TMAPS] = {&pool, &arena, &nn};
     for (uint32_t k = 0; k < l.n_tmaps; ++k) args[3 + k] = &net->maps[li][k];
-    if (pdl || cl > 1) {
+    if (l.zero_offset >= 0)      // the persistent kernel's barrier counter
+      CU_CHECK(C->p_cuMemsetD32Async(net->arena + (CUdeviceptr)l.zero_offset, 0, 1, s));
+    if (pdl || cl > 1 || l.cooperative) {
       // programmatic dependent launch: the next kernel's CTAs are scheduled while
       // this one drains; each kernel starts with griddepcontrol.wait.
       // Clusters: CTA pairs for the tcgen05 cta_group::2 GEMM.
-      CUlaunchAttribute attr[2];
+      CUlaunchAttribute attr[3];
       unsigned na = 0;
+      if (l.cooperative) {
+        attr[na].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+        attr[na].value.cooperative = 1;
+        ++na;
+      }
       if (pdl) {
         attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
         attr[na].value.programmaticStreamSerializationAllowed = 1;
@@ -518,6 +526,10 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   net->maps.resize(net->launches.size());
   for (size_t i = 0; i < net->launches.size(); ++i) {
     const nnb_launch &l = net->launches[i];
+    if (l.zero_offset >= 0 && ((uint64_t)l.zero_offset + 4 > net->arena_bytes || l.zero_offset % 4)) {
+      fail(NNB_ERR_ARGUMENT, "launch %zu: zero_offset outside the arena", i);
+      return bail(NNB_ERR_ARGUMENT);
+    }
     if (l.n_tmaps != 0 && l.n_tmaps != NNB_MAX_TMAPS) { fail(NNB_ERR_ARGUMENT, "launch %zu: n_tmaps must be 0 or %d", i, NNB_MAX_TMAPS); return bail(NNB_ERR_ARGUMENT); }
     net->maps[i].resize(l.n_tmaps);
     for (uint32_t k = 0; k < l.n_tmaps; ++k) {

@@ -20,6 +20,8 @@ weight pool (a deduplicated, 256-byte aligned blob, cf. codegen/pool.py).
 import hashlib
 from dataclasses import dataclass, field
 
+import re
+
 import numpy as np
 
 from .errors import UnsupportedLayer
@@ -36,6 +38,8 @@ TC_MIN_K = 32         # tensor-core GEMM eligibility (contraction and output wid
 TC_MIN_N = 32
 TC_MIN_ROWS = 2048    # GEMM rows per launch from which the tcgen05 kernel is used
 SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
+MEGA_MAX_N = 8         # batches up to this run as one persistent kernel (when eligible)
+MEGA_THREADS = 256     # its block size (units with larger blocks opt it out)
 MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS)
 ELEM_BLOCK = 256
 
@@ -57,6 +61,8 @@ class Launch:
     grid_cap: int = 0                 # persistent kernels: at most this many CTAs
     tmaps: list = field(default_factory=list)   # TMA descriptors (see nnb_tmap)
     cluster: int = 1                  # thread-block cluster size along x (CTA pairs: 2)
+    cooperative: bool = False         # co-resident grid (the batch-1 persistent kernel)
+    zero_offset: int = -1             # arena byte offset of a u32 zeroed before the launch
 
 
 class DevicePool:
@@ -90,6 +96,8 @@ class Specialization:
     sources: list = field(default_factory=list)      # one TU per kernel (NVRTC jobs)
     kernel_source: list = field(default_factory=list)
     notes: dict = field(default_factory=dict)
+    arena_extra: int = 0        # bytes the runtime appends to the arena (mega barrier)
+    mega_source: str = ""       # the persistent kernel's TU ("" when not generated)
 
 
 def _cfg_struct(name, fields):
@@ -110,7 +118,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75):
+                 pair=True, tc_tile_use=0.75, mega=False):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -119,6 +127,8 @@ class Specializer:
         self.split_rn = split_rn
         self.pair = pair
         self.tc_tile_use = tc_tile_use
+        self.mega = mega
+        self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
         self.tmem_a = tmem_a
@@ -161,6 +171,7 @@ class Specializer:
             self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min, n_max,
                                         unit_pos, note, grid_cap, list(tmaps), cluster))
             return
+        self.unit_src[len(self.launches)] = (cfg, body, template, dynamic_smem)
         if dynamic_smem:
             call = (f"  extern __shared__ __align__(16) unsigned char nnb_smem[];\n"
                     f"  {template}<{cfg}>::run(pool, arena, n, "
@@ -696,18 +707,101 @@ class Specializer:
                 self.pad(pos, u)
             else:
                 raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
+        self.mega_source = ""
+        arena_extra = self._mega() if self.mega else 0
         head = '#include "nnb_kernels.cuh"\n\n'
-        src = head + "\n\n".join(self.chunks) + "\n"
+        # one TU with every regular unit (inspection, the nvcc build check);
+        # the persistent kernel is its own TU (compiled with NNB_MEGA=1)
+        src = head + "\n\n".join(c for c in self.chunks if not c.startswith("#define NNB_MEGA")) + "\n"
         sources, index, ks = [], {}, []
         for chunk in self.chunks:
-            tu = head + chunk
+            tu = chunk if chunk.startswith("#define NNB_MEGA") else head + chunk
             if tu not in index:
                 index[tu] = len(sources)
                 sources.append(tu)
             ks.append(index[tu])
         return Specialization(source=src, launches=self.launches, pool=bytes(self.pool.data),
                               kernel_names=list(self.names), sources=sources,
-                              kernel_source=ks)
+                              kernel_source=ks, arena_extra=arena_extra,
+                              mega_source=self.mega_source)
+
+    def _mega(self):
+        """Batch-1 persistent kernel: for n <= NB one
+        cooperative launch walks every launch unit of the schedule in order --
+        each unit's own template, fed virtual block indices by a grid-stride
+        loop -- with a grid-wide barrier between units, instead of one graph
+        node per unit.  NB is the largest batch <= MEGA_MAX_N whose units are
+        all non-TMA kernels with blocks <= MEGA_THREADS.  The regular launches
+        then start at NB + 1.  Returns the arena bytes it needs (the barrier
+        counter).
+
+        Opt-in (``mega=True``): measured on B200 it is slower than the graph
+        replay with programmatic dependent launch -- batch-1 latency is the
+        units' own dependent-load latency, not launch overhead, and a
+        grid-wide barrier costs about what a graph node does (cfg0 27 -> 35
+        us, cfg2 35 -> 37 us, cfg3 107 -> 126 us; "full" 148-CTA grids and
+        backoff in the barrier did not change that)."""
+        NB = 0
+        for n in range(1, min(MEGA_MAX_N, self.max_batch) + 1):
+            act = [l for l in self.launches if l.n_min <= n <= l.n_max]
+            if any(l.tmaps or l.block > MEGA_THREADS for l in act):
+                break
+            NB = n
+        if NB == 0:
+            return 0
+        parts = [i for i, l in enumerate(self.launches) if l.n_min <= NB]
+        if len(parts) < 2:
+            return 0
+        sync_off = self.asg.arena_size * self.cap          # appended 256 bytes
+        smem, width, gmax = 0, 0, 1
+        body = ["#define NNB_MEGA 1", '#include "nnb_kernels.cuh"', ""]
+        code = []
+        for k, i in enumerate(parts):
+            l = self.launches[i]
+            cfg, struct, template, dyn = self.unit_src[i]
+            body.append(struct)
+            width = max(width, l.block)
+            smem = max(smem, l.smem)
+            if template == "nnb::DenseSmallM":
+                f = dict(re.findall(r"static constexpr long long (\w+) = (-?\d+)LL", struct))
+                smem = max(smem, int(f["KS"]) * int(f["MB"]) * 32 * 4)
+            gmax = max(gmax, -(-NB * l.items_per_image // l.items_per_block) * l.grid_mult)
+            call = (f"{template}<{cfg}>::run(pool, arena, n, *reinterpret_cast<{template}<{cfg}>::Smem*>"
+                    f"(nnb_dyn_smem))" if dyn else f"{template}<{cfg}>::run(pool, arena, n)")
+            last = k == len(parts) - 1
+            code.append(
+                f"  if (n >= {l.n_min} && n <= {min(l.n_max, NB)}) {{   // {l.kernel}\n"
+                f"    const long long g = (((long long)n * {l.items_per_image} + {l.items_per_block - 1})"
+                f" / {l.items_per_block}) * {l.grid_mult};\n"
+                f"    for (long long vb = blockIdx.x; vb < g; vb += gridDim.x) {{\n"
+                f"      __syncthreads();\n"
+                f"      if (threadIdx.x == 0) {{ nnb::nnb_mega_bid = (int)vb; nnb::nnb_mega_bdim = {l.block}; }}\n"
+                f"      __syncthreads();\n"
+                f"      if (threadIdx.x < {l.block}) {call};\n"
+                f"    }}\n"
+                + ("" if last else "    nnb::mega_grid_sync(sync, (++epoch) * gridDim.x);\n")
+                + "  }\n")
+        grid = self.sm_count if self.mega == "full" else min(self.sm_count, gmax)
+        body.append(
+            f"\nextern \"C\" __global__ void __launch_bounds__({width}, 1) nnb_mega("
+            f"const float* __restrict__ pool, float* __restrict__ arena, int n) {{\n"
+            f"  NNB_PDL_PROLOGUE\n"
+            f"  extern __shared__ __align__(16) unsigned char nnb_dyn_smem[];\n"
+            f"  unsigned* sync = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(arena) + {sync_off}LL);\n"
+            f"  unsigned epoch = 0;\n" + "".join(code) + "}\n")
+        kname = "nnb_mega"
+        self.chunks.append("\n".join(body))
+        self.names.append(kname)
+        # the regular launches take over above NB
+        for i in parts:
+            self.launches[i].n_min = max(self.launches[i].n_min, NB + 1)
+        self.launches = [l for l in self.launches if l.n_min <= l.n_max]
+        self.launches.append(Launch(kname, width, smem, 1, 1 << 30, grid_mult=grid, n_min=1,
+                                    n_max=NB, unit=-1,
+                                    note=f"persistent: {len(parts)} units, {grid} CTAs, n <= {NB}",
+                                    cooperative=True, zero_offset=sync_off))
+        self.mega_source = self.chunks[-1]
+        return 256
 
 
 def tf32_split_hi(w, rn=True):
@@ -724,7 +818,8 @@ def tf32_split_hi(w, rn=True):
 
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
-               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75):
+               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
+               mega=False):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair, tc_tile_use).run()
+                       split_rn, pair, tc_tile_use, mega).run()

@@ -81,7 +81,7 @@ class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
                  nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
-                 split_rn=True, pair=True, tc_tile_use=0.75):
+                 split_rn=True, pair=True, tc_tile_use=0.75, mega=False):
         import torch
 
         t0 = time.perf_counter()
@@ -103,8 +103,8 @@ class CompiledNetwork:
                           tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
                           tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack, epi_tma=epi_tma,
                           csplit=csplit, chunk=chunk, split_rn=split_rn,
-                          pair=pair, tc_tile_use=tc_tile_use)
-        arena_bytes = self.assignment.arena_size * cap
+                          pair=pair, tc_tile_use=tc_tile_use, mega=mega)
+        arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 
         def io(tids):
             return [(self.assignment.offsets[t][0] * cap, 4 * self.plan.tensors[t].elements)
@@ -125,7 +125,8 @@ class CompiledNetwork:
             launches[i] = _native.Launch(index[l.kernel], l.block, l.smem, l.grid_mult,
                                          l.items_per_image, l.items_per_block,
                                          l.n_min, min(l.n_max, 1 << 30), l.grid_cap,
-                                         len(l.tmaps), tm, l.cluster)
+                                         len(l.tmaps), tm, l.cluster, int(l.cooperative),
+                                         l.zero_offset)
         in_arr = (_native.IO * max(len(ins), 1))(*[_native.IO(o, b) for o, b in ins])
         out_arr = (_native.IO * max(len(outs), 1))(*[_native.IO(o, b) for o, b in outs])
         pool_buf = ctypes.create_string_buffer(spec.pool, max(len(spec.pool), 1))

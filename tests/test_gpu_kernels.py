@@ -338,7 +338,8 @@ def test_integration_md_binding_stub_runs():
     plan = build_plan(build_graph(m, w))
     asg = plan_buffers(plan)
     cap, n = 16, 4
-    ex = ns["DeviceExecutable"](specialize(plan, asg, EXACT, n, cap), asg.arena_size * cap, max_batch=n)
+    spec = specialize(plan, asg, EXACT, n, cap)
+    ex = ns["DeviceExecutable"](spec, asg.arena_size * cap + spec.arena_extra, max_batch=n)
     tin, tout = plan.input_ids[0], plan.output_ids[0]
     view = lambda t: torch.as_tensor(_DeviceArray(ex, ex.arena_address(asg.offsets[t][0] * cap),
                                                   (cap,) + tuple(plan.tensors[t].dims)), device="cuda")
@@ -366,3 +367,18 @@ def test_multi_device_network_shards_batch_over_replicas():
         net.run([x[:5]])
     with pytest.raises(ValueError):
         compile_model(m, w, EXACT, batch=1, devices=[0, 0])
+
+
+@pytest.mark.parametrize("cfg", [0, 2, 3])
+def test_batch1_persistent_kernel_matches_oracle(cfg):
+    """mega=True: small batches run as one cooperative kernel walking every
+    unit with grid barriers (opt-in; see kernels.Specializer._mega)."""
+    m, w = zoo.build(cfg)
+    for n in (1, 3):
+        x = zoo.inputs(cfg, n)
+        net = compile_model(m, w, EXACT, batch=n, mega=True)
+        coop = [l for l in net.artifact.launches if l.cooperative]
+        got = net.run([x])[0].cpu().numpy()
+        np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+        if n == 1:
+            assert coop and net.launches_for(1) == [net.artifact.launches.index(coop[0])]

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_mapping_without_gpu():
     lib = _native.lib()
-    assert lib.nnb_abi_version() == 3
+    assert lib.nnb_abi_version() == 4
     try:
         import torch
         has_gpu = torch.cuda.is_available()
@@ -74,7 +74,7 @@ def test_compiled_network_requires_device():
 def test_nvrtc_builds_sm100a_cubin(tmp_path):
     m, w = zoo.build(0)
     plan = build_plan(build_graph(m, w))
-    spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), 1, 16)
+    spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), 1, 16, mega=True)
     cubin, ms = _native.compile_source(spec.source, cache_dir=str(tmp_path))
     assert cubin[:4] == b"\x7fELF"
     p = tmp_path / "k.cubin"
@@ -82,7 +82,12 @@ def test_nvrtc_builds_sm100a_cubin(tmp_path):
     out = subprocess.run(["cuobjdump", "-elf", str(p)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     for name in spec.kernel_names:
-        assert name.encode() in cubin
+        if name != "nnb_mega":
+            assert name.encode() in cubin
+    # the batch-1 persistent kernel is its own translation unit (NNB_MEGA=1)
+    assert "nnb_mega" in spec.kernel_names and spec.mega_source
+    mega, _ = _native.compile_source(spec.mega_source, cache_dir=str(tmp_path))
+    assert b"nnb_mega" in mega
     again, ms2 = _native.compile_source(spec.source, cache_dir=str(tmp_path))
     assert again == cubin                       # served from the cubin cache
     assert list(tmp_path.glob("*.cubin"))
