@@ -211,6 +211,16 @@ __device__ __forceinline__ void mma_tf32_ts_pair(u32 tmem_d, u32 tmem_a, u64 bde
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void mma_tf32_pair(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_pair(u64* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -372,7 +382,7 @@ struct GemmTc {
   // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
   static constexpr bool AL = C::ALDG != 0;
   static_assert(!(AL && TA), "A via LDGSTS lives in shared memory");
-  static_assert(!PAIR || (TA && !C::CONV && C::BN % 32 == 0), "CTA pairs: rows mode, A in TMEM");
+  static_assert(!PAIR || (!AL && C::BN % 16 == 0 && (C::BN / 2) % 8 == 0), "CTA-pair tile shape");
   static constexpr int CONV_WARPS = (TA || AL) ? 4 : 2;           // A splitters
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
@@ -549,10 +559,14 @@ struct GemmTc {
               const u32 dc = CS ? d + C::BN : d;                 // its correction columns
               const u32 accum = ks >= NACC;
               const u32 acc_c = CS ? accum : 1u;
-              if (PAIR) {
+              if (PAIR && TA) {
                 mma_tf32_ts_pair(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts_pair(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
                 mma_tf32_ts_pair(dc, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+              } else if (PAIR) {
+                mma_tf32_pair(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_tf32_pair(dc, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
+                mma_tf32_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               } else if (TA) {
                 mma_tf32_ts(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
@@ -717,7 +731,7 @@ struct GemmTc {
             lo[i] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&lo_ready[s]);
+          arrive_mma(&lo_ready[s]);
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
       }

@@ -410,7 +410,12 @@ class Specializer:
         # CTA pairs (cta_group::2, 256-row tiles, each CTA holds half of B):
         # the BN = 128 row GEMMs, whose single-CTA form is bound by
         # shared-memory bandwidth (B is re-read by every product)
-        pair = bool(self.pair and not conv and tmem_a and BN == 128 and K >= 256)
+        # Narrow-N convs are bound by tcgen05 instruction dispatch, not MMA
+        # math (ncu: TC pipe 66% busy, tensor math 23% at N=48): a pair issues
+        # one M=256 instruction where two CTAs issued two.
+        pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0
+                    and ((not conv and tmem_a and BN == 128 and K >= 256)
+                         or conv))
         stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * (BN // 2 if pair else BN) * BK * 4
         # epilogue through TMA stores (and a TMA-prefetched residual) for plain
         # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
@@ -490,7 +495,7 @@ class Specializer:
         if conv:
             ow = 16 - (kw - 1) if kpack else 16
             tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // ow)
-            ipi, ipb = tpi, 1
+            ipi, ipb = tpi, 2 if pair else 1
             tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
         else:
             ipi, ipb = rows, 256 if pair else 128
