@@ -118,7 +118,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75, mega=False):
+                 pair=True, tc_tile_use=0.75, mega=False, abuf=None):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -128,6 +128,7 @@ class Specializer:
         self.pair = pair
         self.tc_tile_use = tc_tile_use
         self.mega = mega
+        self.abuf = abuf
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
@@ -407,6 +408,11 @@ class Specializer:
         chunk = self.chunk or (16 if K <= 1024 else 8)
         cw = (2 if csplit else 1) * BN                # TMEM columns per accumulator chain
         ABUF = 1 if (tmem_a and BN > 64 and csplit) else 2
+        if not tmem_a and self.abuf:
+            # more accumulator buffers let the MMA run further ahead of the
+            # epilogue: a tile's commit -> drain -> release round trip costs
+            # ~1-2 us, which short tiles (few k-blocks) cannot hide with two
+            ABUF = max(1, min(self.abuf, 512 // (NACC * cw)))
         # CTA pairs (cta_group::2, 256-row tiles, each CTA holds half of B):
         # the BN = 128 row GEMMs, whose single-CTA form is bound by
         # shared-memory bandwidth (B is re-read by every product)
@@ -824,7 +830,7 @@ def tf32_split_hi(w, rn=True):
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False):
+               mega=False, abuf=None):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair, tc_tile_use, mega).run()
+                       split_rn, pair, tc_tile_use, mega, abuf).run()
