@@ -43,3 +43,18 @@ def test_tensor_core_path_vs_oracle(cfg, n):
     got = net.run([x])[0].cpu().numpy()
     want = oracle.run(m, w, [x], "exact")[0]
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("cfg,n", [(0, 4096), (1, 65536), (2, 1024), (3, 256), (4, 64)])
+def test_baseline_batch_sampled_images_vs_oracle(cfg, n):
+    """At the BASELINE batch sizes (the bench workloads): images are
+    independent, so a seeded sample of the batch is checked against the
+    oracle run on just those images, plus finiteness of the whole output."""
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=n)
+    x = zoo.inputs(cfg, n)
+    got = net.run([x])[0].cpu().numpy()
+    assert np.isfinite(got).all()
+    idx = np.sort(np.random.default_rng(cfg).choice(n, size=min(n, 6), replace=False))
+    want = oracle.run(m, w, [x[idx]], "exact")[0]
+    np.testing.assert_allclose(got[idx], want, rtol=RTOL, atol=ATOL)
