@@ -65,7 +65,26 @@ struct DenseSmallM {
       acc[r] = 0.f;
       xr[r] = x + (row0 + r < nrows ? in_row(row0 + r) : 0);
     }
-    if (j < C::CO) {
+    // float4 row loads when every warp's k range is 4-aligned (same fmaf
+    // order as the scalar loop, so results are identical)
+    constexpr bool V4 = C::K % (4 * C::KS) == 0 && C::IN_IMG % 16 == 0;
+    if (j < C::CO && V4) {
+#pragma unroll 2
+      for (int k = k0; k < k1; k += 4) {
+        float wv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wv[q] = __ldg(w + (i64)(k + q) * C::CO + j);
+#pragma unroll
+        for (int r = 0; r < C::MB; ++r)
+          if (row0 + r < nrows) {
+            const float4 xv = lda(reinterpret_cast<const float4*>(xr[r] + k));
+            acc[r] = fmaf(xv.x, wv[0], acc[r]);
+            acc[r] = fmaf(xv.y, wv[1], acc[r]);
+            acc[r] = fmaf(xv.z, wv[2], acc[r]);
+            acc[r] = fmaf(xv.w, wv[3], acc[r]);
+          }
+      }
+    } else if (j < C::CO) {
 #pragma unroll 4
       for (int k = k0; k < k1; ++k) {
         float wv = __ldg(w + (i64)k * C::CO + j);

@@ -118,7 +118,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75, mega=False, abuf=None):
+                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -129,6 +129,7 @@ class Specializer:
         self.tc_tile_use = tc_tile_use
         self.mega = mega
         self.abuf = abuf
+        self.small_dense_rows = small_dense_rows
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
@@ -252,6 +253,15 @@ class Specializer:
             if self.max_batch <= SMALL_M:
                 return
             n_min = SMALL_M + 1
+            # a few hundred rows: the same split-K kernel with 8 rows per block
+            # keeps every SM busy, where a tiled GEMM would run a handful of
+            # CTAs through a serial K loop
+            if self.small_dense_rows > SMALL_M:
+                hi = min(self.small_dense_rows, self.max_batch)
+                self._dense_small(pos, u, wmat, CI, CO, softmax, n_max=hi, mb=8, n_min=n_min)
+                if self.max_batch <= hi:
+                    return
+                n_min = hi + 1
         else:
             n_min = 1
 
@@ -536,7 +546,7 @@ class Specializer:
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
                        f"{4 if pool_fused else pxt}")
 
-    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None):
+    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None, n_min=1):
         """Split-K GEMV/GEMM for few rows: Dense at n <= n_max (MB = n_max
         rows per block), or a 1x1 conv whose n*rows pixels are the rows (MB
         = ``mb`` per block)."""
@@ -555,7 +565,7 @@ class Specializer:
             raise UnsupportedLayer("fused softmax needs <= 32 units")
         nj = (CO + 31) // 32
         self.emit(pos, "gemv" if rows == 1 else "conv1x1_rows", "nnb::DenseSmallM", fields,
-                  32 * KS, 0, rows, MB, grid_mult=nj, n_max=n_max,
+                  32 * KS, 0, rows, MB, grid_mult=nj, n_min=n_min, n_max=n_max,
                   note=f"split-K rows K={K} N={CO} ks={KS} rows/block {MB}")
 
     def depthwise(self, pos, u):
@@ -830,7 +840,7 @@ def tf32_split_hi(w, rn=True):
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False, abuf=None):
+               mega=False, abuf=None, small_dense_rows=512):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair, tc_tile_use, mega, abuf).run()
+                       split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows).run()

@@ -81,7 +81,8 @@ class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
                  nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
-                 split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None):
+                 split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
+                 small_dense_rows=512):
         import torch
 
         t0 = time.perf_counter()
@@ -103,7 +104,8 @@ class CompiledNetwork:
                           tc_min_rows=TC_MIN_ROWS if tc_min_rows is None else tc_min_rows,
                           tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack, epi_tma=epi_tma,
                           csplit=csplit, chunk=chunk, split_rn=split_rn,
-                          pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf)
+                          pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf,
+                          small_dense_rows=small_dense_rows)
         arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 
         def io(tids):
