@@ -2,7 +2,7 @@
 // CO <= 32): the network stems and the small encoder layers.
 //
 // At K = KH*KW*CI <= 144 an implicit GEMM spends its time on tile staging and
-// index arithmetic, not on FMAs.  Here every thread owns PY x PX output pixels
+// index arithmetic, not on FMAs.  Here every thread owns NP output pixels
 // and all CO output channels in registers, walks the taps in the interpreter's
 // (ky, kx, ci) order (accumulators start at the bias; pkg/src/nnjit/
 // interpreter.py:52-62) with float4 loads along the channels when CI % 4 == 0,
@@ -33,13 +33,49 @@ struct ConvDirect {
     for (int i = threadIdx.x; i < C::CO; i += nnb_bdim()) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
     nnb_sync();
 
+    // Pixel ownership.  POOL: a thread owns one 2x2 window (consecutive lanes,
+    // consecutive windows).  Otherwise the PX pixels of a thread are 32 apart
+    // in the flattened (image, row, column) order and consecutive lanes take
+    // consecutive pixels, so every warp load covers 32 neighbouring pixels
+    // (PX adjacent pixels per thread made lanes PX*S pixels apart: 4-8x the
+    // cache lines per load).
     const i64 cell = nnb_bid() * nnb_bdim() + threadIdx.x;
-    if (cell >= (i64)n * CELLS_Y * CELLS_X) return;
-    const int cx = (int)(cell % CELLS_X);
-    const int cy = (int)((cell / CELLS_X) % CELLS_Y);
-    const i64 img = cell / ((i64)CELLS_X * CELLS_Y);
-    const int oy0 = cy * PY, ox0 = cx * PX;
-    const float* in = at<float>(arena, C::IN_OFF + img * C::IN_IMG);
+    int oyp[NP], oxp[NP];
+    const float* inp[NP];
+    i64 imgp[NP];
+    bool live[NP];
+    if (C::POOL) {
+      const bool ok = cell < (i64)n * CELLS_Y * CELLS_X;
+      const int cx = (int)(cell % CELLS_X);
+      const int cy = (int)((cell / CELLS_X) % CELLS_Y);
+      const i64 img = ok ? cell / ((i64)CELLS_X * CELLS_Y) : 0;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        oyp[p] = cy * PY + p / PX;
+        oxp[p] = cx * PX + p % PX;
+        imgp[p] = img;
+        live[p] = ok;
+      }
+      if (!ok) return;
+    } else {
+      constexpr i64 HW = (i64)C::HO * C::WO;
+      const i64 base = (cell >> 5) * (32 * PX) + (cell & 31);
+      bool any = false;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const i64 q = base + 32 * p;
+        live[p] = q < (i64)n * HW;
+        any |= live[p];
+        const i64 qq = live[p] ? q : 0;
+        imgp[p] = qq / HW;
+        const int r = (int)(qq - imgp[p] * HW);
+        oyp[p] = r / C::WO;
+        oxp[p] = r % C::WO;
+      }
+      if (!any) return;
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) inp[p] = at<float>(arena, C::IN_OFF + imgp[p] * C::IN_IMG);
 
     float acc[NP][C::CO];
 #pragma unroll
@@ -56,10 +92,10 @@ struct ConvDirect {
           float xv[NP][CV];
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
-            const int iy = (oy0 + p / PX) * C::S - C::PT + ky;
-            const int ix = (ox0 + p % PX) * C::S - C::PL + kx;
+            const int iy = oyp[p] * C::S - C::PT + ky;
+            const int ix = oxp[p] * C::S - C::PL + kx;
             const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
-            const float* src = in + ((i64)iy * C::W + ix) * C::CI + c0;
+            const float* src = inp[p] + ((i64)iy * C::W + ix) * C::CI + c0;
             if (CV == 4) {
               float4 v = ok ? lda(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
               xv[p][0] = v.x; xv[p][CV > 1 ? 1 : 0] = v.y; xv[p][CV > 2 ? 2 : 0] = v.z; xv[p][CV > 3 ? 3 : 0] = v.w;
@@ -102,22 +138,34 @@ struct ConvDirect {
 #pragma unroll
       for (int o = 0; o < C::CO; ++o) acc[p][o] = finish<C::ACT, C::MODE, C::POST>(acc[p][o], ps, po, o);
 
-    float* out = at<float>(arena, C::OUT_OFF + img * C::OUT_IMG);
     if (C::POOL) {
-      float* dst = out + ((i64)cy * C::PWO + cx) * C::CO;
+      float* dst = at<float>(arena, C::OUT_OFF + imgp[0] * C::OUT_IMG) +
+                   ((i64)(oyp[0] / 2) * C::PWO + oxp[0] / 2) * C::CO;
+      if (C::CO % 4 == 0) {
 #pragma unroll
-      for (int o = 0; o < C::CO; ++o)
-        dst[o] = fmaxf(fmaxf(acc[0][o], acc[1][o]), fmaxf(acc[2][o], acc[3][o]));
+        for (int o = 0; o < C::CO; o += 4) {
+          float m4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            m4[i] = fmaxf(fmaxf(acc[0][o + i], acc[1][o + i]), fmaxf(acc[2][o + i], acc[3][o + i]));
+          *reinterpret_cast<float4*>(dst + o) = make_float4(m4[0], m4[1], m4[2], m4[3]);
+        }
+      } else {
+#pragma unroll
+        for (int o = 0; o < C::CO; ++o)
+          dst[o] = fmaxf(fmaxf(acc[0][o], acc[1][o]), fmaxf(acc[2][o], acc[3][o]));
+      }
       return;
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const int oy = oy0 + p / PX, ox = ox0 + p % PX;
-      if (ox >= C::WO) continue;
+      const int oy = oyp[p], ox = oxp[p];
+      if (!live[p]) continue;
+      float* out = at<float>(arena, C::OUT_OFF + imgp[p] * C::OUT_IMG);
       const i64 pix = (i64)oy * C::WO + ox;
       float* dst = out + (C::UPF > 1 ? ((i64)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) : pix) * C::CO;
       if (C::RES) {
-        const float* res = at<float>(arena, C::RES_OFF + img * C::OUT_IMG) + pix * C::CO;
+        const float* res = at<float>(arena, C::RES_OFF + imgp[p] * C::OUT_IMG) + pix * C::CO;
 #pragma unroll
         for (int o = 0; o < C::CO; ++o) acc[p][o] = add(acc[p][o], lda(res + o));
       }

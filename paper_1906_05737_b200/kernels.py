@@ -539,9 +539,11 @@ class Specializer:
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO))
-        cells = PHO * PWO if pool_fused else HO * -(-WO // pxt)
+        # pool: one 2x2 window per thread; else pxt pixels per thread, the
+        # 128-thread block covering 128*pxt consecutive pixels
+        ipi, ipb = (PHO * PWO, 128) if pool_fused else (HO * WO, 128 * pxt)
         smem = 4 * (KH * KW * CI * CO + CO)
-        self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, cells, 128,
+        self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, ipi, ipb,
                   dynamic_smem=True, n_min=n_min,
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
                        f"{4 if pool_fused else pxt}")
