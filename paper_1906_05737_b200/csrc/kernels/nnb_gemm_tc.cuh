@@ -371,8 +371,18 @@ struct GemmTc {
   // tensor core reads only B from shared memory -- for narrow N the A re-reads
   // (three products per k-step) otherwise saturate shared-memory bandwidth.
   static constexpr bool TA = C::TMEM_A != 0;
-  static constexpr int A_SMEM = TA ? A_BYTES : 2 * A_BYTES;     // A (+ A_lo) in smem
-  static constexpr int STAGE = A_SMEM + 2 * B_BYTES;
+  // DWF: a depthwise conv fused as the A producer of this 1x1 conv.  A stage
+  // then carries the depthwise INPUT halo of the 8 x 16 pixel tile (one 4-D
+  // TMA box, zero-filled borders = 'same' padding) instead of an A tile; the
+  // A-split warps compute the depthwise output (bias, taps in order, mul then
+  // add, activation / post-BN) and hand it to the MMA like any A tile.
+  static constexpr bool DWF = C::DWF != 0;
+  static constexpr int HALO_W = DWF ? 15 * C::DW_S + C::DW_KW : 0;   // (16-1)*S + KW
+  static constexpr int HALO_H = DWF ? 7 * C::DW_S + C::DW_KH : 0;    // (8-1)*S + KH
+  static constexpr int HALO_TX = HALO_W * HALO_H * BK * 4;           // bytes the box delivers
+  static constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
+  static constexpr int A_SMEM = (TA ? (DWF ? 0 : A_BYTES) : 2 * A_BYTES);  // A (+ A_lo) in smem
+  static constexpr int STAGE = A_SMEM + 2 * B_BYTES + HALO_BYTES;
   static constexpr int KB = (C::K + BK - 1) / BK;
   static constexpr int NTN = C::NPAD / C::BN;
   // One accumulator buffer = main (a_hi*b_hi) + correction (a_hi*b_lo + a_lo*b_hi)
@@ -411,7 +421,7 @@ struct GemmTc {
   static constexpr bool AL = C::ALDG != 0;
   static_assert(!(AL && TA), "A via LDGSTS lives in shared memory");
   static_assert(!PAIR || (!AL && C::BN % 16 == 0 && (C::BN / 2) % 8 == 0), "CTA-pair tile shape");
-  static constexpr int CONV_WARPS = (TA || AL) ? 4 : 2;           // A splitters
+  static constexpr int CONV_WARPS = (TA || AL || DWF) ? 4 : 2;    // A splitters
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
@@ -435,6 +445,8 @@ struct GemmTc {
   static_assert(!KP || (C::CONV && !C::POOL && !C::RES && C::CO % 16 == 0 &&
                         C::KW * C::CO == C::N), "KPACK geometry");
   static_assert(STAGE % 1024 == 0, "stage alignment");
+  static_assert(!DWF || (C::CONV && !KP && !AL && C::KW == 1 && C::CI % BK == 0),
+                "depthwise fusion: 1x1 conv tiles");
   // EPI_TMA: the epilogue writes the tile into 64B-swizzled shared-memory
   // boxes of 32 rows x 16 columns (the layout a lane = row thread writes
   // without bank conflicts) and stores them with TMA; a residual operand is
@@ -460,6 +472,7 @@ struct GemmTc {
                                    (reinterpret_cast<u64>(smem_raw) + 1023) & ~(u64)1023)
                              : smem_raw;
     if (!TA && (smem_u32(smem_raw) & 1023u)) __trap();
+    if (blockDim.x != THREADS) __trap();          // role layout needs every warp
     float4* epi_stage = reinterpret_cast<float4*>(smem + C::NS * STAGE);
     u64* bars = reinterpret_cast<u64*>(smem + C::NS * STAGE + EPI_STAGE);
     u64* full = bars;                 // [NS]  TMA landed
@@ -533,11 +546,18 @@ struct GemmTc {
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
-            mbar_expect_tx(&full[s], (NNB_TC_DBG & 2) ? 0 : (AL ? 0 : A_BYTES) + 2 * B_BYTES);
+            mbar_expect_tx(&full[s], (NNB_TC_DBG & 2) ? 0
+                                     : (AL ? 0 : DWF ? HALO_TX : A_BYTES) + 2 * B_BYTES);
             if (NNB_TC_DBG & 2) {
               // diagnostic: no operand traffic
             } else if (AL) {
               // A is gathered by the loader warps
+            } else if (DWF) {
+              // depthwise input halo of the tile, channel block kb
+              const int img = mb / TPI, tt = mb % TPI;
+              tma_load_4d(st + A_SMEM + 2 * B_BYTES, tmA, &full[s], kb * BK,
+                          (tt % TX) * TW * C::DW_S - C::DW_PL,
+                          (tt / TX) * TH * C::DW_S - C::DW_PT, img);
             } else if (C::CONV) {
               // tap (ky, kx) and channel block cb of an 8x16 output-pixel tile;
               // out-of-image coordinates are zero-filled = 'same' padding
@@ -627,6 +647,84 @@ struct GemmTc {
           }
         }
       }
+      }
+    } else if (warp < EPI_W0 && DWF) {
+      // ---------------- depthwise producer: halo -> A tile (TMEM or smem) ----------------
+      const int q = warp & 3, r = q * 32 + lane;      // tile pixel = A row = TMEM lane
+      const int ty = r / TW, tx = r % TW;
+      const float* dwk = at<float>(pool, C::DW_W_OFF);
+      const float* dwb = at<float>(pool, C::DW_B_OFF);
+      const float* dps = at<float>(pool, C::DW_PS_OFF);
+      const float* dpo = at<float>(pool, C::DW_PO_OFF);
+      int s = 0;
+      u32 ph = 0;
+      for (int t = t0; t < tiles; t += tstep) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[s], ph);
+          const unsigned char* halo = smem + s * STAGE + A_SMEM + 2 * B_BYTES;
+          unsigned char* arow = smem + s * STAGE + r * ROWB;
+          const int c0 = kb * BK;
+          const u32 ta = tmem + ((u32)(q * 32) << 16) + A_TCOL + s * 2 * BK;
+#pragma unroll
+          for (int hh = 0; hh < BK / 16; ++hh) {
+            float a[16];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = hh * 4 + jj;
+              float4 acc = __ldg(reinterpret_cast<const float4*>(dwb + c0 + 4 * j));
+#pragma unroll
+              for (int ky = 0; ky < C::DW_KH; ++ky)
+#pragma unroll
+                for (int kx = 0; kx < C::DW_KW; ++kx) {
+                  const int hp = (ty * C::DW_S + ky) * HALO_W + tx * C::DW_S + kx;
+                  const int pj = ROWB == 128 ? (j ^ (hp & 7)) : (j ^ ((hp >> 1) & 3));
+                  const float4 x = *reinterpret_cast<const float4*>(halo + hp * ROWB + (pj << 4));
+                  const float4 w = __ldg(reinterpret_cast<const float4*>(
+                      dwk + (ky * C::DW_KW + kx) * C::CI + c0 + 4 * j));
+                  acc.x = add(acc.x, mul(x.x, w.x)); acc.y = add(acc.y, mul(x.y, w.y));
+                  acc.z = add(acc.z, mul(x.z, w.z)); acc.w = add(acc.w, mul(x.w, w.w));
+                }
+              const int c = c0 + 4 * j;
+              a[4 * jj + 0] = finish<C::DW_ACT, EMODE, C::DW_POST>(acc.x, dps, dpo, c);
+              a[4 * jj + 1] = finish<C::DW_ACT, EMODE, C::DW_POST>(acc.y, dps, dpo, c + 1);
+              a[4 * jj + 2] = finish<C::DW_ACT, EMODE, C::DW_POST>(acc.z, dps, dpo, c + 2);
+              a[4 * jj + 3] = finish<C::DW_ACT, EMODE, C::DW_POST>(acc.w, dps, dpo, c + 3);
+            }
+            if constexpr (TA) {
+              u32 hi[16], lo[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                hi[i] = split_hi(a[i]);
+                lo[i] = __float_as_uint(a[i] - __uint_as_float(hi[i]));
+              }
+              tmem_st<16>(ta + hh * 16, hi);
+              tmem_st<16>(ta + BK + hh * 16, lo);
+            } else {
+              // raw value as A (the tensor core truncates it) and lo = a - trunc(a)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int j = hh * 4 + jj;
+                const int pj = ROWB == 128 ? (j ^ (r & 7)) : (j ^ ((r >> 1) & 3));
+                float4 v = make_float4(a[4 * jj], a[4 * jj + 1], a[4 * jj + 2], a[4 * jj + 3]);
+                float4 l;
+                l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                *reinterpret_cast<float4*>(arow + (pj << 4)) = v;
+                *reinterpret_cast<float4*>(arow + A_BYTES + (pj << 4)) = l;
+              }
+            }
+          }
+          if constexpr (TA) {
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+          } else {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
+          arrive_mma(&lo_ready[s]);
+          if (++s == C::NS) { s = 0; ph ^= 1; }
+        }
       }
     } else if (warp < EPI_W0 && TA) {
       // ---------------- converter: A row -> (hi, lo) columns in TMEM ----------------

@@ -118,7 +118,8 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512):
+                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
+                 tc_min_k=TC_MIN_K):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -130,6 +131,7 @@ class Specializer:
         self.mega = mega
         self.abuf = abuf
         self.small_dense_rows = small_dense_rows
+        self.tc_min_k = tc_min_k
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
@@ -277,7 +279,7 @@ class Specializer:
         n_max = 1 << 30
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
                    and u.dw is None
-                   and PT == PL == 0 and K % 4 == 0 and K >= TC_MIN_K and CO >= TC_MIN_N)
+                   and PT == PL == 0 and K % 4 == 0 and K >= self.tc_min_k and CO >= TC_MIN_N)
         # implicit-GEMM tiles are 8 x 16 output pixels of one image: small images
         # waste most of a tile (cfg0's 8x8 conv: 0.103 ms on tensor cores vs
         # 0.046 ms as an FFMA GEMM), so require tc_tile_use (75%) useful pixels
@@ -285,7 +287,14 @@ class Specializer:
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
                    and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16
                    and tile_use >= self.tc_tile_use)
-        if tc_rows or tc_conv:
+        # pointwise conv with its depthwise producer fused in (planner
+        # fuse_dw_pw): 8 x 16-pixel tiles whose A operand the split warps
+        # compute from a TMA'd depthwise-input halo
+        tc_dwf = (self.use_tc and u.dw is not None and u.kind == "Conv2D" and not softmax
+                  and not pool_fused and UPF == 1 and not concat and KH == KW == S == 1
+                  and CI % 16 == 0 and CO >= 16 and u.dw.stride in (1, 2)
+                  and tile_use >= self.tc_tile_use)
+        if tc_rows or tc_conv or tc_dwf:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
             if n_tc <= self.max_batch:
                 conv = None
@@ -293,6 +302,9 @@ class Specializer:
                     conv = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, KW=KW, PT=PT, PL=PL,
                                 POOL=pool_fused, PHO=PHO, PWO=PWO, C0=C0,
                                 CONCAT=concat, UPF=UPF)
+                if tc_dwf:
+                    conv = dict(H=HO, W=WO, CI=CI, HO=HO, WO=WO, KW=1, PT=0, PL=0,
+                                POOL=False, PHO=1, PWO=1, C0=CI, CONCAT=False, UPF=1, DWF=1)
                 self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
                               rows_geo=dict(HO=HO, WO=WO, UPF=UPF))
                 n_max = n_tc - 1
@@ -365,8 +377,9 @@ class Specializer:
             simt(TM, n_min, n_max)
 
     def _dw_fields(self, u):
-        """Fields of a fused depthwise producer (GemmSimt DW loader)."""
-        d = u.dw
+        """Fields of a fused depthwise producer (GemmSimt DW loader, tcgen05
+        DWF); defaults when ``u`` is None or has none."""
+        d = u.dw if u is not None else None
         if d is None:
             return dict(DW=0, DW_H=1, DW_W=1, DW_S=1, DW_PT=0, DW_PL=0, DW_KH=1, DW_KW=1,
                         DW_W_OFF=0, DW_B_OFF=0, DW_ACT=0, DW_POST=0, DW_PS_OFF=0, DW_PO_OFF=0)
@@ -400,8 +413,15 @@ class Specializer:
         if kpack:
             BN = CO
         NPAD = -(-CO // BN) * BN
+        dwf = bool(conv and conv.get("DWF"))
         KPAD = -(-K // 32) * 32 if not conv or conv["CI"] % 32 == 0 else -(-K // 16) * 16
         BK = 32 if (not conv or (conv["CI"] % 32 == 0 and conv["C0"] % 32 == 0)) else 16
+        if dwf and u.dw.stride > 1:
+            BK = 16                                 # the stride-2 halo is 33 x 17 pixels
+        halo_w = halo_h = 0
+        if dwf:
+            dkh, dkw = u.dw.kernel_hw
+            halo_w, halo_h = 15 * u.dw.stride + dkw, 7 * u.dw.stride + dkh
         sw = 3 if BK == 32 else 2                  # TMA swizzle: 128 B or 64 B rows
         # independent accumulator chains fill TMEM (2 buffers x NACC x (main, corr))
         NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
@@ -432,7 +452,9 @@ class Specializer:
         pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0
                     and ((not conv and tmem_a and BN == 128 and K >= 256)
                          or conv))
-        stage = (1 if tmem_a else 2) * 128 * BK * 4 + 2 * (BN // 2 if pair else BN) * BK * 4
+        a_smem = (0 if dwf else 128 * BK * 4) if tmem_a else 2 * 128 * BK * 4
+        halo_bytes = -(-(halo_w * halo_h * BK * 4) // 1024) * 1024
+        stage = a_smem + 2 * (BN // 2 if pair else BN) * BK * 4 + halo_bytes
         # epilogue through TMA stores (and a TMA-prefetched residual) for plain
         # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
         res = u.residual_id is not None
@@ -453,7 +475,7 @@ class Specializer:
         lo = (wt - hi).astype(F32)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
-                   C0=1, CONCAT=0, UPF=1)
+                   C0=1, CONCAT=0, UPF=1, DWF=0)
         if conv:
             geo.update(conv, CONV=1)
         elif rows_geo:
@@ -478,6 +500,7 @@ class Specializer:
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO_real))
+        fields.update(self._dw_fields(u) if dwf else self._dw_fields(None))
         if conv:
             H, W = conv["H"], conv["W"]
 
@@ -488,6 +511,12 @@ class Specializer:
             tm_a = act_map(u.input_ids[0], conv["C0"])
             tm_a1 = (act_map(u.input_ids[1], conv["CI"] - conv["C0"]) if conv["CONCAT"]
                      else tm_a)
+            if dwf:                # the depthwise input, one halo box per tile
+                dh, dw_, dc = u.dw.input_shapes[0].dims
+                tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
+                            dims=(dc, dw_, dh, self.cap), box=(BK, halo_w, halo_h, 1),
+                            strides=(4 * dc, 4 * dc * dw_, 4 * dc * dw_ * dh), swizzle=sw)
+                tm_a1 = tm_a
 
             def out_map(tid):      # epilogue boxes: 16 channels x 16 px x 2 rows
                 return dict(space=1, offset=self.arena_off(tid), dims=(CO, conv["WO"], conv["HO"], self.cap),
@@ -516,7 +545,7 @@ class Specializer:
         else:
             ipi, ipb = rows, 256 if pair else 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg) else 384, smem,
+        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
                   n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r],
@@ -526,6 +555,7 @@ class Specializer:
                        f" chains {NACC} bufs {ABUF}{'' if csplit else ' merged-corr'}"
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
+                       f"{' depthwise fused' if dwf else ''}"
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
@@ -842,7 +872,8 @@ def tf32_split_hi(w, rn=True):
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False, abuf=None, small_dense_rows=512):
+               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows).run()
+                       split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows,
+                       tc_min_k).run()

@@ -486,9 +486,13 @@ def fuse_dw_pw(plan):
 
 def build_plan(graph, gpu_fusion=True, dw_fusion=False):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
-    ``dw_fusion`` (off by default: measured slower than a depthwise kernel
-    followed by the tcgen05 pointwise GEMM) folds depthwise convs into the
-    pointwise conv's FFMA loader."""
+    ``dw_fusion`` (off by default) folds depthwise convs into the pointwise
+    conv's operand loader -- the FFMA GEMM's, or the tcgen05 GEMM's split
+    warps (kernels.py tc_dwf).  Measured on B200 it only breaks even with a
+    depthwise kernel followed by the tcgen05 pointwise GEMM (cfg3 @256: 30.6
+    vs 32.4 us, 37.7 vs 34.0 us per block; cfg2 @1024: 113 vs 109 us): the
+    fused kernel is bound by the depthwise math on its four split warps, and
+    images under 75% of a 8 x 16 tile fall back to the slower FFMA form."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
         fuse_pool(plan)

@@ -104,7 +104,8 @@ def test_decoder_fusions(c0, c1, co, up_src, tc):
 
 @pytest.mark.parametrize("h,w,c,co,s,act,bn,n", [
     (9, 13, 8, 16, 1, "relu6", True, 3), (16, 16, 16, 32, 2, "relu", False, 2),
-    (7, 10, 64, 128, 2, "elu", True, 2), (8, 8, 128, 96, 1, "linear", False, 5)])
+    (7, 10, 64, 128, 2, "elu", True, 2), (8, 8, 128, 96, 1, "linear", False, 5),
+    (20, 35, 32, 64, 1, "relu6", True, 3), (33, 30, 16, 48, 2, "relu", True, 2)])
 def test_depthwise_pointwise_fusion(h, w, c, co, s, act, bn, n):
     """DepthwiseConv2D (+BN+act) computed inside the pointwise conv's loader."""
     rng = np.random.default_rng(h * w + c)
@@ -124,6 +125,10 @@ def test_depthwise_pointwise_fusion(h, w, c, co, s, act, bn, n):
     got, net = gpu(m, wt, xin, dw_fusion=True)
     assert [u.kind for u in net.plan.units] == ["Conv2D"] and net.plan.units[0].dw is not None
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+    if c % 16 == 0 and co >= 16:          # the tcgen05 form (halo TMA + fused split warps)
+        got, net = gpu(m, wt, xin, dw_fusion=True, tc_min_rows=1, tc_tile_use=0)
+        assert any("depthwise fused" in l.note for l in net.artifact.launches)
+        np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
 
 @pytest.mark.parametrize("k,units,act,n", [
