@@ -217,7 +217,10 @@ def ncu_traffic(kernel):
     try:
         rows = list(csv.reader(open(p)))
         h, units, v = rows[0], rows[1], rows[2]
-        if v[h.index("Kernel Name")] != kernel:
+        # kernel names end in a schedule index (nnb_u<unit>_<kind>_<i>); the
+        # capture matches when the unit and kind agree
+        stem = lambda k: k.rsplit("_", 1)[0]
+        if stem(v[h.index("Kernel Name")].strip('"')) != stem(kernel):
             return {"traffic": None}
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = sum(float(v[h.index(m)]) * scale[units[h.index(m)]]
