@@ -49,6 +49,9 @@
 #ifndef NNB_SPLIT_RN
 #define NNB_SPLIT_RN 1
 #endif
+#ifndef NNB_WIDE_STREAM
+#define NNB_WIDE_STREAM 0
+#endif
 #ifndef NNB_HI_INPLACE
 #define NNB_HI_INPLACE 0
 #endif
@@ -409,11 +412,21 @@ struct GemmTc {
   static constexpr int ABUF = C::ABUF;
   static constexpr int A_TCOL = ABUF * ACC_COLS;                 // first A column (TA)
   static constexpr int TMEM_NEED = TA ? ABUF * ACC_COLS + C::NS * 2 * BK : ABUF * ACC_COLS;
+#ifdef NNB_TC_NDBG
+  static constexpr int TMEM_COLS = 512;
+#else
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64
                                  : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+#endif
   static_assert(TMEM_NEED <= 512, "TMEM budget");
+#ifdef NNB_TC_NDBG
+  // diagnostic: issue MMAs of width NNB_TC_NDBG (results meaningless)
+  static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(NNB_TC_NDBG >> 3) << 17) |
+                               ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
+#else
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
+#endif
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
@@ -427,7 +440,17 @@ struct GemmTc {
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
   static constexpr int CHUNK_KB = C::CHUNK;          // k-blocks per TMEM chunk
   static constexpr int NCHUNK = (KB + CHUNK_KB - 1) / CHUNK_KB;
-  static_assert(C::BN % 16 == 0 && C::BN >= 16 && C::BN <= 128, "UMMA N / TMEM budget");
+  // WIDE: N = 256 per MMA (a tcgen05 kind::tf32 instruction costs ~100
+  // cycles at N <= 128 and ~1.4x that at N = 256, scripts/mma_n256.py), with
+  // the whole K in one accumulator chunk and the epilogue streaming each
+  // 16-column group TMEM -> activation -> TMA box (no register-resident sums)
+  static constexpr bool WIDE = C::BN > 128;
+  static_assert(C::BN % 16 == 0 && C::BN >= 16 && (C::BN <= 128 || C::BN == 256),
+                "UMMA N / TMEM budget");
+  static_assert(!C::CORR_WHOLE || (CS && C::NACC == 1), "whole-K correction chain");
+  static_assert(!WIDE || (!TA && C::NACC == 1 && !C::CONV && !C::RES && C::UPF == 1 &&
+                          C::EPI_TMA && C::ABUF * (C::CSPLIT ? 2 : 1) * C::BN <= 512),
+                "N = 256 tiles: A in shared memory, TMA epilogue, 512 TMEM columns");
   // spatial (implicit-GEMM convolution) tiling: 8 x 16 output pixels per tile
   static constexpr int TH = 8, TW = 16;
   // KPACK: the KW horizontal taps are packed into N (N = KW*CO, K = KH*CI): a
@@ -610,10 +633,17 @@ struct GemmTc {
             for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
               const int ks = kc * (BK / 8) + k;                  // k-step within the chunk
+#ifdef NNB_TC_NDBG
+              const u32 d = tmem, dc = tmem;                     // diagnostic width test
+#else
               const u32 d = dbuf + (ks % NACC) * CW;             // this step's chain
               const u32 dc = CS ? d + C::BN : d;                 // its correction columns
+#endif
               const u32 accum = ks >= NACC;
-              const u32 acc_c = CS ? accum : 1u;
+              // CORR_WHOLE: the correction chain runs over the whole K (its
+              // values are ~2^-11 of the main sum, so its truncations are
+              // negligible); only the main chain restarts per chunk
+              const u32 acc_c = CS ? (C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : accum) : 1u;
               if (PAIR && TA) {
                 mma_tf32_ts_pair(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts_pair(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
@@ -991,6 +1021,48 @@ struct GemmTc {
           }
           continue;
         }
+        if constexpr (WIDE && NNB_WIDE_STREAM) {
+          static_assert(NCHUNK == 1, "N = 256 tiles keep the whole K in one chunk");
+          mbar_wait(&tfull[acc], aph);
+          tc_fence_after();
+#pragma unroll 1
+          for (int g = 0; g < EPI_COLS / 16; ++g) {
+            const int col0 = nb * C::BN + cbeg + g * 16;
+            if (col0 >= C::N) break;                           // warp-uniform
+            u32 rv[16], rc[16];
+            const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + cbeg + g * 16;
+            tmem_ld16_async(ta, rv);
+            tmem_ld16_async(ta + C::BN, rc);
+            tmem_wait_ld();
+            tmem_pin(rv);
+            tmem_pin(rc);
+            float4* b = ebuf + (g % NBUF) * 128;
+            if (lane == 0) bulk_wait_read<NBUF - 1>();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float y[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int k = 4 * j + i;
+                const int col = col0 + k < C::N ? col0 + k : C::N - 1;
+                y[i] = finish<C::ACT, EMODE, C::POST>(
+                    __uint_as_float(rv[k]) + __uint_as_float(rc[k]) + __ldg(bias + col), ps, po, col);
+              }
+              b[stage_slot<16>(lane, j)] = make_float4(y[0], y[1], y[2], y[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              box_io(false, b, col0);
+              bulk_commit();
+            }
+          }
+          tc_fence_before();
+          arrive_mma(&tempty[acc]);
+          if (++acc == ABUF) { acc = 0; aph ^= 1; }
+          continue;
+        }
         // FP32 (round-to-nearest) reduction of the per-chunk tensor-core sums
         float run[EPI_COLS];
 #pragma unroll
@@ -1004,6 +1076,7 @@ struct GemmTc {
           // (32 loaded registers per batch: the 64-column running sums stay in
           // registers next to them)
           constexpr int GB = (EPI_COLS / 16 >= 2 && !CS) ? 2 : 1;
+          const bool rd_c = CS && (!C::CORR_WHOLE || ch == NCHUNK - 1);   // correction read
 #pragma unroll
           for (int g0 = 0; g0 < ((NNB_TC_DBG & 8) ? 0 : EPI_COLS / 16); g0 += GB) {
             if (cbeg + g0 * 16 < C::BN) {            // warp-uniform (whole batch valid)
@@ -1016,17 +1089,17 @@ struct GemmTc {
                   const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + c * CW +
                                  cbeg + (g0 + b) * 16;
                   tmem_ld16_async(ta, rv[b]);
-                  if (CS) tmem_ld16_async(ta + C::BN, rc[b]);
+                  if (rd_c) tmem_ld16_async(ta + C::BN, rc[b]);
                 }
                 tmem_wait_ld();
 #pragma unroll
                 for (int b = 0; b < GB; ++b) {
                   tmem_pin(rv[b]);
-                  if (CS) tmem_pin(rc[b]);
+                  if (rd_c) tmem_pin(rc[b]);
 #pragma unroll
                   for (int i = 0; i < 16; ++i)
-                    run[(g0 + b) * 16 + i] += CS ? __uint_as_float(rv[b][i]) + __uint_as_float(rc[b][i])
-                                                 : __uint_as_float(rv[b][i]);
+                    run[(g0 + b) * 16 + i] += rd_c ? __uint_as_float(rv[b][i]) + __uint_as_float(rc[b][i])
+                                                   : __uint_as_float(rv[b][i]);
                 }
               }
             }

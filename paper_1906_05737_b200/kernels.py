@@ -119,7 +119,8 @@ class Specializer:
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
-                 tc_min_k=TC_MIN_K):
+                 tc_min_k=TC_MIN_K, wide=False, wide_bk=32, wide_chunk=None,
+                 wide_csplit=True):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -132,6 +133,10 @@ class Specializer:
         self.abuf = abuf
         self.small_dense_rows = small_dense_rows
         self.tc_min_k = tc_min_k
+        self.wide = wide
+        self.wide_bk = wide_bk
+        self.wide_chunk = wide_chunk
+        self.wide_csplit = wide_csplit
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
@@ -412,6 +417,14 @@ class Specializer:
         BN = min(128, -(-CO // 16) * 16) if CO < 32 else min(128, -(-CO // 32) * 32)
         if kpack:
             BN = CO
+        # N = 256 tiles for wide row GEMMs whose K fits one accumulator chunk:
+        # a kind::tf32 MMA costs ~1.4x at N = 256 what it costs at N = 128
+        res_ = u.residual_id is not None
+        wide = bool(self.wide and not conv and CO >= 256 and K <= 1024 and not res_
+                    and self.pair and not self.aldg and self.epi_tma and CO % 4 == 0
+                    and (not rows_geo or rows_geo.get("UPF", 1) == 1))
+        if wide:
+            BN = 256
         NPAD = -(-CO // BN) * BN
         dwf = bool(conv and conv.get("DWF"))
         KPAD = -(-K // 32) * 32 if not conv or conv["CI"] % 32 == 0 else -(-K // 16) * 16
@@ -427,6 +440,9 @@ class Specializer:
         NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
         aldg = self.aldg
         tmem_a = self.tmem_a and NACC == 1 and not aldg and (BN <= 64 or BN == 128)
+        if wide:
+            BK = self.wide_bk
+            sw = 3 if BK == 32 else 2
         csplit = self.csplit
         # k-blocks (of 32) per TMEM accumulator chunk: every chunk ends in a
         # drain the MMAs wait for (one accumulator buffer at BN = 128), so
@@ -436,8 +452,23 @@ class Specializer:
         # / 32; K=4096: 0.77 / 0.83 / 0.89.  dense 1024->512: 0.40 / 0.34 /
         # 0.32 ms at 65536 rows.
         chunk = self.chunk or (16 if K <= 1024 else 8)
+        corr_whole = False
+        if wide:
+            # one accumulator buffer of (main, correction) = 512 TMEM columns;
+            # the main chain restarts every 16 k-blocks (an accuracy bound: the
+            # tensor core truncates per MMA) while the small correction chain
+            # spans the whole K, so a mid-tile drain reads only the main half.
+            # Measured (tc_error.py / tc_error_wide.py, dense 1024->512 at
+            # 65536 rows): whole K in one chunk 0.26 ms but up to 1.05 of the
+            # FP32 tolerance on N(0,1) data; 16 k-blocks 0.317 ms at <= 0.69
+            # (BN = 128: 0.337 ms at <= 0.67); merged chains with two buffers
+            # 0.30-0.35 ms.  Opt-in (wide=True) until the accuracy matches.
+            csplit = self.wide_csplit
+            corr_whole = csplit
+            if not self.chunk:
+                chunk = self.wide_chunk or (16 if csplit else 4)
         cw = (2 if csplit else 1) * BN                # TMEM columns per accumulator chain
-        ABUF = 1 if (tmem_a and BN > 64 and csplit) else 2
+        ABUF = 1 if ((tmem_a and BN > 64 and csplit) or (wide and csplit)) else 2
         if not tmem_a and self.abuf:
             # more accumulator buffers let the MMA run further ahead of the
             # epilogue: a tile's commit -> drain -> release round trip costs
@@ -451,7 +482,7 @@ class Specializer:
         # one M=256 instruction where two CTAs issued two.
         pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0
                     and ((not conv and tmem_a and BN == 128 and K >= 256)
-                         or conv))
+                         or conv or wide))
         a_smem = (0 if dwf else 128 * BK * 4) if tmem_a else 2 * 128 * BK * 4
         halo_bytes = -(-(halo_w * halo_h * BK * 4) // 1024) * 1024
         stage = a_smem + 2 * (BN // 2 if pair else BN) * BK * 4 + halo_bytes
@@ -483,6 +514,7 @@ class Specializer:
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
+                      CORR_WHOLE=int(corr_whole),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
@@ -524,7 +556,7 @@ class Specializer:
                                                          self.img_bytes(tid)), swizzle=2)
         else:
             tm_a = dict(space=1, offset=self.arena_off(u.input_ids[0]),
-                        dims=(K, self.cap * rows), strides=(4 * K,), box=(32, 128))
+                        dims=(K, self.cap * rows), strides=(4 * K,), box=(BK, 128), swizzle=sw)
             tm_a1 = tm_a
 
             def out_map(tid):      # epilogue boxes: 16 columns x 32 rows
@@ -872,8 +904,9 @@ def tf32_split_hi(w, rn=True):
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K):
+               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K, wide=False,
+               wide_bk=32, wide_chunk=None, wide_csplit=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
                        split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows,
-                       tc_min_k).run()
+                       tc_min_k, wide, wide_bk, wide_chunk, wide_csplit).run()

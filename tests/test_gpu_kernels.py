@@ -387,3 +387,15 @@ def test_batch1_persistent_kernel_matches_oracle(cfg):
         np.testing.assert_allclose(got, ref(m, w, x), **TOL)
         if n == 1:
             assert coop and net.launches_for(1) == [net.artifact.launches.index(coop[0])]
+
+
+@pytest.mark.parametrize("k,units", [(1024, 512), (512, 256), (300, 260)])
+def test_wide_n256_tiles_opt_in(k, units):
+    """wide=True: N = 256 tcgen05 tiles (CTA pairs, whole-K correction chain,
+    main chain restarted every 16 k-blocks) against the oracle."""
+    rng = np.random.default_rng(k)
+    m, w = dense_net(rng, k, units, "tanh")
+    x = rng.uniform(-2, 2, (2100, k)).astype(F32)
+    got, net = gpu(m, w, x, wide=True)
+    assert any("256x256" in l.note for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
