@@ -49,9 +49,6 @@
 #ifndef NNB_SPLIT_RN
 #define NNB_SPLIT_RN 1
 #endif
-#ifndef NNB_WIDE_STREAM
-#define NNB_WIDE_STREAM 0
-#endif
 #ifndef NNB_HI_INPLACE
 #define NNB_HI_INPLACE 0
 #endif
@@ -441,9 +438,8 @@ struct GemmTc {
   static constexpr int CHUNK_KB = C::CHUNK;          // k-blocks per TMEM chunk
   static constexpr int NCHUNK = (KB + CHUNK_KB - 1) / CHUNK_KB;
   // WIDE: N = 256 per MMA (a tcgen05 kind::tf32 instruction costs ~100
-  // cycles at N <= 128 and ~1.4x that at N = 256, scripts/mma_n256.py), with
-  // the whole K in one accumulator chunk and the epilogue streaming each
-  // 16-column group TMEM -> activation -> TMA box (no register-resident sums)
+  // cycles at N <= 128 and ~1.4x that at N = 256, scripts/mma_n256.py); the
+  // epilogue keeps 128 running sums per thread (384 threads: 168 registers)
   static constexpr bool WIDE = C::BN > 128;
   static_assert(C::BN % 16 == 0 && C::BN >= 16 && (C::BN <= 128 || C::BN == 256),
                 "UMMA N / TMEM budget");
@@ -1019,48 +1015,6 @@ struct GemmTc {
             }
             __syncwarp();
           }
-          continue;
-        }
-        if constexpr (WIDE && NNB_WIDE_STREAM) {
-          static_assert(NCHUNK == 1, "N = 256 tiles keep the whole K in one chunk");
-          mbar_wait(&tfull[acc], aph);
-          tc_fence_after();
-#pragma unroll 1
-          for (int g = 0; g < EPI_COLS / 16; ++g) {
-            const int col0 = nb * C::BN + cbeg + g * 16;
-            if (col0 >= C::N) break;                           // warp-uniform
-            u32 rv[16], rc[16];
-            const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + cbeg + g * 16;
-            tmem_ld16_async(ta, rv);
-            tmem_ld16_async(ta + C::BN, rc);
-            tmem_wait_ld();
-            tmem_pin(rv);
-            tmem_pin(rc);
-            float4* b = ebuf + (g % NBUF) * 128;
-            if (lane == 0) bulk_wait_read<NBUF - 1>();
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float y[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int k = 4 * j + i;
-                const int col = col0 + k < C::N ? col0 + k : C::N - 1;
-                y[i] = finish<C::ACT, EMODE, C::POST>(
-                    __uint_as_float(rv[k]) + __uint_as_float(rc[k]) + __ldg(bias + col), ps, po, col);
-              }
-              b[stage_slot<16>(lane, j)] = make_float4(y[0], y[1], y[2], y[3]);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              box_io(false, b, col0);
-              bulk_commit();
-            }
-          }
-          tc_fence_before();
-          arrive_mma(&tempty[acc]);
-          if (++acc == ABUF) { acc = 0; aph ^= 1; }
           continue;
         }
         // FP32 (round-to-nearest) reduction of the per-chunk tensor-core sums
