@@ -437,6 +437,12 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
             "compile_ms": net.compile_ms, "configs": extra,
         }
+        import torch as _t
+        if world > max(1, _t.cuda.device_count()):
+            # several ranks on one device: their replays time-slice the GPU, so
+            # per-rank device times do not add up to a job rate
+            line["config"]["note"] = (f"{world} ranks share {_t.cuda.device_count()} GPU(s): "
+                                      "functional check only, value is not a throughput")
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
