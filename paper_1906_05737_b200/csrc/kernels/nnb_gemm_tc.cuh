@@ -1,33 +1,34 @@
-// nnb_gemm_tc.cuh -- tcgen05 (5th-gen tensor core) GEMM for Dense and 1x1
-// convolutions, FP32-accurate through the 3xTF32 split.
+// nnb_gemm_tc.cuh -- tcgen05 (5th-gen tensor core) GEMM for Dense layers, 1x1
+// convolutions ("rows" mode) and stride-1 KxK convolutions ("conv" mode:
+// implicit GEMM over 8 x 16-pixel tiles), FP32-accurate through 3xTF32.
 //
 //   C[m, j] = sum_k A[m, k] * B[k, j]            A: activations  [M, K] row-major
 //                                                B: weights, stored transposed
 //                                                   [Npad, Kpad] (K-major)
-// FP32 parity (rtol 1e-4 / atol 1e-5, BASELINE.json north_star) with TF32
-// inputs: every operand is split a = hi + lo with hi = a with the 13 low
-// mantissa bits cleared (exactly representable in TF32) and lo = a - hi
-// (exact in FP32), and the product is a_hi*b_hi + a_hi*b_lo + a_lo*b_hi
-// accumulated in FP32 in tensor memory -- the dropped a_lo*b_lo term and the
-// TF32 rounding of lo are below 2^-21 relative.  Weights are split once at
-// compile() time (B_hi, B_lo in the device pool); activations are split in
-// shared memory by two converter warps while the tensor core works on the
-// previous stage.
+// Every operand is split a = hi + lo (hi exactly representable in TF32, lo =
+// a - hi exact in FP32); the product is a_hi*b_hi + (a_hi*b_lo + a_lo*b_hi),
+// the first into a main TMEM chain and the two small ones into a correction
+// chain, both restarted every CHUNK k-blocks (the tensor core truncates once
+// per MMA) and summed in FP32 by the epilogue.  Weights are split at
+// compile() time (B_hi, B_lo in the pool); activations by the split warps.
+// Error bound and measurements: DESIGN.md section 4.
 //
-// Warp roles (384 threads, one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer: A tile [128 x 32] and B_hi/B_lo tiles [BN x 32],
-//               128B-swizzled, into an NS-stage ring (mbarrier full/empty)
-//   warp 1      TMEM allocator + single-thread MMA issuer:
-//               tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8
-//   warps 2-3   converter: A -> (A_hi in place, A_lo) in the same swizzled
-//               layout (elementwise, so the layout is preserved)
-//   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (the hardware's
-//               lane-quarter rule) and half of the tile's columns;
-//               tcgen05.ld 32 lanes x 16 columns, bias, activation,
-//               post-affine, then a shared-memory transpose so residual
-//               loads and stores are row-coalesced float4s.  The accumulator is
-//               double-buffered in TMEM so the epilogue of tile t overlaps the
-//               MMAs of tile t+1.
+// Warp roles (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A tile [128 x BK] (rows: 2-D box; conv: 4-D box
+//               of an 8x16-pixel tile per tap, zero-filled borders = 'same'
+//               padding; DWF: the depthwise input halo) and B_hi/B_lo tiles,
+//               swizzled, into an NS-stage mbarrier ring
+//   warp 1      TMEM allocator + single-thread MMA issuer
+//               (tcgen05.mma kind::tf32, M=128, or M=256 over a CTA pair)
+//   warps 2..   A-split warps: 2 (A_lo into shared memory) or 4 (A hi/lo into
+//               TMEM for the "ts" MMA form, or the fused depthwise producer)
+//   last 8      epilogue: warp w reads TMEM lanes 32*(w%4).. (lane-quarter
+//               rule) and half of the tile's columns; bias, activation,
+//               post-affine, residual, then TMA-store boxes (or staged /
+//               direct stores for pooled, upsampled and KPACK tiles)
+// Options per instantiation (Cfg fields): TMEM_A, PAIR (cta_group::2),
+// KPACK (horizontal taps packed into N), CONCAT (second A source), POOL,
+// UPF, RES, EPI_TMA, CSPLIT / CORR_WHOLE, CHUNK, ABUF, NACC, DWF, BN = 256.
 #pragma once
 #include "nnb_common.cuh"
 
