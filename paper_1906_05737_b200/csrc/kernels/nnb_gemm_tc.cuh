@@ -732,12 +732,18 @@ struct GemmTc {
               for (int jj = 0; jj < 4; ++jj) {
                 const int j = hh * 4 + jj;
                 const int pj = ROWB == 128 ? (j ^ (r & 7)) : (j ^ ((r >> 1) & 3));
-                float4 v = make_float4(a[4 * jj], a[4 * jj + 1], a[4 * jj + 2], a[4 * jj + 3]);
-                float4 l;
-                l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                const float4 full4 = make_float4(a[4 * jj], a[4 * jj + 1], a[4 * jj + 2], a[4 * jj + 3]);
+                float4 v = full4, l;
+                if (C::RN_SS) {            // RN hi written as the A value, lo = a - hi
+                  v = make_float4(__uint_as_float(split_hi(full4.x)), __uint_as_float(split_hi(full4.y)),
+                                  __uint_as_float(split_hi(full4.z)), __uint_as_float(split_hi(full4.w)));
+                  l.x = full4.x - v.x; l.y = full4.y - v.y; l.z = full4.z - v.z; l.w = full4.w - v.w;
+                } else {
+                  l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                  l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                  l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                  l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                }
                 *reinterpret_cast<float4*>(arow + (pj << 4)) = v;
                 *reinterpret_cast<float4*>(arow + A_BYTES + (pj << 4)) = l;
               }
@@ -883,11 +889,20 @@ struct GemmTc {
 #pragma unroll 4
           for (int i = ct; i < A_BYTES / 16; i += 64) {
             float4 v = a[i], h, l;
-            h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
-            h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
-            h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
-            h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
-            if (NNB_HI_INPLACE) a[i] = h;
+            if (C::RN_SS) {
+              // round-to-nearest split written back: lo of either sign, so
+              // its own TF32 truncation is unbiased (the raw tile would be
+              // truncated by the hardware, leaving lo >= 0 and biased)
+              h.x = __uint_as_float(split_hi(v.x)); h.y = __uint_as_float(split_hi(v.y));
+              h.z = __uint_as_float(split_hi(v.z)); h.w = __uint_as_float(split_hi(v.w));
+            } else {
+              h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+              h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+              h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+              h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            }
+            l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+            if (NNB_HI_INPLACE || C::RN_SS) a[i] = h;
             lo[i] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -120,7 +120,7 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=False, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True):
+                 wide_csplit=True, rn_ss=True):
         self.use_tc = use_tc
         self.aldg = aldg
         self.kpack = kpack
@@ -137,6 +137,7 @@ class Specializer:
         self.wide_bk = wide_bk
         self.wide_chunk = wide_chunk
         self.wide_csplit = wide_csplit
+        self.rn_ss = rn_ss
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self.chunk = chunk
         self.nacc = nacc
@@ -514,7 +515,7 @@ class Specializer:
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
-                      CORR_WHOLE=int(corr_whole),
+                      CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
@@ -905,8 +906,8 @@ def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_c
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
                mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K, wide=False,
-               wide_bk=32, wide_chunk=None, wide_csplit=True):
+               wide_bk=32, wide_chunk=None, wide_csplit=True, rn_ss=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
                        split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows,
-                       tc_min_k, wide, wide_bk, wide_chunk, wide_csplit).run()
+                       tc_min_k, wide, wide_bk, wide_chunk, wide_csplit, rn_ss).run()
