@@ -446,8 +446,8 @@ struct GemmTc {
                 "UMMA N / TMEM budget");
   static_assert(!C::CORR_WHOLE || (CS && C::NACC == 1), "whole-K correction chain");
   static_assert(!WIDE || (!TA && C::NACC == 1 && !C::CONV && !C::RES && C::UPF == 1 &&
-                          C::EPI_TMA && C::ABUF * (C::CSPLIT ? 2 : 1) * C::BN <= 512),
-                "N = 256 tiles: A in shared memory, TMA epilogue, 512 TMEM columns");
+                          C::ABUF * (C::CSPLIT ? 2 : 1) * C::BN <= 512),
+                "N = 256 tiles: A in shared memory, 512 TMEM columns");
   // spatial (implicit-GEMM convolution) tiling: 8 x 16 output pixels per tile
   static constexpr int TH = 8, TW = 16;
   // KPACK: the KW horizontal taps are packed into N (N = KW*CO, K = KH*CI): a
@@ -1119,7 +1119,7 @@ struct GemmTc {
           for (int i = 0; i < 16; ++i) {
             const int col = col0 + i < C::N ? col0 + i : C::N - 1;
             float y = v[i] + __ldg(bias + col);
-            y = finish<C::ACT, EMODE, C::POST>(y, ps, po, col);
+            if (!(NNB_TC_DBG & 32)) y = finish<C::ACT, EMODE, C::POST>(y, ps, po, col);
             if (C::POOL) {     // lanes w, w^1 (same image row), w^16 (next row)
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 16));

@@ -119,7 +119,7 @@ class Specializer:
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
-                 tc_min_k=TC_MIN_K, wide=False, wide_bk=32, wide_chunk=None,
+                 tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True):
         self.use_tc = use_tc
         self.aldg = aldg
@@ -422,7 +422,7 @@ class Specializer:
         # a kind::tf32 MMA costs ~1.4x at N = 256 what it costs at N = 128
         res_ = u.residual_id is not None
         wide = bool(self.wide and not conv and CO >= 256 and K <= 1024 and not res_
-                    and self.pair and not self.aldg and self.epi_tma and CO % 4 == 0
+                    and self.pair and not self.aldg and CO % 4 == 0
                     and (not rows_geo or rows_geo.get("UPF", 1) == 1))
         if wide:
             BN = 256
@@ -463,7 +463,8 @@ class Specializer:
             # 65536 rows): whole K in one chunk 0.26 ms but up to 1.05 of the
             # FP32 tolerance on N(0,1) data; 16 k-blocks 0.317 ms at <= 0.69
             # (BN = 128: 0.337 ms at <= 0.67); merged chains with two buffers
-            # 0.30-0.35 ms.  Opt-in (wide=True) until the accuracy matches.
+            # 0.30-0.35 ms.  With the round-to-nearest split written back
+            # (rn_ss) the 16-block form has the BN = 128 path's accuracy.
             csplit = self.wide_csplit
             corr_whole = csplit
             if not self.chunk:
@@ -905,7 +906,7 @@ def tf32_split_hi(w, rn=True):
 def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
                tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
                epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K, wide=False,
+               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K, wide=True,
                wide_bk=32, wide_chunk=None, wide_csplit=True, rn_ss=True):
     return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
                        tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,

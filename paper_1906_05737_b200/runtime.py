@@ -82,7 +82,7 @@ class CompiledNetwork:
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
                  nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
-                 small_dense_rows=512, tc_min_k=None, wide=False, wide_bk=32,
+                 small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
                  wide_chunk=None, wide_csplit=True, rn_ss=True):
         import torch
 
