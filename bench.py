@@ -372,6 +372,10 @@ def main():
                                "(8192^3, best of 5; MEASURED_PEAKS.json has bf16 only: "
                                f"{peaks['bf16_tflops']} TF/s)",
                 "achieved_counts": "3 x 2MNK tensor flops (3xTF32 split) per launch",
+                "peak_note": "the live cuBLAS TF32 GEMM is the measured denominator (a good "
+                             "kernel can read a little above it); nominal dense TF32 is "
+                             "1100 TFLOP/s (B200_PROFILING.md)",
+                "frac_of_nominal_tf32": achieved / 1100.0,
                 "fp32_equivalent_tflops": fp32_equiv,
                 "fp32_ffma_peak_tflops": peak_fp32}
     else:
