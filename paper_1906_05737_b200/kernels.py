@@ -41,6 +41,7 @@ SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
 MEGA_MAX_N = 8         # batches up to this run as one persistent kernel (when eligible)
 MEGA_THREADS = 256     # its block size (units with larger blocks opt it out)
 MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS)
+NARROW_MAX_W = 2048   # K*CO bound of the narrow row GEMM (weights unrolled into its code)
 ELEM_BLOCK = 256
 
 
@@ -100,14 +101,48 @@ class Specialization:
     mega_source: str = ""       # the persistent kernel's TU ("" when not generated)
 
 
-def _cfg_struct(name, fields):
+def _cfg_struct(name, fields, code=""):
+    """``struct name`` of constexpr fields, plus generated member functions."""
     lines = [f"struct {name} {{"]
     for k, v in fields.items():
         if isinstance(v, bool):
             v = int(v)
         lines.append(f"  static constexpr long long {k} = {int(v)}LL;")
+    if code:
+        lines.append(code)
     lines.append("};")
     return "\n".join(lines)
+
+
+def _flit(x):
+    """Exact CUDA literal of a float32 value (hex float; bit pattern if not finite)."""
+    x = np.float32(x)
+    if np.isfinite(x):
+        return float(x).hex() + "f"
+    return f"__int_as_float(0x{int(np.array(x).view(np.uint32)):08x})"
+
+
+def _narrow_code(wmat, bias, K, CO, KS):
+    """Members ``bias(j)`` and ``dot(a, acc, ks)`` of a RowsNarrow config: the
+    unrolled K x CO FFMAs of k-slice ``ks`` with every weight an immediate
+    (k ascending within the slice, columns innermost)."""
+    w = np.asarray(wmat, F32).reshape(K, CO)
+    out = ["  __device__ static __forceinline__ float bias(int j) {",
+           f"    const float b[{CO}] = {{{', '.join(_flit(v) for v in np.asarray(bias, F32))}}};",
+           "    return b[j];", "  }",
+           "  __device__ static __forceinline__ void dot(const float* a, float* acc, int ks) {",
+           "    float4 v;", "    switch (ks) {"]
+    per = K // KS
+    for ks in range(KS):
+        out.append(f"    case {ks}:")
+        for k4 in range(ks * per, (ks + 1) * per, 4):
+            out.append(f"      v = *reinterpret_cast<const float4*>(a + {k4});")
+            for q, c in enumerate("xyzw"):
+                out.extend(f"      acc[{j}] = fmaf(v.{c}, {_flit(w[k4 + q, j])}, acc[{j}]);"
+                           for j in range(CO))
+        out.append("      break;")
+    out += ["    }", "  }"]
+    return "\n".join(out)
 
 
 def _pad4(x):
@@ -120,8 +155,9 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True):
+                 wide_csplit=True, rn_ss=True, narrow=True):
         self.use_tc = use_tc
+        self.narrow = narrow
         self.aldg = aldg
         self.kpack = kpack
         self.epi_tma = epi_tma
@@ -163,10 +199,10 @@ class Specializer:
 
     def emit(self, unit_pos, tag, template, fields, block, smem, ipi, ipb,
              grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note="",
-             tmaps=(), grid_cap=0, cluster=1):
+             tmaps=(), grid_cap=0, cluster=1, code=""):
         kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
         cfg = f"Cfg_{len(self.names)}"
-        body = _cfg_struct(cfg, fields)
+        body = _cfg_struct(cfg, fields, code)
         if tmaps:
             body += (f"\nextern \"C\" __global__ void __launch_bounds__({block}, 1) {kname}("
                      f"const float* __restrict__ pool, float* __restrict__ arena, int n, "
@@ -194,7 +230,7 @@ class Specializer:
         self.chunks.append(body)
         self.names.append(kname)
         self.launches.append(Launch(kname, block, smem, ipi, ipb, grid_mult, n_min,
-                                    n_max, unit_pos, note))
+                                    n_max, unit_pos, note, grid_cap))
 
     def epilogue_fields(self, u, co):
         ps = po = self.pool.zeros_offset(co)
@@ -314,6 +350,42 @@ class Specializer:
                 self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
                               rows_geo=dict(HO=HO, WO=WO, UPF=UPF))
                 n_max = n_tc - 1
+                if n_max < n_min:
+                    return
+
+        # many rows, at most 32 columns: stream contiguous row tiles through a
+        # cp.async ring, weights baked into the code (nnb_rows.cuh), once the
+        # batch gives every SM a tile
+        rows_contig = (u.kind == "Dense" or (KH == KW == S == 1 and PT == PL == 0 and not concat
+                                             and not pool_fused and UPF == 1 and u.dw is None))
+        if self.narrow and rows_contig and CO <= 32 and K % 4 == 0 and K * CO <= NARROW_MAX_W:
+            KS = next(ks for ks in (4, 2, 1) if K % (4 * ks) == 0 and K // ks >= 16 or ks == 1)
+            TR = 32 if KS > 1 else 64
+            ast = K + 4 if ((K + 4) // 4) % 2 else K + 8
+            fixed = (max(KS - 1, 1) + 1) * TR * (CO | 1)
+            NS = min(4, (SMEM_MAX // 16 - fixed) // (TR * ast))    # four CTAs per SM
+            if NS < 2:
+                NS = min(4, (SMEM_MAX // 8 - fixed) // (TR * ast))
+            if NS < 2:
+                NS = min(4, (SMEM_MAX // 4 - fixed) // (TR * ast))
+            n_lo = max(n_min, -(-self.sm_count * TR // rows))
+            if NS >= 2 and n_lo <= min(n_max, self.max_batch):
+                smem = 4 * (NS * TR * ast + fixed)
+                fields = dict(K=K, CO=CO, TR=TR, NS=NS, KS=KS, ROWS=rows,
+                              IN_OFF=self.arena_off(u.input_ids[0]),
+                              OUT_OFF=self.arena_off(u.output_id),
+                              RES=u.residual_id is not None,
+                              RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
+                              SOFTMAX=softmax, SMEXP=SMEXP_CODE[self.opt.softmax_exp])
+                fields.update(self.epilogue_fields(u, CO))
+                per_sm = max(1, min(SMEM_MAX // (smem + 1024), 2048 // (TR * KS)))
+                self.emit(pos, "dense_narrow" if u.kind == "Dense" else "conv1x1_narrow", "nnb::RowsNarrow",
+                          fields, TR * KS, smem, rows, TR, n_min=n_lo, n_max=n_max, dynamic_smem=True,
+                          grid_cap=self.sm_count * per_sm,
+                          code=_narrow_code(wmat, u.bias, K, CO, KS),
+                          note=f"narrow rows M=n*{rows} N={CO} K={K} {TR}-row tiles, K in {KS} slices, "
+                               f"{NS}-stage cp.async ring, weights as FFMA immediates")
+                n_max = n_lo - 1
                 if n_max < n_min:
                     return
 
@@ -903,12 +975,7 @@ def tf32_split_hi(w, rn=True):
     return t.view(F32)
 
 
-def specialize(plan, assignment, options, max_batch, capacity, use_tc=True, sm_count=148,
-               tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False, kpack=True,
-               epi_tma=True, csplit=True, chunk=None, split_rn=True, pair=True, tc_tile_use=0.75,
-               mega=False, abuf=None, small_dense_rows=512, tc_min_k=TC_MIN_K, wide=True,
-               wide_bk=32, wide_chunk=None, wide_csplit=True, rn_ss=True):
-    return Specializer(plan, assignment, options, max_batch, capacity, use_tc, sm_count,
-                       tc_min_rows, tmem_a, nacc, aldg, kpack, epi_tma, csplit, chunk,
-                       split_rn, pair, tc_tile_use, mega, abuf, small_dense_rows,
-                       tc_min_k, wide, wide_bk, wide_chunk, wide_csplit, rn_ss).run()
+def specialize(plan, assignment, options, max_batch, capacity, **tuning):
+    """Specialise every launch unit; ``tuning`` are the Specializer's keyword
+    options (use_tc, sm_count, tc_min_rows, ...)."""
+    return Specializer(plan, assignment, options, max_batch, capacity, **tuning).run()

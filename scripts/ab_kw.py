@@ -1,7 +1,8 @@
 """A/B CompiledNetwork keyword options: replay + per-launch times of one zoo config.
 usage: ab_kw.py CONFIG BATCH 'epi_tma=True' 'epi_tma=False D:NNB_TC_DBG=1' ...
 (D:NAME=VAL entries are prepended to every kernel source as #defines;
- M:mode selects the activation approximation mode, default exact)"""
+ M:mode / S:mode select the activation / softmax-exp approximation modes,
+ default exact)"""
 import sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np  # noqa: E402
@@ -14,9 +15,13 @@ x = torch.from_numpy(zoo.inputs(cfg, batch))
 ref = None
 orig = K.Specializer.run
 for variant in sys.argv[3:]:
-    kw = {k: eval(v) for k, v in (a.split("=") for a in variant.split() if not a[:2] in ("D:", "M:"))}
+    kw = {k: eval(v) for k, v in (a.split("=") for a in variant.split() if not a[:2] in ("D:", "M:", "S:"))}
     modes = [a[2:] for a in variant.split() if a.startswith("M:")]
-    opts = ApproximationOptions(activation_mode=modes[0]) if modes else EXACT
+    smx = [a[2:] for a in variant.split() if a.startswith("S:")]
+    opts = EXACT
+    if modes or smx:
+        opts = ApproximationOptions(activation_mode=modes[0] if modes else EXACT.activation_mode,
+                                    softmax_exp=smx[0] if smx else EXACT.softmax_exp)
     defs = "".join(f"#define {a[2:].split('=')[0]} {a.split('=')[1]}\n"
                    for a in variant.split() if a.startswith("D:"))
 

@@ -399,3 +399,51 @@ def test_wide_n256_tiles_opt_in(k, units):
     got, net = gpu(m, w, x, wide=True)
     assert any("256x256" in l.note for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+
+
+@pytest.mark.parametrize("k,units,head", [(128, 10, "softmax"), (4, 1, "linear"), (64, 24, "tanh"), (256, 8, "relu"),
+                                          (64, 3, "add"), (36, 17, "softmax")])
+def test_narrow_row_gemm(k, units, head):
+    """Many rows, <= 32 columns (nnb_rows.cuh): a ragged last tile, fused
+    softmax / residual, against the oracle; with K in one slice (and no
+    softmax) bit-identical to the FFMA tile GEMM (same fmaf order: bias first,
+    k ascending)."""
+    rng = np.random.default_rng(k * 7 + units)
+    b = NetBuilder()
+    x_ = b.input((k,))
+
+    def dense(src, act):
+        return b.layer("Dense", [src], {"units": units, "activation": act},
+                       [("kernel", he(rng, (k, units), k)),
+                        ("bias", (rng.standard_normal(units) * 0.1).astype(F32))])
+    if head == "add":
+        y = b.layer("Add", [dense(x_, "relu"), dense(x_, "linear")])
+    elif head == "softmax":
+        y = b.layer("Softmax", [dense(x_, "linear")])
+    else:
+        y = dense(x_, head)
+    m, w = b.build([y])
+    n = 148 * 128 + 57
+    x = rng.uniform(-2, 2, (n, k)).astype(F32)
+    got, net = gpu(m, w, x)
+    assert any("narrow" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+    simt, net2 = gpu(m, w, x, narrow=False)
+    assert not any("narrow" in l.kernel for l in net2.artifact.launches)
+    if head != "softmax" and any("K in 1 slices" in l.note for l in net.artifact.launches):
+        np.testing.assert_array_equal(got, simt)
+    else:    # k slices summed in slice order / the FP32 exact-mode softmax
+        np.testing.assert_allclose(got, simt, rtol=2e-6, atol=1e-7)
+
+
+def test_narrow_row_gemm_pixels():
+    """A stride-1 1x1 conv with few output channels: pixel rows contiguous
+    across images, one narrow launch for the whole batch."""
+    rng = np.random.default_rng(5)
+    m, w = conv_net(rng, 20, 24, 16, 3, k=1, act="sigmoid")
+    x = rng.uniform(-1, 1, (41, 20, 24, 16)).astype(F32)
+    got, net = gpu(m, w, x)
+    assert any("conv1x1_narrow" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+    simt, _ = gpu(m, w, x, narrow=False)
+    np.testing.assert_array_equal(got, simt)
