@@ -49,10 +49,15 @@ def kernel_check(configs=range(5), batch=4096):
     jobs = []
     for c in configs:
         m, w = zoo.build(c)
-        plan = build_plan(build_graph(m, w))
-        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch, mega=True)
+        g = build_graph(m, w)
+        plan = build_plan(g)
+        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch)
         tus = [(f"cfg{c}", spec.source)]
-        if spec.mega_source:                      # the batch-1 persistent kernel's own TU
+        # the batch-1 persistent kernel's own TU (over the plan without the
+        # depthwise fusion, as CompiledNetwork(mega=True) builds it)
+        plan = build_plan(g, dw_fusion=False)
+        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch, mega=True)
+        if spec.mega_source:
             tus.append((f"cfg{c}_mega", spec.mega_source))
         for tag, text in tus:
             cu = bdir / f"kcheck_{tag}.cu"

@@ -6,5 +6,6 @@
 #include "nnb_small.cuh"
 #include "nnb_gemm_simt.cuh"
 #include "nnb_rows.cuh"
+#include "nnb_sep.cuh"
 #include "nnb_gemm_tc.cuh"
 #include "nnb_conv_direct.cuh"

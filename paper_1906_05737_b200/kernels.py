@@ -26,6 +26,7 @@ import numpy as np
 
 from .errors import UnsupportedLayer
 from .graph import same_padding
+from .planner import sep_narrow_geometry
 
 F32 = np.float32
 
@@ -43,6 +44,7 @@ MEGA_THREADS = 256     # its block size (units with larger blocks opt it out)
 MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS)
 NARROW_MAX_W = 2048   # K*CO bound of the narrow row GEMM (weights unrolled into its code)
 ELEM_BLOCK = 256
+SEP_BLOCK = 128
 
 
 @dataclass
@@ -142,6 +144,29 @@ def _narrow_code(wmat, bias, K, CO, KS):
                            for j in range(CO))
         out.append("      break;")
     out += ["    }", "  }"]
+    return "\n".join(out)
+
+
+def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias):
+    """Members of a SepNarrow config: ``dww(i)`` / ``dwb(c)`` (depthwise
+    weights in (ky, kx, c) order and bias, folded to immediates once the
+    kernel's loops are unrolled), ``bias(j)`` and ``dotr(a, acc)``: the
+    unrolled K x CO pointwise FFMAs over a register row ``a`` with every
+    weight an immediate (k ascending, columns innermost: RowsNarrow's order
+    with one K slice)."""
+    w = np.asarray(wmat, F32).reshape(K, CO)
+    lit = lambda arr: ", ".join(_flit(v) for v in np.asarray(arr, F32).ravel())
+    dwk = np.asarray(dw_kernel, F32).ravel()
+    out = ["  __device__ static __forceinline__ float dww(int i) {",
+           f"    const float v[{dwk.size}] = {{{lit(dwk)}}};", "    return v[i];", "  }",
+           "  __device__ static __forceinline__ float dwb(int i) {",
+           f"    const float v[{K}] = {{{lit(dw_bias)}}};", "    return v[i];", "  }",
+           "  __device__ static __forceinline__ float bias(int j) {",
+           f"    const float b[{CO}] = {{{lit(bias)}}};", "    return b[j];", "  }",
+           f"  __device__ static __forceinline__ void dotr(const float (&a)[{K}], float* acc) {{"]
+    for k in range(K):
+        out.extend(f"    acc[{j}] = fmaf(a[{k}], {_flit(w[k, j])}, acc[{j}]);" for j in range(CO))
+    out.append("  }")
     return "\n".join(out)
 
 
@@ -309,6 +334,14 @@ class Specializer:
         else:
             n_min = 1
 
+        # depthwise producer + narrow pointwise conv: one fused kernel
+        # (nnb_sep.cuh, all batch sizes)
+        if u.dw is not None and self.narrow:
+            geo = sep_narrow_geometry(u.dw, u)
+            if geo is not None:
+                self._sep_narrow(pos, u, wmat, CI, CO, geo)
+                return
+
         # narrow inputs: direct FFMA convolution (all batch sizes)
         if (u.kind == "Conv2D" and not softmax and CO <= 32 and u.dw is None
                 and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
@@ -453,6 +486,31 @@ class Specializer:
                 simt(TM, n_split, n_max)
         else:
             simt(TM, n_min, n_max)
+
+    def _sep_narrow(self, pos, u, wmat, CI, CO, geo):
+        """Depthwise unit ``u.dw`` + 1x1 conv ``u`` (<= 32 output channels) as
+        one SepNarrow launch: zero-haloed row bands through a cp.async ring,
+        one thread per output pixel."""
+        d = u.dw
+        HO, WO, _ = u.output_shape.dims
+        dwf = self._dw_fields(u)
+        fields = dict(H=dwf["DW_H"], W=dwf["DW_W"], CI=CI, S=dwf["DW_S"], KH=dwf["DW_KH"],
+                      KW=dwf["DW_KW"], PT=dwf["DW_PT"], PL=dwf["DW_PL"], HO=HO, WO=WO, CO=CO,
+                      TH=geo["TH"], NS=geo["NS"], NT=geo["NT"],
+                      IN_OFF=self.arena_off(u.input_ids[0]), OUT_OFF=self.arena_off(u.output_id),
+                      RES=u.residual_id is not None,
+                      RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
+                      DW_ACT=dwf["DW_ACT"], DW_POST=dwf["DW_POST"], DW_PS_OFF=dwf["DW_PS_OFF"],
+                      DW_PO_OFF=dwf["DW_PO_OFF"])
+        fields.update(self.epilogue_fields(u, CO))
+        tpi = -(-HO // geo["TH"])
+        per_sm = max(1, min(SMEM_MAX // (geo["smem"] + 1024), 2048 // geo["NT"]))
+        kh, kw = d.kernel_hw
+        self.emit(pos, f"sep{kh}x{kw}_narrow", "nnb::SepNarrow", fields, geo["NT"], geo["smem"],
+                  tpi, 1, dynamic_smem=True, grid_cap=self.sm_count * per_sm,
+                  code=_sep_code(wmat, u.bias, CI, CO, d.kernel, d.bias),
+                  note=f"dw{kh}x{kw}/s{d.stride} C={CI} + pw N={CO}: {geo['TH']}x{WO}-pixel tiles, "
+                       f"{geo['NS']}-stage cp.async ring, zero halo, weights as immediates")
 
     def _dw_fields(self, u):
         """Fields of a fused depthwise producer (GemmSimt DW loader, tcgen05

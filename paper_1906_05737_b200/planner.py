@@ -462,10 +462,49 @@ def fuse_concat(plan):
     return plan
 
 
-def fuse_dw_pw(plan):
+SEP_SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
+
+
+def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX):
+    """Tile geometry (TH output rows, NS ring stages, NT threads, shared bytes)
+    of the fused depthwise + narrow pointwise kernel (nnb_sep.cuh) for the
+    depthwise unit ``d`` feeding the 1x1 conv ``u``, or None when the pair is
+    outside that kernel: pointwise with <= 32 output channels over <= 32
+    input channels (weights as FFMA immediates) and a zero-haloed input band
+    that leaves >= 2 CTAs of >= 128 threads per SM.  Stride-2 depthwise
+    layers need 4x the band per output pixel and fall outside."""
+    h, w, c = d.input_shapes[0].dims
+    ho, wo, _ = d.output_shape.dims
+    co = u.output_shape.c
+    kh, kw = d.kernel_hw
+    s = d.stride
+    if not (c % 4 == 0 and c <= 32 and co <= 32 and wo <= 512 and kh <= 7 and kw <= 7
+            and not u.pool_after and u.upsample_after == 1 and not u.softmax_after
+            and not u.concat_in):
+        return None
+    cp = c + 4 if ((c + 4) // 4) % 2 else c + 8
+    wb = (wo - 1) * s + kw
+    th0 = max(1, min(ho, 256 // wo))
+    for per_sm in (3, 2):
+        for th in range(th0, 0, -1):
+            if th * wo < min(128, ho * wo):
+                break
+            ri = (th - 1) * s + kh
+            nt = -(-th * wo // 32) * 32
+            for ns in (3, 2):
+                rs = (co | 1) if co % 4 else (co + 4 if ((co + 4) // 4) % 2 else co + 8)
+                smem = 4 * (ns * ri * wb * cp + th * wo * rs)
+                if smem + 1024 <= smem_max // per_sm:
+                    return dict(TH=th, NS=ns, NT=nt, smem=smem)
+    return None
+
+
+def fuse_dw_pw(plan, narrow_only=False):
     """DepthwiseConv2D feeding only a pointwise (1x1, stride 1) Conv2D becomes
     that conv's operand loader: the depthwise output is computed on the fly
-    and never written to memory (separable-conv blocks of cfg2/cfg3)."""
+    and never written to memory (separable-conv blocks of cfg2/cfg3).  With
+    ``narrow_only`` only pairs the fused depthwise + narrow pointwise kernel
+    takes (``sep_narrow_geometry``) are fused."""
     pos = 1
     while pos < len(plan.units):
         u, d = plan.units[pos], plan.units[pos - 1]
@@ -473,6 +512,7 @@ def fuse_dw_pw(plan):
                 and u.stride == 1 and u.input_ids == (d.output_id,) and u.dw is None
                 and not u.concat_in and d.residual_id is None and not d.pool_after
                 and d.upsample_after == 1 and d.input_shapes[0].c % 4 == 0
+                and (not narrow_only or sep_narrow_geometry(d, u) is not None)
                 and _private(plan, d.output_id)):
             u.dw = d
             u.input_ids = d.input_ids
@@ -484,15 +524,17 @@ def fuse_dw_pw(plan):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion=False):
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow"):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
-    ``dw_fusion`` (off by default) folds depthwise convs into the pointwise
-    conv's operand loader -- the FFMA GEMM's, or the tcgen05 GEMM's split
-    warps (kernels.py tc_dwf).  Measured on B200 it only breaks even with a
-    depthwise kernel followed by the tcgen05 pointwise GEMM (cfg3 @256: 30.6
-    vs 32.4 us, 37.7 vs 34.0 us per block; cfg2 @1024: 113 vs 109 us): the
-    fused kernel is bound by the depthwise math on its four split warps, and
-    images under 75% of a 8 x 16 tile fall back to the slower FFMA form."""
+    ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
+    them.  "narrow" (default): only pairs whose pointwise conv has <= 32
+    output channels, run by the fused depthwise + narrow pointwise kernel
+    (nnb_sep.cuh).  True: every pair, the wider ones through the FFMA GEMM's
+    operand loader or the tcgen05 GEMM's split warps (kernels.py tc_dwf) --
+    measured on B200 that only breaks even with a depthwise kernel followed by
+    the tcgen05 pointwise GEMM (cfg3 @256: 30.6 vs 32.4 us, 37.7 vs 34.0 us
+    per block; cfg2 @1024: 113 vs 109 us): the fused kernel is bound by the
+    depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
         fuse_pool(plan)
@@ -501,7 +543,7 @@ def build_plan(graph, gpu_fusion=True, dw_fusion=False):
         fuse_upsample(plan)
         fuse_concat(plan)
         if dw_fusion:
-            fuse_dw_pw(plan)
+            fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")
     return plan
 
 

@@ -80,7 +80,7 @@ class _Handle:
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
                  gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
-                 nacc=None, aldg=False, kpack=True, dw_fusion=False, epi_tma=True, csplit=True, chunk=None,
+                 nacc=None, aldg=False, kpack=True, dw_fusion="narrow", epi_tma=True, csplit=True, chunk=None,
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
                  wide_chunk=None, wide_csplit=True, rn_ss=True, narrow=True):
@@ -96,6 +96,8 @@ class CompiledNetwork:
             raise ValueError("batch must be >= 1")
         _, _, sm_count = _native.device_check(device)
         self.graph = build_graph(manifest, weights)
+        if mega and dw_fusion == "narrow":
+            dw_fusion = False      # the persistent kernel walks the unfused templates
         self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion, dw_fusion=dw_fusion)
         self.assignment = plan_buffers(self.plan)
         cap = _capacity(self.max_batch)
