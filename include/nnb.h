@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define NNB_ABI_VERSION 4
+#define NNB_ABI_VERSION 5
 #define NNB_MAX_TMAPS 6
 
 typedef enum {
@@ -145,6 +145,19 @@ nnb_status nnb_apply(nnb_net *net, int32_t n, void *stream);
  * pointers (pinned memory is fastest, see nnb_host_alloc). */
 nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs,
                         void *const *outputs, void *stream);
+
+/* nnb_run_host without the final wait (the copies and the replay are queued
+ * on `stream`; the caller synchronises). */
+nnb_status nnb_enqueue_host(nnb_net *net, int32_t n, const void *const *inputs,
+                            void *const *outputs, void *stream);
+
+/* Pipelined host-buffer call over k networks compiled from the same model
+ * (each for >= ceil(n/k) images, same device): image chunk j of the host
+ * buffers goes through nets[j] on streams[j]; every chunk is queued before
+ * any is waited for, so chunk j's H2D copy overlaps chunk j-1's replay and
+ * D2H copy.  Returns when all chunks are done. */
+nnb_status nnb_run_host_chunked(nnb_net *const *nets, const void *const *streams, int32_t k,
+                                int64_t n, const void *const *inputs, void *const *outputs);
 
 nnb_status nnb_sync(nnb_net *net, void *stream);
 

@@ -20,7 +20,7 @@ NNB_OK, NNB_ERR_ARGUMENT, NNB_ERR_NO_DRIVER, NNB_ERR_NO_DEVICE, NNB_ERR_ARCH, \
     NNB_ERR_NVRTC, NNB_ERR_CUDA, NNB_ERR_OOM, NNB_ERR_BATCH = range(9)
 
 EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "nnb_apply",
-            "nnb_run_host", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_host_alloc", "nnb_host_free",
+            "nnb_run_host", "nnb_enqueue_host", "nnb_run_host_chunked", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_host_alloc", "nnb_host_free",
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
 
@@ -91,6 +91,8 @@ def lib():
         "nnb_arena_ptr": (I32, [VP, U64, P(VP)]),
         "nnb_apply": (I32, [VP, I32, VP]),
         "nnb_run_host": (I32, [VP, I32, P(VP), P(VP), VP]),
+        "nnb_enqueue_host": (I32, [VP, I32, P(VP), P(VP), VP]),
+        "nnb_run_host_chunked": (I32, [P(VP), P(VP), I32, ctypes.c_int64, P(VP), P(VP)]),
         "nnb_sync": (I32, [VP, VP]),
         "nnb_time_apply": (I32, [VP, I32, I32, VP, P(ctypes.c_double)]),
         "nnb_time_launch": (I32, [VP, I32, I32, I32, VP, P(ctypes.c_double)]),

@@ -70,7 +70,7 @@ struct Cu {
   CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
   CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
   CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled) CU_FN(cuLaunchKernelEx)
-  CU_FN(cuMemsetD32Async)
+  CU_FN(cuMemsetD32Async) CU_FN(cuCtxGetCurrent)
 #undef CU_FN
   void load() {
     const char *names[] = {"libcuda.so.1", "libcuda.so"};
@@ -93,7 +93,7 @@ struct Cu {
     CU_LOAD(cuGraphDestroy) CU_LOAD(cuGraphExecDestroy) CU_LOAD(cuEventCreate)
     CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
     CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString) CU_LOAD(cuTensorMapEncodeTiled)
-    CU_LOAD(cuLaunchKernelEx) CU_LOAD(cuMemsetD32Async)
+    CU_LOAD(cuLaunchKernelEx) CU_LOAD(cuMemsetD32Async) CU_LOAD(cuCtxGetCurrent)
 #undef CU_LOAD
     CUresult r = p_cuInit(0);
     if (r != CUDA_SUCCESS) {
@@ -597,23 +597,64 @@ nnb_status nnb_sync(nnb_net *net, void *stream) {
   return NNB_OK;
 }
 
-nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs, void *const *outputs,
-                        void *stream) {
+// H2D of images [first, first + n) of every host input into the arena's
+// first n rows, one replay, D2H of the outputs to the same image range of the
+// host outputs; all on `stream`, nothing waited for.
+static nnb_status enqueue_host(nnb_net *net, int32_t n, int64_t first, const void *const *inputs,
+                               void *const *outputs, CUstream s) {
   if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
   if (n < 1 || n > net->max_batch)
     return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
   CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
-  CUstream s = reinterpret_cast<CUstream>(stream);
-  for (size_t i = 0; i < net->inputs.size(); ++i)
-    CU_CHECK(C->p_cuMemcpyHtoDAsync(net->arena + net->inputs[i].offset, inputs[i],
-                                    (size_t)n * net->inputs[i].image_bytes, s));
-  nnb_status st = nnb_apply(net, n, stream);
+  for (size_t i = 0; i < net->inputs.size(); ++i) {
+    const uint64_t b = net->inputs[i].image_bytes;
+    CU_CHECK(C->p_cuMemcpyHtoDAsync(net->arena + net->inputs[i].offset,
+                                    static_cast<const char *>(inputs[i]) + first * b, (size_t)n * b, s));
+  }
+  nnb_status st = nnb_apply(net, n, s);
   if (st != NNB_OK) return st;
-  for (size_t i = 0; i < net->outputs.size(); ++i)
-    CU_CHECK(C->p_cuMemcpyDtoHAsync(outputs[i], net->arena + net->outputs[i].offset,
-                                    (size_t)n * net->outputs[i].image_bytes, s));
-  CU_CHECK(C->p_cuStreamSynchronize(s));
+  for (size_t i = 0; i < net->outputs.size(); ++i) {
+    const uint64_t b = net->outputs[i].image_bytes;
+    CU_CHECK(C->p_cuMemcpyDtoHAsync(static_cast<char *>(outputs[i]) + first * b,
+                                    net->arena + net->outputs[i].offset, (size_t)n * b, s));
+  }
+  return NNB_OK;
+}
+
+nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs, void *const *outputs,
+                        void *stream) {
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  nnb_status st = enqueue_host(net, n, 0, inputs, outputs, s);
+  if (st != NNB_OK) return st;
+  CU_CHECK(cu()->p_cuStreamSynchronize(s));
+  return NNB_OK;
+}
+
+nnb_status nnb_enqueue_host(nnb_net *net, int32_t n, const void *const *inputs,
+                            void *const *outputs, void *stream) {
+  return enqueue_host(net, n, 0, inputs, outputs, reinterpret_cast<CUstream>(stream));
+}
+
+nnb_status nnb_run_host_chunked(nnb_net *const *nets, const void *const *streams, int32_t k,
+                                int64_t n, const void *const *inputs, void *const *outputs) {
+  if (!nets || !streams || k < 1 || n < 1) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  for (int32_t j = 0; j < k; ++j)
+    if (!nets[j]) return fail(NNB_ERR_ARGUMENT, "net %d is NULL", j);
+  const int64_t per = (n + k - 1) / k;
+  // every chunk is enqueued before anything is waited for: chunk j's H2D
+  // overlaps chunk j-1's replay and D2H (copy engines vs SMs)
+  int32_t used = 0;
+  for (int64_t first = 0; first < n; first += per, ++used) {
+    const int32_t m = (int32_t)(n - first < per ? n - first : per);
+    nnb_status st = enqueue_host(nets[used], m, first, inputs, outputs,
+                                 reinterpret_cast<CUstream>(const_cast<void *>(streams[used])));
+    if (st != NNB_OK) return st;
+  }
+  for (int32_t j = 0; j < used; ++j) {
+    CU_CHECK(cu()->p_cuCtxSetCurrent(nets[j]->ctx));
+    CU_CHECK(cu()->p_cuStreamSynchronize(reinterpret_cast<CUstream>(const_cast<void *>(streams[j]))));
+  }
   return NNB_OK;
 }
 
@@ -699,6 +740,16 @@ nnb_status nnb_time_sequence(nnb_net *net, int32_t n, int32_t iters, void *strea
 nnb_status nnb_host_alloc(uint64_t bytes, void **ptr) {
   Cu *C = cu();
   if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());
+  // page-locked memory needs a context: device 0's primary one when the
+  // calling thread has none yet (it is portable across contexts anyway)
+  CUcontext cur = nullptr;
+  CU_CHECK(C->p_cuCtxGetCurrent(&cur));
+  if (!cur) {
+    CUdevice dev;
+    CU_CHECK(C->p_cuDeviceGet(&dev, 0));
+    CU_CHECK(C->p_cuDevicePrimaryCtxRetain(&cur, dev));
+    CU_CHECK(C->p_cuCtxSetCurrent(cur));
+  }
   CU_CHECK(C->p_cuMemAllocHost(ptr, bytes));
   return NNB_OK;
 }

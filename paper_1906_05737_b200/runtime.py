@@ -313,16 +313,79 @@ class _PinnedArray(np.ndarray):
     pass
 
 
-def compile_model(manifest, weights, options=None, devices=None, **kw):
+class PipelinedNetwork:
+    """Host-buffer inference over a large batch with the PCIe copies hidden
+    behind the compute: ``chunks`` CompiledNetworks of ceil(batch/chunks)
+    images each (same model, same device, one CUDA stream each; the
+    specialised kernels are shared through the cubin cache).  ``run_host``
+    hands the host buffers to ``nnb_run_host_chunked``, which queues every
+    chunk's H2D copy, replay and D2H copy before waiting for any, so chunk
+    j's upload overlaps chunk j-1's replay and download.  Outputs are
+    identical to one CompiledNetwork over the whole batch (images are
+    independent and every kernel is batch-size invariant per image)."""
+
+    def __init__(self, manifest, weights, options=None, *, batch, chunks=4, device=0, **kw):
+        import torch
+        if batch < 1 or chunks < 1:
+            raise ValueError("batch and chunks must be >= 1")
+        self._torch = torch
+        self.batch = self.max_batch = int(batch)
+        self.chunks = max(1, min(int(chunks), self.batch))
+        per = -(-self.batch // self.chunks)
+        self.nets = [CompiledNetwork(manifest, weights, options, batch=per, device=device, **kw)
+                     for _ in range(self.chunks)]
+        self.streams = [torch.cuda.Stream(device=torch.device("cuda", device))
+                        for _ in range(self.chunks)]
+        self.options = self.nets[0].options
+        self.plan = self.nets[0].plan
+        self.artifact = self.nets[0].artifact
+        self.compile_ms = sum(n.compile_ms for n in self.nets)
+
+    @property
+    def output_shapes(self):
+        return [tuple(v.shape[1:]) for v in self.nets[0].output_views]
+
+    def run_host(self, inputs, outputs=None, n=None):
+        """``n`` (default ``batch``) images of C-contiguous float32 host
+        ``inputs`` (pinned: ``pinned_empty``) in, the outputs written into
+        ``outputs`` (allocated when None) and returned."""
+        n = self.batch if n is None else int(n)
+        if not 1 <= n <= self.batch:
+            raise InputShapeMismatch(f"batch {n} outside [1, {self.batch}]")
+        xs = [np.ascontiguousarray(x, np.float32) for x in inputs]
+        for x, v in zip(xs, self.nets[0].input_views):
+            if x.shape[0] < n or tuple(x.shape[1:]) != tuple(v.shape[1:]):
+                raise InputShapeMismatch(f"input shape {x.shape} does not match "
+                                         f"({n}, {tuple(v.shape[1:])})")
+        if outputs is None:
+            outputs = [np.empty((n,) + s, np.float32) for s in self.output_shapes]
+        VP = ctypes.c_void_p
+        nets = (VP * self.chunks)(*[net._h.ptr for net in self.nets])
+        streams = (VP * self.chunks)(*[st.cuda_stream for st in self.streams])
+        ip = (VP * len(xs))(*[x.ctypes.data for x in xs])
+        op = (VP * len(outputs))(*[o.ctypes.data for o in outputs])
+        _native.check(_native.lib().nnb_run_host_chunked(nets, streams, self.chunks, n, ip, op),
+                      "run_host_chunked")
+        return outputs
+
+
+def compile_model(manifest, weights, options=None, devices=None, host_chunks=None, **kw):
     """pkg/src/nnjit/runtime.py:101-104.  ``devices=[...]`` (additive) shards
-    ``batch`` over one replica per listed GPU (``replicas.MultiDeviceNetwork``)."""
+    ``batch`` over one replica per listed GPU (``replicas.MultiDeviceNetwork``);
+    ``host_chunks=k`` (additive) returns a ``PipelinedNetwork`` whose
+    ``run_host`` overlaps the host copies of k batch chunks with compute."""
     if devices is not None:
         from .replicas import MultiDeviceNetwork
         return MultiDeviceNetwork(manifest, weights, options, devices=devices, **kw)
+    if host_chunks is not None:
+        return PipelinedNetwork(manifest, weights, options, chunks=host_chunks, **kw)
     return CompiledNetwork(manifest, weights, options, **kw)
 
 
-def compile_file(manifest_path, blob_path=None, options=None, devices=None, **kw):
-    """pkg/src/nnjit/runtime.py:105-107 (same ``devices`` extension)."""
+def compile_file(manifest_path, blob_path=None, options=None, devices=None, host_chunks=None,
+                 **kw):
+    """pkg/src/nnjit/runtime.py:105-107 (same ``devices`` / ``host_chunks``
+    extensions)."""
     manifest, weights = load_model(manifest_path, blob_path)
-    return compile_model(manifest, weights, options, devices=devices, **kw)
+    return compile_model(manifest, weights, options, devices=devices, host_chunks=host_chunks,
+                         **kw)

@@ -58,3 +58,26 @@ def test_baseline_batch_sampled_images_vs_oracle(cfg, n):
     idx = np.sort(np.random.default_rng(cfg).choice(n, size=min(n, 6), replace=False))
     want = oracle.run(m, w, [x[idx]], "exact")[0]
     np.testing.assert_allclose(got[idx], want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("cfg,n,k", [(1, 5000, 4), (0, 999, 3), (3, 20, 8)])
+def test_pipelined_host_call(cfg, n, k):
+    """compile_model(host_chunks=k) -> PipelinedNetwork: nnb_run_host_chunked
+    splits the host buffers into k chunks (ragged last chunk) over k
+    networks and streams; same results as the oracle, and as one network."""
+    from paper_1906_05737_b200 import PipelinedNetwork, pinned_empty
+    m, w = zoo.build(cfg)
+    net = compile_model(m, w, EXACT, batch=n, host_chunks=k)
+    assert isinstance(net, PipelinedNetwork) and len(net.nets) == k
+    x = zoo.inputs(cfg, n)
+    hx = pinned_empty(x.shape)
+    hx[...] = x
+    got = net.run_host([hx])[0]
+    idx = np.sort(np.random.default_rng(cfg).choice(n, size=min(n, 8), replace=False))
+    idx[-1] = n - 1                                         # the ragged last chunk
+    want = oracle.run(m, w, [x[idx]], "exact")[0]
+    np.testing.assert_allclose(got[idx], want, rtol=RTOL, atol=ATOL)
+    one = compile_model(m, w, EXACT, batch=n).run_host([hx])[0]
+    np.testing.assert_allclose(got, one, rtol=RTOL, atol=ATOL)
+    part = net.run_host([hx], n=n // 2 + 1)[0]               # fewer images than the batch
+    np.testing.assert_allclose(part, one[:n // 2 + 1], rtol=RTOL, atol=ATOL)
