@@ -24,14 +24,16 @@ struct ConvDirect {
   static constexpr int CELLS_Y = C::POOL ? C::PHO : C::HO;
   static constexpr int CELLS_X = C::POOL ? C::PWO : (C::WO + PX - 1) / PX;
 
-  struct Smem { alignas(16) float w[WN]; float b[C::CO]; };
+  struct Smem { alignas(16) float w[C::WIMM ? 4 : WN]; float b[C::CO]; };
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
                              Smem& sm) {
-    const float* wg = at<float>(pool, C::W_OFF);
-    for (int i = threadIdx.x; i < WN; i += nnb_bdim()) sm.w[i] = __ldg(wg + i);
-    for (int i = threadIdx.x; i < C::CO; i += nnb_bdim()) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
-    nnb_sync();
+    if (!C::WIMM) {
+      const float* wg = at<float>(pool, C::W_OFF);
+      for (int i = threadIdx.x; i < WN; i += nnb_bdim()) sm.w[i] = __ldg(wg + i);
+      for (int i = threadIdx.x; i < C::CO; i += nnb_bdim()) sm.b[i] = __ldg(at<float>(pool, C::B_OFF) + i);
+      nnb_sync();
+    }
 
     // Pixel ownership.  POOL: a thread owns one 2x2 window (consecutive lanes,
     // consecutive windows).  Otherwise the PX pixels of a thread are 32 apart
@@ -81,9 +83,12 @@ struct ConvDirect {
 #pragma unroll
     for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int o = 0; o < C::CO; ++o) acc[p][o] = sm.b[o];
+      for (int o = 0; o < C::CO; ++o) acc[p][o] = C::WIMM ? C::bias(o) : sm.b[o];
 
-#pragma unroll 1
+    // weights as immediates (Cfg::wt, WIMM): every loop below is unrolled,
+    // so each FFMA takes its weight from the instruction stream; otherwise
+    // warp-uniform LDS.128 broadcasts from shared memory
+#pragma unroll
     for (int ky = 0; ky < C::KH; ++ky) {
 #pragma unroll
       for (int kx = 0; kx < C::KW; ++kx) {
@@ -105,8 +110,16 @@ struct ConvDirect {
           }
 #pragma unroll
           for (int c = 0; c < CV; ++c) {
-            const float* wr = sm.w + ((ky * C::KW + kx) * C::CI + c0 + c) * C::CO;
-            if (C::CO % 4 == 0) {             // one LDS.128 broadcast feeds 4*NP FMAs
+            const int wi = ((ky * C::KW + kx) * C::CI + c0 + c) * C::CO;
+            const float* wr = sm.w + wi;
+            if (C::WIMM) {
+#pragma unroll
+              for (int o = 0; o < C::CO; ++o) {
+                const float wv = C::wt(wi + o);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) acc[p][o] = fmaf(xv[p][c], wv, acc[p][o]);
+              }
+            } else if (C::CO % 4 == 0) {      // one LDS.128 broadcast feeds 4*NP FMAs
 #pragma unroll
               for (int o = 0; o < C::CO; o += 4) {
                 const float4 w4 = *reinterpret_cast<const float4*>(wr + o);

@@ -45,6 +45,7 @@ MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS
 NARROW_MAX_W = 2048   # K*CO bound of the narrow row GEMM (weights unrolled into its code)
 ELEM_BLOCK = 256
 SEP_BLOCK = 128
+DIRECT_IMM_MAX = 2048  # direct-conv weights unrolled into the code as immediates
 
 
 @dataclass
@@ -170,6 +171,19 @@ def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias):
     return "\n".join(out)
 
 
+def _imm_tables(**tables):
+    """Members ``name(i)`` returning element i of a float32 table; once the
+    caller's loops are unrolled the index is a constant and the value an
+    instruction immediate."""
+    out = []
+    for name, arr in tables.items():
+        a = np.asarray(arr, F32).ravel()
+        out += [f"  __device__ static __forceinline__ float {name}(int i) {{",
+                f"    const float v[{a.size}] = {{{', '.join(_flit(v) for v in a)}}};",
+                "    return v[i];", "  }"]
+    return "\n".join(out)
+
+
 def _pad4(x):
     return (x + 3) // 4 * 4
 
@@ -180,8 +194,9 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, narrow=True):
+                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True):
         self.use_tc = use_tc
+        self.direct_imm = direct_imm
         self.narrow = narrow
         self.aldg = aldg
         self.kpack = kpack
@@ -733,12 +748,16 @@ class Specializer:
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO))
+        # weights (<= DIRECT_IMM_MAX) as immediates in the generated code
+        wimm = self.direct_imm and KH * KW * CI * CO <= DIRECT_IMM_MAX
+        fields["WIMM"] = wimm
+        code = _imm_tables(wt=wmat, bias=u.bias) if wimm else ""
         # pool: one 2x2 window per thread; else pxt pixels per thread, the
         # 128-thread block covering 128*pxt consecutive pixels
         ipi, ipb = (PHO * PWO, 128) if pool_fused else (HO * WO, 128 * pxt)
-        smem = 4 * (KH * KW * CI * CO + CO)
+        smem = 4 * ((4 if wimm else KH * KW * CI * CO) + CO)
         self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, ipi, ipb,
-                  dynamic_smem=True, n_min=n_min,
+                  dynamic_smem=True, n_min=n_min, code=code,
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
                        f"{4 if pool_fused else pxt}")
 
