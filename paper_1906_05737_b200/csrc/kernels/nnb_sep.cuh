@@ -139,10 +139,17 @@ struct SepNarrow {
             for (int kx = 0; kx < KW; ++kx) {
               const float4 x = *reinterpret_cast<const float4*>(band + (ky * WB + kx) * CP + 4 * q);
               const int wi = (ky * KW + kx) * CI + 4 * q;
-              acc.x = add(acc.x, mul(x.x, C::dww(wi + 0)));
-              acc.y = add(acc.y, mul(x.y, C::dww(wi + 1)));
-              acc.z = add(acc.z, mul(x.z, C::dww(wi + 2)));
-              acc.w = add(acc.w, mul(x.w, C::dww(wi + 3)));
+              if (C::DW_FMA) {       // one rounding per tap (within the FP32 gate)
+                acc.x = fmaf(x.x, C::dww(wi + 0), acc.x);
+                acc.y = fmaf(x.y, C::dww(wi + 1), acc.y);
+                acc.z = fmaf(x.z, C::dww(wi + 2), acc.z);
+                acc.w = fmaf(x.w, C::dww(wi + 3), acc.w);
+              } else {               // the interpreter's mul-then-add: bit-exact
+                acc.x = add(acc.x, mul(x.x, C::dww(wi + 0)));
+                acc.y = add(acc.y, mul(x.y, C::dww(wi + 1)));
+                acc.z = add(acc.z, mul(x.z, C::dww(wi + 2)));
+                acc.w = add(acc.w, mul(x.w, C::dww(wi + 3)));
+              }
             }
           a[4 * q + 0] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.x, dps, dpo, 4 * q + 0);
           a[4 * q + 1] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.y, dps, dpo, 4 * q + 1);

@@ -194,9 +194,10 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True):
+                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True):
         self.use_tc = use_tc
         self.direct_imm = direct_imm
+        self.sep_fma = sep_fma
         self.narrow = narrow
         self.aldg = aldg
         self.kpack = kpack
@@ -516,7 +517,7 @@ class Specializer:
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
                       DW_ACT=dwf["DW_ACT"], DW_POST=dwf["DW_POST"], DW_PS_OFF=dwf["DW_PS_OFF"],
-                      DW_PO_OFF=dwf["DW_PO_OFF"])
+                      DW_PO_OFF=dwf["DW_PO_OFF"], DW_FMA=self.sep_fma)
         fields.update(self.epilogue_fields(u, CO))
         tpi = -(-HO // geo["TH"])
         per_sm = max(1, min(SMEM_MAX // (geo["smem"] + 1024), 2048 // geo["NT"]))

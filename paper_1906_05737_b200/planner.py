@@ -484,18 +484,26 @@ def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX):
         return None
     cp = c + 4 if ((c + 4) // 4) % 2 else c + 8
     wb = (wo - 1) * s + kw
+    rs = (co | 1) if co % 4 else (co + 4 if ((co + 4) // 4) % 2 else co + 8)
     th0 = max(1, min(ho, 256 // wo))
     for per_sm in (3, 2):
+        best = None
         for th in range(th0, 0, -1):
             if th * wo < min(128, ho * wo):
                 break
             ri = (th - 1) * s + kh
             nt = -(-th * wo // 32) * 32
             for ns in (3, 2):
-                rs = (co | 1) if co % 4 else (co + 4 if ((co + 4) // 4) % 2 else co + 8)
                 smem = 4 * (ns * ri * wb * cp + th * wo * rs)
                 if smem + 1024 <= smem_max // per_sm:
-                    return dict(TH=th, NS=ns, NT=nt, smem=smem)
+                    # warps issued over an image (idle lanes of the last warp,
+                    # ragged last band), then taller bands
+                    key = (nt // 32 * -(-ho // th), -th, -ns)
+                    if best is None or key < best[0]:
+                        best = (key, dict(TH=th, NS=ns, NT=nt, smem=smem))
+                    break
+        if best:
+            return best[1]
     return None
 
 

@@ -83,7 +83,8 @@ class CompiledNetwork:
                  nacc=None, aldg=False, kpack=True, dw_fusion="narrow", epi_tma=True, csplit=True, chunk=None,
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
-                 wide_chunk=None, wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True):
+                 wide_chunk=None, wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True,
+                 sep_fma=True):
         import torch
 
         t0 = time.perf_counter()
@@ -110,7 +111,7 @@ class CompiledNetwork:
                           pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf,
                           small_dense_rows=small_dense_rows, wide=wide, wide_bk=wide_bk,
                           wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss,
-                          narrow=narrow, direct_imm=direct_imm,
+                          narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
                           **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
         arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 

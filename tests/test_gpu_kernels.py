@@ -145,10 +145,13 @@ def test_sep_narrow(h, w, c, co, k, s, pad, dwbias, res, n):
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
     unf, net2 = gpu(m, wt, xin, dw_fusion=False)
     assert len(net2.launches_for()) == 2
-    if c < 32 and not any("_tc_" in l.kernel for l in net2.artifact.launches):
-        np.testing.assert_array_equal(got, unf)
-    else:
-        np.testing.assert_allclose(got, unf, rtol=2e-6, atol=2e-6)
+    np.testing.assert_allclose(got, unf, rtol=1e-5, atol=5e-6)   # FFMA vs mul+add taps
+    if len(net.plan.units) == 1 and c < 32 and not any("_tc_" in l.kernel
+                                                       for l in net2.artifact.launches):
+        # the interpreter's mul-then-add depthwise taps: bit-identical to the
+        # unfused depthwise kernel + pointwise GEMM
+        exact, _ = gpu(m, wt, xin, sep_fma=False)
+        np.testing.assert_array_equal(exact, unf)
 
 
 @pytest.mark.parametrize("h,w,c,co,s,act,bn,n", [
