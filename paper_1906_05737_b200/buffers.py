@@ -69,17 +69,36 @@ def _reads(u):
                                  is not None else ())
 
 
-def compute_lifetimes(plan, pin_inputs=True):
+def head_pairs(plan):
+    """Positions of Dense units whose output feeds only the next unit, a
+    Dense head with <= 16 outputs: the tcgen05 GEMM may compute that head in
+    its epilogue (kernels.py HEAD), i.e. write the head's output while still
+    reading its own input."""
+    out = []
+    for pos in range(len(plan.units) - 1):
+        u, v = plan.units[pos], plan.units[pos + 1]
+        if (u.kind == "Dense" and v.kind == "Dense" and v.input_ids == (u.output_id,)
+                and v.kernel.shape[1] <= 16 and u.output_id not in plan.output_ids
+                and plan.consumer_count(u.output_id) == 1):
+            out.append(pos)
+    return out
+
+
+def compute_lifetimes(plan, pin_inputs=True, reserve_heads=False):
+    """``reserve_heads`` (the B200 runtime) keeps the inputs of a head-fusable
+    Dense (``head_pairs``) live through its head, so the head's output never
+    takes their space."""
     end = len(plan.units)
     first, last = {}, {}
     for t in plan.input_ids:
         first[t] = -1
         last[t] = end if pin_inputs else -1
+    heads = set(head_pairs(plan)) if reserve_heads else set()
     for pos, u in enumerate(plan.units):
         first.setdefault(u.output_id, pos)
         last[u.output_id] = max(last.get(u.output_id, pos), pos)
         for t in _reads(u):
-            last[t] = max(last.get(t, pos), pos)
+            last[t] = max(last.get(t, pos), pos + 1 if pos in heads else pos)
     for t in plan.output_ids:
         last[t] = end
     out = []
@@ -149,8 +168,8 @@ def assign_buffers(intervals, plan):
     return asg
 
 
-def plan_buffers(plan, pin_inputs=True):
-    return assign_buffers(compute_lifetimes(plan, pin_inputs), plan)
+def plan_buffers(plan, pin_inputs=True, reserve_heads=False):
+    return assign_buffers(compute_lifetimes(plan, pin_inputs, reserve_heads), plan)
 
 
 def verify_assignment(plan, assignment):

@@ -51,7 +51,8 @@ def kernel_check(configs=range(5), batch=4096):
         m, w = zoo.build(c)
         g = build_graph(m, w)
         plan = build_plan(g)
-        spec = specialize(plan, plan_buffers(plan), ApproximationOptions(), batch, batch)
+        spec = specialize(plan, plan_buffers(plan, reserve_heads=True), ApproximationOptions(), batch,
+                          batch)
         tus = [(f"cfg{c}", spec.source)]
         # the batch-1 persistent kernel's own TU (over the plan without the
         # depthwise fusion, as CompiledNetwork(mega=True) builds it)

@@ -31,6 +31,7 @@
 // UPF, RES, EPI_TMA, CSPLIT / CORR_WHOLE, CHUNK, ABUF, NACC, DWF, BN = 256.
 #pragma once
 #include "nnb_common.cuh"
+#include "nnb_softmax.cuh"
 
 // NNB_TC_DBG (diagnostics only, results are garbage): bit 0 skips the MMAs,
 // bit 1 the TMA operand loads, bit 2 the A split, bit 3 the epilogue's TMEM
@@ -245,6 +246,10 @@ __device__ __forceinline__ u32 cluster_rank() {
   u32 r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
+}
+// named barrier over the two warps (64 threads) sharing a TMEM lane quarter
+__device__ __forceinline__ void named_sync64(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -477,7 +482,30 @@ struct GemmTc {
   static_assert(!ET || !(C::POOL || C::UPF > 1 || KP), "TMA epilogue: plain row tiles only");
   static_assert(!(C::RES && C::UPF > 1), "residual fusion excludes upsampling (planner)");
   static constexpr int EPI_STAGE = EPI_WARPS * NBUF * 2048;       // 32 x 16 fp32 per buffer
+  // HEAD: a following Dense with HN <= 16 outputs (a classifier head, e.g.
+  // cfg1's 128 -> 10 + softmax) computed in this epilogue from the finished
+  // tile row: each of the two warps holding a row's column halves forms the
+  // head's partial dot over its columns (weights as immediates, Cfg::hw /
+  // hbias), the upper half hands its partials over through the (otherwise
+  // unused) staging boxes, and the lower half adds them, applies the head's
+  // activation / softmax and stores the HN outputs.  This GEMM's own output
+  // is never written.  One N tile (BN >= N) so a CTA owns whole rows.
+  static constexpr bool HEAD = C::HEAD != 0;
+  static_assert(!HEAD || (NTN == 1 && !C::CONV && !C::RES && C::UPF == 1 && !KP && !WIDE &&
+                          C::HN <= 16 && C::BN >= 32), "fused head");
   static constexpr int SMEM = C::NS * STAGE + EPI_STAGE + 1024 /*align*/ + 512 /*barriers*/;
+
+  // the head's partial dot over this warp's columns [CB, CB + EPI_COLS)
+  template <int CB>
+  __device__ static __forceinline__ void head_dot(const float (&run)[EPI_COLS], float (&hp)[C::HN]) {
+#pragma unroll
+    for (int i = 0; i < EPI_COLS; ++i) {
+      if (CB + i < C::N) {
+#pragma unroll
+        for (int j = 0; j < C::HN; ++j) hp[j] = fmaf(run[i], C::hw((CB + i) * C::HN + j), hp[j]);
+      }
+    }
+  }
 
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
                              const TmaDesc* tmA, const TmaDesc* tmB, const TmaDesc* tmBlo,
@@ -1110,6 +1138,48 @@ struct GemmTc {
           return live;
         };
         const float* res = at<float>(arena, C::RES_OFF);
+        if constexpr (HEAD) {
+#pragma unroll
+          for (int i = 0; i < EPI_COLS; ++i) {
+            const int col = cbeg + i < C::N ? cbeg + i : C::N - 1;
+            run[i] = finish<C::ACT, EMODE, C::POST>(run[i] + __ldg(bias + col), ps, po, col);
+          }
+          float hp[C::HN];
+          float* xch = reinterpret_cast<float*>(epi_stage + (ew & 3) * NBUF * 128);   // [HN][32]
+          if (cbeg == 0) {
+#pragma unroll
+            for (int j = 0; j < C::HN; ++j) hp[j] = C::hbias(j);
+            head_dot<0>(run, hp);
+            named_sync64(1 + q);                     // partials stored
+#pragma unroll
+            for (int j = 0; j < C::HN; ++j) hp[j] = add(hp[j], xch[j * 32 + lane]);
+            named_sync64(5 + q);                     // partials consumed
+            const float* hps = at<float>(pool, C::H_PS_OFF);
+            const float* hpo = at<float>(pool, C::H_PO_OFF);
+            float hv[C::HN];
+#pragma unroll
+            for (int j = 0; j < C::HN; ++j) hv[j] = finish<C::H_ACT, EMODE, C::H_POST>(hp[j], hps, hpo, j);
+            if (C::H_SOFTMAX) {
+              if (C::H_SMEXP == SMEXP_EXACT) softmax_row_regs_f32<C::HN, C::HN>(hv);
+              else softmax_row_regs<C::HN, C::HN, C::H_SMEXP>(hv);
+            }
+            const long long m = (long long)mb * BM + r;
+            if (m < rows) {
+              float* d = at<float>(arena, C::H_OUT_OFF) + m * C::HN;
+#pragma unroll
+              for (int j = 0; j < C::HN; ++j) d[j] = hv[j];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < C::HN; ++j) hp[j] = 0.f;
+            if (cbeg < C::N) head_dot<EPI_COLS>(run, hp);
+#pragma unroll
+            for (int j = 0; j < C::HN; ++j) xch[j * 32 + lane] = hp[j];
+            named_sync64(1 + q);
+            named_sync64(5 + q);
+          }
+          continue;
+        }
 #pragma unroll
         for (int g = 0; g < EPI_COLS / 16; ++g) {
           const int col0 = nb * C::BN + cbeg + g * 16;

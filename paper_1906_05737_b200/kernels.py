@@ -26,7 +26,7 @@ import numpy as np
 
 from .errors import UnsupportedLayer
 from .graph import same_padding
-from .planner import sep_narrow_geometry
+from .planner import _private, sep_narrow_geometry
 
 F32 = np.float32
 
@@ -194,8 +194,12 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True):
+                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True):
         self.use_tc = use_tc
+        self.head = head
+        self.head_cap = {}           # unit pos -> largest n its own launches serve
+        self._n_cap = None
+        self.narrow_geo = narrow_geo
         self.direct_imm = direct_imm
         self.sep_fma = sep_fma
         self.narrow = narrow
@@ -241,6 +245,10 @@ class Specializer:
     def emit(self, unit_pos, tag, template, fields, block, smem, ipi, ipb,
              grid_mult=1, n_min=1, n_max=1 << 30, dynamic_smem=False, note="",
              tmaps=(), grid_cap=0, cluster=1, code=""):
+        if self._n_cap is not None:          # batches above the cap run fused elsewhere
+            n_max = min(n_max, self._n_cap)
+            if n_min > n_max:
+                return
         kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
         cfg = f"Cfg_{len(self.names)}"
         body = _cfg_struct(cfg, fields, code)
@@ -397,7 +405,8 @@ class Specializer:
                     conv = dict(H=HO, W=WO, CI=CI, HO=HO, WO=WO, KW=1, PT=0, PL=0,
                                 POOL=False, PHO=1, PWO=1, C0=CI, CONCAT=False, UPF=1, DWF=1)
                 self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
-                              rows_geo=dict(HO=HO, WO=WO, UPF=UPF))
+                              rows_geo=dict(HO=HO, WO=WO, UPF=UPF),
+                              head=self._head_candidate(pos, u) if not conv else None)
                 n_max = n_tc - 1
                 if n_max < n_min:
                     return
@@ -410,6 +419,8 @@ class Specializer:
         if self.narrow and rows_contig and CO <= 32 and K % 4 == 0 and K * CO <= NARROW_MAX_W:
             KS = next(ks for ks in (4, 2, 1) if K % (4 * ks) == 0 and K // ks >= 16 or ks == 1)
             TR = 32 if KS > 1 else 64
+            if self.narrow_geo:                      # (KS, TR) override for experiments
+                KS, TR = self.narrow_geo
             ast = K + 4 if ((K + 4) // 4) % 2 else K + 8
             fixed = (max(KS - 1, 1) + 1) * TR * (CO | 1)
             NS = min(4, (SMEM_MAX // 16 - fixed) // (TR * ast))    # four CTAs per SM
@@ -545,7 +556,25 @@ class Specializer:
                     DW_ACT=ep["ACT"], DW_POST=ep["POST"], DW_PS_OFF=ep["PS_OFF"],
                     DW_PO_OFF=ep["PO_OFF"])
 
-    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None):
+    def _head_candidate(self, pos, u):
+        """The Dense head (<= 16 outputs) right after Dense unit ``u`` that
+        the tcgen05 epilogue can compute from u's finished rows (HEAD), or
+        None.  u's output must feed only the head, and the head's output must
+        not overlap u's input (the fused kernel reads one while writing the
+        other)."""
+        if not self.head or u.kind != "Dense" or u.residual_id is not None or pos + 1 >= len(self.plan.units):
+            return None
+        v = self.plan.units[pos + 1]
+        if (v.kind != "Dense" or v.input_ids != (u.output_id,) or v.residual_id is not None
+                or v.kernel.shape[1] > 16 or not _private(self.plan, u.output_id)):
+            return None
+        o_in, s_in = self.asg.offsets[u.input_ids[0]]
+        o_out, s_out = self.asg.offsets[v.output_id]
+        if o_out < o_in + s_in and o_in < o_out + s_out:
+            return None
+        return v
+
+    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None, head=None):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
@@ -717,6 +746,26 @@ class Specializer:
         tm_r = out_map(u.residual_id) if (epi_tma and res) else tm_o
         smem = NS * stage + epi_bytes + 1024 + 512
         ntn = NPAD // BN
+        code = ""
+        hn = 0
+        # the head's FFMAs lengthen the epilogue: only when a second accumulator
+        # buffer keeps the MMA from waiting on it (measured: cfg0 Dense 256->32
+        # + 32->2, two buffers: replay -1.3%; cfg1 256->128 + 128->10, one
+        # buffer: +1%)
+        if (head is not None and ntn == 1 and BN >= 32 and not wide and not res and not kpack
+                and ABUF >= 2):
+            hn = head.kernel.shape[1]
+            hep = self.epilogue_fields(head, hn)
+            fields.update(HEAD=1, HN=hn, H_ACT=hep["ACT"], H_POST=hep["POST"],
+                          H_PS_OFF=hep["PS_OFF"], H_PO_OFF=hep["PO_OFF"],
+                          H_SOFTMAX=bool(head.softmax_after),
+                          H_SMEXP=SMEXP_CODE[self.opt.softmax_exp],
+                          H_OUT_OFF=self.arena_off(head.output_id))
+            code = _imm_tables(hw=np.asarray(head.kernel, F32), hbias=head.bias)
+            self.head_cap[pos + 1] = n_min - 1
+        else:
+            fields.update(HEAD=0, HN=1, H_ACT=0, H_POST=0, H_PS_OFF=0, H_PO_OFF=0, H_SOFTMAX=0,
+                          H_SMEXP=0, H_OUT_OFF=0)
         if conv:
             ow = 16 - (kw - 1) if kpack else 16
             tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // ow)
@@ -728,7 +777,7 @@ class Specializer:
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
-                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r],
+                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
                   grid_cap=self.sm_count - self.sm_count % 2 if pair else self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile {256 if pair else 128}x{BN}x{BK}"
                        f"{' CTA pair' if pair else ''} stages {NS}"
@@ -736,7 +785,8 @@ class Specializer:
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
                        f"{' depthwise fused' if dwf else ''}"
-                       f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma else ''}")
+                       f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
+                       f"{f' + fused Dense head N={hn}' if hn else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
                      PHO, PWO, UPF=1, n_min=1):
@@ -924,6 +974,7 @@ class Specializer:
 
     def run(self):
         for pos, u in enumerate(self.plan.units):
+            self._n_cap = self.head_cap.get(pos)
             if u.kind in ("Dense", "Conv2D"):
                 self.gemm(pos, u)
             elif u.kind == "DepthwiseConv2D":
@@ -944,6 +995,7 @@ class Specializer:
                 self.pad(pos, u)
             else:
                 raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
+        self._n_cap = None
         self.mega_source = ""
         arena_extra = self._mega() if self.mega else 0
         head = '#include "nnb_kernels.cuh"\n\n'

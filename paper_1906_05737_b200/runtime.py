@@ -84,7 +84,7 @@ class CompiledNetwork:
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
                  wide_chunk=None, wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True,
-                 sep_fma=True):
+                 sep_fma=True, narrow_geo=None, head=True):
         import torch
 
         t0 = time.perf_counter()
@@ -100,7 +100,7 @@ class CompiledNetwork:
         if mega and dw_fusion == "narrow":
             dw_fusion = False      # the persistent kernel walks the unfused templates
         self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion, dw_fusion=dw_fusion)
-        self.assignment = plan_buffers(self.plan)
+        self.assignment = plan_buffers(self.plan, reserve_heads=head)
         cap = _capacity(self.max_batch)
         from .kernels import TC_MIN_ROWS
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
@@ -112,6 +112,7 @@ class CompiledNetwork:
                           small_dense_rows=small_dense_rows, wide=wide, wide_bk=wide_bk,
                           wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss,
                           narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
+                          narrow_geo=narrow_geo, head=head,
                           **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
         arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 

@@ -501,3 +501,37 @@ def test_narrow_row_gemm_pixels():
     np.testing.assert_allclose(got, ref(m, w, x), **TOL)
     simt, _ = gpu(m, w, x, narrow=False)
     np.testing.assert_array_equal(got, simt)
+
+
+@pytest.mark.parametrize("k,n1,act1,n2,head,n", [
+    (256, 128, "elu", 10, "softmax", 4100), (64, 32, "relu", 2, "softmax", 2500),
+    (128, 96, "tanh", 16, "sigmoid", 3001), (96, 64, "linear", 7, "bn", 2048),
+    (256, 128, "elu", 10, "softmax", 600)])
+def test_fused_dense_head(k, n1, act1, n2, head, n):
+    """Dense (tcgen05) -> Dense head with <= 16 outputs (+ softmax / act /
+    BatchNorm): the head computed in the tcgen05 epilogue (HEAD), its input
+    never stored; below the tensor-core batch threshold the head stays its
+    own launch."""
+    rng = np.random.default_rng(k + n1 + n2)
+    b = NetBuilder()
+    x_ = b.input((k,))
+    h = b.layer("Dense", [x_], {"units": n1, "activation": act1},
+                [("kernel", he(rng, (k, n1), k)), ("bias", (rng.standard_normal(n1) * 0.1).astype(F32))])
+    y = b.layer("Dense", [h], {"units": n2, "activation": head if head in ("sigmoid",) else "linear"},
+                [("kernel", he(rng, (n1, n2), n1)), ("bias", (rng.standard_normal(n2) * 0.1).astype(F32))])
+    if head == "softmax":
+        y = b.layer("Softmax", [y])
+    elif head == "bn":
+        y = b.layer("BatchNorm", [y], None, bn_params(rng, n2))
+    m, w = b.build([y])
+    x = rng.uniform(-2, 2, (n, k)).astype(F32)
+    got, net = gpu(m, w, x)
+    fused = any("fused Dense head" in net.artifact.launches[i].note for i in net.launches_for())
+    if n < 2048:
+        assert not fused, net.describe()
+    elif n1 <= 64:                 # two accumulator buffers: the head is fused
+        assert fused, net.describe()
+    assert len(net.launches_for()) == (1 if fused else 2)
+    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+    unf, _ = gpu(m, w, x, head=False)
+    np.testing.assert_allclose(got, unf, rtol=1e-5, atol=2e-6)
