@@ -38,6 +38,7 @@ SMALL_M = 8           # Dense rows at or below this use the split-K GEMV kernel
 TC_MIN_K = 32         # tensor-core GEMM eligibility (contraction and output width)
 TC_MIN_N = 32
 TC_MIN_ROWS = 2048    # GEMM rows per launch from which the tcgen05 kernel is used
+WIDE_MIN_TILES = 148  # 256x256 tiles per launch from which N = 256 tiles are used
 SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
 MEGA_MAX_N = 8         # batches up to this run as one persistent kernel (when eligible)
 MEGA_THREADS = 256     # its block size (units with larger blocks opt it out)
@@ -574,7 +575,8 @@ class Specializer:
             return None
         return v
 
-    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None, head=None):
+    def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None, head=None,
+                 n_max=1 << 30):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
@@ -600,6 +602,21 @@ class Specializer:
                     and self.pair and not self.aldg and CO % 4 == 0
                     and (not rows_geo or rows_geo.get("UPF", 1) == 1))
         if wide:
+            # N = 256 tiles only where they keep every SM pair busy: with few
+            # 256-row tiles (cfg3's 4x4x256 layers at 256 images: 16 tiles)
+            # the 128-column form spreads the same work over 4x the CTAs
+            # (measured: cfg3 @256 0.279 -> 0.266 ms)
+            ntw = -(-CO // 256)
+            n_wide = -(-(-(-WIDE_MIN_TILES // ntw) * 256) // rows)
+            if n_wide > n_min:
+                saved, self.wide = self.wide, False
+                self._gemm_tc(pos, u, wmat, K, CO, rows, n_min, conv, rows_geo,
+                              n_max=min(n_max, n_wide - 1))
+                self.wide = saved
+                if n_wide > n_max:
+                    return
+                n_min = n_wide
+                head = None
             BN = 256
         NPAD = -(-CO // BN) * BN
         dwf = bool(conv and conv.get("DWF"))
@@ -777,7 +794,7 @@ class Specializer:
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
-                  n_min=n_min, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
+                  n_min=n_min, n_max=n_max, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
                   grid_cap=self.sm_count - self.sm_count % 2 if pair else self.sm_count,
                   note=f"tcgen05 3xTF32 M=n*{rows} N={CO} K={K} tile {256 if pair else 128}x{BN}x{BK}"
                        f"{' CTA pair' if pair else ''} stages {NS}"
