@@ -21,7 +21,8 @@ Keys beyond the base contract:
                peak (tcgen05 kernels).
   cpu_baseline the C oracle (oracle/nnoracle.c, the reference interpreter
                restated) on all host threads over a bounded sample.
-  parity       max |GPU - oracle| over sampled images of the timed batch.
+  parity       max |GPU - oracle| over sampled images of the timed batch
+               (evaluated by the cpu_baseline leg, rank 0 at N=1).
   configs      all five BASELINE configs: batch-1 latency and large-batch
                throughput (L2 flushed between timed replays), fraction of the
                layerwise roofline of SURVEY.md 8(d).
@@ -151,9 +152,12 @@ def max_over_ranks(world, value, local):
     return float(t.item())
 
 
-def cpu_reference(cfg, batch, seconds, threads=None):
+def cpu_reference(cfg, batch, seconds, threads=None, check=None):
     """Time the C oracle (reference interpreter restated) on host threads.
-    Returns (images/s, sample images, threads, seconds)."""
+    Returns (images/s, sample images, threads, seconds, parity).  ``check`` =
+    (inputs, gpu_outputs) of sampled images of the timed batch: the oracle
+    also evaluates those, as the checker of the GPU outputs (the only other
+    use of oracle/ in this file)."""
     from oracle import oracle
     from paper_1906_05737_b200 import zoo
     threads = threads or os.cpu_count() or 1
@@ -172,7 +176,14 @@ def cpu_reference(cfg, batch, seconds, threads=None):
     t0 = time.perf_counter()
     oracle.run_graph(g, [x], "exact", threads)
     dt = time.perf_counter() - t0
-    return sample / dt, sample, threads, dt
+    parity = None
+    if check is not None:
+        xs, got = check
+        want = oracle.run_graph(g, [xs], "exact", threads)[0]
+        parity = {"images": len(xs), "max_abs": float(np.abs(got - want).max()),
+                  "ok": bool(np.allclose(got, want, rtol=1e-4, atol=1e-5)),
+                  "tolerance": "rtol 1e-4 / atol 1e-5 vs oracle/nnoracle.c (exact)"}
+    return sample / dt, sample, threads, dt, parity
 
 
 def reference_arm(args, world, rank):
@@ -185,7 +196,7 @@ def reference_arm(args, world, rank):
     sample = threads = None
     budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
     for i in range(args.warmup + args.steps):
-        v, sample, threads, _ = cpu_reference(cfg, batch, budget)
+        v, sample, threads, _, _ = cpu_reference(cfg, batch, budget)
         if i >= args.warmup:
             vals.append(v)
     v = float(np.mean(vals))
@@ -324,14 +335,11 @@ def main():
     value = world * B * args.steps / (ms / 1e3)
     n_launch = len(net.launches_for(B))
 
-    # ---------------- parity on sampled images of this batch ----------------
-    from oracle import oracle
+    # sampled outputs of this batch (checked against the oracle on the
+    # cpu_baseline leg, and against the e2e path below)
     idx = np.linspace(0, B - 1, 16).astype(int)
     got = net.output_views[0][torch.as_tensor(idx, device=dev)].cpu().numpy()
-    want = oracle.run(m, w, [x[idx]], "exact")[0]
-    parity = {"images": len(idx), "max_abs": float(np.abs(got - want).max()),
-              "ok": bool(np.allclose(got, want, rtol=1e-4, atol=1e-5)),
-              "tolerance": "rtol 1e-4 / atol 1e-5 vs oracle/nnoracle.c (exact)"}
+    parity = None
 
     # ---------------- e2e through the C-ABI host-buffer call ----------------
     from paper_1906_05737_b200 import pinned_empty
@@ -405,7 +413,8 @@ def main():
     extra = None
     cpu = None
     if rank == 0 and world == 1:
-        c_val, c_n, c_thr, c_dt = cpu_reference(cfg, B, args.cpu_seconds)
+        c_val, c_n, c_thr, c_dt, parity = cpu_reference(cfg, B, args.cpu_seconds,
+                                                        check=(x[idx], got))
         cpu = {"value": c_val, "unit": "images/s", "cores": c_thr, "kind": "port",
                "sample": f"{c_n} images of {zoo.CONFIGS[cfg]['name']} through "
                          f"oracle/nnoracle.c in {c_dt:.1f} s"}
