@@ -195,8 +195,9 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True):
+                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
+        self.sep_geo = sep_geo
         self.head = head
         self.head_cap = {}           # unit pos -> largest n its own launches serve
         self._n_cap = None
@@ -363,6 +364,8 @@ class Specializer:
         # (nnb_sep.cuh, all batch sizes)
         if u.dw is not None and self.narrow:
             geo = sep_narrow_geometry(u.dw, u)
+            if geo is not None and self.sep_geo:
+                geo = sep_narrow_geometry(u.dw, u, force=self.sep_geo)
             if geo is not None:
                 self._sep_narrow(pos, u, wmat, CI, CO, geo)
                 return

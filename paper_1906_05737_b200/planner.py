@@ -465,7 +465,7 @@ def fuse_concat(plan):
 SEP_SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
 
 
-def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX):
+def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
     """Tile geometry (TH output rows, NS ring stages, NT threads, shared bytes)
     of the fused depthwise + narrow pointwise kernel (nnb_sep.cuh) for the
     depthwise unit ``d`` feeding the 1x1 conv ``u``, or None when the pair is
@@ -485,25 +485,32 @@ def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX):
     cp = c + 4 if ((c + 4) // 4) % 2 else c + 8
     wb = (wo - 1) * s + kw
     rs = (co | 1) if co % 4 else (co + 4 if ((co + 4) // 4) % 2 else co + 8)
-    th0 = max(1, min(ho, 256 // wo))
-    for per_sm in (3, 2):
-        best = None
-        for th in range(th0, 0, -1):
-            if th * wo < min(128, ho * wo):
-                break
-            ri = (th - 1) * s + kh
-            nt = -(-th * wo // 32) * 32
-            for ns in (3, 2):
-                smem = 4 * (ns * ri * wb * cp + th * wo * rs)
-                if smem + 1024 <= smem_max // per_sm:
-                    # warps issued over an image (idle lanes of the last warp,
-                    # ragged last band), then taller bands
-                    key = (nt // 32 * -(-ho // th), -th, -ns)
-                    if best is None or key < best[0]:
-                        best = (key, dict(TH=th, NS=ns, NT=nt, smem=smem))
-                    break
-        if best:
-            return best[1]
+    if force:                                       # (TH, NS) for experiments
+        th, ns = force
+        ri = (th - 1) * s + kh
+        smem = 4 * (ns * ri * wb * cp + th * wo * rs)
+        return dict(TH=th, NS=ns, NT=-(-th * wo // 32) * 32, smem=smem)
+    # two ring stages, tiles of 4-8 warps; the band height that issues the
+    # fewest warps per image (idle lanes of a tile's last warp, ragged last
+    # band), then the smaller tile (more CTAs per SM).  Measured (cfg2 block 1,
+    # 1024 images): TH 2/3/4/5/6/8 -> 73.9/63.9/70.6/74.0/70.5/74.3 us (three
+    # stages never helped); cfg3 block 1 (64 px rows): TH 2/4 -> 31.1/29.2 us.
+    best = None
+    for th in range(1, ho + 1):
+        if th * wo < min(97, ho * wo):
+            continue
+        ri = (th - 1) * s + kh
+        nt = -(-th * wo // 32) * 32
+        if nt > max(256, -(-wo // 32) * 32):
+            break
+        smem = 4 * (2 * ri * wb * cp + th * wo * rs)
+        if smem + 1024 > smem_max:
+            break
+        key = (nt // 32 * -(-ho // th), th)
+        if best is None or key < best[0]:
+            best = (key, dict(TH=th, NS=2, NT=nt, smem=smem))
+    if best:
+        return best[1]
     return None
 
 

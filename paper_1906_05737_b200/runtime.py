@@ -84,7 +84,7 @@ class CompiledNetwork:
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
                  wide_chunk=None, wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True,
-                 sep_fma=True, narrow_geo=None, head=True):
+                 sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         import torch
 
         t0 = time.perf_counter()
@@ -112,7 +112,7 @@ class CompiledNetwork:
                           small_dense_rows=small_dense_rows, wide=wide, wide_bk=wide_bk,
                           wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss,
                           narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
-                          narrow_geo=narrow_geo, head=head,
+                          narrow_geo=narrow_geo, head=head, sep_geo=sep_geo,
                           **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
         arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 
@@ -206,7 +206,11 @@ class CompiledNetwork:
             raise InputShapeMismatch(f"expected {len(self.input_views)} inputs, got {len(inputs)}")
         count = None
         for view, x in zip(self.input_views, inputs):
-            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, np.float32))
+            if not isinstance(x, torch.Tensor):
+                x = np.asarray(x, np.float32)
+                if not x.flags.writeable:             # torch.from_numpy wants writable memory
+                    x = x.copy()
+            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(x)
             if self.batch is None:
                 if tuple(t.shape) != tuple(view.shape):
                     raise InputShapeMismatch(f"input shape {tuple(t.shape)} does not match "
