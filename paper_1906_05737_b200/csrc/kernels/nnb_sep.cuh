@@ -48,7 +48,7 @@ struct SepNarrow {
   static constexpr int PXT = TH * WO;                               // output pixels per tile
   static constexpr int CQ = CI / 4;
   static constexpr int BAND = RI * WB * CP;                         // floats per stage
-  static_assert(CI % 4 == 0 && CI <= 32 && CO <= 32 && PXT <= NT && NT % 32 == 0 && NT <= 1024,
+  static_assert(CI % 4 == 0 && CI <= 128 && CO <= 128 && PXT <= NT && NT % 32 == 0 && NT <= 1024,
                 "depthwise + narrow pointwise");
   // staging row stride: 16-byte rows at an odd 16-byte stride (conflict-free
   // float4 writes) when CO % 4 == 0, else an odd float stride

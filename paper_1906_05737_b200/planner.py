@@ -463,6 +463,8 @@ def fuse_concat(plan):
 
 
 SEP_SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
+SEP_CI_MAX = 32            # depthwise channels = pointwise K of the fused kernel
+SEP_CO_MAX = 32            # pointwise outputs (weights as FFMA immediates)
 
 
 def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
@@ -478,7 +480,7 @@ def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
     co = u.output_shape.c
     kh, kw = d.kernel_hw
     s = d.stride
-    if not (c % 4 == 0 and c <= 32 and co <= 32 and wo <= 512 and kh <= 7 and kw <= 7
+    if not (c % 4 == 0 and c <= SEP_CI_MAX and co <= SEP_CO_MAX and wo <= 512 and kh <= 7 and kw <= 7
             and not u.pool_after and u.upsample_after == 1 and not u.softmax_after
             and not u.concat_in):
         return None
