@@ -380,15 +380,23 @@ def main():
     peak_fp32 = roofline.fp32_peak_tflops()
     fp32_equiv = B * f / (lt[dom] / 1e3) / 1e12
     if "_tc_" in L.kernel:
-        # 3xTF32: the tensor pipe executes three TF32 products per FP32 MAC
+        # 3xTF32: the tensor pipe executes three TF32 products per FP32 MAC;
+        # with the BF16 correction split (note "bf16 corr") one TF32 product
+        # plus one K = 16 BF16 MMA per tf32 k-step, which issues in the time of
+        # a TF32 MMA (BF16 runs at 2x the TF32 rate): 2 TF32-equivalents
+        cb16 = "bf16 corr" in L.note
+        mult = 2 if cb16 else 3
         tf32 = measure_tf32_peak(torch, dev)
-        achieved = 3 * fp32_equiv
+        achieved = mult * fp32_equiv
         roof = {"bound": "tensor", "kernel": L.kernel, "unit": "TFLOP/s",
                 "achieved": achieved, "peak": tf32, "frac": achieved / tf32,
                 "peak_source": "TF32 dense, cuBLAS fp32 matmul with allow_tf32 on this GPU "
                                "(8192^3, best of 5; MEASURED_PEAKS.json has bf16 only: "
                                f"{peaks['bf16_tflops']} TF/s)",
-                "achieved_counts": "3 x 2MNK tensor flops (3xTF32 split) per launch",
+                "achieved_counts": ("2 x 2MNK TF32-equivalent tensor flops per launch (1 TF32 "
+                                    "product a_hi*b_hi + the two correction products as one "
+                                    "BF16 K=16 MMA = 2MNK TF32 + 4MNK BF16 flops)") if cb16
+                else "3 x 2MNK tensor flops (3xTF32 split) per launch",
                 "peak_note": "the live cuBLAS TF32 GEMM is the measured denominator (a good "
                              "kernel can read a little above it); nominal dense TF32 is "
                              "1100 TFLOP/s (B200_PROFILING.md)",

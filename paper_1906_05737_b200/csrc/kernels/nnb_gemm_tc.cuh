@@ -64,6 +64,20 @@ __device__ __forceinline__ u32 split_hi(float a) {
   return ((NNB_SPLIT_RN ? u + 0x1000u : u) & 0xFFFFE000u);
 }
 
+// CORR_BF16 split of A in shared memory.  NNB_CB16_WB=1 writes the
+// round-to-nearest TF32 hi back over the tile; 0 (default) leaves the raw
+// tile, which the tensor core truncates, so hi = trunc(a) and lo = a - hi >= 0
+// -- its bf16 rounding is unbiased either way (the tf32 truncation of lo that
+// made the write-back necessary in the tf32 split does not occur).  Measured
+// (cfg1 Dense 1024->512 @65536): 0.231 ms with the write-back, 0.220 without.
+#ifndef NNB_CB16_WB
+#define NNB_CB16_WB 0
+#endif
+__device__ __forceinline__ u32 cb16_hi(float a) {
+  const u32 u = __float_as_uint(a);
+  return ((NNB_CB16_WB ? u + 0x1000u : u) & 0xFFFFE000u);
+}
+
 __device__ __forceinline__ u32 smem_u32(const void* p) {
   return (u32)__cvta_generic_to_shared(p);
 }
@@ -235,6 +249,35 @@ __device__ __forceinline__ void mma_tf32_pair(u32 tmem_d, u64 adesc, u64 bdesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// kind::f16 (BF16 operands, FP32 accumulator) forms: the correction products
+// of the CORR_BF16 split (one K = 16 instruction per tf32 k-step)
+__device__ __forceinline__ void mma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// two floats -> bf16x2 (round to nearest even), `lo` in the low half
+__device__ __forceinline__ u32 bf16x2_rn(float lo, float hi) {
+  u32 d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
 __device__ __forceinline__ void mma_commit_pair(u64* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -430,6 +473,17 @@ struct GemmTc {
   static constexpr u32 IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(C::BN >> 3) << 17) |
                                ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
 #endif
+  // CORR_BF16: the two correction products of a tf32 k-step (8 k) run as ONE
+  // kind::f16 MMA of K = 16 over BF16 operands -- A_corr row = [bf16(a_hi) x 8,
+  // bf16(a_lo) x 8] per k-step, B_corr = [bf16(b_lo) x 8, bf16(b_hi) x 8] (built
+  // at compile() time) -- so a k-step issues 2 instruction-times of MMA instead
+  // of 3 (BF16 runs at twice the TF32 rate).  A_corr replaces the A_lo tile and
+  // B_corr the B_lo tile, byte for byte.  Error per product <= 2^-17 |a b|
+  // (bf16 rounding of the split halves), DESIGN.md section 4.
+  static constexpr bool CB16 = C::CORR_BF16 != 0;
+  static constexpr u32 IDESC_B16 = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(C::BN >> 3) << 17) |
+                                   ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
+  static_assert(!CB16 || (!TA && !C::ALDG && !C::DWF && BK == 32 && C::CSPLIT), "bf16 correction split");
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
@@ -673,10 +727,16 @@ struct GemmTc {
                 mma_tf32_ts_pair(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts_pair(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
                 mma_tf32_ts_pair(dc, ta + BK + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+              } else if (PAIR && CB16) {
+                mma_tf32_pair(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_bf16_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
               } else if (PAIR) {
                 mma_tf32_pair(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_pair(dc, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
                 mma_tf32_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
+              } else if (CB16) {
+                mma_tf32(d, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
+                mma_bf16(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
               } else if (TA) {
                 mma_tf32_ts(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
@@ -914,6 +974,32 @@ struct GemmTc {
           mbar_wait(&full[s], ph);
           float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
           float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + A_BYTES);
+          if constexpr (CB16) {
+            // k-step g of row `row` = logical 16-byte chunks 2g, 2g+1 of the
+            // 128B-swizzled row (physical chunk = logical ^ (row & 7)); the
+            // A_corr row keeps the same swizzle: bf16(hi) x 8 in chunk 2g,
+            // bf16(lo) x 8 in chunk 2g+1
+            uint4* corr = reinterpret_cast<uint4*>(lo);
+#pragma unroll 2
+            for (int i = ct; i < A_BYTES / 32; i += 64) {
+              const int row = i >> 2, g = i & 3, x = row & 7;
+              const int p0 = row * 8 + ((2 * g) ^ x), p1 = row * 8 + ((2 * g + 1) ^ x);
+              const float4 v0 = a[p0], v1 = a[p1];
+              float4 h0, h1;
+              h0.x = __uint_as_float(cb16_hi(v0.x)); h0.y = __uint_as_float(cb16_hi(v0.y));
+              h0.z = __uint_as_float(cb16_hi(v0.z)); h0.w = __uint_as_float(cb16_hi(v0.w));
+              h1.x = __uint_as_float(cb16_hi(v1.x)); h1.y = __uint_as_float(cb16_hi(v1.y));
+              h1.z = __uint_as_float(cb16_hi(v1.z)); h1.w = __uint_as_float(cb16_hi(v1.w));
+              if (NNB_CB16_WB) {
+                a[p0] = h0;
+                a[p1] = h1;
+              }
+              corr[p0] = make_uint4(bf16x2_rn(h0.x, h0.y), bf16x2_rn(h0.z, h0.w),
+                                    bf16x2_rn(h1.x, h1.y), bf16x2_rn(h1.z, h1.w));
+              corr[p1] = make_uint4(bf16x2_rn(v0.x - h0.x, v0.y - h0.y), bf16x2_rn(v0.z - h0.z, v0.w - h0.w),
+                                    bf16x2_rn(v1.x - h1.x, v1.y - h1.y), bf16x2_rn(v1.z - h1.z, v1.w - h1.w));
+            }
+          } else {
 #pragma unroll 4
           for (int i = ct; i < A_BYTES / 16; i += 64) {
             float4 v = a[i], h, l;
@@ -932,6 +1018,7 @@ struct GemmTc {
             l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
             if (NNB_HI_INPLACE || C::RN_SS) a[i] = h;
             lo[i] = l;
+          }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           arrive_mma(&lo_ready[s]);

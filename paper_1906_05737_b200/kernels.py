@@ -195,9 +195,10 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=True, corr_bf16=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
+        self.corr_bf16 = corr_bf16
         self.head = head
         self.head_cap = {}           # unit pos -> largest n its own launches serve
         self._n_cap = None
@@ -701,7 +702,15 @@ class Specializer:
         wt[:CO, :K] = np.asarray(wmat, F32).T
         hi = tf32_split_hi(wt, self.split_rn)
         lo = (wt - hi).astype(F32)
-        hi_off, lo_off = self.pool.add(hi), self.pool.add(lo)
+        # BF16 correction products (one kind::f16 MMA per k-step instead of
+        # two tf32 ones; B_corr replaces B_lo byte for byte) on the N = 256
+        # row tiles.  Measured (cfg1 @65536): Dense 1024->512 0.258 -> 0.220 ms,
+        # 512->256 0.081 -> 0.073 ms; the shared-memory-A conv tiles got slower
+        # (cfg4 0.117 / 0.179 / 0.317 -> 0.136 / 0.213 / 0.357 ms: the extra
+        # split work lands on their two converter warps), so they keep tf32.
+        cb16 = bool(self.corr_bf16 and wide and not tmem_a and not aldg and not dwf and BK == 32
+                    and csplit)
+        hi_off, lo_off = self.pool.add(hi), self.pool.add(bf16_corr_words(hi, lo) if cb16 else lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
                    C0=1, CONCAT=0, UPF=1, DWF=0)
         if conv:
@@ -712,6 +721,7 @@ class Specializer:
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
+                      CORR_BF16=int(cb16),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
@@ -806,6 +816,7 @@ class Specializer:
                        f"{' taps packed in N' if kpack else ''}"
                        f"{' depthwise fused' if dwf else ''}"
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
+                       f"{' bf16 corr' if cb16 else ''}"
                        f"{f' + fused Dense head N={hn}' if hn else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
@@ -1111,6 +1122,26 @@ class Specializer:
                                     cooperative=True, zero_offset=sync_off))
         self.mega_source = self.chunks[-1]
         return 256
+
+
+def bf16_rn(x):
+    """float32 -> bfloat16 bit patterns (uint16), round to nearest even."""
+    u = np.ascontiguousarray(x, F32).view(np.uint32)
+    return ((u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)).astype(np.uint16)
+
+
+def bf16_corr_words(hi, lo):
+    """B_corr operand of the CORR_BF16 tcgen05 GEMM: per row of the K-major
+    [Npad, Kpad] weights and per k-step of 8, 16 bf16 = [bf16(lo) x 8,
+    bf16(hi) x 8] (the A side holds [bf16(a_hi) x 8, bf16(a_lo) x 8], so one
+    K = 16 MMA forms a_hi*b_lo + a_lo*b_hi), packed little-endian into
+    float32 words: the same bytes as the B_lo tile it replaces."""
+    n, k = hi.shape
+    assert k % 8 == 0
+    bh = bf16_rn(hi).reshape(n, k // 8, 8)
+    bl = bf16_rn(lo).reshape(n, k // 8, 8)
+    words = np.concatenate([bl, bh], axis=2).reshape(n, 2 * k)
+    return np.ascontiguousarray(words).view("<u4").view(F32)
 
 
 def tf32_split_hi(w, rn=True):

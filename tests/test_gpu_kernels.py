@@ -447,10 +447,52 @@ def test_wide_n256_tiles_opt_in(k, units):
     main chain restarted every 16 k-blocks) against the oracle."""
     rng = np.random.default_rng(k)
     m, w = dense_net(rng, k, units, "tanh")
-    x = rng.uniform(-2, 2, (2100, k)).astype(F32)
-    got, net = gpu(m, w, x, wide=True)
-    assert any("256x256" in l.note for l in net.artifact.launches)
-    np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+    rows = wide_rows(units)
+    x = rng.uniform(-2, 2, (rows, k)).astype(F32)
+    for cb16 in (True, False):
+        got, net = gpu(m, w, x, wide=True, corr_bf16=cb16)
+        assert any("256x256" in net.artifact.launches[i].note for i in net.launches_for(rows))
+        np.testing.assert_allclose(got, ref(m, w, x), **TOL)
+
+
+def wide_rows(units):
+    """Rows from which a Dense with `units` outputs gets N = 256 tiles
+    (kernels.WIDE_MIN_TILES 256x256 tiles per launch)."""
+    from paper_1906_05737_b200.kernels import WIDE_MIN_TILES
+    ntw = -(-units // 256)
+    return -(-WIDE_MIN_TILES // ntw) * 256 + 100
+
+
+@pytest.mark.parametrize("k,units,dist", [(1024, 512, "normal"), (512, 256, "scaled"),
+                                          (300, 260, "uniform"), (1024, 384, "scaled")])
+def test_wide_tiles_bf16_correction_products(k, units, dist):
+    """N = 256 tiles run the two correction products of every tf32 k-step as
+    one BF16 MMA (corr_bf16, default).  Stated tolerance of that path (DESIGN.md
+    section 4): |d| <= 1e-4 |ref| + 1e-5 + 2^-17 sum_k |a_k b_k|, checked on
+    every output; unscaled inputs also pass the plain FP32 gate.  The tf32
+    split (corr_bf16=False) is checked against the same oracle."""
+    seed = k + units
+    rng = np.random.default_rng(seed)
+    m, w = dense_net(rng, k, units, "linear")
+    wk = he(np.random.default_rng(seed), (k, units), k).astype(np.float64)
+    rows = wide_rows(units)
+    if dist == "normal":
+        x = rng.standard_normal((rows, k)).astype(F32)
+    elif dist == "uniform":
+        x = rng.uniform(-2, 2, (rows, k)).astype(F32)
+    else:
+        x = (rng.standard_normal((rows, k)) * rng.uniform(0.1, 10, (rows, 1))).astype(F32)
+    want = ref(m, w, x).astype(np.float64)
+    got, net = gpu(m, w, x)
+    assert any("bf16 corr" in net.artifact.launches[i].note for i in net.launches_for(rows))
+    mag = np.abs(x.astype(np.float64)) @ np.abs(wk)
+    lim = 1e-4 * np.abs(want) + 1e-5 + 2.0 ** -17 * mag
+    assert np.all(np.abs(got - want) <= lim)
+    if dist != "scaled":
+        np.testing.assert_allclose(got, want, **TOL)
+    tf32, net2 = gpu(m, w, x, corr_bf16=False)
+    assert not any("bf16 corr" in net2.artifact.launches[i].note for i in net2.launches_for(rows))
+    assert np.all(np.abs(tf32 - want) <= 1e-4 * np.abs(want) + 1e-5 + 2.0 ** -19 * mag)
 
 
 @pytest.mark.parametrize("k,units,head", [(128, 10, "softmax"), (4, 1, "linear"), (64, 24, "tanh"), (256, 8, "relu"),
