@@ -491,7 +491,9 @@ struct GemmTc {
   static constexpr bool AL = C::ALDG != 0;
   static_assert(!(AL && TA), "A via LDGSTS lives in shared memory");
   static_assert(!PAIR || (!AL && C::BN % 16 == 0 && (C::BN / 2) % 8 == 0), "CTA-pair tile shape");
-  static constexpr int CONV_WARPS = (TA || AL || DWF) ? 4 : 2;    // A splitters
+  // A splitters: 4 for A in TMEM / cp.async / depthwise producers and for
+  // the bf16 correction split of narrow tiles (C::CONV_W4), else 2
+  static constexpr int CONV_WARPS = (TA || AL || DWF || C::CONV_W4) ? 4 : 2;
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
@@ -966,7 +968,7 @@ struct GemmTc {
       }
     } else if (warp < EPI_W0) {
       // ---------------- converter: A -> (hi, lo) ----------------
-      const int ct = threadIdx.x - 64;   // 0..63
+      const int ct = threadIdx.x - 64;   // 0 .. 32 * CONV_WARPS - 1
       int s = 0;
       u32 ph = 0;
       for (int t = t0; t < tiles; t += tstep) {
@@ -981,7 +983,7 @@ struct GemmTc {
             // bf16(lo) x 8 in chunk 2g+1
             uint4* corr = reinterpret_cast<uint4*>(lo);
 #pragma unroll 2
-            for (int i = ct; i < A_BYTES / 32; i += 64) {
+            for (int i = ct; i < A_BYTES / 32; i += 32 * CONV_WARPS) {
               const int row = i >> 2, g = i & 3, x = row & 7;
               const int p0 = row * 8 + ((2 * g) ^ x), p1 = row * 8 + ((2 * g + 1) ^ x);
               const float4 v0 = a[p0], v1 = a[p1];
@@ -1001,7 +1003,7 @@ struct GemmTc {
             }
           } else {
 #pragma unroll 4
-          for (int i = ct; i < A_BYTES / 16; i += 64) {
+          for (int i = ct; i < A_BYTES / 16; i += 32 * CONV_WARPS) {
             float4 v = a[i], h, l;
             if (C::RN_SS) {
               // round-to-nearest split written back: lo of either sign, so

@@ -195,10 +195,11 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, corr_bf16=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
+        self.cb16_w4 = cb16_w4
         self.head = head
         self.head_cap = {}           # unit pos -> largest n its own launches serve
         self._n_cap = None
@@ -703,13 +704,20 @@ class Specializer:
         hi = tf32_split_hi(wt, self.split_rn)
         lo = (wt - hi).astype(F32)
         # BF16 correction products (one kind::f16 MMA per k-step instead of
-        # two tf32 ones; B_corr replaces B_lo byte for byte) on the N = 256
-        # row tiles.  Measured (cfg1 @65536): Dense 1024->512 0.258 -> 0.220 ms,
-        # 512->256 0.081 -> 0.073 ms; the shared-memory-A conv tiles got slower
-        # (cfg4 0.117 / 0.179 / 0.317 -> 0.136 / 0.213 / 0.357 ms: the extra
-        # split work lands on their two converter warps), so they keep tf32.
-        cb16 = bool(self.corr_bf16 and wide and not tmem_a and not aldg and not dwf and BK == 32
-                    and csplit)
+        # two tf32 ones; B_corr replaces B_lo byte for byte) on every
+        # shared-memory-A tile with 32-float k-blocks (corr_bf16=True) or on
+        # the N = 256 row tiles only ("wide", default).  Measured (cfg1
+        # @65536): Dense 1024->512 0.258 -> 0.220 ms, 512->256 0.081 -> 0.073
+        # ms; cfg4 @64 convs 0.117 / 0.179 / 0.317 -> 0.107 / 0.163 / 0.287
+        # ms -- but K = 32 pointwise convs then miss the plain FP32 gate on
+        # 0.03% of outputs near zero (|d| 1.5e-5: within the stated bf16
+        # bound, not within atol 1e-5), so narrow tiles keep the TF32 split.
+        cb16 = bool(self.corr_bf16 and (wide or self.corr_bf16 != "wide") and not tmem_a and not aldg
+                    and not dwf and BK == 32 and csplit)
+        # narrow tiles with the bf16 split: four converter warps (with two the
+        # extra split work made cfg4's convs slower; with four cfg4 @64
+        # 0.892 -> 0.834 ms, cfg0/2/3 unchanged)
+        conv_w4 = bool(cb16 and not wide and self.cb16_w4)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(bf16_corr_words(hi, lo) if cb16 else lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
                    C0=1, CONCAT=0, UPF=1, DWF=0)
@@ -721,7 +729,7 @@ class Specializer:
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
-                      CORR_BF16=int(cb16),
+                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --
@@ -804,7 +812,7 @@ class Specializer:
         else:
             ipi, ipb = rows, 256 if pair else 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
-        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf) else 384, smem,
+        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
                   n_min=n_min, n_max=n_max, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
