@@ -126,6 +126,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const TmaDesc* map, u64* 
       : "memory");
 }
 
+// L2 prefetch of a 2-D box (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const TmaDesc* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<u64>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const TmaDesc* map, u64* bar, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -674,6 +682,13 @@ struct GemmTc {
                           (tt % TX) * OW + kx - C::PL, (tt / TX) * TH + ky - C::PT, img);
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
+              if constexpr (C::APF > 0) {
+                // the A box APF k-blocks ahead into L2: its TMA load then
+                // waits on L2, not HBM, latency (the ring is latency-bound)
+                int pkb = kb + C::APF, pt = t;
+                if (pkb >= KB) { pkb -= KB; pt += tstep; }
+                if (pt < tiles) tma_prefetch_2d(tmA, pkb * BK, mb_of(pt) * BM);
+              }
             }
             if (!(NNB_TC_DBG & 2)) {
               const int brow = nb * C::BN + rank * B_ROWS;         // this CTA's B rows

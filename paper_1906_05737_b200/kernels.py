@@ -195,11 +195,12 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
         self.cb16_w4 = cb16_w4
+        self.a_prefetch = a_prefetch
         self.head = head
         self.head_cap = {}           # unit pos -> largest n its own launches serve
         self._n_cap = None
@@ -730,6 +731,7 @@ class Specializer:
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
                       CORR_BF16=int(cb16), CONV_W4=int(conv_w4),
+                      APF=(self.a_prefetch if (wide and not conv) else 0),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual
                       # loads / stores); long-K tiles keep direct row stores --

@@ -83,7 +83,7 @@ class CompiledNetwork:
                  nacc=None, aldg=False, kpack=True, dw_fusion="narrow", epi_tma=True, csplit=True, chunk=None,
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=512, tc_min_k=None, wide=True, wide_bk=32,
-                 wide_chunk=None, wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, narrow=True, direct_imm=True,
+                 wide_chunk=None, wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True,
                  sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         import torch
 
@@ -110,7 +110,7 @@ class CompiledNetwork:
                           csplit=csplit, chunk=chunk, split_rn=split_rn,
                           pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf,
                           small_dense_rows=small_dense_rows, wide=wide, wide_bk=wide_bk,
-                          wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss, corr_bf16=corr_bf16, cb16_w4=cb16_w4,
+                          wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss, corr_bf16=corr_bf16, cb16_w4=cb16_w4, a_prefetch=a_prefetch,
                           narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
                           narrow_geo=narrow_geo, head=head, sep_geo=sep_geo,
                           **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
