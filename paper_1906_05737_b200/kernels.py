@@ -37,7 +37,18 @@ SMEXP_CODE = {"fast": 0, "precise": 1, "exact": 2}
 SMALL_M = 8           # Dense rows at or below this use the split-K GEMV kernel
 TC_MIN_K = 32         # tensor-core GEMM eligibility (contraction and output width)
 TC_MIN_N = 32
-TC_MIN_ROWS = 2048    # GEMM rows per launch from which the tcgen05 kernel is used
+TC_MIN_ROWS = 256     # GEMM rows per launch from which the tcgen05 kernel is used
+# Dense layers up to this many rows take the split-K row kernel (weights read
+# once per 8 rows).  Measured (cfg1): 256 rows 0.062 ms vs 0.070 on tcgen05,
+# 512 rows 0.096 vs 0.070; 1024 rows on the FFMA GEMM 0.228 vs 0.070 (the old
+# 2048-row tcgen05 threshold); cfg3 @64 0.162 -> 0.146 ms with 1x1 convs of
+# 1024 rows on tcgen05.
+SMALL_DENSE_ROWS = 256
+# with mega=True small batches must stay off the TMA-based tcgen05 kernels
+# (the persistent kernel walks plain-pointer units only)
+MEGA_TC_MIN_ROWS = 2048
+TC_MIN_IMAGES = 32    # convolutions: images per launch from which TC_MIN_ROWS applies,
+TC_CONV_MIN_ROWS = 2048   # ... below it this many rows
 WIDE_MIN_TILES = 148  # 256x256 tiles per launch from which N = 256 tiles are used
 SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
 MEGA_MAX_N = 8         # batches up to this run as one persistent kernel (when eligible)
@@ -193,7 +204,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=512,
+                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
@@ -402,6 +413,13 @@ class Specializer:
                   and tile_use >= self.tc_tile_use)
         if tc_rows or tc_conv or tc_dwf:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
+            if rows > 1 and self.tc_min_rows == TC_MIN_ROWS:
+                # convolutions: below TC_MIN_IMAGES images the FFMA kernels
+                # keep launches under TC_CONV_MIN_ROWS rows (measured: with
+                # tcgen05 1x1 convs from 256 rows, batch-1 latency cfg2 41 ->
+                # 47 us, cfg3 141 -> 145 us, cfg3 @16 0.117 -> 0.123 ms; @32
+                # 0.131 -> 0.129, @64 0.161 -> 0.146 ms)
+                n_tc = max(n_min, min(max(n_tc, TC_MIN_IMAGES), -(-TC_CONV_MIN_ROWS // rows)))
             if n_tc <= self.max_batch:
                 conv = None
                 if tc_conv:

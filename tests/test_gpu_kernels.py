@@ -569,7 +569,8 @@ def test_fused_dense_head(k, n1, act1, n2, head, n):
     x = rng.uniform(-2, 2, (n, k)).astype(F32)
     got, net = gpu(m, w, x)
     fused = any("fused Dense head" in net.artifact.launches[i].note for i in net.launches_for())
-    if n < 2048:
+    from paper_1906_05737_b200.kernels import SMALL_DENSE_ROWS, TC_MIN_ROWS
+    if n < max(TC_MIN_ROWS, SMALL_DENSE_ROWS + 1):   # no tcgen05 Dense at this batch
         assert not fused, net.describe()
     elif n1 <= 64:                 # two accumulator buffers: the head is fused
         assert fused, net.describe()
