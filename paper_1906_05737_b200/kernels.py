@@ -47,7 +47,7 @@ SMALL_DENSE_ROWS = 256
 # with mega=True small batches must stay off the TMA-based tcgen05 kernels
 # (the persistent kernel walks plain-pointer units only)
 MEGA_TC_MIN_ROWS = 2048
-TC_MIN_IMAGES = 32    # convolutions: images per launch from which TC_MIN_ROWS applies,
+TC_MIN_IMAGES = 17    # convolutions: images per launch from which TC_MIN_ROWS applies,
 TC_CONV_MIN_ROWS = 2048   # ... below it this many rows
 WIDE_MIN_TILES = 148  # 256x256 tiles per launch from which N = 256 tiles are used
 SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
@@ -204,7 +204,7 @@ class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
-                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS,
+                 pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
@@ -212,6 +212,7 @@ class Specializer:
         self.corr_bf16 = corr_bf16
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
+        self.tc_min_images = tc_min_images
         self.head = head
         self.head_cap = {}           # unit pos -> largest n its own launches serve
         self._n_cap = None
@@ -365,8 +366,12 @@ class Specializer:
             # a few hundred rows: the same split-K kernel with 8 rows per block
             # keeps every SM busy, where a tiled GEMM would run a handful of
             # CTAs through a serial K loop
-            if self.small_dense_rows > SMALL_M:
-                hi = min(self.small_dense_rows, self.max_batch)
+            # (narrow layers hand over to the tensor cores earlier: cfg0's
+            # Dense 256->32 at 256 rows 0.039 -> 0.033 ms replay on tcgen05,
+            # cfg1's 1024->512 at 256 rows 0.062 here vs 0.070 there)
+            sdr = self.small_dense_rows if CO > 64 else min(self.small_dense_rows, 128)
+            if sdr > SMALL_M:
+                hi = min(sdr, self.max_batch)
                 self._dense_small(pos, u, wmat, CI, CO, softmax, n_max=hi, mb=8, n_min=n_min)
                 if self.max_batch <= hi:
                     return
@@ -417,9 +422,10 @@ class Specializer:
                 # convolutions: below TC_MIN_IMAGES images the FFMA kernels
                 # keep launches under TC_CONV_MIN_ROWS rows (measured: with
                 # tcgen05 1x1 convs from 256 rows, batch-1 latency cfg2 41 ->
-                # 47 us, cfg3 141 -> 145 us, cfg3 @16 0.117 -> 0.123 ms; @32
-                # 0.131 -> 0.129, @64 0.161 -> 0.146 ms)
-                n_tc = max(n_min, min(max(n_tc, TC_MIN_IMAGES), -(-TC_CONV_MIN_ROWS // rows)))
+                # 47 us, cfg3 141 -> 145 us, cfg3 @16 0.117 -> 0.123 ms; @20
+                # 0.144 -> 0.125, @24 0.145 -> 0.127, @32 0.131 -> 0.129, @64
+                # 0.161 -> 0.146 ms)
+                n_tc = max(n_min, min(max(n_tc, self.tc_min_images), -(-TC_CONV_MIN_ROWS // rows)))
             if n_tc <= self.max_batch:
                 conv = None
                 if tc_conv:

@@ -83,7 +83,7 @@ class CompiledNetwork:
                  nacc=None, aldg=False, kpack=True, dw_fusion="narrow", epi_tma=True, csplit=True, chunk=None,
                  split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
                  small_dense_rows=None, tc_min_k=None, wide=True, wide_bk=32,
-                 wide_chunk=None, wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True,
+                 wide_chunk=None, wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, tc_min_images=None, narrow=True, direct_imm=True,
                  sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         import torch
 
@@ -102,7 +102,7 @@ class CompiledNetwork:
         self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion, dw_fusion=dw_fusion)
         self.assignment = plan_buffers(self.plan, reserve_heads=head)
         cap = _capacity(self.max_batch)
-        from .kernels import MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_ROWS
+        from .kernels import MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_IMAGES, TC_MIN_ROWS
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
                           use_tc=use_tc, sm_count=sm_count,
                           tc_min_rows=((MEGA_TC_MIN_ROWS if mega else TC_MIN_ROWS) if tc_min_rows is None
@@ -112,6 +112,7 @@ class CompiledNetwork:
                           pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf,
                           small_dense_rows=SMALL_DENSE_ROWS if small_dense_rows is None else small_dense_rows, wide=wide, wide_bk=wide_bk,
                           wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss, corr_bf16=corr_bf16, cb16_w4=cb16_w4, a_prefetch=a_prefetch,
+                          tc_min_images=TC_MIN_IMAGES if tc_min_images is None else tc_min_images,
                           narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
                           narrow_geo=narrow_geo, head=head, sep_geo=sep_geo,
                           **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
