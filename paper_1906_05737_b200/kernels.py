@@ -418,6 +418,8 @@ class Specializer:
                   and tile_use >= self.tc_tile_use)
         if tc_rows or tc_conv or tc_dwf:
             n_tc = max(n_min, -(-self.tc_min_rows // rows))
+            if u.kind == "Dense" and self.tc_min_rows == TC_MIN_ROWS:
+                n_tc = n_min          # right after the split-K row kernel's range
             if rows > 1 and self.tc_min_rows == TC_MIN_ROWS:
                 # convolutions: below TC_MIN_IMAGES images the FFMA kernels
                 # keep launches under TC_CONV_MIN_ROWS rows (measured: with

@@ -1,0 +1,59 @@
+"""Kernel selection per batch size (kernels.py TC_MIN_ROWS, SMALL_DENSE_ROWS,
+TC_MIN_IMAGES), checked on the specialised launch lists without a GPU: the
+thresholds come from scripts/batch_sweep.py on a B200 (profiles/README.md)."""
+import numpy as np
+
+from builders import dense_net
+from paper_1906_05737_b200 import EXACT, zoo
+from paper_1906_05737_b200.buffers import plan_buffers
+from paper_1906_05737_b200.graph import build_graph
+from paper_1906_05737_b200.kernels import (SMALL_DENSE_ROWS, TC_MIN_IMAGES, WIDE_MIN_TILES,
+                                           specialize)
+from paper_1906_05737_b200.planner import build_plan
+
+
+def launches(m, w, max_batch, **kw):
+    plan = build_plan(build_graph(m, w))
+    return specialize(plan, plan_buffers(plan), EXACT, max_batch, max_batch, **kw).launches
+
+
+def serving(ls, unit, n):
+    return [l for l in ls if l.unit == unit and l.n_min <= n <= l.n_max]
+
+
+def test_dense_row_kernel_then_tensor_cores():
+    m, w = dense_net(np.random.default_rng(0), 1024, 512, "tanh")
+    ls = launches(m, w, 65536)
+    for n, want in ((1, "gemv"), (SMALL_DENSE_ROWS, "gemv"), (SMALL_DENSE_ROWS + 1, "dense_tc"),
+                    (1024, "dense_tc"), (65536, "dense_tc")):
+        (l,) = serving(ls, 0, n)
+        assert want in l.kernel, (n, l.kernel)
+    # N = 256 tiles with the BF16 correction split once a launch has enough tiles
+    big = serving(ls, 0, 65536)[0]
+    assert "256x256" in big.note and "bf16 corr" in big.note
+    small = serving(ls, 0, 1024)[0]
+    assert "bf16 corr" not in small.note and "A in TMEM" in small.note
+    edge = -(-WIDE_MIN_TILES // 2) * 256
+    assert "256x256" in serving(ls, 0, edge)[0].note
+    assert "256x256" not in serving(ls, 0, edge - 1)[0].note
+
+
+def test_narrow_dense_hands_over_earlier():
+    m, w = dense_net(np.random.default_rng(1), 256, 32, "relu")
+    ls = launches(m, w, 4096)
+    assert "gemv" in serving(ls, 0, 128)[0].kernel
+    assert "dense_tc" in serving(ls, 0, 129)[0].kernel
+
+
+def test_pointwise_convs_stay_off_tensor_cores_for_a_few_images():
+    m, w = zoo.build(3)                       # MobileNetV1 0.25: 1x1 convs of 16..4096 rows/image
+    ls = launches(m, w, 256)
+    tc_units = {l.unit for l in ls if "_tc_" in l.kernel}
+    assert tc_units
+    for u in tc_units:
+        for n in (1, TC_MIN_IMAGES - 1):
+            rows_ok = [l for l in serving(ls, u, n) if "_tc_" in l.kernel]
+            # below TC_MIN_IMAGES only launches of >= 2048 rows use tcgen05
+            for l in rows_ok:
+                assert n * l.items_per_image >= 2048 or "conv" not in l.kernel, (u, n, l.note)
+        assert any("_tc_" in l.kernel for l in serving(ls, u, 256)), u
