@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define NNB_ABI_VERSION 5
+#define NNB_ABI_VERSION 6
 #define NNB_MAX_TMAPS 6
 
 typedef enum {
@@ -129,8 +129,19 @@ nnb_status nnb_device_check(int32_t device, int32_t *cc_major, int32_t *cc_minor
 nnb_status nnb_compile(const char *source, const char *include_dir, const char *cache_dir,
                        void **cubin_out, uint64_t *cubin_bytes, double *compile_ms);
 
-/* Build a network: compile (or load from cache), upload the pool, allocate
- * and zero the arena.  CUDA graphs are captured lazily per batch size. */
+/* NVRTC over n_sources translation units on up to hardware_concurrency
+ * threads -- the same job pool nnb_create uses (no GPU needed).  *wall_ms is
+ * the wall time, *sum_ms the sum of the per-source times (either may be NULL).
+ * The CPU test-suite bounds compile() time with it. */
+nnb_status nnb_compile_parallel(const char *const *sources, int32_t n_sources,
+                                const char *include_dir, const char *cache_dir, double *wall_ms,
+                                double *sum_ms);
+
+/* Build a network: compile (or load from cache) the kernels a replay over
+ * max_batch images runs, upload the pool, allocate and zero the arena.  The
+ * kernels of other batch sizes are compiled on their first replay (or every
+ * kernel up front with NNB_EAGER=1); CUDA graphs are captured lazily per
+ * batch size. */
 nnb_status nnb_create(const nnb_net_desc *desc, nnb_net **out);
 
 /* Device address of arena byte `offset` (for zero-copy tensor views). */

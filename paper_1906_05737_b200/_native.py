@@ -19,7 +19,7 @@ KERNEL_DIR = PKG_DIR / "csrc" / "kernels"
 NNB_OK, NNB_ERR_ARGUMENT, NNB_ERR_NO_DRIVER, NNB_ERR_NO_DEVICE, NNB_ERR_ARCH, \
     NNB_ERR_NVRTC, NNB_ERR_CUDA, NNB_ERR_OOM, NNB_ERR_BATCH = range(9)
 
-EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_create", "nnb_arena_ptr", "nnb_apply",
+EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_compile_parallel", "nnb_create", "nnb_arena_ptr", "nnb_apply",
             "nnb_run_host", "nnb_enqueue_host", "nnb_run_host_chunked", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_host_alloc", "nnb_host_free",
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
@@ -87,6 +87,8 @@ def lib():
         "nnb_device_check": (I32, [I32, P(I32), P(I32), P(I32)]),
         "nnb_compile": (I32, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, P(VP), P(U64),
                               P(ctypes.c_double)]),
+        "nnb_compile_parallel": (I32, [P(ctypes.c_char_p), I32, ctypes.c_char_p, ctypes.c_char_p,
+                                       P(ctypes.c_double), P(ctypes.c_double)]),
         "nnb_create": (I32, [P(NetDesc), P(VP)]),
         "nnb_arena_ptr": (I32, [VP, U64, P(VP)]),
         "nnb_apply": (I32, [VP, I32, VP]),
@@ -156,3 +158,14 @@ def compile_source(source, cache_dir=None):
     finally:
         lib().nnb_free(ptr)
     return data, ms.value
+
+
+def compile_parallel(sources, cache_dir=None):
+    """NVRTC-compile translation units on the runtime's own job pool (what
+    nnb_create does); returns (wall ms, sum of per-source ms).  No GPU."""
+    arr = (ctypes.c_char_p * max(len(sources), 1))(*[s.encode() for s in sources])
+    wall, tot = ctypes.c_double(), ctypes.c_double()
+    check(lib().nnb_compile_parallel(arr, len(sources), str(KERNEL_DIR).encode(),
+                                     cache_dir.encode() if cache_dir else None,
+                                     ctypes.byref(wall), ctypes.byref(tot)), "nnb_compile_parallel")
+    return wall.value, tot.value

@@ -83,21 +83,34 @@ struct ConvDirect {
 #pragma unroll
     for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int o = 0; o < C::CO; ++o) acc[p][o] = C::WIMM ? C::bias(o) : sm.b[o];
+      for (int o = 0; o < C::CO; ++o) {
+        if constexpr (C::WIMM) acc[p][o] = C::bias(o);
+        else acc[p][o] = sm.b[o];
+      }
 
     // weights as immediates (Cfg::wt, WIMM): every loop below is unrolled,
     // so each FFMA takes its weight from the instruction stream; otherwise
-    // warp-uniform LDS.128 broadcasts from shared memory
+    // warp-uniform LDS.128 broadcasts from shared memory, and the kernel-row
+    // loop stays rolled (ROLL_KY) when the unrolled body would make NVRTC
+    // slow (kernels.py DIRECT_UNROLL_MAX)
+    // ROLL_KY = 1: the ky loop is rolled; 2: ky and kx are (one rolled loop
+    // over the KH*KW taps)
+    constexpr int TAPS_ROLLED = C::ROLL_KY == 2 ? C::KH * C::KW : C::ROLL_KY == 1 ? C::KH : 1;
+    constexpr int KX_UNROLLED = C::ROLL_KY == 2 ? 1 : C::KW;
 #pragma unroll
-    for (int ky = 0; ky < C::KH; ++ky) {
+    for (int ky = 0; ky < C::KH * C::KW / (TAPS_ROLLED * KX_UNROLLED); ++ky) {
+#pragma unroll 1
+     for (int tr = 0; tr < TAPS_ROLLED; ++tr) {
 #pragma unroll
-      for (int kx = 0; kx < C::KW; ++kx) {
+      for (int kxu = 0; kxu < KX_UNROLLED; ++kxu) {
+        const int ky_ = C::ROLL_KY == 2 ? tr / C::KW : C::ROLL_KY == 1 ? tr : ky;
+        const int kx = C::ROLL_KY == 2 ? tr % C::KW : kxu;
 #pragma unroll
         for (int c0 = 0; c0 < C::CI; c0 += CV) {
           float xv[NP][CV];
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
-            const int iy = oyp[p] * C::S - C::PT + ky;
+            const int iy = oyp[p] * C::S - C::PT + ky_;
             const int ix = oxp[p] * C::S - C::PL + kx;
             const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
             const float* src = inp[p] + ((i64)iy * C::W + ix) * C::CI + c0;
@@ -110,9 +123,9 @@ struct ConvDirect {
           }
 #pragma unroll
           for (int c = 0; c < CV; ++c) {
-            const int wi = ((ky * C::KW + kx) * C::CI + c0 + c) * C::CO;
+            const int wi = ((ky_ * C::KW + kx) * C::CI + c0 + c) * C::CO;
             const float* wr = sm.w + wi;
-            if (C::WIMM) {
+            if constexpr (C::WIMM) {
 #pragma unroll
               for (int o = 0; o < C::CO; ++o) {
                 const float wv = C::wt(wi + o);
@@ -142,6 +155,7 @@ struct ConvDirect {
           }
         }
       }
+     }
     }
 
     const float* ps = at<float>(pool, C::PS_OFF);

@@ -780,7 +780,10 @@ struct GemmTc {
         }
       }
       }
-    } else if (warp < EPI_W0 && DWF) {
+    } else if (warp < EPI_W0) {
+     // (role bodies selected at compile time: only the instantiated form is
+     // compiled -- NVRTC time)
+     if constexpr (DWF) {
       // ---------------- depthwise producer: halo -> A tile (TMEM or smem) ----------------
       const int q = warp & 3, r = q * 32 + lane;      // tile pixel = A row = TMEM lane
       const int ty = r / TW, tx = r % TW;
@@ -864,7 +867,7 @@ struct GemmTc {
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
       }
-    } else if (warp < EPI_W0 && TA) {
+     } else if constexpr (TA) {
       // ---------------- converter: A row -> (hi, lo) columns in TMEM ----------------
       const int q = warp & 3, r = q * 32 + lane;      // this thread's tile row = TMEM lane
       int s = 0;
@@ -905,7 +908,7 @@ struct GemmTc {
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
       }
-    } else if (warp < EPI_W0 && AL) {
+     } else if constexpr (AL) {
       // ---------------- loader: cp.async gather of A, then split in place ----------------
       constexpr int CH = BK / 4;                       // 16-byte chunks per row
       constexpr int PER = BM * CH / 128;               // chunks per loader thread
@@ -981,7 +984,7 @@ struct GemmTc {
         if (it + D < total) issue(it + D);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-    } else if (warp < EPI_W0) {
+     } else {
       // ---------------- converter: A -> (hi, lo) ----------------
       const int ct = threadIdx.x - 64;   // 0 .. 32 * CONV_WARPS - 1
       int s = 0;
@@ -1042,6 +1045,7 @@ struct GemmTc {
           if (++s == C::NS) { s = 0; ph ^= 1; }
         }
       }
+     }
     } else {
       // ---------------- epilogue ----------------
       const int q = warp & 3;                    // TMEM lane quarter of this warp

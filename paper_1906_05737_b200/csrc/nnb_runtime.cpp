@@ -260,6 +260,32 @@ nnb_status compile_cubin(const char *source, const char *include_dir, const char
   return NNB_OK;
 }
 
+// Makes `ctx` current for the scope of an entry point and restores the
+// caller's context on every exit path: the CUDA runtime (torch) follows the
+// driver's current context, so leaving a replica's context bound would move
+// the caller's default device.
+struct CtxScope {
+  CUcontext prev = nullptr;
+  bool bound = false;
+  CUresult r = CUDA_SUCCESS;
+  explicit CtxScope(CUcontext ctx) {
+    Cu *C = cu();
+    r = C->p_cuCtxGetCurrent(&prev);
+    if (r == CUDA_SUCCESS && prev != ctx) {
+      r = C->p_cuCtxSetCurrent(ctx);
+      bound = r == CUDA_SUCCESS;
+    }
+  }
+  ~CtxScope() {
+    if (bound) cu()->p_cuCtxSetCurrent(prev);
+  }
+};
+
+#define CTX_SCOPE(ctx)                                                           \
+  CtxScope ctx_scope_(ctx);                                                      \
+  if (ctx_scope_.r != CUDA_SUCCESS)                                              \
+    return fail(NNB_ERR_CUDA, "cannot make the network's context current (%d)", (int)ctx_scope_.r);
+
 nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
   Cu *C = cu();
   if (!C->ok) return fail(NNB_ERR_NO_DRIVER, "%s", C->why.c_str());
@@ -273,7 +299,6 @@ nnb_status device_ctx(int32_t device, CUcontext *ctx, CUdevice *dev) {
   if (maj != 10)
     return fail(NNB_ERR_ARCH, "device %d has compute capability %d.x; kernels target sm_100a", device, maj);
   CU_CHECK(C->p_cuDevicePrimaryCtxRetain(ctx, *dev));
-  CU_CHECK(C->p_cuCtxSetCurrent(*ctx));
   return NNB_OK;
 }
 
@@ -289,8 +314,16 @@ struct nnb_net {
   bool pdl = true;
   std::vector<std::vector<CUtensorMap>> maps;   // per launch
   CUcontext ctx = nullptr;
-  std::vector<CUmodule> mods;
-  std::vector<CUfunction> fns;
+  // kernels are compiled lazily per batch size: nnb_create compiles the
+  // sources of the launches a replay over max_batch images runs; the
+  // batch-size variants for smaller n (FFMA / split-K kernels) are compiled
+  // the first time such an n is replayed or timed
+  std::vector<std::string> sources;
+  std::string include_dir, cache_dir, digest;
+  std::vector<std::string> kernel_names;
+  std::vector<int32_t> kernel_source;
+  std::vector<CUmodule> mods;                    // per source, null until loaded
+  std::vector<CUfunction> fns;                   // per kernel, null until loaded
   std::vector<nnb_launch> launches;
   CUdeviceptr arena = 0, pool = 0;
   uint64_t arena_bytes = 0, pool_bytes = 0;
@@ -305,12 +338,84 @@ struct nnb_net {
 
 namespace {
 
+struct CompileJob { std::string cubin, err; nnb_status st = NNB_OK; double ms = 0; bool hit = false; };
+
+// NVRTC over `srcs` on up to hardware_concurrency threads; returns the wall
+// milliseconds in *wall_ms.
+void compile_parallel(const std::vector<const char *> &srcs, const char *include_dir,
+                      const char *cache_dir, const std::string &digest,
+                      std::vector<CompileJob> &jobs, double *wall_ms) {
+  jobs.assign(srcs.size(), CompileJob());
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  unsigned nthreads = std::min<unsigned>(hw, (unsigned)std::max<size_t>(srcs.size(), 1));
+  std::vector<std::thread> pool;
+  std::atomic<size_t> next{0};
+  for (unsigned t = 0; t < nthreads; ++t)
+    pool.emplace_back([&] {
+      for (size_t i = next++; i < srcs.size(); i = next++) {
+        CompileJob &j = jobs[i];
+        j.st = compile_cubin(srcs[i], include_dir, cache_dir, digest, &j.cubin, &j.ms, &j.hit);
+        if (j.st != NNB_OK) j.err = g_err;
+      }
+    });
+  for (auto &th : pool) th.join();
+  if (wall_ms)
+    *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+bool serves(const nnb_launch &l, int n) { return n >= l.n_min && n <= l.n_max; }
+
+// Compile (or load from the cubin cache) and load every module the launches
+// of a replay over n images need; n <= 0 loads everything.  Must not run
+// inside a stream capture.
+nnb_status ensure_loaded(nnb_net *net, int n, double *wall_ms = nullptr, bool *all_hit = nullptr) {
+  Cu *C = cu();
+  std::vector<int> need;
+  std::vector<char> want(net->sources.size(), 0);
+  for (const nnb_launch &l : net->launches)
+    if (n <= 0 || serves(l, n)) want[net->kernel_source[l.kernel]] = 1;
+  for (size_t i = 0; i < want.size(); ++i)
+    if (want[i] && !net->mods[i]) need.push_back((int)i);
+  if (wall_ms) *wall_ms = 0;
+  if (all_hit) *all_hit = true;
+  if (need.empty()) return NNB_OK;
+  std::vector<const char *> srcs;
+  for (int i : need) srcs.push_back(net->sources[i].c_str());
+  std::vector<CompileJob> jobs;
+  compile_parallel(srcs, net->include_dir.c_str(),
+                   net->cache_dir.empty() ? nullptr : net->cache_dir.c_str(), net->digest, jobs,
+                   wall_ms);
+  for (auto &j : jobs) {
+    if (j.st != NNB_OK) { g_err = j.err; return j.st; }
+    if (all_hit) *all_hit = *all_hit && j.hit;
+  }
+  for (size_t k = 0; k < need.size(); ++k) {
+    CUresult r = C->p_cuModuleLoadData(&net->mods[need[k]], jobs[k].cubin.data());
+    if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "cuModuleLoadData failed (%d)", (int)r);
+  }
+  for (size_t i = 0; i < net->fns.size(); ++i) {
+    const int src = net->kernel_source[i];
+    if (net->fns[i] || !net->mods[src]) continue;
+    CUresult r = C->p_cuModuleGetFunction(&net->fns[i], net->mods[src], net->kernel_names[i].c_str());
+    if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "kernel %s not in module", net->kernel_names[i].c_str());
+  }
+  for (const nnb_launch &l : net->launches) {
+    if (!net->fns[l.kernel] || l.smem_bytes <= 48 * 1024) continue;
+    CUresult r = C->p_cuFuncSetAttribute(net->fns[l.kernel], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                         (int)l.smem_bytes);
+    if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "smem %u bytes rejected", l.smem_bytes);
+  }
+  return NNB_OK;
+}
+
 // One launch of the schedule over n images (no-op when it is not part of
 // the replay for n or its grid is empty).
 nnb_status launch_one(nnb_net *net, size_t li, int n, CUstream s, bool pdl) {
   Cu *C = cu();
   const nnb_launch &l = net->launches[li];
   if (n < l.n_min || n > l.n_max) return NNB_OK;
+  if (!net->fns[l.kernel]) return fail(NNB_ERR_ARGUMENT, "kernel %d is not loaded for batch %d", l.kernel, n);
   {
     uint64_t items = (uint64_t)n * l.items_per_image;
     uint64_t gx = (items + l.items_per_block - 1) / l.items_per_block * l.grid_mult;
@@ -376,6 +481,8 @@ nnb_status graph_for(nnb_net *net, int n, CUgraphExec *out) {
   auto it = net->graphs.find(n);
   if (it != net->graphs.end()) { *out = it->second; return NNB_OK; }
   Cu *C = cu();
+  nnb_status lst = ensure_loaded(net, n);
+  if (lst != NNB_OK) return lst;
   CU_CHECK(C->p_cuStreamBeginCapture(net->capture_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
   nnb_status st = enqueue(net, n, net->capture_stream);
   CUgraph g = nullptr;
@@ -441,6 +548,25 @@ nnb_status nnb_compile(const char *source, const char *include_dir, const char *
   return NNB_OK;
 }
 
+nnb_status nnb_compile_parallel(const char *const *sources, int32_t n_sources,
+                                const char *include_dir, const char *cache_dir, double *wall_ms,
+                                double *sum_ms) {
+  if (!sources || n_sources < 0) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  std::vector<const char *> srcs(sources, sources + n_sources);
+  for (auto p : srcs)
+    if (!p) return fail(NNB_ERR_ARGUMENT, "source is NULL");
+  std::string digest = headers_digest(include_dir ? include_dir : ".");
+  std::vector<CompileJob> jobs;
+  compile_parallel(srcs, include_dir, cache_dir, digest, jobs, wall_ms);
+  double sum = 0;
+  for (auto &j : jobs) {
+    if (j.st != NNB_OK) { g_err = j.err; return j.st; }
+    sum += j.ms;
+  }
+  if (sum_ms) *sum_ms = sum;
+  return NNB_OK;
+}
+
 void nnb_free(void *p) { free(p); }
 
 nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
@@ -461,56 +587,32 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   CUdevice dev;
   nnb_status st = device_ctx(d->device, &net->ctx, &dev);
   if (st != NNB_OK) { delete net; return st; }
+  CtxScope scope(net->ctx);
+  if (scope.r != CUDA_SUCCESS) { delete net; return fail(NNB_ERR_CUDA, "cannot make device %d current", d->device); }
 
-  // one NVRTC program per source, compiled in parallel, one module each
-  struct Job { std::string cubin, err; nnb_status st = NNB_OK; double ms = 0; bool hit = false; };
-  std::vector<Job> jobs(d->n_sources);
-  std::string digest = headers_digest(d->include_dir ? d->include_dir : ".");
-  {
-    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    unsigned nthreads = std::min<unsigned>(hw, (unsigned)d->n_sources);
-    std::vector<std::thread> pool;
-    std::atomic<int> next{0};
-    auto auto_t0 = std::chrono::steady_clock::now();
-    for (unsigned t = 0; t < std::max(1u, nthreads); ++t)
-      pool.emplace_back([&] {
-        for (int i = next++; i < d->n_sources; i = next++) {
-          Job &j = jobs[i];
-          j.st = compile_cubin(d->sources[i], d->include_dir, d->cache_dir, digest, &j.cubin,
-                              &j.ms, &j.hit);
-          if (j.st != NNB_OK) j.err = g_err;
-        }
-      });
-    for (auto &th : pool) th.join();
-    net->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - auto_t0).count();
-  }
-  net->cache_hit = true;
-  for (auto &j : jobs) {
-    if (j.st != NNB_OK) { g_err = j.err; nnb_status s2 = j.st; delete net; return s2; }
-    net->cache_hit = net->cache_hit && j.hit;
-  }
   auto bail = [&](nnb_status s) { nnb_destroy(net); return s; };
-  net->mods.resize(d->n_sources, nullptr);
-  CUresult r;
-  for (int i = 0; i < d->n_sources; ++i) {
-    r = C->p_cuModuleLoadData(&net->mods[i], jobs[i].cubin.data());
-    if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "cuModuleLoadData failed (%d)", (int)r); return bail(NNB_ERR_CUDA); }
-  }
-  net->fns.resize(d->n_kernels);
+  for (int i = 0; i < d->n_sources; ++i) net->sources.emplace_back(d->sources[i]);
+  net->include_dir = d->include_dir ? d->include_dir : ".";
+  net->cache_dir = d->cache_dir ? d->cache_dir : "";
+  net->digest = headers_digest(net->include_dir.c_str());
   for (int i = 0; i < d->n_kernels; ++i) {
-    int src = d->kernel_source ? d->kernel_source[i] : 0;
+    net->kernel_names.emplace_back(d->kernel_names[i]);
+    const int src = d->kernel_source ? d->kernel_source[i] : 0;
     if (src < 0 || src >= d->n_sources) { fail(NNB_ERR_ARGUMENT, "kernel %d has no source", i); return bail(NNB_ERR_ARGUMENT); }
-    r = C->p_cuModuleGetFunction(&net->fns[i], net->mods[src], d->kernel_names[i]);
-    if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "kernel %s not in module", d->kernel_names[i]); return bail(NNB_ERR_CUDA); }
+    net->kernel_source.push_back(src);
   }
+  net->mods.assign(d->n_sources, nullptr);
+  net->fns.assign(d->n_kernels, nullptr);
   net->launches.assign(d->launches, d->launches + d->n_launches);
-  for (auto &l : net->launches) {
-    if (l.smem_bytes > 48 * 1024) {
-      r = C->p_cuFuncSetAttribute(net->fns[l.kernel], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                  (int)l.smem_bytes);
-      if (r != CUDA_SUCCESS) { fail(NNB_ERR_CUDA, "smem %u bytes rejected", l.smem_bytes); return bail(NNB_ERR_CUDA); }
-    }
+  {
+    // the sources a replay over max_batch images needs, compiled in parallel
+    // (NNB_EAGER=1: every batch-size variant up front)
+    const char *e = getenv("NNB_EAGER");
+    const bool eager = e && atoi(e) != 0;
+    nnb_status cst = ensure_loaded(net, eager ? 0 : net->max_batch, &net->compile_ms, &net->cache_hit);
+    if (cst != NNB_OK) return bail(cst);
   }
+  CUresult r;
   net->pool_bytes = d->pool_bytes;
   net->arena_bytes = d->arena_bytes;
   r = C->p_cuMemAlloc(&net->pool, std::max<uint64_t>(d->pool_bytes, 256));
@@ -583,7 +685,7 @@ nnb_status nnb_apply(nnb_net *net, int32_t n, void *stream) {
   if (n < 1 || n > net->max_batch)
     return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
-  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CTX_SCOPE(net->ctx)
   CUgraphExec ex;
   nnb_status st = graph_for(net, n, &ex);
   if (st != NNB_OK) return st;
@@ -593,6 +695,7 @@ nnb_status nnb_apply(nnb_net *net, int32_t n, void *stream) {
 
 nnb_status nnb_sync(nnb_net *net, void *stream) {
   if (!net) return fail(NNB_ERR_ARGUMENT, "net is NULL");
+  CTX_SCOPE(net->ctx)
   CU_CHECK(cu()->p_cuStreamSynchronize(reinterpret_cast<CUstream>(stream)));
   return NNB_OK;
 }
@@ -606,7 +709,7 @@ static nnb_status enqueue_host(nnb_net *net, int32_t n, int64_t first, const voi
   if (n < 1 || n > net->max_batch)
     return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
-  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CTX_SCOPE(net->ctx)
   for (size_t i = 0; i < net->inputs.size(); ++i) {
     const uint64_t b = net->inputs[i].image_bytes;
     CU_CHECK(C->p_cuMemcpyHtoDAsync(net->arena + net->inputs[i].offset,
@@ -627,6 +730,7 @@ nnb_status nnb_run_host(nnb_net *net, int32_t n, const void *const *inputs, void
   CUstream s = reinterpret_cast<CUstream>(stream);
   nnb_status st = enqueue_host(net, n, 0, inputs, outputs, s);
   if (st != NNB_OK) return st;
+  CTX_SCOPE(net->ctx)
   CU_CHECK(cu()->p_cuStreamSynchronize(s));
   return NNB_OK;
 }
@@ -652,7 +756,7 @@ nnb_status nnb_run_host_chunked(nnb_net *const *nets, const void *const *streams
     if (st != NNB_OK) return st;
   }
   for (int32_t j = 0; j < used; ++j) {
-    CU_CHECK(cu()->p_cuCtxSetCurrent(nets[j]->ctx));
+    CTX_SCOPE(nets[j]->ctx)
     CU_CHECK(cu()->p_cuStreamSynchronize(reinterpret_cast<CUstream>(const_cast<void *>(streams[j]))));
   }
   return NNB_OK;
@@ -660,8 +764,10 @@ nnb_status nnb_run_host_chunked(nnb_net *const *nets, const void *const *streams
 
 nnb_status nnb_time_apply(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms) {
   if (!net || iters < 1 || !ms) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  if (n < 1 || n > net->max_batch)
+    return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
-  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CTX_SCOPE(net->ctx)
   CUstream s = reinterpret_cast<CUstream>(stream);
   CUgraphExec ex;
   nnb_status st = graph_for(net, n, &ex);
@@ -683,8 +789,10 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
   if (n < 1 || n > net->max_batch)
     return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
-  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CTX_SCOPE(net->ctx)
   CUstream s = reinterpret_cast<CUstream>(stream);
+  nnb_status lst = ensure_loaded(net, n);
+  if (lst != NNB_OK) return lst;
   CU_CHECK(C->p_cuEventRecord(net->ev0, s));
   for (int i = 0; i < iters; ++i) {
     nnb_status st = launch_one(net, (size_t)index, n, s, false);
@@ -703,11 +811,12 @@ nnb_status nnb_time_sequence(nnb_net *net, int32_t n, int32_t iters, void *strea
   if (n < 1 || n > net->max_batch)
     return fail(NNB_ERR_BATCH, "batch %d outside [1, %d]", n, net->max_batch);
   Cu *C = cu();
-  CU_CHECK(C->p_cuCtxSetCurrent(net->ctx));
+  CTX_SCOPE(net->ctx)
   CUstream s = reinterpret_cast<CUstream>(stream);
   const size_t L = net->launches.size();
+  nnb_status st = ensure_loaded(net, n);
+  if (st != NNB_OK) return st;
   std::vector<CUevent> ev(L + 1, nullptr);
-  nnb_status st = NNB_OK;
   for (auto &e : ev)
     if (C->p_cuEventCreate(&e, CU_EVENT_DEFAULT) != CUDA_SUCCESS) st = fail(NNB_ERR_CUDA, "cuEventCreate failed");
   std::vector<double> acc(L, 0.0);
@@ -773,7 +882,7 @@ void nnb_destroy(nnb_net *net) {
   if (!net) return;
   Cu *C = cu();
   if (C->ok) {
-    C->p_cuCtxSetCurrent(net->ctx);
+    CtxScope scope(net->ctx);
     for (auto &kv : net->graphs) C->p_cuGraphExecDestroy(kv.second);
     if (net->ev0) C->p_cuEventDestroy(net->ev0);
     if (net->ev1) C->p_cuEventDestroy(net->ev1);

@@ -57,7 +57,10 @@ MAX_TMAPS = 6         # tensor-map parameters of every TMA kernel (NNB_MAX_TMAPS
 NARROW_MAX_W = 2048   # K*CO bound of the narrow row GEMM (weights unrolled into its code)
 ELEM_BLOCK = 256
 SEP_BLOCK = 128
-DIRECT_IMM_MAX = 2048  # direct-conv weights unrolled into the code as immediates
+# direct conv: taps fully unrolled with the weights as immediates up to this
+# many unrolled FFMAs per thread (KH*KW*CI*CO*pixels); beyond it shared-memory
+# weights and a rolled kernel-row loop keep NVRTC under the compile budget
+DIRECT_UNROLL_MAX = 2048
 
 
 @dataclass
@@ -117,16 +120,42 @@ class Specialization:
 
 
 def _cfg_struct(name, fields, code=""):
-    """``struct name`` of constexpr fields, plus generated member functions."""
-    lines = [f"struct {name} {{"]
+    """``struct name`` of constexpr fields, plus generated member functions.
+    ``code`` is member source text, or an :class:`ImmTables` (whose tables
+    are emitted at namespace scope in front of the struct), or a list of
+    both."""
+    parts = code if isinstance(code, list) else [code]
+    pre = [p.declarations(name) for p in parts if isinstance(p, ImmTables)]
+    members = [p.members(name) if isinstance(p, ImmTables) else p for p in parts]
+    lines = pre + [f"struct {name} {{"]
     for k, v in fields.items():
         if isinstance(v, bool):
             v = int(v)
         lines.append(f"  static constexpr long long {k} = {int(v)}LL;")
-    if code:
-        lines.append(code)
+    lines += [m for m in members if m]
     lines.append("};")
     return "\n".join(lines)
+
+
+class ImmTables:
+    """float32 tables read as ``Cfg::name(i)``.  Each is a namespace-scope
+    ``__device__ const`` array: once the caller's loops are unrolled the index
+    is a constant and NVVM folds the load into an instruction immediate.
+    (A function-local ``const float v[N] = {...}`` gives the same code but
+    is re-materialised at every call site: cfg0's direct conv with 1152
+    weights took 43 s of NVRTC that way, 1.2 s with this form.)"""
+
+    def __init__(self, **tables):
+        self.tables = {k: np.asarray(v, F32).ravel() for k, v in tables.items()}
+
+    def declarations(self, cfg):
+        return "\n".join(f"__device__ const float nnb_{cfg}_{k}[{max(a.size, 1)}] = "
+                         f"{{{', '.join(_flit(v) for v in a) or '0.0f'}}};"
+                         for k, a in self.tables.items())
+
+    def members(self, cfg):
+        return "\n".join(f"  __device__ static __forceinline__ float {k}(int i) "
+                         f"{{ return nnb_{cfg}_{k}[i]; }}" for k in self.tables)
 
 
 def _flit(x):
@@ -168,32 +197,18 @@ def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias):
     weight an immediate (k ascending, columns innermost: RowsNarrow's order
     with one K slice)."""
     w = np.asarray(wmat, F32).reshape(K, CO)
-    lit = lambda arr: ", ".join(_flit(v) for v in np.asarray(arr, F32).ravel())
-    dwk = np.asarray(dw_kernel, F32).ravel()
-    out = ["  __device__ static __forceinline__ float dww(int i) {",
-           f"    const float v[{dwk.size}] = {{{lit(dwk)}}};", "    return v[i];", "  }",
-           "  __device__ static __forceinline__ float dwb(int i) {",
-           f"    const float v[{K}] = {{{lit(dw_bias)}}};", "    return v[i];", "  }",
-           "  __device__ static __forceinline__ float bias(int j) {",
-           f"    const float b[{CO}] = {{{lit(bias)}}};", "    return b[j];", "  }",
-           f"  __device__ static __forceinline__ void dotr(const float (&a)[{K}], float* acc) {{"]
+    out = [f"  __device__ static __forceinline__ void dotr(const float (&a)[{K}], float* acc) {{"]
     for k in range(K):
         out.extend(f"    acc[{j}] = fmaf(a[{k}], {_flit(w[k, j])}, acc[{j}]);" for j in range(CO))
     out.append("  }")
-    return "\n".join(out)
+    return [ImmTables(dww=dw_kernel, dwb=dw_bias, bias=bias), "\n".join(out)]
 
 
 def _imm_tables(**tables):
     """Members ``name(i)`` returning element i of a float32 table; once the
     caller's loops are unrolled the index is a constant and the value an
-    instruction immediate."""
-    out = []
-    for name, arr in tables.items():
-        a = np.asarray(arr, F32).ravel()
-        out += [f"  __device__ static __forceinline__ float {name}(int i) {{",
-                f"    const float v[{a.size}] = {{{', '.join(_flit(v) for v in a)}}};",
-                "    return v[i];", "  }"]
-    return "\n".join(out)
+    instruction immediate (see :class:`ImmTables`)."""
+    return ImmTables(**tables)
 
 
 def _pad4(x):
@@ -399,15 +414,19 @@ class Specializer:
 
         # tensor-core path for large dense contractions (3xTF32, FP32-accurate)
         n_max = 1 << 30
+        # (a concatenated input is not one row-major matrix: the row GEMM's
+        # single A map cannot read it, so fused concats go to the conv tiles
+        # or the SIMT loader)
         tc_rows = (self.use_tc and not softmax and not pool_fused and KH == KW == S == 1
-                   and u.dw is None
+                   and u.dw is None and not concat
                    and PT == PL == 0 and K % 4 == 0 and K >= self.tc_min_k and CO >= TC_MIN_N)
         # implicit-GEMM tiles are 8 x 16 output pixels of one image: small images
         # waste most of a tile (cfg0's 8x8 conv: 0.103 ms on tensor cores vs
         # 0.046 ms as an FFMA GEMM), so require tc_tile_use (75%) useful pixels
         tile_use = (HO * WO) / ((-(-HO // 8) * 8) * (-(-WO // 16) * 16))
         tc_conv = (self.use_tc and not tc_rows and u.kind == "Conv2D" and not softmax
-                   and S == 1 and KH * KW > 1 and CI % 16 == 0 and C0 % 16 == 0 and CO >= 16
+                   and S == 1 and (KH * KW > 1 or concat) and CI % 16 == 0 and C0 % 16 == 0
+                   and CO >= 16
                    and tile_use >= self.tc_tile_use)
         # pointwise conv with its depthwise producer fused in (planner
         # fuse_dw_pw): 8 x 16-pixel tiles whose A operand the split warps
@@ -866,9 +885,20 @@ class Specializer:
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0)
         fields.update(self.epilogue_fields(u, CO))
-        # weights (<= DIRECT_IMM_MAX) as immediates in the generated code
-        wimm = self.direct_imm and KH * KW * CI * CO <= DIRECT_IMM_MAX
+        # Every tap unrolled with the weights as immediates is the fastest
+        # form, but NVRTC time grows with the unrolled FFMA count; above
+        # DIRECT_UNROLL_MAX the weights are shared-memory broadcasts and the
+        # kernel-row loop stays rolled (compile-time bound, see DESIGN)
+        np_ = 4 if pool_fused else pxt
+        unrolled = KH * KW * CI * CO * np_
+        wimm = bool(self.direct_imm) and unrolled <= DIRECT_UNROLL_MAX
+        if self.direct_imm == "force":
+            wimm = True
         fields["WIMM"] = wimm
+        roll = 0
+        if not wimm and unrolled > DIRECT_UNROLL_MAX and KH > 1:
+            roll = 1 if unrolled // KH <= DIRECT_UNROLL_MAX // 2 else 2
+        fields["ROLL_KY"] = roll
         code = _imm_tables(wt=wmat, bias=u.bias) if wimm else ""
         # pool: one 2x2 window per thread; else pxt pixels per thread, the
         # 128-thread block covering 128*pxt consecutive pixels

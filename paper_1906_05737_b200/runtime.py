@@ -234,12 +234,20 @@ class CompiledNetwork:
         """End-to-end call through the C ABI with host buffers: H2D copy of the
         inputs, one graph replay, D2H copy of the outputs, synchronise.
         ``inputs``/``outputs`` are C-contiguous float32 numpy arrays (pinned
-        memory from ``pinned_empty`` is fastest)."""
+        memory from ``pinned_empty`` is fastest) holding at least ``n`` images;
+        anything else raises ``InputShapeMismatch`` before the C ABI sees a
+        pointer."""
         n = n if n is not None else self.max_batch
-        xs = [np.ascontiguousarray(x, np.float32) for x in inputs]
+        if not 1 <= n <= self.max_batch:
+            raise InputShapeMismatch(f"batch {n} outside [1, {self.max_batch}]")
+        per = lambda v: tuple(v.shape[1:]) if self.batch is not None else tuple(v.shape)
+        xs = _host_buffers(inputs, [per(v) for v in self.input_views], n, "input",
+                           batched=self.batch is not None)
         if outputs is None:
-            outputs = [np.empty((n,) + tuple(v.shape[1:] if self.batch is not None else v.shape),
-                                np.float32) for v in self.output_views]
+            outputs = [np.empty(((n,) if self.batch is not None else ()) + per(v), np.float32)
+                       for v in self.output_views]
+        _host_buffers(outputs, [per(v) for v in self.output_views], n, "output",
+                      batched=self.batch is not None, writable=True)
         ip = (ctypes.c_void_p * len(xs))(*[x.ctypes.data for x in xs])
         op = (ctypes.c_void_p * len(outputs))(*[o.ctypes.data for o in outputs])
         _native.check(_native.lib().nnb_run_host(self._h.ptr, n, ip, op, self._stream()), "run_host")
@@ -291,6 +299,35 @@ class CompiledNetwork:
                      f"compiled in {self.compile_ms:.2f} ms (NVRTC {self.nvrtc_ms:.1f} ms, "
                      f"cache {'hit' if self.cubin_cache_hit else 'miss'})")
         return "\n".join(lines)
+
+
+def _host_buffers(arrays, shapes, n, what, batched=True, writable=False):
+    """Validate host buffers before their raw pointers cross the C ABI: one
+    per network input/output, float32, C-contiguous, per-image shape
+    ``shapes[i]`` and at least ``n`` images (``batched``), writable for
+    outputs.  Inputs that are not float32 C-contiguous are converted (a copy);
+    outputs must already be right, since the D2H copy writes through them."""
+    arrays = list(arrays)
+    if len(arrays) != len(shapes):
+        raise InputShapeMismatch(f"expected {len(shapes)} {what}s, got {len(arrays)}")
+    out = []
+    for i, (a, shape) in enumerate(zip(arrays, shapes)):
+        if not isinstance(a, np.ndarray):
+            if writable:
+                raise InputShapeMismatch(f"{what} {i} must be a numpy array")
+            a = np.asarray(a)
+        if not writable:
+            a = np.ascontiguousarray(a, np.float32)
+        elif a.dtype != np.float32 or not a.flags.c_contiguous or not a.flags.writeable:
+            raise InputShapeMismatch(f"{what} {i} must be a writable C-contiguous float32 array "
+                                     f"(got {a.dtype}, contiguous={a.flags.c_contiguous}, "
+                                     f"writable={a.flags.writeable})")
+        got = tuple(a.shape[1:]) if batched else tuple(a.shape)
+        if got != tuple(shape) or (batched and a.shape[0] < n):
+            want = f"(>= {n}, {tuple(shape)})" if batched else f"{tuple(shape)}"
+            raise InputShapeMismatch(f"{what} {i} shape {tuple(a.shape)} does not match {want}")
+        out.append(a)
+    return out
 
 
 def pinned_empty(shape):
@@ -360,13 +397,11 @@ class PipelinedNetwork:
         n = self.batch if n is None else int(n)
         if not 1 <= n <= self.batch:
             raise InputShapeMismatch(f"batch {n} outside [1, {self.batch}]")
-        xs = [np.ascontiguousarray(x, np.float32) for x in inputs]
-        for x, v in zip(xs, self.nets[0].input_views):
-            if x.shape[0] < n or tuple(x.shape[1:]) != tuple(v.shape[1:]):
-                raise InputShapeMismatch(f"input shape {x.shape} does not match "
-                                         f"({n}, {tuple(v.shape[1:])})")
+        xs = _host_buffers(inputs, [tuple(v.shape[1:]) for v in self.nets[0].input_views], n,
+                           "input")
         if outputs is None:
             outputs = [np.empty((n,) + s, np.float32) for s in self.output_shapes]
+        _host_buffers(outputs, self.output_shapes, n, "output", writable=True)
         VP = ctypes.c_void_p
         nets = (VP * self.chunks)(*[net._h.ptr for net in self.nets])
         streams = (VP * self.chunks)(*[st.cuda_stream for st in self.streams])

@@ -103,6 +103,33 @@ def test_decoder_fusions(c0, c1, co, up_src, tc):
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
 
+@pytest.mark.parametrize("c0,c1,co,n", [(32, 32, 64, 64), (16, 48, 32, 40), (32, 32, 16, 3)])
+def test_concat_into_pointwise(c0, c1, co, n):
+    """Concatenate fused into a 1x1 conv's loader at batches above the
+    tensor-core threshold (default selection): the row GEMM cannot read a
+    two-source operand, so the conv tiles (second TMA map) or the SIMT loader
+    serve it (a 1x1 conv fed by a concat went to the row GEMM)."""
+    rng = np.random.default_rng(c0 * c1 + co + n)
+    b = NetBuilder()
+    x = b.input((16, 16, 4))
+    a = b.layer("Conv2D", [x], {"filters": c0, "kernel_size": 3, "padding": "same",
+                                "activation": "relu"},
+                [("kernel", he(rng, (3, 3, 4, c0), 36)), ("bias", np.zeros(c0, F32))])
+    bb = b.layer("Conv2D", [x], {"filters": c1, "kernel_size": 3, "padding": "same",
+                                 "activation": "tanh"},
+                 [("kernel", he(rng, (3, 3, 4, c1), 36)), ("bias", np.zeros(c1, F32))])
+    cat = b.layer("Concatenate", [a, bb])
+    y = b.layer("Conv2D", [cat], {"filters": co, "kernel_size": 1, "activation": "relu"},
+                [("kernel", he(rng, (1, 1, c0 + c1, co), c0 + c1)),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (n, 16, 16, 4)).astype(F32)
+    got, net = gpu(m, wt, xin)
+    assert "Concat" not in [u.kind for u in net.plan.units]
+    assert not any("conv1x1_tc" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+
+
 @pytest.mark.parametrize("h,w,c,co,k,s,pad,dwbias,res,n", [
     (9, 13, 8, 16, 3, 1, "same", False, False, 3), (16, 16, 16, 32, 3, 2, "same", True, False, 2),
     (64, 64, 8, 16, 3, 1, "same", False, False, 7), (30, 40, 16, 32, 3, 1, "same", False, False, 37),
@@ -354,6 +381,21 @@ def test_errors():
         net.run([])
     with pytest.raises(InputShapeMismatch):
         net.apply(5)
+    with pytest.raises(InputShapeMismatch):            # nnb_time_apply range check
+        net.time_apply(5)
+    # host buffers are validated before their pointers reach the C ABI
+    with pytest.raises(InputShapeMismatch):
+        net.run_host([np.zeros((3, 1024), F32)])
+    with pytest.raises(InputShapeMismatch):
+        net.run_host([np.zeros((4, 1024), F32)], [np.zeros((4, 10), np.float64)])
+    with pytest.raises(InputShapeMismatch):
+        net.run_host([np.zeros((4, 1024), F32)], [np.zeros((2, 10), F32)])
+    (y,) = net.run_host([np.zeros((4, 1024), F32)])
+    assert y.shape == (4, 10)
+    import torch
+    dev = torch.cuda.current_device()
+    net.apply()
+    assert torch.cuda.current_device() == dev          # the caller's context is restored
 
 
 def test_deterministic_outputs_across_compiles():

@@ -57,3 +57,31 @@ def test_pointwise_convs_stay_off_tensor_cores_for_a_few_images():
             for l in rows_ok:
                 assert n * l.items_per_image >= 2048 or "conv" not in l.kernel, (u, n, l.note)
         assert any("_tc_" in l.kernel for l in serving(ls, u, 256)), u
+
+
+def test_concat_fed_pointwise_conv_never_takes_the_row_gemm():
+    """a 1x1 conv whose input is a fused Concatenate must
+    not be served by the tcgen05 row GEMM (one A map over input 0 only)."""
+    from builders import he
+    from paper_1906_05737_b200.zoo import NetBuilder
+    rng = np.random.default_rng(3)
+    b = NetBuilder()
+    x = b.input((16, 16, 4))
+    a = b.layer("Conv2D", [x], {"filters": 32, "kernel_size": 3, "padding": "same", "use_bias": False},
+                [("kernel", he(rng, (3, 3, 4, 32), 36))])
+    c = b.layer("Conv2D", [x], {"filters": 32, "kernel_size": 3, "padding": "same", "use_bias": False},
+                [("kernel", he(rng, (3, 3, 4, 32), 36))])
+    cat = b.layer("Concatenate", [a, c])
+    y = b.layer("Conv2D", [cat], {"filters": 64, "kernel_size": 1, "use_bias": False},
+                [("kernel", he(rng, (1, 1, 64, 64), 64))])
+    m, w = b.build([y])
+    plan = build_plan(build_graph(m, w))
+    assert "Concat" not in [u.kind for u in plan.units]
+    pos = next(i for i, u in enumerate(plan.units) if u.concat_in)
+    ls = specialize(plan, plan_buffers(plan), EXACT, 64, 64).launches
+    for n in (1, 8, 64):
+        (l,) = serving(ls, pos, n)
+        if "_tc_" in l.kernel:         # only the conv-mode tiles: 4-D boxes, two A maps
+            assert len(l.tmaps[0]["dims"]) == 4, (n, l.kernel, l.note)
+            assert l.tmaps[3]["offset"] != l.tmaps[0]["offset"], l.note
+    assert "_tc_" in serving(ls, pos, 64)[0].kernel

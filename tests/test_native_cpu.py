@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_mapping_without_gpu():
     lib = _native.lib()
-    assert lib.nnb_abi_version() == 5
+    assert lib.nnb_abi_version() == 6
     try:
         import torch
         has_gpu = torch.cuda.is_available()
