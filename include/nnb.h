@@ -187,6 +187,12 @@ nnb_status nnb_time_launch(nnb_net *net, int32_t index, int32_t n, int32_t iters
  * pass.  ms must hold one entry per launch of the schedule. */
 nnb_status nnb_time_sequence(nnb_net *net, int32_t n, int32_t iters, void *stream, double *ms);
 
+/* FP32 FFMA throughput of `device` (TFLOP/s, 2 flops per FMA): a
+ * microbenchmark of 16 independent FMA chains per thread, 8 blocks of 256
+ * threads per SM, `iters` iterations, best of 5 timed launches (CUDA
+ * events).  The measured SIMT roofline denominator (roofline.py). */
+nnb_status nnb_ffma_peak(int32_t device, int32_t iters, double *tflops, double *ms);
+
 nnb_status nnb_host_alloc(uint64_t bytes, void **ptr);
 void nnb_host_free(void *ptr);
 void nnb_free(void *ptr);

@@ -20,7 +20,7 @@ NNB_OK, NNB_ERR_ARGUMENT, NNB_ERR_NO_DRIVER, NNB_ERR_NO_DEVICE, NNB_ERR_ARCH, \
     NNB_ERR_NVRTC, NNB_ERR_CUDA, NNB_ERR_OOM, NNB_ERR_BATCH = range(9)
 
 EXPORTED = ("nnb_device_check", "nnb_compile", "nnb_compile_parallel", "nnb_create", "nnb_arena_ptr", "nnb_apply",
-            "nnb_run_host", "nnb_enqueue_host", "nnb_run_host_chunked", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_host_alloc", "nnb_host_free",
+            "nnb_run_host", "nnb_enqueue_host", "nnb_run_host_chunked", "nnb_sync", "nnb_time_apply", "nnb_time_launch", "nnb_time_sequence", "nnb_ffma_peak", "nnb_host_alloc", "nnb_host_free",
             "nnb_free", "nnb_net_info", "nnb_last_error", "nnb_abi_version", "nnb_destroy")
 
 
@@ -99,6 +99,7 @@ def lib():
         "nnb_time_apply": (I32, [VP, I32, I32, VP, P(ctypes.c_double)]),
         "nnb_time_launch": (I32, [VP, I32, I32, I32, VP, P(ctypes.c_double)]),
         "nnb_time_sequence": (I32, [VP, I32, I32, VP, P(ctypes.c_double)]),
+        "nnb_ffma_peak": (I32, [I32, I32, P(ctypes.c_double), P(ctypes.c_double)]),
         "nnb_host_alloc": (I32, [U64, P(VP)]),
         "nnb_host_free": (None, [VP]),
         "nnb_free": (None, [VP]),
@@ -169,3 +170,11 @@ def compile_parallel(sources, cache_dir=None):
                                      cache_dir.encode() if cache_dir else None,
                                      ctypes.byref(wall), ctypes.byref(tot)), "nnb_compile_parallel")
     return wall.value, tot.value
+
+
+def ffma_peak(device=0, iters=4096):
+    """Measured FP32 FFMA TFLOP/s of `device` (nnb_ffma_peak) and the ms of
+    the best timed launch."""
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    check(lib().nnb_ffma_peak(device, iters, ctypes.byref(tf), ctypes.byref(ms)), "nnb_ffma_peak")
+    return tf.value, ms.value

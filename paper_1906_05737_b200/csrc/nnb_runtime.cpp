@@ -567,6 +567,75 @@ nnb_status nnb_compile_parallel(const char *const *sources, int32_t n_sources,
   return NNB_OK;
 }
 
+// FP32 FFMA throughput microbenchmark (the SIMT roofline denominator of
+// roofline.py; SURVEY.md 8(d) asked for it to be measured, not derived).
+// Every thread runs 16 independent FMA chains (no dependency stalls at 8
+// warps per scheduler); 8 resident 256-thread blocks per SM, `waves` grids.
+static const char *kFfmaSrc = R"(
+extern "C" __global__ void __launch_bounds__(256) nnb_ffma_probe(float* out, int iters, float a, float b) {
+  float x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = threadIdx.x * 1e-3f + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += x[j];
+  if (s == 1234.5f) out[blockIdx.x] = s;
+}
+)";
+
+nnb_status nnb_ffma_peak(int32_t device, int32_t iters, double *tflops, double *ms) {
+  if (!tflops || iters < 1) return fail(NNB_ERR_ARGUMENT, "bad arguments");
+  CUcontext ctx;
+  CUdevice dev;
+  nnb_status st = device_ctx(device, &ctx, &dev);
+  if (st != NNB_OK) return st;
+  CTX_SCOPE(ctx)
+  Cu *C = cu();
+  int sms = 0;
+  CU_CHECK(C->p_cuDeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
+  std::string cubin;
+  double cms = 0;
+  bool hit = false;
+  st = compile_cubin(kFfmaSrc, ".", nullptr, "", &cubin, &cms, &hit);
+  if (st != NNB_OK) return st;
+  CUmodule mod = nullptr;
+  CU_CHECK(C->p_cuModuleLoadData(&mod, cubin.data()));
+  CUfunction fn = nullptr;
+  CUdeviceptr out = 0;
+  CUevent e0 = nullptr, e1 = nullptr;
+  float best = 1e30f;
+  const unsigned blocks = (unsigned)sms * 8;
+  CUresult r = C->p_cuModuleGetFunction(&fn, mod, "nnb_ffma_probe");
+  if (r == CUDA_SUCCESS) r = C->p_cuMemAlloc(&out, 4 * blocks);
+  if (r == CUDA_SUCCESS) r = C->p_cuEventCreate(&e0, CU_EVENT_DEFAULT);
+  if (r == CUDA_SUCCESS) r = C->p_cuEventCreate(&e1, CU_EVENT_DEFAULT);
+  for (int rep = 0; rep < 6 && r == CUDA_SUCCESS; ++rep) {
+    float a = 0.999f, b = 1e-3f;
+    int it = iters;
+    void *args[] = {&out, &it, &a, &b};
+    r = C->p_cuEventRecord(e0, nullptr);
+    if (r == CUDA_SUCCESS) r = C->p_cuLaunchKernel(fn, blocks, 1, 1, 256, 1, 1, 0, nullptr, args, nullptr);
+    if (r == CUDA_SUCCESS) r = C->p_cuEventRecord(e1, nullptr);
+    if (r == CUDA_SUCCESS) r = C->p_cuEventSynchronize(e1);
+    float f = 0;
+    if (r == CUDA_SUCCESS) r = C->p_cuEventElapsedTime(&f, e0, e1);
+    if (r == CUDA_SUCCESS && rep > 0) best = std::min(best, f);     // first run: warm-up
+  }
+  if (e0) C->p_cuEventDestroy(e0);
+  if (e1) C->p_cuEventDestroy(e1);
+  if (out) C->p_cuMemFree(out);
+  C->p_cuModuleUnload(mod);
+  if (r != CUDA_SUCCESS) return fail(NNB_ERR_CUDA, "ffma probe failed (%d)", (int)r);
+  const double flops = 2.0 * 16.0 * iters * 256.0 * blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  if (ms) *ms = best;
+  return NNB_OK;
+}
+
 void nnb_free(void *p) { free(p); }
 
 nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
