@@ -2,30 +2,41 @@
 """Benchmark of the B200 CompiledNN path (contract: one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nnb|reference]
-                    [--config C] [--batch B] [--no-extra]
+                    [--config C] [--batch B] [--global-batch G]
+                    [--options default|exact] [--no-extra]
 
 Workload: BASELINE.json configs[1] (the dense MLP, 1024 -> 512 tanh -> 256
 sigmoid -> 128 elu -> 10 softmax) at batch 65536 per GPU, FP32 in and out,
-exact (interpreter-grade) transcendentals.  A *step* is one ``apply()`` --
-one CUDA-graph replay of the whole network over the batch already resident
-in HBM.  Inputs (256 MiB per GPU) are larger than the 126 MB L2, so no flush
-is needed between steps.  N GPUs run N independent replicas (weak scaling,
-no collective on the data path); the time is the max over ranks.
+the reference's DEFAULT ApproximationOptions (rational tanh/sigmoid, fast
+softmax exp: pkg/src/nnjit/options.py:9-27 -- the options the reference arm
+runs too; ``--options exact`` for interpreter-grade transcendentals).  A
+*step* is one ``apply()`` -- one CUDA-graph replay of the whole network over
+the batch already resident in HBM.  Inputs (256 MiB per GPU) are larger than
+the 126 MB L2, so no flush is needed between steps (smaller batches flush L2
+before every timed replay).  N GPUs run N independent replicas with no
+collective on the data path; the time is the max over ranks.  Weak scaling by
+default (B images per GPU); ``--global-batch G`` shards G images over the
+ranks instead (strong scaling, BASELINE configs[3] and [4]: cfg3 @256, cfg4
+@64 over 1/2/4/8 GPUs).
 
 Keys beyond the base contract:
-  e2e          the same metric through ``CompiledNetwork.run_host`` (the C-ABI
-               host-buffer call): H2D of the step's inputs from pinned memory,
-               replay, D2H of the softmax outputs, every step.
-  roofline     dominant kernel: algorithmic FLOPs per launch / its CUDA-event
-               time, against the FP32 FFMA peak (SIMT kernels) or TF32 tensor
-               peak (tcgen05 kernels).
-  cpu_baseline the C oracle (oracle/nnoracle.c, the reference interpreter
-               restated) on all host threads over a bounded sample.
-  parity       max |GPU - oracle| over sampled images of the timed batch
-               (evaluated by the cpu_baseline leg, rank 0 at N=1).
+  e2e          the same metric through ``compile_model(host_chunks=8).run_host``
+               (the C-ABI host-buffer call): H2D of the step's inputs from
+               pinned memory, replay, D2H of the outputs, every step.
+  roofline     dominant kernel: algorithmic work per launch / its CUDA-event
+               time against its own pipe (roofline.py: tcgen05 -> TF32 = half
+               the measured bf16 rate x products per MAC; FFMA -> the measured
+               FFMA peak; HBM -> measured copy bandwidth).
+  launches     every launch of the step: pipe, algorithmic flops / bytes, roof
+               and measured µs, fraction.
+  cpu_baseline the unmodified reference (oracle/_ref nnjit.CompiledNetwork) on
+               all host cores over a bounded sample; the C port of its
+               interpreter as a secondary figure.
+  parity       sampled images of the timed batch vs the oracle on EVERY rank;
+               a failure marks the line invalid and exits 1.
   configs      all five BASELINE configs: batch-1 latency and large-batch
-               throughput (L2 flushed between timed replays), fraction of the
-               layerwise roofline of SURVEY.md 8(d).
+               throughput (L2 flushed between timed replays), per-launch
+               roofline fractions, the reference's CPU batch-1 latency.
 """
 
 import argparse
@@ -41,6 +52,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+RTOL, ATOL = 1e-4, 1e-5           # BASELINE.json north_star FP32 tolerance
+ARITHMETIC = ("FP32 in HBM, FP32 FFMA kernels; tcgen05 GEMMs (Dense, 1x1 and KxK convs above "
+              "the selection thresholds) as a 3xTF32 split a_hi*b_hi + a_hi*b_lo + a_lo*b_hi "
+              "with FP32 accumulation in TMEM (chunked every 16 k-blocks); N=256 row tiles form "
+              "the two correction products as one BF16 K=16 MMA.  Stated bound per output: "
+              "|d| <= 1e-4|ref| + 1e-5 + 2^-19 sum|a_k b_k| (TF32 split), + 2^-17 sum|a_k b_k| "
+              "(BF16 correction) -- DESIGN.md section 4; every bench/test case passes the "
+              "plain FP32 gate")
 METRIC = "images/sec per net (batch-1 latency + batched) at 1/2/4/8 B200; % roofline"
 BIG_BATCH = {0: 4096, 1: 65536, 2: 1024, 3: 256, 4: 64}
 
@@ -53,9 +72,23 @@ def parse():
     p.add_argument("--impl", default="nnb", choices=("nnb", "reference"))
     p.add_argument("--config", type=int, default=1)
     p.add_argument("--batch", type=int, default=None)
+    p.add_argument("--global-batch", type=int, default=None,
+                   help="strong scaling: shard this many images over the ranks")
+    p.add_argument("--options", default="default", choices=("default", "exact"))
     p.add_argument("--no-extra", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     return p.parse_args()
+
+
+def options(args):
+    from paper_1906_05737_b200 import EXACT, ApproximationOptions
+    return EXACT if args.options == "exact" else ApproximationOptions()
+
+
+def options_desc(opts):
+    return (f"activation_mode={opts.activation_mode} softmax_exp={opts.softmax_exp}"
+            + (" (the reference's defaults)" if (opts.activation_mode, opts.softmax_exp)
+               == ("rational", "fast") else " (interpreter-grade: float64 rounded once)"))
 
 
 class ClockSampler:
@@ -152,53 +185,114 @@ def max_over_ranks(world, value, local):
     return float(t.item())
 
 
-def cpu_reference(cfg, batch, seconds, threads=None, check=None):
-    """Time the C oracle (reference interpreter restated) on host threads.
-    Returns (images/s, sample images, threads, seconds, parity).  ``check`` =
-    (inputs, gpu_outputs) of sampled images of the timed batch: the oracle
-    also evaluates those, as the checker of the GPU outputs (the only other
-    use of oracle/ in this file)."""
+def cpu_port(cfg, batch, seconds, opts, threads=None):
+    """The C restatement of the reference interpreter (oracle/nnoracle.c) on
+    host threads over a bounded sample -- the secondary CPU figure.
+    Returns (images/s, sample images, threads, seconds)."""
     from oracle import oracle
     from paper_1906_05737_b200 import zoo
-    threads = threads or os.cpu_count() or 1
-    m, w = zoo.build(cfg)
     from paper_1906_05737_b200.graph import build_graph
-    g = build_graph(m, w)
+    threads = threads or os.cpu_count() or 1
+    g = build_graph(*zoo.build(cfg))
     probe = max(threads, 1)
     x = zoo.inputs(cfg, probe, seed=7)
     t0 = time.perf_counter()
-    oracle.run_graph(g, [x], "exact", threads)
-    dt = time.perf_counter() - t0
-    per_img = dt / probe
+    oracle.run_graph(g, [x], opts, threads)
+    per_img = (time.perf_counter() - t0) / probe
     sample = int(min(batch, max(probe, seconds / max(per_img, 1e-9))))
     sample = max(threads, sample // threads * threads)
     x = zoo.inputs(cfg, sample, seed=7)
     t0 = time.perf_counter()
-    oracle.run_graph(g, [x], "exact", threads)
+    oracle.run_graph(g, [x], opts, threads)
     dt = time.perf_counter() - t0
-    parity = None
-    if check is not None:
-        xs, got = check
-        want = oracle.run_graph(g, [xs], "exact", threads)[0]
-        parity = {"images": len(xs), "max_abs": float(np.abs(got - want).max()),
-                  "ok": bool(np.allclose(got, want, rtol=1e-4, atol=1e-5)),
-                  "tolerance": "rtol 1e-4 / atol 1e-5 vs oracle/nnoracle.c (exact)"}
-    return sample / dt, sample, threads, dt, parity
+    return sample / dt, sample, threads, dt
+
+
+def oracle_check(cfg, xs, got, opts):
+    """The sampled GPU outputs against the oracle on the same images and the
+    same approximation options (the oracle's use here: the checker)."""
+    from oracle import oracle
+    from paper_1906_05737_b200 import zoo
+    from paper_1906_05737_b200.graph import build_graph
+    want = oracle.run_graph(build_graph(*zoo.build(cfg)), [xs], opts)[0]
+    return {"images": len(xs), "max_abs": float(np.abs(got - want).max()),
+            "ok": bool(np.allclose(got, want, rtol=RTOL, atol=ATOL)),
+            "tolerance": f"rtol {RTOL:g} / atol {ATOL:g} vs oracle/nnoracle.c with the same "
+                         "ApproximationOptions (models of pkg/src/nnjit/codegen/approx.py)"}
+
+
+def reference_cpu(cfg, seconds, steps=1, warmup=0):
+    """The reference's own compiled x86 path (oracle/_ref: the unmodified
+    nnjit package, CompiledNetwork, default options, BASELINE.md stand-ins)
+    on every usable host core, one network per forked worker.  Returns
+    (per-step images/s list, images per step, info) or None when oracle/_ref
+    is not installed."""
+    from oracle import refbench
+    try:
+        refbench.nnjit()
+    except ImportError:
+        return None
+    tp = refbench.Throughput(cfg)
+    try:
+        n = tp.images_for(seconds)
+        vals = []
+        for i in range(warmup + steps):
+            v, n_done, _ = tp.step(n)
+            if i >= warmup:
+                vals.append(v)
+    finally:
+        tp.close()
+    info = {**refbench.host_info(), "workers": tp.procs, "compile_ms": tp.compile_ms,
+            "stand_ins": refbench.STAND_INS[cfg]}
+    return vals, n_done, info
+
+
+def reference_extras(seconds=2.0):
+    """Batch-1 latency of the reference's compiled path for all five configs
+    (median over >= ``seconds``), its compile time and the interpreter on one
+    image."""
+    from oracle import refbench
+    from paper_1906_05737_b200 import zoo
+    out = {}
+    for c in range(5):
+        try:
+            net, cms = refbench.compile_reference(c)
+            us, calls = refbench.batch1_latency_us(c, seconds, net=net)
+            out[zoo.CONFIGS[c]["name"]] = {
+                "batch1_latency_us": us, "calls": calls, "compile_ms": cms,
+                "interpreter_one_image_ms": refbench.interpreter_one_image_ms(c),
+                "stand_ins": refbench.STAND_INS[c]}
+        except Exception as e:  # report, never hide
+            out[zoo.CONFIGS[c]["name"]] = {"error": repr(e)[:300]}
+    return out
 
 
 def reference_arm(args, world, rank):
+    """``--impl reference``: the reference's own CPU implementation of the
+    path on this host, on this arm's config / metric (rank 0 only)."""
     if rank != 0:
         return
     cfg = args.config
     batch = args.batch or BIG_BATCH[cfg]
-    from paper_1906_05737_b200 import zoo  # noqa: F401
-    vals = []
-    sample = threads = None
-    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
-    for i in range(args.warmup + args.steps):
-        v, sample, threads, _, _ = cpu_reference(cfg, batch, budget)
-        if i >= args.warmup:
-            vals.append(v)
+    from paper_1906_05737_b200 import zoo
+    budget = min(5.0, max(1.0, 120.0 / max(1, args.steps + args.warmup)))
+    got = reference_cpu(cfg, budget, args.steps, args.warmup)
+    if got is not None:
+        vals, sample, info = got
+        kind, cores = "reference", info["workers"]
+        what = (f"{sample} images of {zoo.CONFIGS[cfg]['name']} per step through the unmodified "
+                f"reference (oracle/_ref nnjit.CompiledNetwork, SSE4.1 code, default options, "
+                f"stand-in: {info['stand_ins']}), {cores} forked workers x one network each, input "
+                f"view rewritten before every apply()")
+    else:   # oracle/_ref absent: the C restatement of the interpreter
+        vals, sample, threads = [], None, None
+        for i in range(args.warmup + args.steps):
+            v, sample, threads, _ = cpu_port(cfg, batch, budget, options(args))
+            if i >= args.warmup:
+                vals.append(v)
+        kind, cores, info = "port", threads, {}
+        what = (f"{sample} images of {zoo.CONFIGS[cfg]['name']} per step through "
+                "oracle/nnoracle.c (reference interpreter restated; oracle/_ref not installed)")
     v = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
@@ -206,77 +300,51 @@ def reference_arm(args, world, rank):
         "ms_per_step": 1e3 * sample / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.md section 2)",
         "config": {"workload": zoo.CONFIGS[cfg]["name"], "global_batch": batch,
-                   "parallelism": "host threads", "sample_images_per_step": sample},
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} images of {zoo.CONFIGS[cfg]['name']} per step "
-                                   "through oracle/nnoracle.c (reference interpreter "
-                                   "restated, float32 per-op rounding)"},
+                   "parallelism": f"{cores} host workers", "sample_images_per_step": sample},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": kind,
+                         "sample": what, **info},
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if kind == "reference" and not args.no_extra:
+        line["configs"] = reference_extras()
     print(json.dumps(line), flush=True)
 
 
-_TF32 = {}
-
-
 def ncu_traffic(kernel):
-    """dram read + write bytes per launch of `kernel` from the committed
-    `ncu --set full` capture (profiles/r01_dense_tc_ncu_raw.csv), or None."""
+    """dram read + write bytes per launch of `kernel` from a committed
+    `ncu --set full` capture (profiles/*_ncu_raw.csv: one row per launch), or
+    None when no capture of that kernel is committed."""
     import csv
-    p = pathlib.Path(ROOT) / "profiles" / "r01_dense_tc_ncu_raw.csv"
-    try:
-        rows = list(csv.reader(open(p)))
-        h, units, v = rows[0], rows[1], rows[2]
-        # kernel names end in a schedule index (nnb_u<unit>_<kind>_<i>); the
-        # capture matches when the unit and kind agree
-        stem = lambda k: k.rsplit("_", 1)[0]
-        if stem(v[h.index("Kernel Name")].strip('"')) != stem(kernel):
-            return {"traffic": None}
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        tot = sum(float(v[h.index(m)]) * scale[units[h.index(m)]]
-                  for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        return {"traffic": tot, "traffic_source": f"{p.name} (ncu --set full, cold cache, one launch)"}
-    except (OSError, ValueError, IndexError, KeyError):
-        return {"traffic": None}
-
-
-def measure_tf32_peak(torch, dev):
-    """cuBLAS TF32 dense throughput on this GPU (the roofline denominator for
-    the 3xTF32 tcgen05 kernels)."""
-    if dev in _TF32:
-        return _TF32[dev]
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        n = 8192
-        a = torch.randn(n, n, device=dev)
-        b = torch.randn(n, n, device=dev)
-        for _ in range(2):
-            a @ b
-        best = 1e9
-        for _ in range(5):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            a @ b
-            e1.record()
-            torch.cuda.synchronize(dev)
-            best = min(best, e0.elapsed_time(e1))
-        _TF32[dev] = 2 * n ** 3 / (best / 1e3) / 1e12
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    return _TF32[dev]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    # kernel names end in a schedule index (nnb_u<unit>_<kind>_<i>); a capture
+    # matches when the unit and kind agree
+    stem = lambda k: k.rsplit("_", 1)[0]
+    for p in sorted((pathlib.Path(ROOT) / "profiles").glob("*_ncu_raw.csv"), reverse=True):
+        try:
+            rows = list(csv.reader(open(p)))
+            h, units = rows[0], rows[1]
+            for v in rows[2:]:
+                if stem(v[h.index("Kernel Name")].strip('"')) != stem(kernel):
+                    continue
+                tot = sum(float(v[h.index(m)].replace(",", "")) * scale[units[h.index(m)]]
+                          for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                return {"traffic": tot,
+                        "traffic_source": f"profiles/{p.name} (ncu --set full, one launch)"}
+        except (OSError, ValueError, IndexError, KeyError):
+            continue
+    return {"traffic": None}
 
 
 def flush_l2(buf):
     buf.zero_()
 
 
-def time_config(cfg, batch, device, torch, iters=20):
+def time_config(cfg, batch, device, torch, opts, iters=20):
     """(ms per replay with L2 flushed before each, net)."""
-    from paper_1906_05737_b200 import EXACT, compile_model, zoo
+    from paper_1906_05737_b200 import compile_model, zoo
     m, w = zoo.build(cfg)
-    net = compile_model(m, w, EXACT, batch=batch, device=device)
+    net = compile_model(m, w, opts, batch=batch, device=device)
     net.input_views[0].copy_(torch.from_numpy(zoo.inputs(cfg, batch)))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MiB > L2
     for _ in range(3):
@@ -295,6 +363,52 @@ def time_config(cfg, batch, device, torch, iters=20):
     return float(np.median(times)), net
 
 
+def dominant_roofline(net, B, lt, peaks, ffma):
+    """The `roofline` object of the launch with the largest share of the pass."""
+    from paper_1906_05737_b200 import roofline
+    dom = max(lt, key=lt.get)
+    L = net.artifact.launches[dom]
+    r = roofline.launch_roofline(net.plan.units[L.unit], L, B, peaks, ffma)
+    t = lt[dom] / 1e3
+    share = lt[dom] / sum(lt.values())
+    if r["bound"] == "hbm":
+        achieved = r["bytes"] / t / 1e9
+        roof = {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "frac": achieved / peaks["hbm_gbs"],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"}
+    elif r["pipe"] == "tensor":
+        achieved = r["products_per_mac"] * r["flops"] / t / 1e12
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved,
+                "peak": r["peak_tflops"], "frac": achieved / r["peak_tflops"],
+                "peak_source": "dense TF32 = MEASURED_PEAKS.json bf16_tflops / 2 "
+                               f"({peaks['bf16_tflops']} / 2)",
+                "achieved_counts": (f"{r['products_per_mac']} x 2MNK TF32-equivalent tensor "
+                                    "flops per launch ("
+                                    + ("1 TF32 product a_hi*b_hi + the two correction products "
+                                       "as one BF16 K=16 MMA" if r["products_per_mac"] == 2
+                                       else "3xTF32 split") + ")"),
+                "fp32_equivalent_tflops": r["flops"] / t / 1e12}
+    else:
+        achieved = r["flops"] / t / 1e12
+        roof = {"bound": "fp32_ffma", "unit": "TFLOP/s", "achieved": achieved,
+                "peak": ffma[0], "frac": achieved / ffma[0], "peak_source": ffma[1]}
+    roof.update({"kernel": L.kernel, "algorithmic_per_launch": {"flops": r["flops"],
+                                                               "bytes": r["bytes"]},
+                 "kernel_ms": lt[dom], "share_of_step": share,
+                 "hbm_frac_at_same_time": r["bytes"] / t / 1e9 / peaks["hbm_gbs"],
+                 "timing": "CUDA events between consecutive launches of full passes on the "
+                           "launching stream (nnb_time_sequence), mean over the step count",
+                 **ncu_traffic(L.kernel)})
+    return roof
+
+
+def launch_table(net, B, lt, peaks, ffma):
+    from paper_1906_05737_b200 import roofline
+    rows, roof_us = roofline.net_roofline(net, B, peaks, ffma[0], lt)
+    meas_us = sum(r.get("measured_us", 0.0) for r in rows)
+    return rows, roof_us, meas_us
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup(args.gpus)
@@ -302,44 +416,67 @@ def main():
         reference_arm(args, world, rank)
         return
     import torch
-    from paper_1906_05737_b200 import EXACT, compile_model, roofline, zoo
+    from paper_1906_05737_b200 import _native, compile_model, roofline, zoo
     from paper_1906_05737_b200.planner import build_reference_plan
     from paper_1906_05737_b200.graph import build_graph
+    from paper_1906_05737_b200.replicas import shard
 
+    opts = options(args)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = args.config
-    B = args.batch or BIG_BATCH[cfg]
+    if args.global_batch:
+        start, B = shard(args.global_batch, world, rank)
+        scaling, G = "strong", args.global_batch
+    else:
+        B = args.batch or BIG_BATCH[cfg]
+        start, scaling, G = rank * B, "weak", world * B
     m, w = zoo.build(cfg)
-    net = compile_model(m, w, EXACT, batch=B, device=local)
+    net = compile_model(m, w, opts, batch=B, device=local)
     x = zoo.inputs(cfg, B, seed=1 + rank)
     net.input_views[0].copy_(torch.from_numpy(x))
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         net.apply()
     torch.cuda.synchronize(dev)
+    flush = None
+    if x.nbytes < 126e6:
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB
 
     # ---------------- timed region: K replays, inputs resident --------------
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            net.apply()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                net.apply()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1)
+        else:   # inputs smaller than L2: flush before every replay, time replays only
+            ms = 0.0
+            for _ in range(args.steps):
+                flush_l2(flush)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                net.apply()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                ms += e0.elapsed_time(e1)
     barrier(world)
-    ms = max_over_ranks(world, e0.elapsed_time(e1), local)
+    ms = max_over_ranks(world, ms, local)
     ms_step = ms / args.steps
-    value = world * B * args.steps / (ms / 1e3)
+    value = G * args.steps / (ms / 1e3)
     n_launch = len(net.launches_for(B))
 
-    # sampled outputs of this batch (checked against the oracle on the
-    # cpu_baseline leg, and against the e2e path below)
-    idx = np.linspace(0, B - 1, 16).astype(int)
+    # ---------------- parity: sampled images of this batch, every rank -------
+    idx = np.unique(np.linspace(0, B - 1, min(B, 16)).astype(int))
     got = net.output_views[0][torch.as_tensor(idx, device=dev)].cpu().numpy()
-    parity = None
+    parity = oracle_check(cfg, x[idx], got, opts)
+    ok = max_over_ranks(world, 0.0 if parity["ok"] else 1.0, local) == 0.0
+    parity["ranks_ok"] = ok
 
     # ---------------- e2e through the C-ABI host-buffer call ----------------
     from paper_1906_05737_b200 import pinned_empty
@@ -351,122 +488,109 @@ def main():
     # host_chunks=8) -> PipelinedNetwork.run_host -> nnb_run_host_chunked
     # (chunk j's H2D overlaps chunk j-1's replay + D2H; 8 chunks measured
     # best: 1 / 2 / 4 / 8 / 16 -> 12.3 / 12.8 / 13.0 / 13.0 / 12.9 M img/s)
-    pnet = compile_model(m, w, EXACT, batch=B, device=local, host_chunks=8)
+    chunks = 8 if B >= 8192 else 1
+    pnet = compile_model(m, w, opts, batch=B, device=local, host_chunks=chunks)
     pnet.run_host([hx], [hy])
     # same outputs as the resident-input path (checked on the sampled images)
-    np.testing.assert_allclose(hy[idx], got, rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(hy[idx], got, rtol=RTOL, atol=ATOL)
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         pnet.run_host([hx], [hy])
     e2e_s = max_over_ranks(world, time.perf_counter() - t0, local)
-    e2e = {"value": world * B * e2e_steps / e2e_s, "unit": "images/s",
+    e2e = {"value": G * e2e_steps / e2e_s, "unit": "images/s",
            "h2d_bytes_per_step": int(hx.nbytes), "d2h_bytes_per_step": int(hy.nbytes),
-           "path": "compile_model(host_chunks=8).run_host -> nnb_run_host_chunked (pinned host "
-                   "buffers, 8 chunks on 8 streams)"}
+           "path": f"compile_model(host_chunks={chunks}).run_host -> nnb_run_host_chunked "
+                   f"(pinned host buffers, {chunks} chunk(s) on {chunks} stream(s))"}
     del pnet
 
-    # ---------------- roofline of the dominant kernel -----------------------
+    # ---------------- roofline of the dominant kernel + every launch --------
     peaks = roofline.measured_peaks()
+    ffma = roofline.ffma_peak_tflops(_native.ffma_peak(local, 4096)[0])
     # per-launch CUDA-event durations inside full passes (same order, same
     # inputs as the timed replays, events between consecutive launches)
     lt = net.time_sequence(B, iters=max(3, args.steps))
-    dom = max(lt, key=lt.get)
-    L = net.artifact.launches[dom]
-    u = net.plan.units[L.unit]
-    f, io, wb = roofline.unit_work(u)
-    share = lt[dom] / sum(lt.values())
+    roof = dominant_roofline(net, B, lt, peaks, ffma)
+    rows, roof_us, meas_us = launch_table(net, B, lt, peaks, ffma)
     clocks = clk.summary()
-    peak_fp32 = roofline.fp32_peak_tflops()
-    fp32_equiv = B * f / (lt[dom] / 1e3) / 1e12
-    if "_tc_" in L.kernel:
-        # 3xTF32: the tensor pipe executes three TF32 products per FP32 MAC;
-        # with the BF16 correction split (note "bf16 corr") one TF32 product
-        # plus one K = 16 BF16 MMA per tf32 k-step, which issues in the time of
-        # a TF32 MMA (BF16 runs at 2x the TF32 rate): 2 TF32-equivalents
-        cb16 = "bf16 corr" in L.note
-        mult = 2 if cb16 else 3
-        tf32 = measure_tf32_peak(torch, dev)
-        achieved = mult * fp32_equiv
-        roof = {"bound": "tensor", "kernel": L.kernel, "unit": "TFLOP/s",
-                "achieved": achieved, "peak": tf32, "frac": achieved / tf32,
-                "peak_source": "TF32 dense, cuBLAS fp32 matmul with allow_tf32 on this GPU "
-                               "(8192^3, best of 5; MEASURED_PEAKS.json has bf16 only: "
-                               f"{peaks['bf16_tflops']} TF/s)",
-                "achieved_counts": ("2 x 2MNK TF32-equivalent tensor flops per launch (1 TF32 "
-                                    "product a_hi*b_hi + the two correction products as one "
-                                    "BF16 K=16 MMA = 2MNK TF32 + 4MNK BF16 flops)") if cb16
-                else "3 x 2MNK tensor flops (3xTF32 split) per launch",
-                "peak_note": "the live cuBLAS TF32 GEMM is the measured denominator (a good "
-                             "kernel can read a little above it); nominal dense TF32 is "
-                             "1100 TFLOP/s (B200_PROFILING.md)",
-                "frac_of_nominal_tf32": achieved / 1100.0,
-                "fp32_equivalent_tflops": fp32_equiv,
-                "fp32_ffma_peak_tflops": peak_fp32}
-    else:
-        achieved = fp32_equiv
-        roof = {"bound": "fp32_ffma", "kernel": L.kernel, "unit": "TFLOP/s",
-                "achieved": achieved, "peak": peak_fp32, "frac": achieved / peak_fp32,
-                "peak_source": "derived 148 SM x 128 FFMA lanes x 2 x 1965 MHz (no tensor "
-                               "cores in this kernel)"}
-    roof.update({"algorithmic_per_launch": {"flops": B * f, "bytes": B * io + wb},
-                 "kernel_ms": lt[dom], "share_of_step": share,
-                 "hbm_frac_at_same_time": (B * io + wb) / (lt[dom] / 1e3) / 1e9 / peaks["hbm_gbs"],
-                 "launch_ms": {net.artifact.launches[i].kernel: v for i, v in lt.items()},
-                 "timing": "CUDA events between consecutive launches of the pass, "
-                           "mean over the step count",
-                 **ncu_traffic(L.kernel)})
 
     # ---------------- per-config extras (rank 0, N == 1) ---------------------
     extra = None
     cpu = None
     if rank == 0 and world == 1:
-        c_val, c_n, c_thr, c_dt, parity = cpu_reference(cfg, B, args.cpu_seconds,
-                                                        check=(x[idx], got))
-        cpu = {"value": c_val, "unit": "images/s", "cores": c_thr, "kind": "port",
-               "sample": f"{c_n} images of {zoo.CONFIGS[cfg]['name']} through "
-                         f"oracle/nnoracle.c in {c_dt:.1f} s"}
+        ref = reference_cpu(cfg, min(10.0, args.cpu_seconds))
+        c_val, c_n, c_thr, c_dt = cpu_port(cfg, B, min(5.0, args.cpu_seconds), opts)
+        port = {"value": c_val, "unit": "images/s", "cores": c_thr,
+                "sample": f"{c_n} images through oracle/nnoracle.c (the reference interpreter "
+                          f"restated in C, {options_desc(opts)}) in {c_dt:.1f} s"}
+        if ref is not None:
+            vals, n_ref, info = ref
+            cpu = {"value": float(np.mean(vals)), "unit": "images/s", "cores": info["workers"],
+                   "kind": "reference",
+                   "sample": f"{n_ref} images of {zoo.CONFIGS[cfg]['name']} through the "
+                             "unmodified reference (oracle/_ref nnjit.CompiledNetwork, SSE4.1, "
+                             f"default options, stand-in: {info['stand_ins']}), "
+                             f"{info['workers']} forked workers x one network",
+                   "cpu_model": info["cpu_model"], "secondary_port": port}
+        else:
+            cpu = dict(port, kind="port")
+        ref_b1 = {}
+        if not args.no_extra and ref is not None:
+            ref_b1 = reference_extras(seconds=1.0)
         if not args.no_extra:
             extra = {}
             for c in range(5):
+                name = zoo.CONFIGS[c]["name"]
                 try:
                     big = BIG_BATCH[c]
-                    ms_b, netb = time_config(c, big, local, torch)
-                    ms_1, net1 = time_config(c, 1, local, torch, iters=50)
-                    g = build_graph(*zoo.build(c))
-                    rp = build_reference_plan(g)
-                    t_roof = roofline.layerwise_roof_s(rp, big, peaks["hbm_gbs"], peak_fp32)
-                    t_fused = roofline.fused_ideal_s(rp, big, peaks["hbm_gbs"], peak_fp32)
-                    extra[zoo.CONFIGS[c]["name"]] = {
-                        "batch": big, "ms": ms_b, "images_per_s": big / (ms_b / 1e3),
-                        "batch1_latency_us": ms_1 * 1e3,
-                        "launches": len(netb.launches_for(big)),
-                        "layerwise_roof_ms": t_roof * 1e3,
-                        "layerwise_roofline_frac": t_roof * 1e3 / ms_b,
-                        "fused_ideal_frac": t_fused * 1e3 / ms_b,
-                        "gflop_per_batch": big * roofline.total_flops(rp) / 1e9,
-                        "compile_ms": netb.compile_ms,
-                    }
+                    ms_b, netb = time_config(c, big, local, torch, opts)
+                    ms_1, net1 = time_config(c, 1, local, torch, opts, iters=50)
+                    ltb = netb.time_sequence(big, iters=5)
+                    rws, r_us, m_us = launch_table(netb, big, ltb, peaks, ffma)
+                    rp = build_reference_plan(build_graph(*zoo.build(c)))
+                    t_s = roofline.survey_layerwise_roof_s(rp, big, peaks["hbm_gbs"],
+                                                           roofline.fp32_peak_tflops())
+                    e = {"batch": big, "ms": ms_b, "images_per_s": big / (ms_b / 1e3),
+                         "batch1_latency_us": ms_1 * 1e3,
+                         "launches": len(netb.launches_for(big)),
+                         "roof_us": r_us, "roofline_frac": r_us / (ms_b * 1e3),
+                         "sum_launch_us": m_us,
+                         "launch_rows": [{k: (round(v, 3) if isinstance(v, float) else v)
+                                          for k, v in r.items()} for r in rws],
+                         "survey_ffma_only_frac": t_s * 1e3 / ms_b,
+                         "gflop_per_batch": big * roofline.total_flops(rp) / 1e9,
+                         "compile_ms": netb.compile_ms}
+                    if name in ref_b1 and "batch1_latency_us" in ref_b1[name]:
+                        e["reference_cpu"] = ref_b1[name]
+                        e["batch1_speedup_vs_reference_cpu"] = (
+                            ref_b1[name]["batch1_latency_us"] / e["batch1_latency_us"])
+                    extra[name] = e
                     del netb, net1
-                except Exception as e:  # report, never hide
-                    extra[zoo.CONFIGS[c]["name"]] = {"error": repr(e)[:300]}
+                except Exception as ex:  # report, never hide
+                    extra[name] = {"error": repr(ex)[:300]}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded weights/inputs, BASELINE.md section 2)",
-            "config": {"workload": zoo.CONFIGS[cfg]["name"], "global_batch": world * B,
+            "config": {"workload": zoo.CONFIGS[cfg]["name"], "global_batch": G,
                        "per_gpu_batch": B, "parallelism": f"replicas x{world}",
-                       "l2": "inputs larger than L2 (no flush)" if x.nbytes > 126e6
-                       else "inputs smaller than L2",
-                       "transcendentals": "exact mode (tanh/sigmoid/elu float64-rounded in "
-                                          "FFMA kernels; FP32 within 2 ulp in tcgen05 epilogues)"},
+                       "l2": "inputs larger than L2 (no flush)" if flush is None
+                       else "L2 flushed (256 MiB write) before every timed replay",
+                       "options": options_desc(opts), "arithmetic": ARITHMETIC},
             "e2e": e2e, "gpu_launches": n_launch * args.steps, "clocks": clocks,
-            "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "roofline": roof, "step_roofline": {"roof_us": roof_us, "sum_launch_us": meas_us,
+                                                "frac": roof_us / (ms_step * 1e3)},
+            "launches": [{k: (round(v, 3) if isinstance(v, float) else v)
+                          for k, v in r.items()} for r in rows],
+            "ffma_peak": {"tflops": ffma[0], "source": ffma[1]},
+            "cpu_baseline": cpu, "parity": parity,
             "compile_ms": net.compile_ms, "configs": extra,
         }
+        if not ok:
+            line["invalid"] = "parity check against the oracle failed on at least one rank"
         import torch as _t
         if world > max(1, _t.cuda.device_count()):
             # several ranks on one device: their replays time-slice the GPU, so
@@ -477,6 +601,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
 
 
 if __name__ == "__main__":

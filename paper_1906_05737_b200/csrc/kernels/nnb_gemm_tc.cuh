@@ -456,8 +456,9 @@ struct GemmTc {
   // the TMEM columns, so BN = 128 keeps two accumulator buffers next to a
   // TMEM-resident A); the chunk length CHUNK then bounds the truncation error.
   static constexpr bool CS = C::CSPLIT != 0;
-  // exact-mode activations in FP32 (no FP64: it issues on the MMA's pipe)
-  static constexpr int EMODE = C::MODE == MODE_EXACT ? MODE_EXACT_F32 : C::MODE;
+  // epilogue activation mode: exact mode stays float64-rounded-once (the
+  // interpreter's semantics, interpreter.py:102-112) here as everywhere
+  static constexpr int EMODE = C::MODE;
   static constexpr int CW = (CS ? 2 : 1) * C::BN;         // columns per chain
   static constexpr int ACC_COLS = NACC * CW;              // fp32 columns per buffer
   // ABUF accumulator buffers: 2 lets the epilogue drain one while the MMA fills
@@ -1268,8 +1269,7 @@ struct GemmTc {
 #pragma unroll
             for (int j = 0; j < C::HN; ++j) hv[j] = finish<C::H_ACT, EMODE, C::H_POST>(hp[j], hps, hpo, j);
             if (C::H_SOFTMAX) {
-              if (C::H_SMEXP == SMEXP_EXACT) softmax_row_regs_f32<C::HN, C::HN>(hv);
-              else softmax_row_regs<C::HN, C::HN, C::H_SMEXP>(hv);
+              softmax_row_regs<C::HN, C::HN, C::H_SMEXP>(hv);
             }
             const long long m = (long long)mb * BM + r;
             if (m < rows) {

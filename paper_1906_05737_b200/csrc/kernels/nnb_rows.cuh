@@ -22,8 +22,8 @@
 //     sums are added in slice order -- within the FP32 gate of the
 //     reference interpreter's single ascending chain
 //     (pkg/src/nnjit/interpreter.py:52-62), identical to it when KS = 1;
-//   * epilogue (activation, post-BN, residual, softmax -- exact mode in
-//     FP32, nnb_softmax.cuh softmax_row_regs_f32) in registers, the
+//   * epilogue (activation, post-BN, residual, softmax in the selected
+//     mode, nnb_softmax.cuh softmax_row_regs) in registers, the
 //     tile staged in smem (odd row stride: conflict-free for any CO) and
 //     written back as coalesced float4 stores.
 #pragma once
@@ -121,8 +121,7 @@ struct RowsNarrow {
           for (int j = 0; j < CO; ++j) acc[j] = add(acc[j], __ldg(res + j));
         }
         if (C::SOFTMAX) {
-          if (C::SMEXP == SMEXP_EXACT) softmax_row_regs_f32<CO, CO>(acc);
-          else softmax_row_regs<CO, CO, C::SMEXP>(acc);
+          softmax_row_regs<CO, CO, C::SMEXP>(acc);
         }
 #pragma unroll
         for (int j = 0; j < CO; ++j) sm.o[r][j] = acc[j];

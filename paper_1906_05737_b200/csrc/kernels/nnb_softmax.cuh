@@ -42,27 +42,6 @@ __device__ __forceinline__ void softmax_row_regs(float (&v)[TN]) {
   }
 }
 
-// SMEXP_EXACT evaluated in FP32 (the streaming Dense head, nnb_rows.cuh,
-// where the float64 exp sat on the critical path): exp_f32 (~2 ulp), a float32
-// sum in column order and one correctly rounded division per element --
-// a few ulp from the float64 form, far inside the FP32 gate.  Differences
-// below -87 give 0 (the float64 form's result there is < 2^-125 anyway).
-template <int TN, int L>
-__device__ __forceinline__ void softmax_row_regs_f32(float (&v)[TN]) {
-  float m = v[0];
-#pragma unroll
-  for (int j = 1; j < L; ++j) m = fmaxf(m, v[j]);
-  float s = 0.0f;
-#pragma unroll
-  for (int j = 0; j < L; ++j) {
-    const float d = v[j] - m;
-    v[j] = d < -87.0f ? 0.0f : exp_f32(d);
-    s = add(s, v[j]);
-  }
-#pragma unroll
-  for (int j = 0; j < L; ++j) v[j] = __fdiv_rn(v[j], s);
-}
-
 // One row spread across a warp, one value per lane (lanes with live == false
 // hold padding and do not contribute).
 template <int SMEXP>

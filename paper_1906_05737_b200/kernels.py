@@ -870,6 +870,8 @@ class Specializer:
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
                        f"{' depthwise fused' if dwf else ''}"
+                       f"{' 8x16-pixel conv tiles' if conv else ' row tiles'}"
+                       f"{' concat (2 A maps)' if conv and conv.get('CONCAT') else ''}"
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
                        f"{' bf16 corr' if cb16 else ''}"
                        f"{f' + fused Dense head N={hn}' if hn else ''}")
@@ -1224,5 +1226,6 @@ def tf32_split_hi(w, rn=True):
 
 def specialize(plan, assignment, options, max_batch, capacity, **tuning):
     """Specialise every launch unit; ``tuning`` are the Specializer's keyword
-    options (use_tc, sm_count, tc_min_rows, ...)."""
+    options (use_tc, sm_count, tc_min_rows, ...).  A plan made by the
+    reference's planner goes through planner.adopt_plan first."""
     return Specializer(plan, assignment, options, max_batch, capacity, **tuning).run()

@@ -554,14 +554,59 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow"):
     depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
-        fuse_pool(plan)
-        fuse_residual(plan)
-        fuse_softmax(plan)
-        fuse_upsample(plan)
-        fuse_concat(plan)
-        if dw_fusion:
-            fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")
+        apply_gpu_fusions(plan, dw_fusion)
     return plan
+
+
+def apply_gpu_fusions(plan, dw_fusion="narrow"):
+    """The B200 epilogue fusions, in place, on a reference-fused plan."""
+    fuse_pool(plan)
+    fuse_residual(plan)
+    fuse_softmax(plan)
+    fuse_upsample(plan)
+    fuse_concat(plan)
+    if dw_fusion:
+        fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")
+    return plan
+
+
+# fields of the reference's CompilationUnit (pkg/src/nnjit/optimizer.py:35-57)
+REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input_shapes",
+                         "output_shape", "kernel", "bias", "activation", "post_scale",
+                         "post_offset", "scale", "offset", "stride", "padding", "kernel_hw",
+                         "pool_op", "factor", "in_place_preference")
+
+
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow"):
+    """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
+    pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
+    :35-91) as this package's FusionPlan, with the B200 epilogue fusions
+    applied on top -- the binding that lets a maintainer keep the reference's
+    planner and hand its output to ``kernels.specialize`` (INTEGRATION.md
+    section 3).  A plan of this package passes through unchanged.  Unit
+    fields are copied by name, tensor shapes re-made as graph.TensorShape;
+    the folded arrays are used as they are (bit-identical either way,
+    tests/test_planner.py)."""
+    if isinstance(plan, FusionPlan):
+        return plan
+
+    def shape(s):
+        return TensorShape(tuple(int(d) for d in s.dims))
+
+    units = []
+    for u in plan.units:
+        kw = {f: getattr(u, f) for f in REFERENCE_UNIT_FIELDS}
+        kw["input_ids"] = tuple(kw["input_ids"])
+        kw["input_shapes"] = tuple(shape(s) for s in kw["input_shapes"])
+        kw["output_shape"] = shape(kw["output_shape"])
+        if kw["kernel_hw"] is not None:
+            kw["kernel_hw"] = tuple(kw["kernel_hw"])
+        units.append(CompilationUnit(**kw))
+    ours = FusionPlan(units, {t: shape(s) for t, s in plan.tensors.items()},
+                      tuple(plan.input_ids), tuple(plan.output_ids), dict(plan.node_units))
+    if gpu_fusion:
+        apply_gpu_fusions(ours, dw_fusion)
+    return ours
 
 
 def describe_plan(plan):

@@ -142,5 +142,6 @@ class MultiDeviceNetwork:
         for i in range(len(self.replicas[0].output_views)):
             parts = [rep.output_views[i].to(dev, non_blocking=True) for rep in self.replicas]
             outs.append(torch.cat(parts))
-        torch.cuda.synchronize(dev)
+        for d in sorted(set(self.devices) | {dev.index}):
+            torch.cuda.synchronize(d)       # every replica's device, not only the gather's
         return outs

@@ -1,21 +1,32 @@
-"""Algorithmic work per launch unit and the per-layer roofline of SURVEY.md 8(d).
+"""Algorithmic work per launch and the per-launch roofline.
 
-    T_roof(N) = sum_u max(N * F_u / P_pipe(u), (N * (In_u + Out_u) + W_u) / BW)
+    T_roof(N) = sum_launch max(N * F_u * m(k) / P_pipe(k), (N * (In_u + Out_u) + W_u) / BW)
 
-* ``F_u``: 2 x MACs for Dense / Conv2D / DepthwiseConv2D, one op per element
-  per tap for pooling, one per element per input for Add, one per element for
-  BatchNorm / activation / softmax; data movement (upsample, concat, pad) is
-  free.
-* ``In_u`` / ``Out_u``: float32 activation bytes per image; ``W_u``: weight,
-  bias and affine bytes, read once per batch.
-* ``P_pipe``: FP32 FFMA peak of the B200 = 148 SM x 128 lanes x 2 x f_clk
-  (74.4 TFLOP/s at the 1965 MHz max clock; derived, not measured), the TF32
-  tensor peak for tensor-core units.
+summed over the launches a replay over N images runs, each launch ``k``
+serving one fused unit ``u`` of the plan actually compiled:
+
+* ``F_u``: 2 x MACs for Dense / Conv2D / DepthwiseConv2D (a fused depthwise
+  producer adds its own), one op per element per tap for pooling, one per
+  element per input for Add, one per element for BatchNorm / activation /
+  softmax; data movement (upsample, concat, pad) is free.
+* ``In_u`` / ``Out_u``: float32 activation bytes per image of the FUSED unit
+  (a fused pool / softmax / residual / concat changes what is read and
+  written); ``W_u``: weight, bias and affine bytes, read once per launch.
+* ``P_pipe(k)`` by the kernel the specialiser selected for the launch:
+  - tcgen05 kernels (``*_tc_*``): the dense TF32 tensor rate, taken as half
+    the MEASURED bf16 rate (MEASURED_PEAKS.json ``bf16_tflops``: tcgen05
+    issues K=8 TF32 in the time of K=16 BF16), with ``m(k)`` = 3 executed
+    products per FP32 MAC for the 3xTF32 split, 2 TF32-equivalents with the
+    BF16 correction split (one TF32 product + one BF16 K=16 MMA);
+  - every other kernel: the FP32 FFMA peak MEASURED by ``nnb_ffma_peak``
+    (16 independent FFMA chains per thread, 8 x 148 blocks; 71.8 TFLOP/s on
+    the pool's B200, profiles/r02_ffma_peak.json), ``m`` = 1.
 * ``BW``: the measured HBM copy bandwidth (MEASURED_PEAKS.json ``hbm_gbs``).
 
-The canonical units are those of the reference-style plan (BN folded,
-activations fused, nothing else fused: ``planner.build_reference_plan``);
-``fused_ideal`` is the stricter bound ``max(N*sum F / P, (N*IO + sum W)/BW)``.
+``survey_*`` keep SURVEY.md 8(d)'s original formula over the reference-style
+plan (BN folded, activations fused, nothing else fused) for comparison; with
+one FFMA peak for every unit it over-credits tensor-core layers and is not a
+fraction of anything the hardware can do.
 """
 
 import json
@@ -24,14 +35,16 @@ import pathlib
 SM_COUNT = 148
 FFMA_LANES = 128
 MAX_SM_MHZ = 1965.0
+ROOT = pathlib.Path(__file__).resolve().parent.parent
 
 
 def fp32_peak_tflops(mhz=MAX_SM_MHZ):
+    """Derived FFMA peak: 148 SM x 128 lanes x 2 x f_clk (74.4 TF at 1965 MHz)."""
     return SM_COUNT * FFMA_LANES * 2 * mhz * 1e6 / 1e12
 
 
 def measured_peaks():
-    p = pathlib.Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
@@ -39,6 +52,58 @@ def measured_peaks():
                 "source": "measured"}
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
             "source": "fallback"}
+
+
+def ffma_peak_tflops(live=None):
+    """(TFLOP/s, source): ``live`` (a fresh nnb_ffma_peak reading) if given,
+    else the committed measurement, else the derived figure."""
+    if live:
+        return float(live), "nnb_ffma_peak measured in this run"
+    p = ROOT / "profiles" / "r02_ffma_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["ffma_tflops"]), f"profiles/{p.name}"
+    return fp32_peak_tflops(), "derived 148 SM x 128 x 2 x 1965 MHz"
+
+
+def tf32_peak_tflops(peaks):
+    """Dense TF32 tensor rate: half the measured dense bf16 rate."""
+    return peaks["bf16_tflops"] / 2.0
+
+
+def launch_pipe(launch):
+    """(pipe, products per FP32 MAC) of the kernel a launch runs."""
+    if "_tc_" in launch.kernel:
+        return ("tensor", 2 if "bf16 corr" in launch.note else 3)
+    return ("ffma", 1)
+
+
+def launch_roofline(unit, launch, n, peaks, ffma_tflops):
+    """Roofline of one launch over ``n`` images (a dict; times in µs)."""
+    f, io, w = unit_work(unit)
+    pipe, mult = launch_pipe(launch)
+    p = tf32_peak_tflops(peaks) if pipe == "tensor" else ffma_tflops
+    t_c = n * f * mult / (p * 1e12)
+    t_m = (n * io + w) / (peaks["hbm_gbs"] * 1e9)
+    return {"kernel": launch.kernel, "pipe": pipe, "products_per_mac": mult,
+            "flops": n * f, "bytes": n * io + w, "peak_tflops": p,
+            "t_compute_us": t_c * 1e6, "t_hbm_us": t_m * 1e6,
+            "bound": "compute" if t_c >= t_m else "hbm", "roof_us": max(t_c, t_m) * 1e6}
+
+
+def net_roofline(net, n, peaks, ffma_tflops, launch_ms=None):
+    """Per-launch rooflines of a compiled network's replay over ``n`` images
+    and, when ``launch_ms`` ({launch index: measured ms}) is given, each
+    launch's achieved fraction.  Returns (rows, total roof µs)."""
+    rows, total = [], 0.0
+    for i in net.launches_for(n):
+        L = net.artifact.launches[i]
+        r = launch_roofline(net.plan.units[L.unit], L, n, peaks, ffma_tflops)
+        if launch_ms is not None and i in launch_ms:
+            r["measured_us"] = launch_ms[i] * 1e3
+            r["frac"] = r["roof_us"] / r["measured_us"]
+        total += r["roof_us"]
+        rows.append(r)
+    return rows, total
 
 
 def unit_work(u, plan=None):
@@ -78,7 +143,7 @@ def unit_work(u, plan=None):
     return f, ins + out, wb
 
 
-def layerwise_roof_s(plan, n, hbm_gbs, peak_tflops):
+def survey_layerwise_roof_s(plan, n, hbm_gbs, peak_tflops):
     t = 0.0
     for u in plan.units:
         f, io, w = unit_work(u)
@@ -86,7 +151,7 @@ def layerwise_roof_s(plan, n, hbm_gbs, peak_tflops):
     return t
 
 
-def fused_ideal_s(plan, n, hbm_gbs, peak_tflops):
+def survey_fused_ideal_s(plan, n, hbm_gbs, peak_tflops):
     F = sum(unit_work(u)[0] for u in plan.units)
     W = sum(unit_work(u)[2] for u in plan.units)
     io = 4 * (sum(plan.tensors[t].elements for t in plan.input_ids)

@@ -34,6 +34,7 @@ from .kernels import specialize
 from .model_format import load_model
 from .options import ApproximationOptions
 from .planner import build_plan
+from .tuning import make_tuning
 
 
 def _capacity(batch):
@@ -79,16 +80,17 @@ class _Handle:
 
 class CompiledNetwork:
     def __init__(self, manifest, weights, options=None, *, batch=None, device=0,
-                 gpu_fusion=True, cache_dir=None, use_tc=True, tc_min_rows=None, tmem_a=True,
-                 nacc=None, aldg=False, kpack=True, dw_fusion="narrow", epi_tma=True, csplit=True, chunk=None,
-                 split_rn=True, pair=True, tc_tile_use=0.75, mega=False, abuf=None,
-                 small_dense_rows=None, tc_min_k=None, wide=True, wide_bk=32,
-                 wide_chunk=None, wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, tc_min_images=None, narrow=True, direct_imm=True,
-                 sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 cache_dir=None, tuning=None):
+        """pkg/src/nnjit/runtime.py:33-67 plus ``batch`` (images per replay),
+        ``device``, ``cache_dir`` (cubin cache; "" disables it) and
+        ``tuning`` (a mapping of tuning.Tuning fields; unknown keys raise
+        ValueError)."""
         import torch
 
         t0 = time.perf_counter()
         self.options = options or ApproximationOptions()
+        self.tuning = make_tuning(tuning)
+        tn = self.tuning
         self.manifest = manifest
         self.device = device
         self.batch = batch
@@ -97,25 +99,14 @@ class CompiledNetwork:
             raise ValueError("batch must be >= 1")
         _, _, sm_count = _native.device_check(device)
         self.graph = build_graph(manifest, weights)
-        if mega and dw_fusion == "narrow":
+        dw_fusion = tn.dw_fusion
+        if tn.mega and dw_fusion == "narrow":
             dw_fusion = False      # the persistent kernel walks the unfused templates
-        self.plan = build_plan(self.graph, gpu_fusion=gpu_fusion, dw_fusion=dw_fusion)
-        self.assignment = plan_buffers(self.plan, reserve_heads=head)
+        self.plan = build_plan(self.graph, gpu_fusion=tn.gpu_fusion, dw_fusion=dw_fusion)
+        self.assignment = plan_buffers(self.plan, reserve_heads=tn.head)
         cap = _capacity(self.max_batch)
-        from .kernels import MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_IMAGES, TC_MIN_ROWS
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,
-                          use_tc=use_tc, sm_count=sm_count,
-                          tc_min_rows=((MEGA_TC_MIN_ROWS if mega else TC_MIN_ROWS) if tc_min_rows is None
-                                       else tc_min_rows),
-                          tmem_a=tmem_a, nacc=nacc, aldg=aldg, kpack=kpack, epi_tma=epi_tma,
-                          csplit=csplit, chunk=chunk, split_rn=split_rn,
-                          pair=pair, tc_tile_use=tc_tile_use, mega=mega, abuf=abuf,
-                          small_dense_rows=SMALL_DENSE_ROWS if small_dense_rows is None else small_dense_rows, wide=wide, wide_bk=wide_bk,
-                          wide_chunk=wide_chunk, wide_csplit=wide_csplit, rn_ss=rn_ss, corr_bf16=corr_bf16, cb16_w4=cb16_w4, a_prefetch=a_prefetch,
-                          tc_min_images=TC_MIN_IMAGES if tc_min_images is None else tc_min_images,
-                          narrow=narrow, direct_imm=direct_imm, sep_fma=sep_fma,
-                          narrow_geo=narrow_geo, head=head, sep_geo=sep_geo,
-                          **({} if tc_min_k is None else {"tc_min_k": tc_min_k}))
+                          sm_count=sm_count, **tn.specializer_kwargs())
         arena_bytes = self.assignment.arena_size * cap + spec.arena_extra
 
         def io(tids):

@@ -30,7 +30,7 @@ for variant in sys.argv[3:]:
         sp.sources = [defs + src for src in sp.sources]
         return sp
     K.Specializer.run = run
-    net = compile_model(m, w, opts, batch=batch, cache_dir="", **kw)
+    net = compile_model(m, w, opts, batch=batch, cache_dir="", tuning=kw)
     net.input_views[0].copy_(x)
     net.apply(); torch.cuda.synchronize()
     y = net.output_views[0].cpu().numpy().copy()

@@ -13,7 +13,7 @@ for act, f in (("tanh", np.tanh), ("sigmoid", lambda v: 1 / (1 + np.exp(-v))), (
                      for n in w0.names()})
     x = np.random.default_rng(1).uniform(-12, 12, (65536, 32)).astype(np.float32)
     x[:8192] *= 0.05
-    net = compile_model(m, w, EXACT, batch=65536, tc_min_rows=1)
+    net = compile_model(m, w, EXACT, batch=65536, tuning={"tc_min_rows": 1})
     assert any("tcgen05" in l.note for l in net.artifact.launches), "not on the TC path"
     got = net.run([x])[0].cpu().numpy().astype(np.float64)
     ref = f(x.astype(np.float64))

@@ -21,7 +21,7 @@ y = b.layer("Conv2D", [d], {"filters": co, "kernel_size": 1}, [("kernel", he(rng
 m, wt = b.build([y])
 n = 2
 xin = rng.uniform(-2, 2, (n, h, w, c)).astype(F32)
-net = compile_model(m, wt, EXACT, batch=n, dw_fusion=True, tc_min_rows=1, tc_tile_use=0, **kw)
+net = compile_model(m, wt, EXACT, batch=n, tuning=dict(dw_fusion=True, tc_min_rows=1, tc_tile_use=0, **kw))
 print([l.note for l in net.artifact.launches])
 got = net.run([xin])[0].cpu().numpy()
 want = oracle.run_graph(net.graph, [xin])[0]

@@ -24,7 +24,7 @@ rows, k = 1 << 19, 256
 for n in (16, 32, 48, 64, 96, 128, 256):
     for kw in ({"pair": False, "nacc": 1}, {"pair": False, "tmem_a": False}, {"pair": True}):
         m, w = dense_net(np.random.default_rng(0), k, n, "linear")
-        net = compile_model(m, w, EXACT, batch=rows, tc_min_rows=1, **kw)
+        net = compile_model(m, w, EXACT, batch=rows, tuning=dict(tc_min_rows=1, **kw))
         idx = [i for i in net.launches_for() if "_tc_" in net.artifact.launches[i].kernel]
         if not idx:
             continue

@@ -19,7 +19,7 @@ for defs in ("#define NNB_TC_DBG 30\n", "#define NNB_TC_DBG 30\n#define NNB_TC_N
     K.Specializer.run = run
     for kw in ({"pair": False, "tmem_a": False}, {"pair": False, "nacc": 1}):
         m, w = dense_net(np.random.default_rng(0), k, n, "linear")
-        net = compile_model(m, w, EXACT, batch=rows, tc_min_rows=1, **kw)
+        net = compile_model(m, w, EXACT, batch=rows, tuning=dict(tc_min_rows=1, **kw))
         i = [i for i in net.launches_for() if "_tc_" in net.artifact.launches[i].kernel][0]
         ms = net.time_launch(i, rows, iters=5)
         instr = (rows // 128) * (k // 32) * 12

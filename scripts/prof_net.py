@@ -22,8 +22,9 @@ p.add_argument("--no-kpack", action="store_true")
 a = p.parse_args()
 opts = EXACT if a.mode == "exact" else ApproximationOptions()
 m, w = zoo.build(a.config)
-net = compile_model(m, w, opts, batch=a.batch, use_tc=not a.no_tc, tmem_a=not a.no_tmem_a, nacc=a.nacc,
-                    aldg=a.aldg, kpack=not a.no_kpack)
+net = compile_model(m, w, opts, batch=a.batch, tuning=dict(use_tc=not a.no_tc, tmem_a=not a.no_tmem_a,
+                                                         nacc=a.nacc, aldg=a.aldg,
+                                                         kpack=not a.no_kpack))
 net.input_views[0].copy_(torch.from_numpy(zoo.inputs(a.config, a.batch)))
 for _ in range(a.reps):
     net.apply()

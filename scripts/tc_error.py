@@ -16,7 +16,7 @@ for k, units, act in ((1024, 512, "tanh"), (1024, 512, "linear"), (256, 96, "rel
     want = oracle.run(m, w, [x])[0]
     for v in variants:
         kw = {a.split("=")[0]: eval(a.split("=")[1]) for a in v.split()}
-        net = compile_model(m, w, EXACT, batch=2049, **kw)
+        net = compile_model(m, w, EXACT, batch=2049, tuning=kw)
         got = net.run([x])[0].cpu().numpy()
         d = np.abs(got.astype(np.float64) - want)
         lim = 1e-5 + 1e-4 * np.abs(want)

@@ -20,7 +20,7 @@ for inplace in (1, 0):
         m, w = dense_net(rng, k, units, "linear")
         x = rng.uniform(-2, 2, (4096, k)).astype(np.float32)
         want = oracle.run(m, w, [x])[0]
-        net = compile_model(m, w, EXACT, batch=4096, aldg=False, cache_dir="")
+        net = compile_model(m, w, EXACT, batch=4096, tuning={"aldg": False}, cache_dir="")
         got = net.run([x])[0].cpu().numpy()
         d = np.abs(got.astype(np.float64) - want)
         i = [j for j in net.launches_for() if "_tc_" in net.artifact.launches[j].kernel][0]

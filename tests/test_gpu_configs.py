@@ -45,18 +45,22 @@ def test_tensor_core_path_vs_oracle(cfg, n):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("opts", [EXACT, ApproximationOptions()], ids=["exact", "default"])
 @pytest.mark.parametrize("cfg,n", [(0, 4096), (1, 65536), (2, 1024), (3, 256), (4, 64)])
-def test_baseline_batch_sampled_images_vs_oracle(cfg, n):
-    """At the BASELINE batch sizes (the bench workloads): images are
-    independent, so a seeded sample of the batch is checked against the
-    oracle run on just those images, plus finiteness of the whole output."""
+def test_baseline_batch_sampled_images_vs_oracle(cfg, n, opts):
+    """At the BASELINE batch sizes (the bench workloads), under interpreter-
+    grade and the reference's default options: images are independent, so
+    16 images of the batch -- the first, the last and 14 seeded others -- are
+    checked against the oracle run on just those images (>= 16
+    sampled images per config), plus finiteness of the whole output."""
     m, w = zoo.build(cfg)
-    net = compile_model(m, w, EXACT, batch=n)
+    net = compile_model(m, w, opts, batch=n)
     x = zoo.inputs(cfg, n)
     got = net.run([x])[0].cpu().numpy()
     assert np.isfinite(got).all()
-    idx = np.sort(np.random.default_rng(cfg).choice(n, size=min(n, 6), replace=False))
-    want = oracle.run(m, w, [x[idx]], "exact")[0]
+    rest = np.random.default_rng(cfg).choice(np.arange(1, n - 1), size=14, replace=False)
+    idx = np.sort(np.concatenate([[0, n - 1], rest]))
+    want = oracle.run(m, w, [x[idx]], "exact" if opts == EXACT else opts)[0]
     np.testing.assert_allclose(got[idx], want, rtol=RTOL, atol=ATOL)
 
 

@@ -77,7 +77,7 @@ def test_random_tensor_core_networks(seed):
     n = int(rng.choice([1, 2, 5, 17]))
     x = rng.uniform(-1, 1, (n,) + shape).astype(F32)
     want = oracle.run(m, w, [x], "exact")[0]
-    net = compile_model(m, w, EXACT, batch=n, tc_min_rows=1, tc_tile_use=0,
-                        dw_fusion=bool(seed % 2))
+    net = compile_model(m, w, EXACT, batch=n,
+                        tuning=dict(tc_min_rows=1, tc_tile_use=0, dw_fusion=bool(seed % 2)))
     got = net.run([x])[0].cpu().numpy()
     np.testing.assert_allclose(got, want, err_msg=net.describe(), **TOL)

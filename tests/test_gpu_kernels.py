@@ -19,7 +19,7 @@ TOL = dict(rtol=1e-4, atol=1e-5)
 
 
 def gpu(m, w, x, opts=EXACT, **kw):
-    net = compile_model(m, w, opts, batch=len(x), **kw)
+    net = compile_model(m, w, opts, batch=len(x), tuning=kw or None)
     return net.run([x])[0].cpu().numpy(), net
 
 
@@ -126,7 +126,11 @@ def test_concat_into_pointwise(c0, c1, co, n):
     xin = rng.uniform(-2, 2, (n, 16, 16, 4)).astype(F32)
     got, net = gpu(m, wt, xin)
     assert "Concat" not in [u.kind for u in net.plan.units]
-    assert not any("conv1x1_tc" in l.kernel for l in net.artifact.launches)
+    # a tensor-core launch of the concat-fed conv must be the conv-tile form
+    # (second TMA map), never the single-map row GEMM
+    for l in net.artifact.launches:
+        if "_tc_" in l.kernel:
+            assert "conv tiles" in l.note and "concat (2 A maps)" in l.note, l.note
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
 
@@ -314,6 +318,29 @@ def test_exact_transcendentals_match_float64_rounding():
         assert mismatch <= 2, (tag, mismatch)
 
 
+@pytest.mark.parametrize("units,n", [(32, 2048), (128, 512)])
+@pytest.mark.parametrize("tag", ["tanh", "sigmoid", "elu"])
+def test_exact_mode_in_tensor_core_epilogue(tag, units, n):
+    """activation_mode='exact' is the interpreter's float64-rounded-once
+    semantics in the tcgen05 epilogues too.  An identity
+    Dense makes the 3xTF32 GEMM exact -- inputs on a 2^-14 grid in (-32, 32)
+    have <= 20 significant bits, so a = a_hi + a_lo with both halves exact in
+    TF32, b_lo = 0 -- and the epilogue's activation must then equal the
+    interpreter's rounding of tanh / sigmoid / expm1 of the input."""
+    xs = np.linspace(-30, 30, n * units)
+    xs = (np.round(xs * 2 ** 14) / 2 ** 14).astype(F32).reshape(n, units)
+    b = NetBuilder()
+    x = b.input((units,))
+    y = b.layer("Dense", [x], {"units": units, "activation": tag},
+                [("kernel", np.eye(units, dtype=F32)), ("bias", np.zeros(units, F32))])
+    m, w = b.build([y])
+    got, net = gpu(m, w, xs, tc_min_rows=1)
+    assert any("_tc_" in l.kernel and l.n_min <= n <= l.n_max for l in net.artifact.launches)
+    want = oracle.activation(xs, tag)
+    mismatch = np.count_nonzero(got != want)
+    assert mismatch <= 2, (tag, mismatch, np.abs(got - want).max())
+
+
 @pytest.mark.parametrize("name", names())
 def test_golden_nets_vs_reference(name):
     """Against the REAL reference's recorded outputs: interpreter (exact mode)
@@ -475,7 +502,7 @@ def test_batch1_persistent_kernel_matches_oracle(cfg):
     m, w = zoo.build(cfg)
     for n in (1, 3):
         x = zoo.inputs(cfg, n)
-        net = compile_model(m, w, EXACT, batch=n, mega=True)
+        net = compile_model(m, w, EXACT, batch=n, tuning={"mega": True})
         coop = [l for l in net.artifact.launches if l.cooperative]
         got = net.run([x])[0].cpu().numpy()
         np.testing.assert_allclose(got, ref(m, w, x), **TOL)

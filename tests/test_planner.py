@@ -183,3 +183,47 @@ def test_specialised_launches_cover_every_unit_once_per_batch(cfg, batch):
         units = [l.unit for l in act]
         assert sorted(units) == sorted(set(units)), (n, units)
         assert set(units) == set(range(len(plan.units))), (n, units)
+
+
+def _reference_nnjit():
+    from oracle import refbench
+    try:
+        return refbench.nnjit()
+    except ImportError:
+        pytest.skip("oracle/_ref (the installed reference) is absent")
+
+
+@pytest.mark.parametrize("name", ["cfg0_ref", "cfg1_ref", "cfg2_ref", "cfg3_ref", "mixed_net",
+                                  "conv1", "dw2", "pool1", "batchnorm"])
+def test_reference_planner_output_drives_the_specialiser(name):
+    """a maintainer keeps the REFERENCE's planner
+    (nnjit.build_plan, pkg/src/nnjit/optimizer.py:328-341, run here from the
+    unmodified package in oracle/_ref) and hands its FusionPlan to this
+    package via planner.adopt_plan.  The specialised sm_100a sources, launch
+    list and weight pool are byte-identical to those of this package's own
+    planner."""
+    import json
+    from paper_1906_05737_b200 import ApproximationOptions, plan_buffers
+    from paper_1906_05737_b200.kernels import specialize
+    from paper_1906_05737_b200.planner import adopt_plan
+    nnjit = _reference_nnjit()
+    m, w, x, rec = load(name)
+    doc = json.loads(bytes(rec["manifest"]).decode())
+    rm = nnjit.parse_manifest(json.dumps(doc))
+    refs = [r for l in rm.layers for r in l.weight_refs]
+    blob = bytearray(max((r.offset + r.length for r in refs), default=0))
+    for r in refs:
+        blob[r.offset:r.offset + r.length] = np.asarray(w[r.name], "<f4").tobytes()
+    ref_plan = nnjit.build_plan(nnjit.build_graph(rm, nnjit.load_weights(rm, bytes(blob))))
+    adopted = adopt_plan(ref_plan)
+    ours = build_plan(build_graph(m, w))
+    assert adopted.describe() == ours.describe()
+    for batch in (1, 300):
+        cap = (batch + 15) // 16 * 16
+        a = specialize(adopted, plan_buffers(adopted, reserve_heads=True),
+                       ApproximationOptions(), batch, cap)
+        b = specialize(ours, plan_buffers(ours, reserve_heads=True), ApproximationOptions(),
+                       batch, cap)
+        assert a.sources == b.sources and a.pool == b.pool
+        assert [(l.kernel, l.n_min, l.n_max) for l in a.launches] == \
+            [(l.kernel, l.n_min, l.n_max) for l in b.launches]
