@@ -1249,9 +1249,13 @@ struct GemmTc {
         const float* res = at<float>(arena, C::RES_OFF);
         if constexpr (HEAD) {
 #pragma unroll
-          for (int i = 0; i < EPI_COLS; ++i) {
-            const int col = cbeg + i < C::N ? cbeg + i : C::N - 1;
-            run[i] = finish<C::ACT, EMODE, C::POST>(run[i] + __ldg(bias + col), ps, po, col);
+          for (int i = 0; i < EPI_COLS; i += 2) {
+            const int c0 = cbeg + i < C::N ? cbeg + i : C::N - 1;
+            const int c1 = cbeg + i + 1 < C::N ? cbeg + i + 1 : C::N - 1;
+            const float2 y = finish2<C::ACT, EMODE, C::POST>(
+                make_float2(run[i] + __ldg(bias + c0), run[i + 1] + __ldg(bias + c1)), ps, po, c0, c1);
+            run[i] = y.x;
+            run[i + 1] = y.y;
           }
           float hp[C::HN];
           float* xch = reinterpret_cast<float*>(epi_stage + (ew & 3) * NBUF * 128);   // [HN][32]
@@ -1293,6 +1297,18 @@ struct GemmTc {
           const int col0 = nb * C::BN + cbeg + g * 16;
           if (cbeg + g * 16 >= C::BN || col0 >= C::N) continue;   // warp-uniform
           float* v = run + g * 16;
+          if constexpr (paired_act<C::ACT, EMODE>() && !C::POOL) {
+            // two columns per f32x2 instruction (nnb_common.cuh finish2)
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const int c0 = col0 + i < C::N ? col0 + i : C::N - 1;
+              const int c1 = col0 + i + 1 < C::N ? col0 + i + 1 : C::N - 1;
+              float2 y = make_float2(v[i] + __ldg(bias + c0), v[i + 1] + __ldg(bias + c1));
+              if (!(NNB_TC_DBG & 32)) y = finish2<C::ACT, EMODE, C::POST>(y, ps, po, c0, c1);
+              v[i] = y.x;
+              v[i + 1] = y.y;
+            }
+          } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = col0 + i < C::N ? col0 + i : C::N - 1;
@@ -1303,6 +1319,7 @@ struct GemmTc {
               y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 16));
             }
             v[i] = y;
+          }
           }
           if constexpr (ET) {
             float4* b = ebuf + (g % NBUF) * 128;
