@@ -16,7 +16,11 @@ namespace nnb {
 
 template <class C>
 struct ConvDirect {
-  static constexpr int PY = C::POOL ? 2 : 1;
+  // PSPLIT: a 2x2 pool window is shared by two lanes (2l: top row, 2l+1:
+  // bottom row), halving the unrolled FFMAs per thread (NVRTC time) at the
+  // same instruction mix; the window max crosses lanes with one shuffle
+  static constexpr bool PSPLIT = C::POOL && C::PSPLIT;
+  static constexpr int PY = C::POOL && !PSPLIT ? 2 : 1;
   static constexpr int PX = C::POOL ? 2 : C::PXT;
   static constexpr int NP = PY * PX;
   static constexpr int CV = (C::CI % 4 == 0) ? 4 : 1;        // channels per load
@@ -47,13 +51,15 @@ struct ConvDirect {
     i64 imgp[NP];
     bool live[NP];
     if (C::POOL) {
-      const bool ok = cell < (i64)n * CELLS_Y * CELLS_X;
-      const int cx = (int)(cell % CELLS_X);
-      const int cy = (int)((cell / CELLS_X) % CELLS_Y);
-      const i64 img = ok ? cell / ((i64)CELLS_X * CELLS_Y) : 0;
+      const int half = PSPLIT ? (int)(cell & 1) : 0;
+      const i64 win = PSPLIT ? cell >> 1 : cell;
+      const bool ok = win < (i64)n * CELLS_Y * CELLS_X;
+      const int cx = (int)(win % CELLS_X);
+      const int cy = (int)((win / CELLS_X) % CELLS_Y);
+      const i64 img = ok ? win / ((i64)CELLS_X * CELLS_Y) : 0;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        oyp[p] = cy * PY + p / PX;
+        oyp[p] = cy * 2 + (PSPLIT ? half : p / PX);
         oxp[p] = cx * PX + p % PX;
         imgp[p] = img;
         live[p] = ok;
@@ -165,6 +171,35 @@ struct ConvDirect {
 #pragma unroll
       for (int o = 0; o < C::CO; ++o) acc[p][o] = finish<C::ACT, C::MODE, C::POST>(acc[p][o], ps, po, o);
 
+    if (PSPLIT) {
+      // both lanes of a window are live or neither (the early return above
+      // is per window), so the pair exchange needs no full-warp mask
+      const unsigned mask = __activemask();
+      float* dst = at<float>(arena, C::OUT_OFF + imgp[0] * C::OUT_IMG) +
+                   ((i64)(oyp[0] / 2) * C::PWO + oxp[0] / 2) * C::CO;
+      const bool top = (oyp[0] & 1) == 0;
+#pragma unroll
+      for (int o = 0; o < C::CO; o += 4) {
+        float m4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (o + i < C::CO) {
+            const float m = fmaxf(acc[0][o + i], acc[1][o + i]);
+            m4[i] = fmaxf(m, __shfl_xor_sync(mask, m, 1));
+          }
+        }
+        if (top) {
+          if (C::CO % 4 == 0) {
+            *reinterpret_cast<float4*>(dst + o) = make_float4(m4[0], m4[1], m4[2], m4[3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (o + i < C::CO) dst[o + i] = m4[i];
+          }
+        }
+      }
+      return;
+    }
     if (C::POOL) {
       float* dst = at<float>(arena, C::OUT_OFF + imgp[0] * C::OUT_IMG) +
                    ((i64)(oyp[0] / 2) * C::PWO + oxp[0] / 2) * C::CO;

@@ -61,6 +61,7 @@ SEP_BLOCK = 128
 # many unrolled FFMAs per thread (KH*KW*CI*CO*pixels); beyond it shared-memory
 # weights and a rolled kernel-row loop keep NVRTC under the compile budget
 DIRECT_UNROLL_MAX = 2048
+DIRECT_SPLIT_MAX = 2304   # ... and with a pool window split over two lanes
 
 
 @dataclass
@@ -893,10 +894,19 @@ class Specializer:
         # kernel-row loop stays rolled (compile-time bound, see DESIGN)
         np_ = 4 if pool_fused else pxt
         unrolled = KH * KW * CI * CO * np_
-        wimm = bool(self.direct_imm) and unrolled <= DIRECT_UNROLL_MAX
+        # a pool window split over two lanes halves the unrolled body (cfg0's
+        # 16x16x8 -> 16 conv: 4608 -> 2304 FFMAs, immediates kept: 88 -> ~53 us
+        # at 4096 images against the shared-memory form)
+        psplit = bool(pool_fused and unrolled > DIRECT_UNROLL_MAX
+                      and unrolled // 2 <= DIRECT_SPLIT_MAX)
+        if psplit:
+            unrolled //= 2
+        wimm = bool(self.direct_imm) and unrolled <= (DIRECT_SPLIT_MAX if psplit
+                                                      else DIRECT_UNROLL_MAX)
         if self.direct_imm == "force":
             wimm = True
         fields["WIMM"] = wimm
+        fields["PSPLIT"] = psplit
         roll = 0
         if not wimm and unrolled > DIRECT_UNROLL_MAX and KH > 1:
             roll = 1 if unrolled // KH <= DIRECT_UNROLL_MAX // 2 else 2
@@ -904,12 +914,14 @@ class Specializer:
         code = _imm_tables(wt=wmat, bias=u.bias) if wimm else ""
         # pool: one 2x2 window per thread; else pxt pixels per thread, the
         # 128-thread block covering 128*pxt consecutive pixels
-        ipi, ipb = (PHO * PWO, 128) if pool_fused else (HO * WO, 128 * pxt)
+        ipi, ipb = ((PHO * PWO * (2 if psplit else 1), 128) if pool_fused
+                    else (HO * WO, 128 * pxt))
         smem = 4 * ((4 if wimm else KH * KW * CI * CO) + CO)
         self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, ipi, ipb,
                   dynamic_smem=True, n_min=n_min, code=code,
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
-                       f"{4 if pool_fused else pxt}")
+                       f"{(2 if psplit else 4) if pool_fused else pxt}"
+                       f"{' weights as immediates' if wimm else ' weights in smem'}")
 
     def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None, n_min=1):
         """Split-K GEMV/GEMM for few rows: Dense at n <= n_max (MB = n_max

@@ -51,15 +51,27 @@ def test_cold_compile_within_budget(cfg, big):
 
 
 def test_direct_conv_is_not_fully_unrolled_beyond_the_budget():
-    """cfg0's second conv (16x16x8 -> 16, 2x2 pool) has 4608 unrolled FFMAs
-    per thread with immediates; above DIRECT_UNROLL_MAX the taps loop stays
-    rolled over shared-memory weights."""
+    """cfg0's second conv (16x16x8 -> 16, 2x2 pool) would unroll 4608 FFMAs
+    per thread with one pool window per thread; split over two lanes
+    (PSPLIT) it unrolls 2304 and keeps its weights as immediates.  A direct
+    conv beyond both bounds keeps its taps loop rolled over shared-memory
+    weights."""
     from paper_1906_05737_b200 import kernels
     m, w = zoo.build(0)
     plan = build_plan(build_graph(m, w))
     spec = specialize(plan, plan_buffers(plan, reserve_heads=True), EXACT, 1, 16)
     src = spec.sources[spec.kernel_source[spec.kernel_names.index("nnb_u01_conv3x3_direct_1")]]
-    assert "ROLL_KY = 2LL" in src and "WIMM = 0LL" in src
+    assert "PSPLIT = 1LL" in src and "WIMM = 1LL" in src and "ROLL_KY = 0LL" in src
     stem = spec.sources[spec.kernel_source[0]]
     assert "WIMM = 1LL" in stem and "__device__ const float nnb_Cfg_0_wt" in stem
     assert kernels.DIRECT_UNROLL_MAX >= 3 * 3 * 1 * 8 * 4
+    # a larger direct conv (5x5, CI 4 -> CO 32: 3200 FFMAs, no pool to split)
+    # keeps its taps loop rolled
+    from paper_1906_05737_b200.zoo import NetBuilder
+    b = NetBuilder()
+    x = b.input((16, 16, 4))
+    y = b.conv(x, 4, 32, k=5)
+    plan = build_plan(build_graph(*b.build([y])))
+    spec = specialize(plan, plan_buffers(plan), EXACT, 1, 16)
+    src = spec.sources[spec.kernel_source[0]]
+    assert "WIMM = 0LL" in src and "ROLL_KY = 0LL" not in src
