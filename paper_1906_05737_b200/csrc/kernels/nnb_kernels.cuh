@@ -9,3 +9,4 @@
 #include "nnb_sep.cuh"
 #include "nnb_gemm_tc.cuh"
 #include "nnb_conv_direct.cuh"
+#include "nnb_chain.cuh"

@@ -945,6 +945,64 @@ class Specializer:
                   32 * KS, 0, rows, MB, grid_mult=nj, n_min=n_min, n_max=n_max,
                   note=f"split-K rows K={K} N={CO} ks={KS} rows/block {MB}")
 
+    def chain(self, pos, u):
+        """A run of small depthwise / pointwise convs (+ closing global average
+        pool) in one kernel, one CTA per image (nnb_chain.cuh,
+        planner.fuse_chain).  The generated ``body`` calls one step template
+        per layer over shared-memory ping-pong buffers."""
+        from .planner import CHAIN_THREADS, chain_bytes, chain_pw_tile
+        steps = u.steps
+        h, w, c = steps[0].input_shapes[0].dims
+        structs, calls = [], [f"    nnb::chain_stage<{h}, {w}, {c}>(src, x);",
+                               "    __syncthreads();"]
+        cur, flops = "x", 0
+        for i, st in enumerate(steps):
+            if st.kind == "Pool":                         # closing GAP
+                ih, iw, ic = st.input_shapes[0].dims
+                calls.append(f"    nnb::chain_gap<{ih * iw}, {ic}>({cur}, dst);")
+                break
+            nxt = "ab"[i % 2]
+            ep = self.epilogue_fields(st, st.output_shape.c)
+            if st.kind == "DepthwiseConv2D":
+                H, W, C = st.input_shapes[0].dims
+                HO, WO, _ = st.output_shape.dims
+                KH, KW = st.kernel_hw
+                PT = same_padding(H, KH, st.stride)[0] if st.padding == "same" else 0
+                PL = same_padding(W, KW, st.stride)[0] if st.padding == "same" else 0
+                f = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=st.stride, PT=PT, PL=PL,
+                         W_OFF=self.pool.add(st.kernel), B_OFF=self.pool.add(st.bias), **ep)
+                tmpl = "ChainDw"
+            else:
+                HO, WO, CO = st.output_shape.dims
+                CI = st.input_shapes[0].c
+                tp, tc = chain_pw_tile(HO * WO, CO)
+                f = dict(P=HO * WO, CI=CI, CO=CO, TP=tp, TC=tc,
+                         W_OFF=self.pool.add(np.asarray(st.kernel, F32).reshape(CI, CO)),
+                         B_OFF=self.pool.add(st.bias), **ep)
+                tmpl = "ChainPw"
+            structs.append(_cfg_struct(f"S{i}", f).replace("\n", "\n  "))
+            calls += [f"    nnb::{tmpl}<S{i}>::run(pool, {cur}, {nxt});", "    __syncthreads();"]
+            cur = nxt
+            if i == len(steps) - 1:
+                oh, ow, oc = st.output_shape.dims
+                calls.append(f"    nnb::chain_store<{oh * ow}, {oc}>({cur}, dst);")
+        code = "\n".join(["  " + x for x in structs] + [
+            "  __device__ static __forceinline__ void body(const float* __restrict__ pool, "
+            "const float* __restrict__ src, float* __restrict__ dst, float* x, float* a, float* b) {"]
+            + calls + ["  }"])
+        x_floats = chain_bytes(steps[0].input_shapes[0]) // 4
+        ab_floats = max(chain_bytes(st.output_shape) for st in steps[:-1]) // 4
+        fields = dict(IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                      X_FLOATS=x_floats, AB_FLOATS=ab_floats)
+        smem = 4 * (x_floats + 2 * ab_floats)
+        kinds = "".join("d" if st.kind == "DepthwiseConv2D" else "p" if st.kind == "Conv2D"
+                        else "g" for st in steps)
+        self.emit(pos, "chain", "nnb::Chain", fields, CHAIN_THREADS, smem, 1, 1,
+                  dynamic_smem=True, code=code,
+                  note=f"chain of {len(steps)} steps ({kinds}) {steps[0].input_shapes[0]} -> "
+                       f"{u.output_shape}, one CTA per image, {smem // 1024} KB shared")
+
     def depthwise(self, pos, u):
         H, W, C = u.input_shapes[0].dims
         HO, WO, _ = u.output_shape.dims
@@ -1104,6 +1162,8 @@ class Specializer:
                 self.concat(pos, u)
             elif u.kind == "Pad":
                 self.pad(pos, u)
+            elif u.kind == "Chain":
+                self.chain(pos, u)
             else:
                 raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
         self._n_cap = None

@@ -74,6 +74,7 @@ class CompilationUnit:
     pre_up_shape: object = None     # output shape before the fused upsampling
     concat_in: bool = False         # conv reads the channel concat of input_ids
     dw: object = None               # fused depthwise producer (a CompilationUnit)
+    steps: list = None              # Chain: the fused units, in order
 
     def describe(self):
         bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
@@ -96,6 +97,10 @@ class CompilationUnit:
             bits.append(f"+upsample{self.upsample_after}")
         if self.concat_in:
             bits.append("concat-loader")
+        if self.steps:
+            bits.append("[" + " | ".join(
+                f"{st.kind}{'%dx%d/s%d' % (*st.kernel_hw, st.stride) if st.kernel_hw else ''}"
+                f"->{st.output_shape}" for st in self.steps) + "]")
         if self.dw is not None:
             kh, kw = self.dw.kernel_hw
             bits.append(f"dw{kh}x{kw}/s{self.dw.stride}-loader"
@@ -541,7 +546,123 @@ def fuse_dw_pw(plan, narrow_only=False):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion="narrow"):
+# ---------------------------------------------------------------------------
+# layer chains: a run of small depthwise / pointwise layers in one kernel
+
+CHAIN_THREADS = 256          # nnb_chain.cuh block size
+CHAIN_SMEM_MAX = 200 * 1024  # staged input + two activation buffers per CTA
+CHAIN_MIN_STEPS = 4
+
+
+def chain_stride(pixels):
+    """Channel stride (floats) of a channel-major activation in the chain's
+    shared memory: odd, so lanes reading different channels of one pixel hit
+    different banks."""
+    return pixels | 1
+
+
+def chain_bytes(shape):
+    h, w, c = shape.dims
+    return 4 * chain_stride(h * w) * c
+
+
+def chain_pw_tile(pixels, co):
+    """(TP pixels, TC channels) per thread of a chain pointwise step with
+    CHAIN_THREADS threads covering pixels x co outputs, or None."""
+    e = pixels * co
+    if e % CHAIN_THREADS:
+        return None
+    e //= CHAIN_THREADS
+    for tc in (8, 4):
+        if e % tc == 0 and co % tc == 0:
+            tp = e // tc
+            if 1 <= tp <= 8 and pixels % tp == 0:
+                return tp, tc
+    return None
+
+
+def _chain_step_ok(u):
+    if (u.residual_id is not None or u.pool_after or u.upsample_after != 1 or u.softmax_after
+            or u.concat_in or u.dw is not None or u.scale is not None or u.steps
+            or len(u.input_ids) != 1 or u.input_shapes[0].rank != 3):
+        return False
+    if u.kind == "DepthwiseConv2D":
+        return u.kernel_hw[0] <= 5 and u.kernel_hw[1] <= 5
+    if u.kind == "Conv2D":
+        h, w, co = u.output_shape.dims
+        return (u.kernel_hw == (1, 1) and u.stride == 1
+                and chain_pw_tile(h * w, co) is not None)
+    return False
+
+
+def _chain_gap(u):
+    """A global average pool (GlobalAveragePooling2D / AvgPool2D over the
+    whole map) closing a chain."""
+    x = u.input_shapes[0]
+    return (u.kind == "Pool" and u.pool_op == "avg" and x.rank == 3
+            and tuple(u.kernel_hw) == (x.h, x.w) and u.padding == "valid"
+            and u.upsample_after == 1 and u.residual_id is None)
+
+
+def chain_smem(steps):
+    """Shared bytes of a chain: its staged input and two buffers sized for
+    the largest intermediate."""
+    inner = [chain_bytes(st.output_shape) for st in steps[:-1]]
+    return chain_bytes(steps[0].input_shapes[0]) + 2 * max(inner)
+
+
+def fuse_chain(plan, smem_max=CHAIN_SMEM_MAX, min_steps=CHAIN_MIN_STEPS):
+    """Runs of depthwise and pointwise (1x1) convs over small maps -- the
+    8x8 / 4x4 tail of MobileNet-style nets, ending in an optional global
+    average pool -- become one ``Chain`` unit: one CTA per image keeps every
+    intermediate in shared memory (nnb_chain.cuh), so the run costs one
+    launch and one HBM round trip instead of one per layer.  A run starts at
+    the earliest layer whose staged input plus two intermediate buffers fit
+    ``smem_max``."""
+    pos = 0
+    while pos < len(plan.units):
+        run = [pos]
+        while (_chain_step_ok(plan.units[run[-1]]) and run[-1] + 1 < len(plan.units)):
+            nxt = plan.units[run[-1] + 1]
+            prev = plan.units[run[-1]]
+            if not (nxt.input_ids == (prev.output_id,) and _private(plan, prev.output_id)):
+                break
+            if _chain_step_ok(nxt):
+                run.append(run[-1] + 1)
+            elif _chain_gap(nxt):
+                run.append(run[-1] + 1)
+                break
+            else:
+                break
+        if not _chain_step_ok(plan.units[run[0]]):
+            pos += 1
+            continue
+        units = [plan.units[i] for i in run]
+        start = 0
+        while start + min_steps <= len(units) and chain_smem(units[start:]) > smem_max:
+            start += 1
+        units = units[start:]
+        if len(units) < min_steps or chain_smem(units) > smem_max:
+            pos = run[-1] + 1
+            continue
+        first, last = units[0], units[-1]
+        chain = CompilationUnit(uid=first.uid, kind="Chain", name=f"chain({first.name}..{last.name})",
+                                input_ids=first.input_ids, output_id=last.output_id,
+                                input_shapes=first.input_shapes, output_shape=last.output_shape,
+                                steps=units)
+        p0 = run[0] + start
+        for st in units[:-1]:
+            plan.tensors.pop(st.output_id, None)
+        for _ in units:
+            victim = plan.units.pop(p0)
+            plan.node_units = {n: (chain.uid if u == victim.uid else u)
+                               for n, u in plan.node_units.items()}
+        plan.units.insert(p0, chain)
+        pos = p0 + 1
+    return plan
+
+
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=True):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -554,11 +675,11 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow"):
     depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
-        apply_gpu_fusions(plan, dw_fusion)
+        apply_gpu_fusions(plan, dw_fusion, chain)
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow"):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=True):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -567,6 +688,8 @@ def apply_gpu_fusions(plan, dw_fusion="narrow"):
     fuse_concat(plan)
     if dw_fusion:
         fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")
+    if chain:
+        fuse_chain(plan)
     return plan
 
 
@@ -577,7 +700,7 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
                          "pool_op", "factor", "in_place_preference")
 
 
-def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow"):
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=True):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions
@@ -605,7 +728,7 @@ def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow"):
     ours = FusionPlan(units, {t: shape(s) for t, s in plan.tensors.items()},
                       tuple(plan.input_ids), tuple(plan.output_ids), dict(plan.node_units))
     if gpu_fusion:
-        apply_gpu_fusions(ours, dw_fusion)
+        apply_gpu_fusions(ours, dw_fusion, chain)
     return ours
 
 

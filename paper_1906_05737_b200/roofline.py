@@ -117,6 +117,12 @@ def unit_work(u, plan=None):
         if arr is not None:
             wb += 4 * arr.size
     k = u.kind
+    if k == "Chain":               # fused run: its steps' work, chain input + output bytes
+        f = wb = 0
+        for st in u.steps:
+            sf, _, sw = unit_work(st)
+            f, wb = f + sf, wb + sw
+        return f, ins + out, wb
     if k == "Dense":
         kin, units = u.kernel.shape
         f = 2 * kin * units

@@ -102,7 +102,8 @@ class CompiledNetwork:
         dw_fusion = tn.dw_fusion
         if tn.mega and dw_fusion == "narrow":
             dw_fusion = False      # the persistent kernel walks the unfused templates
-        self.plan = build_plan(self.graph, gpu_fusion=tn.gpu_fusion, dw_fusion=dw_fusion)
+        self.plan = build_plan(self.graph, gpu_fusion=tn.gpu_fusion, dw_fusion=dw_fusion,
+                               chain=tn.chain and not tn.mega)
         self.assignment = plan_buffers(self.plan, reserve_heads=tn.head)
         cap = _capacity(self.max_batch)
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,

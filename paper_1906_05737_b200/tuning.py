@@ -21,6 +21,7 @@ class Tuning:
     gpu_fusion: bool = True        # B200 epilogue fusions (pool, residual, softmax, upsample, concat)
     dw_fusion: object = "narrow"   # depthwise->pointwise: "narrow" (SepNarrow), True (all), False
     head: bool = True              # fuse a <=16-wide Dense head into a tcgen05 Dense epilogue
+    chain: bool = True             # small depthwise/pointwise runs as one kernel (fuse_chain)
     # -- kernel selection ----------------------------------------------------
     use_tc: bool = True            # tcgen05 3xTF32 GEMMs for Dense / 1x1 / KxK convs
     tc_min_rows: object = None     # rows per launch from which tcgen05 is used (None: kernels.TC_MIN_ROWS)
@@ -59,7 +60,7 @@ class Tuning:
         filled in where the field is None)."""
         from .kernels import (MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_IMAGES, TC_MIN_K,
                               TC_MIN_ROWS)
-        skip = {"gpu_fusion", "dw_fusion"}
+        skip = {"gpu_fusion", "dw_fusion", "chain"}
         kw = {f.name: getattr(self, f.name) for f in fields(self) if f.name not in skip}
         if kw["tc_min_rows"] is None:
             kw["tc_min_rows"] = MEGA_TC_MIN_ROWS if self.mega else TC_MIN_ROWS

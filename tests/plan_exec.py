@@ -24,6 +24,16 @@ def _post(y, u):
 def run_plan(plan, inputs):
     vals = {t: np.asarray(x, F32) for t, x in zip(plan.input_ids, inputs)}
     for u in plan.units:
+        if u.kind == "Chain":             # a run of fused units, executed in order
+            for st in u.steps:
+                _run_unit(st, vals)
+        else:
+            _run_unit(u, vals)
+    return [vals[t] for t in plan.output_ids]
+
+
+def _run_unit(u, vals):
+    if True:
         x = vals[u.input_ids[0]]
         n = x.shape[0]
         if u.kind == "Dense":
@@ -78,4 +88,3 @@ def run_plan(plan, inputs):
         if f > 1:
             y = np.repeat(np.repeat(y.reshape((n,) + u.pre_up_shape.dims), f, 1), f, 2)
         vals[u.output_id] = y.reshape((n,) + u.output_shape.dims)
-    return [vals[t] for t in plan.output_ids]

@@ -647,3 +647,56 @@ def test_fused_dense_head(k, n1, act1, n2, head, n):
     np.testing.assert_allclose(got, ref(m, w, x), **TOL)
     unf, _ = gpu(m, w, x, head=False)
     np.testing.assert_allclose(got, unf, rtol=1e-5, atol=2e-6)
+
+
+def _chain_net(rng, h, w, c, spec, gap, post_bn):
+    """input h x w x c -> layers from spec: ('p', co, act) pointwise,
+    ('d', k, s, pad, act) depthwise; optional BN after an activation
+    (post-affine) and a closing GlobalAveragePooling2D."""
+    b = NetBuilder()
+    x = b.input((h, w, c))
+    for i, st in enumerate(spec):
+        if st[0] == "p":
+            _, co, act = st
+            x = b.layer("Conv2D", [x], {"filters": co, "kernel_size": 1, "activation": act},
+                        [("kernel", he(rng, (1, 1, c, co), c)),
+                         ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+            c = co
+        else:
+            _, k, s, pad, act = st
+            x = b.layer("DepthwiseConv2D", [x], {"kernel_size": k, "strides": s, "padding": pad,
+                                                 "activation": act},
+                        [("kernel", he(rng, (k, k, c), k * k)),
+                         ("bias", (rng.standard_normal(c) * 0.1).astype(F32))])
+        if post_bn and i % 3 == 1:
+            x = b.layer("BatchNorm", [x], None, bn_params(rng, c))
+    if gap:
+        x = b.layer("GlobalAveragePooling2D", [x])
+    return b.build([x])
+
+
+@pytest.mark.parametrize("n", [1, 3, 37])
+@pytest.mark.parametrize("case", [
+    (16, 16, 32, [("p", 64, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 64, "relu"),
+                  ("d", 3, 2, "same", "relu6"), ("p", 128, "relu6"), ("d", 3, 1, "same", "linear"),
+                  ("p", 128, "relu6")], True, True),
+    (8, 8, 64, [("d", 3, 1, "same", "relu"), ("p", 64, "linear"), ("d", 5, 1, "same", "relu6"),
+                ("p", 128, "tanh"), ("d", 3, 2, "valid", "relu")], False, False),
+    (4, 4, 128, [("p", 256, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 256, "sigmoid"),
+                 ("d", 3, 1, "same", "elu")], True, True)])
+def test_chain_kernel_vs_oracle(case, n):
+    """planner.fuse_chain + nnb_chain.cuh: a run of small depthwise / pointwise
+    layers (strides, 'same' / 'valid', 5x5 taps, post-BN, closing GAP or a
+    stored map) in one CTA-per-image kernel, against the oracle."""
+    h, w, c, spec, gap, post_bn = case
+    rng = np.random.default_rng(len(spec) * 10 + c)
+    m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
+    x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
+    got, net = gpu(m, wt, x)
+    assert [u.kind for u in net.plan.units] == ["Chain"], net.plan.describe()
+    assert any("chain" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, wt, x), **TOL)
+    got2, net2 = gpu(m, wt, x, ApproximationOptions())
+    np.testing.assert_allclose(got2, ref(m, wt, x, ApproximationOptions()), **TOL)
+    unf, _ = gpu(m, wt, x, chain=False)
+    np.testing.assert_allclose(got, unf, **TOL)
