@@ -618,7 +618,14 @@ def fuse_chain(plan, smem_max=CHAIN_SMEM_MAX, min_steps=CHAIN_MIN_STEPS):
     intermediate in shared memory (nnb_chain.cuh), so the run costs one
     launch and one HBM round trip instead of one per layer.  A run starts at
     the earliest layer whose staged input plus two intermediate buffers fit
-    ``smem_max``."""
+    ``smem_max``.
+
+    Opt-in (``tuning={"chain": True}``): measured on B200 (cfg3, 20 steps from
+    16x16x32 to the GAP) 0.399 ms at 256 images and 0.199 ms at one image,
+    against 0.126 / 0.07 ms for the same layers as per-layer launches (tcgen05
+    row GEMMs + depthwise kernels).  One CTA per image is bound by its FFMA
+    issue and L2 weight-load latency (9.5 M FMA per image on one SM), where
+    the per-layer kernels spread every layer over all SMs on tensor cores."""
     pos = 0
     while pos < len(plan.units):
         run = [pos]
@@ -662,7 +669,7 @@ def fuse_chain(plan, smem_max=CHAIN_SMEM_MAX, min_steps=CHAIN_MIN_STEPS):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=True):
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -679,7 +686,7 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=True):
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow", chain=True):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -700,7 +707,7 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
                          "pool_op", "factor", "in_place_preference")
 
 
-def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=True):
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions

@@ -21,7 +21,8 @@ class Tuning:
     gpu_fusion: bool = True        # B200 epilogue fusions (pool, residual, softmax, upsample, concat)
     dw_fusion: object = "narrow"   # depthwise->pointwise: "narrow" (SepNarrow), True (all), False
     head: bool = True              # fuse a <=16-wide Dense head into a tcgen05 Dense epilogue
-    chain: bool = True             # small depthwise/pointwise runs as one kernel (fuse_chain)
+    chain: bool = False            # small depthwise/pointwise runs as one FFMA kernel (fuse_chain;
+                                   # correct, measured slower than the per-layer tcgen05 path)
     # -- kernel selection ----------------------------------------------------
     use_tc: bool = True            # tcgen05 3xTF32 GEMMs for Dense / 1x1 / KxK convs
     tc_min_rows: object = None     # rows per launch from which tcgen05 is used (None: kernels.TC_MIN_ROWS)

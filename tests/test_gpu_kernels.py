@@ -692,11 +692,11 @@ def test_chain_kernel_vs_oracle(case, n):
     rng = np.random.default_rng(len(spec) * 10 + c)
     m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
     x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
-    got, net = gpu(m, wt, x)
+    got, net = gpu(m, wt, x, chain=True)
     assert [u.kind for u in net.plan.units] == ["Chain"], net.plan.describe()
     assert any("chain" in l.kernel for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, wt, x), **TOL)
-    got2, net2 = gpu(m, wt, x, ApproximationOptions())
+    got2, net2 = gpu(m, wt, x, ApproximationOptions(), chain=True)
     np.testing.assert_allclose(got2, ref(m, wt, x, ApproximationOptions()), **TOL)
-    unf, _ = gpu(m, wt, x, chain=False)
+    unf, _ = gpu(m, wt, x)
     np.testing.assert_allclose(got, unf, **TOL)

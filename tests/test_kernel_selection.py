@@ -12,7 +12,7 @@ from paper_1906_05737_b200.kernels import (SMALL_DENSE_ROWS, TC_MIN_IMAGES, WIDE
 from paper_1906_05737_b200.planner import build_plan
 
 
-def launches(m, w, max_batch, chain=True, **kw):
+def launches(m, w, max_batch, chain=False, **kw):
     plan = build_plan(build_graph(m, w), chain=chain)
     return specialize(plan, plan_buffers(plan), EXACT, max_batch, max_batch, **kw).launches
 
@@ -47,7 +47,7 @@ def test_narrow_dense_hands_over_earlier():
 
 def test_pointwise_convs_stay_off_tensor_cores_for_a_few_images():
     m, w = zoo.build(3)                       # MobileNetV1 0.25: 1x1 convs of 16..4096 rows/image
-    ls = launches(m, w, 256, chain=False)     # (the 16x16..4x4 tail otherwise runs as a Chain)
+    ls = launches(m, w, 256)
     tc_units = {l.unit for l in ls if "_tc_" in l.kernel}
     assert tc_units
     for u in tc_units:

@@ -144,6 +144,24 @@ def test_gpu_plan_numerically_sound_on_zoo(cfg, dw_fusion):
     np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
 
 
+def test_chain_fusion_sound_and_shaped_on_cfg3():
+    """planner.fuse_chain (opt-in): cfg3's 16x16 .. 4x4 tail (20 units ending
+    in the GAP) becomes one Chain unit whose shared-memory footprint fits a
+    CTA, and the chained plan computes the unfused graph."""
+    from paper_1906_05737_b200.planner import CHAIN_SMEM_MAX, chain_smem
+    m, w = zoo.build(3)
+    g = build_graph(m, w)
+    plan = build_plan(g, chain=True)
+    chains = [u for u in plan.units if u.kind == "Chain"]
+    assert len(chains) == 1 and len(chains[0].steps) == 20
+    assert chains[0].steps[-1].kind == "Pool" and chain_smem(chains[0].steps) <= CHAIN_SMEM_MAX
+    for st in chains[0].steps[:-1]:
+        assert st.output_id not in plan.tensors          # intermediates never materialise
+    x = zoo.inputs(3, 2)
+    np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
+    assert "Chain" not in kinds(build_plan(g))          # off by default
+
+
 def test_build_plan_idempotent_and_deterministic():
     m, w = zoo.build(3)
     a, b = build_plan(build_graph(m, w)), build_plan(build_graph(m, w))
