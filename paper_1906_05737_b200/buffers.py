@@ -69,6 +69,11 @@ def _reads(u):
                                  is not None else ())
 
 
+def _writes(u):
+    dp = getattr(u, "dual_pool", None)
+    return (u.output_id,) + ((dp.output_id,) if dp is not None else ())
+
+
 def head_pairs(plan):
     """Positions of Dense units whose output feeds only the next unit, a
     Dense head with <= 16 outputs: the tcgen05 GEMM may compute that head in
@@ -95,8 +100,9 @@ def compute_lifetimes(plan, pin_inputs=True, reserve_heads=False):
         last[t] = end if pin_inputs else -1
     heads = set(head_pairs(plan)) if reserve_heads else set()
     for pos, u in enumerate(plan.units):
-        first.setdefault(u.output_id, pos)
-        last[u.output_id] = max(last.get(u.output_id, pos), pos)
+        for w in _writes(u):
+            first.setdefault(w, pos)
+            last[w] = max(last.get(w, pos), pos)
         for t in _reads(u):
             last[t] = max(last.get(t, pos), pos + 1 if pos in heads else pos)
     for t in plan.output_ids:
@@ -206,7 +212,8 @@ def verify_assignment(plan, assignment):
     for pos, u in enumerate(plan.units):
         for t in _reads(u):
             bad += check(t, f"unit {pos} ({u.kind}) read")
-        write(u.output_id)
+        for t in _writes(u):
+            write(t)
     for t in plan.output_ids:
         bad += check(t, "network output")
     end = len(plan.units)

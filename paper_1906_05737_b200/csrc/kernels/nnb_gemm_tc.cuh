@@ -532,6 +532,8 @@ struct GemmTc {
   static constexpr int CB0 = C::CONV ? C::C0 / BK : 1;      // ... from source 0
   static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % BK == 0");
   static_assert(BK == 32 || BK == 16, "K block");
+  static_assert(!C::DPOOL || (C::CONV && !C::POOL && C::UPF == 1 && (KP || C::N % 16 == 0)),
+                "dual pooled store: conv tiles");
   static_assert(!KP || (C::CONV && !C::POOL && !C::RES && C::CO % 16 == 0 &&
                         C::KW * C::CO == C::N), "KPACK geometry");
   static_assert(STAGE % 1024 == 0, "stage alignment");
@@ -569,6 +571,34 @@ struct GemmTc {
 #pragma unroll
         for (int j = 0; j < C::HN; ++j) hp[j] = fmaf(run[i], C::hw((CB + i) * C::HN + j), hp[j]);
       }
+    }
+  }
+
+  // DPOOL: second store of the 2x2/2 max-pooled tile (planner.fuse_pool_dual):
+  // the four pixels of a window sit in lanes w, w^1 (adjacent columns) and
+  // w^16, w^17 (the next image row) of one warp; the lane of the window's top-
+  // left pixel stores the NC maxima of its columns at the pooled position (and
+  // its DP_UPF x DP_UPF replicas when the pooled map is upsampled).
+  template <int NC>
+  __device__ static __forceinline__ void dual_pool_store(float* __restrict__ arena, const float* v,
+                                                         bool lead, int img, int oy, int ox,
+                                                         int cofs, int n) {
+    float m[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const float a = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
+      m[i] = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, 16));
+    }
+    const int py = oy >> 1, px = ox >> 1;
+    if (!(lead && img < n && py < C::DP_PHO && px < C::DP_PWO)) return;
+    constexpr int U = C::DP_UPF, WU = C::DP_PWO * U;
+    float* d = at<float>(arena, C::DP_OFF + (long long)img * C::DP_IMG);
+#pragma unroll
+    for (int rep = 0; rep < U * U; ++rep) {
+      float* dst = d + ((long long)(py * U + rep / U) * WU + px * U + rep % U) * C::CO + cofs;
+#pragma unroll
+      for (int i = 0; i < NC; i += 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(m[i], m[i + 1], m[i + 2], m[i + 3]);
     }
   }
 
@@ -1147,6 +1177,11 @@ struct GemmTc {
             const int col = g * GCO + i;
             y[i] = finish<C::ACT, EMODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
           }
+          if constexpr (C::DPOOL) {
+            const int rr = q * 32 + lane, w = rr % TW;
+            dual_pool_store<GCO>(arena, y, (rr & 17) == 0 && w + 1 < OW, img,
+                                 (tt / TX) * TH + rr / TW, (tt % TX) * OW + w, g * GCO, n);
+          }
 #pragma unroll
           for (int h = 0; h < (GCO + 15) / 16; ++h) {
             constexpr int NC = GCO < 16 ? GCO : 16;
@@ -1320,6 +1355,11 @@ struct GemmTc {
             }
             v[i] = y;
           }
+          }
+          if constexpr (C::DPOOL && C::CONV) {
+            const int img = mb / TPI, tt = mb % TPI;
+            dual_pool_store<16>(arena, v, (r & 17) == 0, img, (tt / TX) * TH + r / TW,
+                                (tt % TX) * TW + r % TW, col0, n);
           }
           if constexpr (ET) {
             float4* b = ebuf + (g % NBUF) * 128;

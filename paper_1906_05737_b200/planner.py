@@ -75,6 +75,8 @@ class CompilationUnit:
     concat_in: bool = False         # conv reads the channel concat of input_ids
     dw: object = None               # fused depthwise producer (a CompilationUnit)
     steps: list = None              # Chain: the fused units, in order
+    dual_pool: object = None        # a 2x2 max-pool (Pool unit) computed from this conv's
+                                    # output in its epilogue while the full output is stored
 
     def describe(self):
         bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
@@ -97,6 +99,10 @@ class CompilationUnit:
             bits.append(f"+upsample{self.upsample_after}")
         if self.concat_in:
             bits.append("concat-loader")
+        if self.dual_pool is not None:
+            bits.append(f"+maxpool2->t{self.dual_pool.output_id}"
+                        + (f"+upsample{self.dual_pool.upsample_after}"
+                           if self.dual_pool.upsample_after > 1 else ""))
         if self.steps:
             bits.append("[" + " | ".join(
                 f"{st.kind}{'%dx%d/s%d' % (*st.kernel_hw, st.stride) if st.kernel_hw else ''}"
@@ -442,6 +448,38 @@ def fuse_upsample(plan):
     return plan
 
 
+def unit_writes(u):
+    """Tensors a unit writes: its output, and a dual-stored pooled map."""
+    dp = getattr(u, "dual_pool", None)
+    return (u.output_id,) + ((dp.output_id,) if dp is not None else ())
+
+
+def fuse_pool_dual(plan):
+    """A 2x2/2 max-pool whose input is a conv output that other units read
+    as well (an encoder skip of cfg4) becomes a second store of that conv's
+    epilogue: the conv writes its full output AND the pooled (and, if the
+    pool's output is upsampled, replicated) map, so the pooled tensor costs
+    no re-read of the full one and no launch.  Kernels that do not implement
+    the second store get the pool as a separate launch (kernels.py)."""
+    pos = 1
+    while pos < len(plan.units):
+        u = plan.units[pos]
+        where = plan.producer_positions()
+        ppos = where.get(u.input_ids[0], -1) if u.kind == "Pool" else -1
+        if ppos >= 0:
+            p = plan.units[ppos]
+            if (p.kind == "Conv2D" and not p.pool_after and p.residual_id is None
+                    and not p.softmax_after and p.upsample_after == 1 and p.dual_pool is None
+                    and p.dw is None and p.output_shape.rank == 3 and _pool_fusable(p, u)
+                    and u.residual_id is None and not _private(plan, p.output_id)
+                    and ppos == pos - 1):
+                p.dual_pool = u
+                _delete(plan, pos, p)
+                continue
+        pos += 1
+    return plan
+
+
 def fuse_concat(plan):
     """A two-way channel Concatenate feeding only a stride-1 Conv2D becomes a
     two-source operand loader of that conv (no concatenated tensor)."""
@@ -692,6 +730,7 @@ def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False):
     fuse_residual(plan)
     fuse_softmax(plan)
     fuse_upsample(plan)
+    fuse_pool_dual(plan)
     fuse_concat(plan)
     if dw_fusion:
         fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")

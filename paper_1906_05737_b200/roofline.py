@@ -141,6 +141,11 @@ def unit_work(u, plan=None):
         f = u.output_shape.elements * max(1, len(u.input_ids))
     else:
         f = 0
+    dp = getattr(u, "dual_pool", None)
+    if dp is not None:             # second, pooled store of the output
+        pf, _, _ = unit_work(dp)
+        f += pf
+        out += 4 * dp.output_shape.elements
     d = getattr(u, "dw", None)
     if d is not None:              # fused depthwise producer
         df, _, dwb = unit_work(d)

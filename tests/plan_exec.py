@@ -88,3 +88,6 @@ def _run_unit(u, vals):
         if f > 1:
             y = np.repeat(np.repeat(y.reshape((n,) + u.pre_up_shape.dims), f, 1), f, 2)
         vals[u.output_id] = y.reshape((n,) + u.output_shape.dims)
+        dp = getattr(u, "dual_pool", None)
+        if dp is not None:                # the conv's second, pooled store
+            _run_unit(dp, vals)

@@ -700,3 +700,45 @@ def test_chain_kernel_vs_oracle(case, n):
     np.testing.assert_allclose(got2, ref(m, wt, x, ApproximationOptions()), **TOL)
     unf, _ = gpu(m, wt, x)
     np.testing.assert_allclose(got, unf, **TOL)
+
+
+@pytest.mark.parametrize("h,w,ci,co,up,n,tc", [
+    (16, 32, 16, 32, False, 3, True), (24, 16, 32, 64, True, 2, True),
+    (30, 40, 16, 32, True, 2, True), (12, 20, 16, 64, False, 2, False),
+    (10, 14, 8, 16, True, 3, False)])
+def test_dual_pooled_store(h, w, ci, co, up, n, tc):
+    """planner.fuse_pool_dual: a conv whose output is both a skip and the
+    input of a 2x2 max-pool stores the pooled (optionally x2 upsampled) map
+    as a second epilogue store -- tcgen05 KPACK (CO=32) and plain conv tiles
+    (CO=64) -- or, for kernels without it, gets the pool as its own launch."""
+    rng = np.random.default_rng(h * w + co)
+    b = NetBuilder()
+    x = b.input((h, w, ci))
+    c = b.layer("Conv2D", [x], {"filters": co, "kernel_size": 3, "padding": "same",
+                                "activation": "relu"},
+                [("kernel", he(rng, (3, 3, ci, co), 9 * ci)),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    p = b.maxpool(c)
+    if up:
+        p = b.layer("UpSample2D", [p], {"factor": 2})
+        cat = b.layer("Concatenate", [c, p])
+        y = b.layer("Conv2D", [cat], {"filters": 16, "kernel_size": 1, "activation": "linear"},
+                    [("kernel", he(rng, (1, 1, 2 * co, 16), 2 * co)), ("bias", np.zeros(16, F32))])
+        outs = [y]
+    else:
+        d = b.layer("Conv2D", [p], {"filters": 16, "kernel_size": 1}, [("kernel", he(rng, (1, 1, co, 16), co)),
+                                                                        ("bias", np.zeros(16, F32))])
+        outs = [d, c]
+    m, wt = b.build(outs)
+    xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
+    kw = dict(tc_min_rows=1, tc_tile_use=0) if tc else dict(use_tc=False)
+    net = compile_model(m, wt, EXACT, batch=n, tuning=kw)
+    got = [o.cpu().numpy() for o in net.run([xin])]
+    conv = [u for u in net.plan.units if u.kind == "Conv2D" and u.dual_pool is not None]
+    assert len(conv) == 1 and "Pool" not in [u.kind for u in net.plan.units]
+    ls = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
+    assert any("pooled second store" in l.note for l in ls) == tc
+    assert any("maxpool" in l.kernel for l in ls) == (not tc)
+    want = oracle.run(m, wt, [xin], "exact")
+    for g, wv in zip(got, want):
+        np.testing.assert_allclose(g, wv, **TOL)

@@ -123,13 +123,18 @@ def test_gpu_fusions_on_zoo():
     assert sum(u.residual_id is not None for u in p2.units) == 1 and "Add" not in kinds(p2)
     p4 = build_plan(build_graph(*zoo.build(4)))
     convs = [u for u in p4.units if u.kind == "Conv2D"]
-    # encoder convs 2 and 3 feed a skip connection: their pools stay separate
+    # encoder convs 2 and 3 feed a skip connection: they store their full output
+    # and, as a second store, the pooled map (fuse_pool_dual; conv 3's pooled map
+    # upsampled for the decoder)
     assert [c.pool_after for c in convs[:3]] == [True, False, False]
+    assert [c.dual_pool is not None for c in convs[:3]] == [False, True, True]
+    assert convs[2].dual_pool.upsample_after == 2 and "Pool" not in kinds(p4)
     assert convs[-1].softmax_after
-    # decoder: pool->upsample and conv->upsample epilogues, concat as operand loader
+    # decoder: conv->upsample epilogue, concat as operand loader
     assert "Upsample" not in kinds(p4) and "Concat" not in kinds(p4)
-    assert sum(u.upsample_after == 2 for u in p4.units) == 2
+    assert sum(u.upsample_after == 2 for u in p4.units) == 1
     assert sum(u.concat_in for u in p4.units) == 2
+    assert kinds(build_plan(build_graph(*zoo.build(4)), gpu_fusion=False)).count("Pool") == 3
 
 
 @pytest.mark.parametrize("cfg", range(5))
