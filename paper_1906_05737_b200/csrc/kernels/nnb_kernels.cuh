@@ -10,3 +10,4 @@
 #include "nnb_gemm_tc.cuh"
 #include "nnb_conv_direct.cuh"
 #include "nnb_chain.cuh"
+#include "nnb_tcchain.cuh"

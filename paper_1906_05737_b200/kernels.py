@@ -1021,6 +1021,78 @@ class Specializer:
                   note=f"chain of {len(steps)} steps ({kinds}) {steps[0].input_shapes[0]} -> "
                        f"{u.output_shape}, one CTA per image, {smem // 1024} KB shared")
 
+    def tc_chain(self, pos, u):
+        """Alternating depthwise / pointwise layers over <= 64-pixel maps on
+        the tensor cores, two images per CTA for the whole run
+        (nnb_tcchain.cuh, planner.fuse_tc_chain).  Pointwise weights are
+        split (3xTF32, round-to-nearest hi) and pre-swizzled into the shared-
+        memory image of a K-major SW128 operand, one [B_hi | B_lo] block per
+        32-wide k-block, streamed by 1-D bulk copies."""
+        steps = u.steps
+        AS = max(st.output_shape.c for st in steps if st.kind == "Conv2D") + 4
+        calls, structs, blocks = [], [], []           # blocks: (pool offset, bytes, layer, stage)
+        layer = 0
+        for i, st in enumerate(steps):
+            last = i == len(steps) - 1
+            ep = self.epilogue_fields(st, st.output_shape.c)
+            if st.kind == "DepthwiseConv2D":
+                H, W, C = st.input_shapes[0].dims
+                HO, WO, _ = st.output_shape.dims
+                KH, KW = st.kernel_hw
+                PT = same_padding(H, KH, st.stride)[0] if st.padding == "same" else 0
+                PL = same_padding(W, KW, st.stride)[0] if st.padding == "same" else 0
+                f = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=st.stride, PT=PT, PL=PL,
+                         W_OFF=self.pool.add(st.kernel), B_OFF=self.pool.add(st.bias),
+                         SRC_GLOBAL=int(i == 0), SRC_IMG=4 * st.input_shapes[0].elements,
+                         AS_IN=AS, KA=C, OUT_IMG=self.img_bytes(u.output_id), **ep)
+                calls.append(f"    nnb::{'TccDwOut' if last else 'TccDwA'}<S{i}>::run(x);")
+            else:
+                HO, WO, N = st.output_shape.dims
+                K = st.input_shapes[0].c
+                wt = np.ascontiguousarray(np.asarray(st.kernel, F32).reshape(K, N).T)   # [N][K]
+                hi = tf32_split_hi(wt, self.split_rn)
+                lo = (wt - hi).astype(F32)
+                blk0 = len(blocks)
+                for kb in range(K // 32):
+                    img = b""
+                    for part in (hi, lo):
+                        blk = part[:, kb * 32:(kb + 1) * 32].reshape(N, 8, 4)
+                        sw = np.empty_like(blk)
+                        rows = np.arange(N)[:, None]
+                        sw[rows, np.arange(8)[None, :] ^ (rows % 8)] = blk
+                        img += np.ascontiguousarray(sw, F32).tobytes()
+                    off = self.pool.add(np.frombuffer(img, F32))
+                    blocks.append((off, len(img), layer, kb))
+                f = dict(K=K, N=N, P=HO * WO, LAYER=layer, BLK0=blk0, B_OFF=self.pool.add(st.bias),
+                         AS_OUT=AS, LAST=int(last), OUT_IMG=self.img_bytes(u.output_id), **ep)
+                calls.append(f"    nnb::TccPw<Cfg_{len(self.names)}, S{i}>::run(x);")
+                layer += 1
+            structs.append(_cfg_struct(f"S{i}", f).replace("\n", "\n  "))
+
+        def table(name, vals):
+            cases = " ".join(f"case {j}: return {v}LL;" for j, v in enumerate(vals))
+            return (f"  __device__ static __forceinline__ long long {name}(int i) "
+                    f"{{ switch (i) {{ {cases} default: return 0; }} }}")
+        code = "\n".join(["  " + x for x in structs] + [
+            table("blk_off", [b[0] for b in blocks]), table("blk_bytes", [b[1] for b in blocks]),
+            table("blk_layer", [b[2] for b in blocks]), table("blk_stage", [b[3] for b in blocks]),
+            "  __device__ static __forceinline__ void body(nnb::TcChainCtx& x) {"] + calls + ["  }"])
+        nstage = max(b[3] for b in blocks) + 1
+        stage_bytes = -(-max(b[1] for b in blocks) // 1024) * 1024
+        act_floats = 2 * 64 * AS
+        fields = dict(IN_OFF=self.arena_off(u.input_ids[0]), IN_IMG=self.img_bytes(u.input_ids[0]),
+                      OUT_OFF=self.arena_off(u.output_id), OUT_IMG=self.img_bytes(u.output_id),
+                      NSTAGE=nstage, STAGE_BYTES=stage_bytes, ACT_FLOATS=act_floats,
+                      NBLK=len(blocks))
+        smem = 1024 + nstage * stage_bytes + 4 * act_floats + 256
+        n_pw = sum(st.kind == "Conv2D" for st in steps)
+        self.emit(pos, "tcchain", "nnb::TcChain", fields, 256, smem, 1, 2,
+                  code=code,
+                  note=f"tcgen05 chain of {len(steps)} layers ({n_pw} pointwise 3xTF32, A in "
+                       f"TMEM) {steps[0].input_shapes[0]} -> {u.output_shape}, 2 images per CTA, "
+                       f"{len(blocks)} weight blocks in a {nstage}-stage ring, {smem // 1024} KB "
+                       "shared")
+
     def depthwise(self, pos, u):
         H, W, C = u.input_shapes[0].dims
         HO, WO, _ = u.output_shape.dims
@@ -1186,6 +1258,8 @@ class Specializer:
                 self.pad(pos, u)
             elif u.kind == "Chain":
                 self.chain(pos, u)
+            elif u.kind == "TcChain":
+                self.tc_chain(pos, u)
             else:
                 raise UnsupportedLayer(f"no kernel for unit kind {u.kind}")
         self._n_cap = None

@@ -707,7 +707,80 @@ def fuse_chain(plan, smem_max=CHAIN_SMEM_MAX, min_steps=CHAIN_MIN_STEPS):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False):
+TC_CHAIN_ROWS = 128          # nnb_tcchain.cuh: two images of <= 64 pixels per M=128 tile
+TC_CHAIN_MIN_PW = 3
+
+
+def _tcc_ok_dw(u, first):
+    if (u.kind != "DepthwiseConv2D" or u.residual_id is not None or u.pool_after
+            or u.upsample_after != 1 or u.softmax_after or u.scale is not None
+            or len(u.input_ids) != 1 or u.input_shapes[0].rank != 3):
+        return False
+    h, w, c = u.input_shapes[0].dims
+    ho, wo, _ = u.output_shape.dims
+    return (c % 32 == 0 and c <= 128 and ho * wo <= 64 and u.kernel_hw[0] <= 5
+            and u.kernel_hw[1] <= 5 and (first or h * w <= 64))
+
+
+def _tcc_ok_pw(u):
+    if (u.kind != "Conv2D" or u.kernel_hw != (1, 1) or u.stride != 1 or u.residual_id is not None
+            or u.pool_after or u.upsample_after != 1 or u.softmax_after or u.concat_in
+            or u.dw is not None or u.dual_pool is not None):
+        return False
+    h, w, n = u.output_shape.dims
+    k = u.input_shapes[0].c
+    return h * w <= 64 and k % 32 == 0 and k <= 128 and n % 16 == 0 and n <= 128
+
+
+def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
+    """Alternating depthwise / pointwise layers over maps of <= 64 pixels (the
+    8x8 stage of MobileNet-style nets) become one ``TcChain`` unit run by a
+    tensor-core kernel holding two images per CTA for the whole run
+    (nnb_tcchain.cuh): dw (CUDA cores, into TMEM), pw (tcgen05 3xTF32),
+    dw, pw, ..., optionally a closing depthwise.  Every intermediate stays on
+    chip.  The run starts at a depthwise layer (its input is read from the
+    arena) and needs ``min_pw`` pointwise layers."""
+    pos = 0
+    while pos < len(plan.units):
+        if not _tcc_ok_dw(plan.units[pos], True):
+            pos += 1
+            continue
+        run = [pos]
+        while run[-1] + 1 < len(plan.units):
+            prev, nxt = plan.units[run[-1]], plan.units[run[-1] + 1]
+            if not (nxt.input_ids == (prev.output_id,) and _private(plan, prev.output_id)):
+                break
+            want_pw = prev.kind == "DepthwiseConv2D"
+            if want_pw and _tcc_ok_pw(nxt) and nxt.input_shapes[0].c == prev.output_shape.c:
+                run.append(run[-1] + 1)
+            elif not want_pw and _tcc_ok_dw(nxt, False):
+                run.append(run[-1] + 1)
+            else:
+                break
+        # a dw that feeds nothing in the run is fine only at the end
+        n_pw = sum(plan.units[i].kind == "Conv2D" for i in run)
+        if n_pw < min_pw:
+            pos = run[-1] + 1
+            continue
+        units = [plan.units[i] for i in run]
+        first, last = units[0], units[-1]
+        chain = CompilationUnit(uid=first.uid, kind="TcChain",
+                                name=f"tcchain({first.name}..{last.name})",
+                                input_ids=first.input_ids, output_id=last.output_id,
+                                input_shapes=first.input_shapes, output_shape=last.output_shape,
+                                steps=units)
+        for st in units[:-1]:
+            plan.tensors.pop(st.output_id, None)
+        for _ in units:
+            victim = plan.units.pop(run[0])
+            plan.node_units = {n: (chain.uid if u == victim.uid else u)
+                               for n, u in plan.node_units.items()}
+        plan.units.insert(run[0], chain)
+        pos = run[0] + 1
+    return plan
+
+
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=True):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -720,11 +793,11 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False):
     depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
-        apply_gpu_fusions(plan, dw_fusion, chain)
+        apply_gpu_fusions(plan, dw_fusion, chain, tc_chain)
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=True):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -734,6 +807,8 @@ def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False):
     fuse_concat(plan)
     if dw_fusion:
         fuse_dw_pw(plan, narrow_only=dw_fusion == "narrow")
+    if tc_chain:
+        fuse_tc_chain(plan)
     if chain:
         fuse_chain(plan)
     return plan
@@ -746,7 +821,7 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
                          "pool_op", "factor", "in_place_preference")
 
 
-def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False):
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=True):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions
@@ -774,7 +849,7 @@ def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False):
     ours = FusionPlan(units, {t: shape(s) for t, s in plan.tensors.items()},
                       tuple(plan.input_ids), tuple(plan.output_ids), dict(plan.node_units))
     if gpu_fusion:
-        apply_gpu_fusions(ours, dw_fusion, chain)
+        apply_gpu_fusions(ours, dw_fusion, chain, tc_chain)
     return ours
 
 

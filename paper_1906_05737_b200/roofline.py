@@ -72,7 +72,7 @@ def tf32_peak_tflops(peaks):
 
 def launch_pipe(launch):
     """(pipe, products per FP32 MAC) of the kernel a launch runs."""
-    if "_tc_" in launch.kernel:
+    if "_tc_" in launch.kernel or "tcchain" in launch.kernel:
         return ("tensor", 2 if "bf16 corr" in launch.note else 3)
     return ("ffma", 1)
 
@@ -117,7 +117,7 @@ def unit_work(u, plan=None):
         if arr is not None:
             wb += 4 * arr.size
     k = u.kind
-    if k == "Chain":               # fused run: its steps' work, chain input + output bytes
+    if k in ("Chain", "TcChain"):  # fused run: its steps' work, chain input + output bytes
         f = wb = 0
         for st in u.steps:
             sf, _, sw = unit_work(st)

@@ -24,7 +24,7 @@ def _post(y, u):
 def run_plan(plan, inputs):
     vals = {t: np.asarray(x, F32) for t, x in zip(plan.input_ids, inputs)}
     for u in plan.units:
-        if u.kind == "Chain":             # a run of fused units, executed in order
+        if u.kind in ("Chain", "TcChain"):     # a run of fused units, executed in order
             for st in u.steps:
                 _run_unit(st, vals)
         else:

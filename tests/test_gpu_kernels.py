@@ -742,3 +742,32 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
     want = oracle.run(m, wt, [xin], "exact")
     for g, wv in zip(got, want):
         np.testing.assert_allclose(g, wv, **TOL)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 64])
+@pytest.mark.parametrize("case", [
+    # cfg3-like: a stride-2 dw from a 16x16 map read from the arena, pw 64->128, then
+    # dw/pw pairs at 8x8, closing stride-2 dw to 4x4 (stored)
+    (16, 16, 64, [("d", 3, 2, "same", "relu6"), ("p", 128, "relu6"), ("d", 3, 1, "same", "relu6"),
+                  ("p", 128, "relu6"), ("d", 3, 1, "same", "relu"), ("p", 128, "linear"),
+                  ("d", 3, 2, "same", "relu6")], False, True),
+    # 7x7 maps (49 of 64 rows live), 5x5 taps, 'valid', a closing pointwise (stored)
+    (9, 9, 32, [("d", 3, 1, "valid", "relu"), ("p", 64, "tanh"), ("d", 5, 1, "same", "relu6"),
+                ("p", 32, "relu"), ("d", 3, 1, "same", "linear"), ("p", 96, "sigmoid")], False, False)])
+def test_tc_chain_vs_oracle(case, n):
+    """planner.fuse_tc_chain + nnb_tcchain.cuh: the 8x8 stage of a MobileNet-
+    style net on the tensor cores, two images per CTA (odd batches leave half
+    a CTA empty), against the oracle; and against the per-layer launches."""
+    h, w, c, spec, gap, post_bn = case
+    rng = np.random.default_rng(len(spec) * 7 + c + n)
+    m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
+    x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
+    got, net = gpu(m, wt, x)
+    assert "TcChain" in [u.kind for u in net.plan.units], net.plan.describe()
+    assert any("tcchain" in l.kernel for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, wt, x), **TOL)
+    got2, _ = gpu(m, wt, x, ApproximationOptions())
+    np.testing.assert_allclose(got2, ref(m, wt, x, ApproximationOptions()), **TOL)
+    unf, net3 = gpu(m, wt, x, tc_chain=False)
+    assert "TcChain" not in [u.kind for u in net3.plan.units]
+    np.testing.assert_allclose(got, unf, **TOL)

@@ -156,7 +156,7 @@ def test_chain_fusion_sound_and_shaped_on_cfg3():
     from paper_1906_05737_b200.planner import CHAIN_SMEM_MAX, chain_smem
     m, w = zoo.build(3)
     g = build_graph(m, w)
-    plan = build_plan(g, chain=True)
+    plan = build_plan(g, chain=True, tc_chain=False)
     chains = [u for u in plan.units if u.kind == "Chain"]
     assert len(chains) == 1 and len(chains[0].steps) == 20
     assert chains[0].steps[-1].kind == "Pool" and chain_smem(chains[0].steps) <= CHAIN_SMEM_MAX
@@ -165,6 +165,21 @@ def test_chain_fusion_sound_and_shaped_on_cfg3():
     x = zoo.inputs(3, 2)
     np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
     assert "Chain" not in kinds(build_plan(g))          # off by default
+
+
+def test_tc_chain_fusion_sound_and_shaped_on_cfg3():
+    """planner.fuse_tc_chain (default): cfg3's 8x8 stage -- the stride-2
+    depthwise from 16x16, six pointwise layers, five 8x8 depthwise layers and
+    the closing stride-2 depthwise to 4x4 -- is one TcChain unit, and the
+    plan computes the unfused graph."""
+    m, w = zoo.build(3)
+    g = build_graph(m, w)
+    plan = build_plan(g)
+    (tc,) = [u for u in plan.units if u.kind == "TcChain"]
+    assert [st.kind[0] for st in tc.steps] == list("DCDCDCDCDCDCD")
+    assert tc.input_shapes[0].dims == (16, 16, 64) and tc.output_shape.dims == (4, 4, 128)
+    x = zoo.inputs(3, 2)
+    np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
 
 
 def test_build_plan_idempotent_and_deterministic():
