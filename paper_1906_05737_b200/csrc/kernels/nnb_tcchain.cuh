@@ -98,7 +98,13 @@ struct TccDwA {
       float a[16];
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
+        // the chunk's weights first, unconditionally: the loads issue back to
+        // back instead of one L1 round trip per tap inside the bounds checks
         float4 acc = __ldg(reinterpret_cast<const float4*>(bs + c0 + j));
+        float4 wt[S::KH * S::KW];
+#pragma unroll
+        for (int t = 0; t < S::KH * S::KW; ++t)
+          wt[t] = __ldg(reinterpret_cast<const float4*>(wk + t * S::C + c0 + j));
 #pragma unroll
         for (int ky = 0; ky < S::KH; ++ky) {
           const int iy = oy * S::S - S::PT + ky;
@@ -106,8 +112,7 @@ struct TccDwA {
           for (int kx = 0; kx < S::KW; ++kx) {
             const int ix = ox * S::S - S::PL + kx;
             if (live && iy >= 0 && iy < S::H && ix >= 0 && ix < S::W) {
-              const float4 w4 = __ldg(reinterpret_cast<const float4*>(
-                  wk + (ky * S::KW + kx) * S::C + c0 + j));
+              const float4 w4 = wt[ky * S::KW + kx];
               const float* pv = S::SRC_GLOBAL ? src + (iy * S::W + ix) * S::C + c0 + j
                                               : src + (iy * S::W + ix) * S::AS_IN + c0 + j;
               const float4 v = S::SRC_GLOBAL ? lda(reinterpret_cast<const float4*>(pv))
@@ -184,6 +189,12 @@ struct TccPw {
 #pragma unroll 1
     for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 16) {
       u32 m[16], cr[16];
+      float bv[16];
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
+        bv[i] = b4.x; bv[i + 1] = b4.y; bv[i + 2] = b4.z; bv[i + 3] = b4.w;
+      }
       tmem_ld16_async(x.tmem + trow + c0, m);
       tmem_ld16_async(x.tmem + trow + S::N + c0, cr);
       tmem_wait_ld();
@@ -193,7 +204,7 @@ struct TccPw {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         y[i] = finish<S::ACT, S::MODE, S::POST>(
-            __uint_as_float(m[i]) + __uint_as_float(cr[i]) + __ldg(bias + c0 + i), ps, po, c0 + i);
+            __uint_as_float(m[i]) + __uint_as_float(cr[i]) + bv[i], ps, po, c0 + i);
       float* d = S::LAST ? (img < x.nimg && p < S::P
                                 ? at<float>(x.dst, (long long)img * S::OUT_IMG) + p * S::N + c0
                                 : nullptr)
@@ -225,6 +236,10 @@ struct TccDwOut {
       const int oy = p / S::WO, ox = p % S::WO;
       const float* src = x.act + img * 64 * S::AS_IN;
       float4 acc = __ldg(reinterpret_cast<const float4*>(bs + c));
+      float4 wt[S::KH * S::KW];
+#pragma unroll
+      for (int t = 0; t < S::KH * S::KW; ++t)
+        wt[t] = __ldg(reinterpret_cast<const float4*>(wk + t * S::C + c));
 #pragma unroll
       for (int ky = 0; ky < S::KH; ++ky) {
         const int iy = oy * S::S - S::PT + ky;
@@ -232,7 +247,7 @@ struct TccDwOut {
         for (int kx = 0; kx < S::KW; ++kx) {
           const int ix = ox * S::S - S::PL + kx;
           if (iy >= 0 && iy < S::H && ix >= 0 && ix < S::W) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4*>(wk + (ky * S::KW + kx) * S::C + c));
+            const float4 w4 = wt[ky * S::KW + kx];
             const float4 v = *reinterpret_cast<const float4*>(src + (iy * S::W + ix) * S::AS_IN + c);
             acc.x = add(acc.x, mul(v.x, w4.x)); acc.y = add(acc.y, mul(v.y, w4.y));
             acc.z = add(acc.z, mul(v.z, w4.z)); acc.w = add(acc.w, mul(v.w, w4.w));
