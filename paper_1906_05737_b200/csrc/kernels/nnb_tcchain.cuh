@@ -32,6 +32,12 @@
 #pragma once
 #include "nnb_gemm_tc.cuh"
 
+// NNB_TCC_DBG (diagnostics only, results are garbage): bit 0 skips the
+// depthwise taps, bit 1 the MMAs (barriers still complete)
+#ifndef NNB_TCC_DBG
+#define NNB_TCC_DBG 0
+#endif
+
 namespace nnb {
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
@@ -89,7 +95,7 @@ struct TccDwA {
     const float* bs = at<float>(x.pool, S::B_OFF);
     const float* ps = at<float>(x.pool, S::PS_OFF);
     const float* po = at<float>(x.pool, S::PO_OFF);
-    const float* src = S::SRC_GLOBAL ? at<float>(x.src, (long long)img * S::SRC_IMG)
+    const float* src = S::SRC_GLOBAL ? at<float>(x.src, (long long)(img < x.nimg ? img : 0) * S::SRC_IMG)
                                      : x.act + img * 64 * S::AS_IN;
     constexpr int CH = S::C / 2;                     // channels of this warp's half
     const u32 trow = (u32)(q * 32) << 16;
@@ -105,21 +111,33 @@ struct TccDwA {
 #pragma unroll
         for (int t = 0; t < S::KH * S::KW; ++t)
           wt[t] = __ldg(reinterpret_cast<const float4*>(wk + t * S::C + c0 + j));
+        // every tap's input loaded unconditionally from a clamped (in-bounds)
+        // address so the loads issue together; out-of-image taps are then
+        // skipped exactly as before (the interpreter's zero padding)
+        float4 xv[S::KH * S::KW];
+        bool ok[S::KH * S::KW];
 #pragma unroll
         for (int ky = 0; ky < S::KH; ++ky) {
           const int iy = oy * S::S - S::PT + ky;
 #pragma unroll
           for (int kx = 0; kx < S::KW; ++kx) {
             const int ix = ox * S::S - S::PL + kx;
-            if (live && iy >= 0 && iy < S::H && ix >= 0 && ix < S::W) {
-              const float4 w4 = wt[ky * S::KW + kx];
-              const float* pv = S::SRC_GLOBAL ? src + (iy * S::W + ix) * S::C + c0 + j
-                                              : src + (iy * S::W + ix) * S::AS_IN + c0 + j;
-              const float4 v = S::SRC_GLOBAL ? lda(reinterpret_cast<const float4*>(pv))
-                                             : *reinterpret_cast<const float4*>(pv);
-              acc.x = add(acc.x, mul(v.x, w4.x)); acc.y = add(acc.y, mul(v.y, w4.y));
-              acc.z = add(acc.z, mul(v.z, w4.z)); acc.w = add(acc.w, mul(v.w, w4.w));
-            }
+            const int t = ky * S::KW + kx;
+            ok[t] = live && iy >= 0 && iy < S::H && ix >= 0 && ix < S::W;
+            const int cy = iy < 0 ? 0 : (iy >= S::H ? S::H - 1 : iy);
+            const int cx = ix < 0 ? 0 : (ix >= S::W ? S::W - 1 : ix);
+            const float* pv = S::SRC_GLOBAL ? src + (cy * S::W + cx) * S::C + c0 + j
+                                            : src + (cy * S::W + cx) * S::AS_IN + c0 + j;
+            xv[t] = S::SRC_GLOBAL ? lda(reinterpret_cast<const float4*>(pv))
+                                  : *reinterpret_cast<const float4*>(pv);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < S::KH * S::KW; ++t) {
+          if (ok[t] && !(NNB_TCC_DBG & 1)) {
+            const float4 v = xv[t], w4 = wt[t];
+            acc.x = add(acc.x, mul(v.x, w4.x)); acc.y = add(acc.y, mul(v.y, w4.y));
+            acc.z = add(acc.z, mul(v.z, w4.z)); acc.w = add(acc.w, mul(v.w, w4.w));
           }
         }
         a[j + 0] = finish<S::ACT, S::MODE, S::POST>(acc.x, ps, po, c0 + j);
@@ -163,7 +181,7 @@ struct TccPw {
         const u32 b_hi = smem_u32(x.ring + s * C::STAGE_BYTES);
         const u32 b_lo = b_hi + S::N * 128;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < ((NNB_TCC_DBG & 2) ? 0 : 4); ++k) {
           const u32 ta = x.tmem + 256 + kb * 32 + 8 * k;
           const u32 accum = (kb | k) != 0;
           mma_tf32_ts(x.tmem, ta, kmajor_desc<128>(b_hi + 32 * k), IDESC, accum);
