@@ -6,8 +6,9 @@
 // Per layer pair, all inside the CTA, no HBM traffic between layers:
 //   depthwise  CUDA cores: thread (pixel row r = TMEM lane, 16 channels)
 //              accumulates the taps in the interpreter's order (bias, then
-//              (ky, kx), __fmul_rn / __fadd_rn, out-of-image taps skipped --
-//              pkg/src/nnjit/interpreter.py:65-73), applies the activation /
+//              (ky, kx), out-of-image taps skipped -- pkg/src/nnjit/
+//              interpreter.py:65-73; FFMA2, two channels per instruction,
+//              since this output only feeds the MMA), applies the activation /
 //              post-BN, splits a = hi + lo (hi = a rounded to TF32, lo exact)
 //              and writes both into TMEM (tcgen05.st) as the A operand;
 //   pointwise  one thread issues the 3xTF32 MMAs (kind::tf32, A from TMEM:
@@ -85,7 +86,14 @@ __device__ __forceinline__ void tcc_issue(TcChainCtx& x, int layer) {
 //    next layer's K)
 template <class S>
 struct TccDwA {
+  // The depthwise output here only feeds the next layer's 3xTF32 MMA (it is
+  // never stored), so its taps use FFMA2 (two channels per instruction, one
+  // rounding per tap) -- within the FP32 gate like every other contraction
+  // of this path; the stored depthwise layers (TccDwOut, the standalone
+  // kernels) keep the interpreter's mul-then-add order.
   __device__ static __forceinline__ void run(TcChainCtx& x) {
+    constexpr int T = S::KH * S::KW;
+    constexpr int PS = S::SRC_GLOBAL ? S::C : S::AS_IN;     // floats per source pixel
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3, half = warp >> 2;
     const int r = q * 32 + lane, img = r >> 6, p = r & 63;
@@ -97,6 +105,23 @@ struct TccDwA {
     const float* po = at<float>(x.pool, S::PO_OFF);
     const float* src = S::SRC_GLOBAL ? at<float>(x.src, (long long)(img < x.nimg ? img : 0) * S::SRC_IMG)
                                      : x.act + img * 64 * S::AS_IN;
+    // the pixel's taps: source offsets (clamped in-bounds, so every load is
+    // valid and they issue together) and which taps lie inside the image
+    int off[T];
+    bool ok[T];
+#pragma unroll
+    for (int ky = 0; ky < S::KH; ++ky) {
+      const int iy = oy * S::S - S::PT + ky;
+#pragma unroll
+      for (int kx = 0; kx < S::KW; ++kx) {
+        const int ix = ox * S::S - S::PL + kx;
+        const int t = ky * S::KW + kx;
+        ok[t] = live && iy >= 0 && iy < S::H && ix >= 0 && ix < S::W && !(NNB_TCC_DBG & 1);
+        const int cy = iy < 0 ? 0 : (iy >= S::H ? S::H - 1 : iy);
+        const int cx = ix < 0 ? 0 : (ix >= S::W ? S::W - 1 : ix);
+        off[t] = (cy * S::W + cx) * PS;
+      }
+    }
     constexpr int CH = S::C / 2;                     // channels of this warp's half
     const u32 trow = (u32)(q * 32) << 16;
 #pragma unroll 1
@@ -104,46 +129,27 @@ struct TccDwA {
       float a[16];
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
-        // the chunk's weights first, unconditionally: the loads issue back to
-        // back instead of one L1 round trip per tap inside the bounds checks
-        float4 acc = __ldg(reinterpret_cast<const float4*>(bs + c0 + j));
-        float4 wt[S::KH * S::KW];
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bs + c0 + j));
+        float2 a01 = make_float2(b4.x, b4.y), a23 = make_float2(b4.z, b4.w);
+        float4 wt[T], xv[T];
 #pragma unroll
-        for (int t = 0; t < S::KH * S::KW; ++t)
+        for (int t = 0; t < T; ++t) {
           wt[t] = __ldg(reinterpret_cast<const float4*>(wk + t * S::C + c0 + j));
-        // every tap's input loaded unconditionally from a clamped (in-bounds)
-        // address so the loads issue together; out-of-image taps are then
-        // skipped exactly as before (the interpreter's zero padding)
-        float4 xv[S::KH * S::KW];
-        bool ok[S::KH * S::KW];
-#pragma unroll
-        for (int ky = 0; ky < S::KH; ++ky) {
-          const int iy = oy * S::S - S::PT + ky;
-#pragma unroll
-          for (int kx = 0; kx < S::KW; ++kx) {
-            const int ix = ox * S::S - S::PL + kx;
-            const int t = ky * S::KW + kx;
-            ok[t] = live && iy >= 0 && iy < S::H && ix >= 0 && ix < S::W;
-            const int cy = iy < 0 ? 0 : (iy >= S::H ? S::H - 1 : iy);
-            const int cx = ix < 0 ? 0 : (ix >= S::W ? S::W - 1 : ix);
-            const float* pv = S::SRC_GLOBAL ? src + (cy * S::W + cx) * S::C + c0 + j
-                                            : src + (cy * S::W + cx) * S::AS_IN + c0 + j;
-            xv[t] = S::SRC_GLOBAL ? lda(reinterpret_cast<const float4*>(pv))
-                                  : *reinterpret_cast<const float4*>(pv);
-          }
+          const float* pv = src + off[t] + c0 + j;
+          xv[t] = S::SRC_GLOBAL ? lda(reinterpret_cast<const float4*>(pv))
+                                : *reinterpret_cast<const float4*>(pv);
         }
 #pragma unroll
-        for (int t = 0; t < S::KH * S::KW; ++t) {
-          if (ok[t] && !(NNB_TCC_DBG & 1)) {
-            const float4 v = xv[t], w4 = wt[t];
-            acc.x = add(acc.x, mul(v.x, w4.x)); acc.y = add(acc.y, mul(v.y, w4.y));
-            acc.z = add(acc.z, mul(v.z, w4.z)); acc.w = add(acc.w, mul(v.w, w4.w));
+        for (int t = 0; t < T; ++t) {
+          if (ok[t]) {
+            a01 = __ffma2_rn(make_float2(xv[t].x, xv[t].y), make_float2(wt[t].x, wt[t].y), a01);
+            a23 = __ffma2_rn(make_float2(xv[t].z, xv[t].w), make_float2(wt[t].z, wt[t].w), a23);
           }
         }
-        a[j + 0] = finish<S::ACT, S::MODE, S::POST>(acc.x, ps, po, c0 + j);
-        a[j + 1] = finish<S::ACT, S::MODE, S::POST>(acc.y, ps, po, c0 + j + 1);
-        a[j + 2] = finish<S::ACT, S::MODE, S::POST>(acc.z, ps, po, c0 + j + 2);
-        a[j + 3] = finish<S::ACT, S::MODE, S::POST>(acc.w, ps, po, c0 + j + 3);
+        a[j + 0] = finish<S::ACT, S::MODE, S::POST>(a01.x, ps, po, c0 + j);
+        a[j + 1] = finish<S::ACT, S::MODE, S::POST>(a01.y, ps, po, c0 + j + 1);
+        a[j + 2] = finish<S::ACT, S::MODE, S::POST>(a23.x, ps, po, c0 + j + 2);
+        a[j + 3] = finish<S::ACT, S::MODE, S::POST>(a23.y, ps, po, c0 + j + 3);
       }
       u32 hi[16], lo[16];
 #pragma unroll
