@@ -166,6 +166,44 @@ struct TccDwA {
   }
 };
 
+// the chain's first layer is a pointwise one: its input (<= 64 pixels x K,
+// HWC in the arena) becomes the A operand directly -- thread (pixel row r,
+// its half of the channels) loads its pixel's channels (independent
+// coalesced float4 loads), splits them and writes both halves to TMEM.
+// S: P (pixels), K, SRC_IMG (bytes per image)
+template <class S>
+struct TccLoadA {
+  __device__ static __forceinline__ void run(TcChainCtx& x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, half = warp >> 2;
+    const int r = q * 32 + lane, img = r >> 6, p = r & 63;
+    const bool live = img < x.nimg && p < S::P;
+    const float* src = at<float>(x.src, (long long)(img < x.nimg ? img : 0) * S::SRC_IMG) +
+                       (p < S::P ? p : 0) * S::K;
+    constexpr int CH = S::K / 2;
+    const u32 trow = (u32)(q * 32) << 16;
+#pragma unroll
+    for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 16) {
+      u32 hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 v4 = lda(reinterpret_cast<const float4*>(src + c0 + j));
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = live ? v[i] : 0.f;
+          hi[j + i] = split_hi(a);
+          lo[j + i] = __float_as_uint(a - __uint_as_float(hi[j + i]));
+        }
+      }
+      tmem_st<16>(x.tmem + trow + 256 + c0, hi);
+      tmem_st<16>(x.tmem + trow + 256 + S::K + c0, lo);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+  }
+};
+
 // pointwise: MMAs over the streamed weight blocks, then the epilogue into
 // the activation buffer (or the arena when LAST).
 // S: K, N, P (output pixels), LAYER (index in the weight stream), BLK0 (its first block),

@@ -1065,6 +1065,11 @@ class Specializer:
                     blocks.append((off, len(img), layer, kb))
                 f = dict(K=K, N=N, P=HO * WO, LAYER=layer, BLK0=blk0, B_OFF=self.pool.add(st.bias),
                          AS_OUT=AS, LAST=int(last), OUT_IMG=self.img_bytes(u.output_id), **ep)
+                if i == 0:                      # the chain input -> A operand
+                    structs.append(_cfg_struct("SA", dict(
+                        P=st.input_shapes[0].h * st.input_shapes[0].w, K=K,
+                        SRC_IMG=4 * st.input_shapes[0].elements)).replace("\n", "\n  "))
+                    calls.append("    nnb::TccLoadA<SA>::run(x);")
                 calls.append(f"    nnb::TccPw<Cfg_{len(self.names)}, S{i}>::run(x);")
                 layer += 1
             structs.append(_cfg_struct(f"S{i}", f).replace("\n", "\n  "))

@@ -733,16 +733,21 @@ def _tcc_ok_pw(u):
 
 
 def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
-    """Alternating depthwise / pointwise layers over maps of <= 64 pixels (the
+    """Alternating pointwise / depthwise layers over maps of <= 64 pixels (the
     8x8 stage of MobileNet-style nets) become one ``TcChain`` unit run by a
     tensor-core kernel holding two images per CTA for the whole run
-    (nnb_tcchain.cuh): dw (CUDA cores, into TMEM), pw (tcgen05 3xTF32),
-    dw, pw, ..., optionally a closing depthwise.  Every intermediate stays on
-    chip.  The run starts at a depthwise layer (its input is read from the
-    arena) and needs ``min_pw`` pointwise layers."""
+    (nnb_tcchain.cuh): pw (tcgen05 3xTF32; the first one reads its input from
+    the arena straight into TMEM), dw (CUDA cores, into TMEM), pw, ...,
+    optionally a closing depthwise.  Every intermediate stays on chip.  The
+    run needs ``min_pw`` pointwise layers.  (A run starting at a depthwise
+    layer would read that layer's 3x3 input windows from L2 -- 4.6x the input
+    bytes through a CTA's load path; the standalone depthwise kernel does that
+    step faster.)"""
     pos = 0
     while pos < len(plan.units):
-        if not _tcc_ok_dw(plan.units[pos], True):
+        u0 = plan.units[pos]
+        if not (_tcc_ok_pw(u0) and u0.input_shapes[0].rank == 3
+                and u0.input_shapes[0].h * u0.input_shapes[0].w <= 64):
             pos += 1
             continue
         run = [pos]
@@ -757,7 +762,6 @@ def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
                 run.append(run[-1] + 1)
             else:
                 break
-        # a dw that feeds nothing in the run is fine only at the end
         n_pw = sum(plan.units[i].kind == "Conv2D" for i in run)
         if n_pw < min_pw:
             pos = run[-1] + 1

@@ -746,12 +746,13 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
 
 @pytest.mark.parametrize("n", [1, 2, 5, 64])
 @pytest.mark.parametrize("case", [
-    # cfg3-like: a stride-2 dw from a 16x16 map read from the arena, pw 64->128, then
-    # dw/pw pairs at 8x8, closing stride-2 dw to 4x4 (stored)
-    (16, 16, 64, [("d", 3, 2, "same", "relu6"), ("p", 128, "relu6"), ("d", 3, 1, "same", "relu6"),
-                  ("p", 128, "relu6"), ("d", 3, 1, "same", "relu"), ("p", 128, "linear"),
-                  ("d", 3, 2, "same", "relu6")], False, True),
-    # 7x7 maps (49 of 64 rows live), 5x5 taps, 'valid', a closing pointwise (stored)
+    # cfg3-like: pw 64->128 reading an 8x8 map from the arena, dw/pw pairs at 8x8,
+    # closing stride-2 dw to 4x4 (stored)
+    (8, 8, 64, [("p", 128, "relu6"), ("d", 3, 1, "same", "relu6"),
+                ("p", 128, "relu6"), ("d", 3, 1, "same", "relu"), ("p", 128, "linear"),
+                ("d", 3, 2, "same", "relu6")], False, True),
+    # 7x7 maps (49 of 64 rows live), 5x5 taps, 'valid' ahead of the chain, a
+    # closing pointwise (stored)
     (9, 9, 32, [("d", 3, 1, "valid", "relu"), ("p", 64, "tanh"), ("d", 5, 1, "same", "relu6"),
                 ("p", 32, "relu"), ("d", 3, 1, "same", "linear"), ("p", 96, "sigmoid")], False, False)])
 def test_tc_chain_vs_oracle(case, n):

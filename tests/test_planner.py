@@ -168,16 +168,16 @@ def test_chain_fusion_sound_and_shaped_on_cfg3():
 
 
 def test_tc_chain_fusion_sound_and_shaped_on_cfg3():
-    """planner.fuse_tc_chain (default): cfg3's 8x8 stage -- the stride-2
-    depthwise from 16x16, six pointwise layers, five 8x8 depthwise layers and
-    the closing stride-2 depthwise to 4x4 -- is one TcChain unit, and the
-    plan computes the unfused graph."""
+    """planner.fuse_tc_chain (default): cfg3's 8x8 stage -- six pointwise
+    layers (the first reading 8x8x64 from the arena), five 8x8 depthwise
+    layers and the closing stride-2 depthwise to 4x4 -- is one TcChain unit,
+    and the plan computes the unfused graph."""
     m, w = zoo.build(3)
     g = build_graph(m, w)
     plan = build_plan(g)
     (tc,) = [u for u in plan.units if u.kind == "TcChain"]
-    assert [st.kind[0] for st in tc.steps] == list("DCDCDCDCDCDCD")
-    assert tc.input_shapes[0].dims == (16, 16, 64) and tc.output_shape.dims == (4, 4, 128)
+    assert [st.kind[0] for st in tc.steps] == list("CDCDCDCDCDCD")
+    assert tc.input_shapes[0].dims == (8, 8, 64) and tc.output_shape.dims == (4, 4, 128)
     x = zoo.inputs(3, 2)
     np.testing.assert_allclose(run_plan(plan, [x])[0], oracle.run_graph(g, [x])[0], **TOL)
 
