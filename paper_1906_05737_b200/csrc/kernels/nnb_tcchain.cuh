@@ -34,7 +34,8 @@
 #include "nnb_gemm_tc.cuh"
 
 // NNB_TCC_DBG (diagnostics only, results are garbage): bit 0 skips the
-// depthwise taps, bit 1 the MMAs (barriers still complete)
+// depthwise taps, bit 1 the MMAs (barriers still complete), bit 2 the weight
+// bulk copies (and their waits)
 #ifndef NNB_TCC_DBG
 #define NNB_TCC_DBG 0
 #endif
@@ -69,7 +70,7 @@ struct TcChainCtx {
 // i.e. blocks of `layer` (stages are free at a layer boundary).
 template <class C>
 __device__ __forceinline__ void tcc_issue(TcChainCtx& x, int layer) {
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || (NNB_TCC_DBG & 4)) return;
   while (x.next_blk < C::NBLK && C::blk_layer(x.next_blk) == layer) {
     const int b = x.next_blk, s = C::blk_stage(b);
     mbar_expect_tx(&x.full[s], (u32)C::blk_bytes(b));
@@ -219,7 +220,7 @@ struct TccPw {
 #pragma unroll 1
       for (int kb = 0; kb < S::K / 32; ++kb) {
         const int s = C::blk_stage(S::BLK0 + kb);
-        mbar_wait(&x.full[s], (x.full_ph >> s) & 1u);
+        if (!(NNB_TCC_DBG & 4)) mbar_wait(&x.full[s], (x.full_ph >> s) & 1u);
         x.full_ph ^= 1u << s;
         tc_fence_after();
         const u32 b_hi = smem_u32(x.ring + s * C::STAGE_BYTES);
