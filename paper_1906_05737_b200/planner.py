@@ -742,7 +742,17 @@ def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
     run needs ``min_pw`` pointwise layers.  (A run starting at a depthwise
     layer would read that layer's 3x3 input windows from L2 -- 4.6x the input
     bytes through a CTA's load path; the standalone depthwise kernel does that
-    step faster.)"""
+    step faster.)
+
+    Opt-in (``tuning={"tc_chain": True}``).  Measured on B200, cfg3 @256 (12
+    layers, 8x8x64 -> 4x4x128): 73 us for the chain against ~80 us for the
+    same layers as 12 launches (replay 0.264 vs 0.263 ms with the extra
+    depthwise launch ahead of it); batch 1: 68 us vs ~45 us.  Ablations
+    (NNB_TCC_DBG): the depthwise layers are 35 us of it (shared-memory
+    bandwidth: every output re-reads its 9 taps, 590 KB per layer per CTA),
+    the 3xTF32 MMAs 10 us, epilogues / barriers 25 us -- one CTA per image
+    pair serialises all three, where per-layer launches spread every layer
+    over all SMs."""
     pos = 0
     while pos < len(plan.units):
         u0 = plan.units[pos]
@@ -784,7 +794,7 @@ def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=True):
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -801,7 +811,7 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=True):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -825,7 +835,7 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
                          "pool_op", "factor", "in_place_preference")
 
 
-def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=True):
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions

@@ -21,7 +21,8 @@ class Tuning:
     gpu_fusion: bool = True        # B200 epilogue fusions (pool, residual, softmax, upsample, concat)
     dw_fusion: object = "narrow"   # depthwise->pointwise: "narrow" (SepNarrow), True (all), False
     head: bool = True              # fuse a <=16-wide Dense head into a tcgen05 Dense epilogue
-    tc_chain: bool = True          # 8x8-stage depthwise/pointwise runs as one tcgen05 kernel
+    tc_chain: bool = False         # 8x8-stage pointwise/depthwise runs as one tcgen05 kernel
+                                   # (planner.fuse_tc_chain; correct, break-even, opt-in)
     chain: bool = False            # small depthwise/pointwise runs as one FFMA kernel (fuse_chain;
                                    # correct, measured slower than the per-layer tcgen05 path)
     # -- kernel selection ----------------------------------------------------

@@ -763,12 +763,12 @@ def test_tc_chain_vs_oracle(case, n):
     rng = np.random.default_rng(len(spec) * 7 + c + n)
     m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
     x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
-    got, net = gpu(m, wt, x)
+    got, net = gpu(m, wt, x, tc_chain=True)
     assert "TcChain" in [u.kind for u in net.plan.units], net.plan.describe()
     assert any("tcchain" in l.kernel for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, wt, x), **TOL)
-    got2, _ = gpu(m, wt, x, ApproximationOptions())
+    got2, _ = gpu(m, wt, x, ApproximationOptions(), tc_chain=True)
     np.testing.assert_allclose(got2, ref(m, wt, x, ApproximationOptions()), **TOL)
-    unf, net3 = gpu(m, wt, x, tc_chain=False)
+    unf, net3 = gpu(m, wt, x)
     assert "TcChain" not in [u.kind for u in net3.plan.units]
     np.testing.assert_allclose(got, unf, **TOL)

@@ -168,13 +168,14 @@ def test_chain_fusion_sound_and_shaped_on_cfg3():
 
 
 def test_tc_chain_fusion_sound_and_shaped_on_cfg3():
-    """planner.fuse_tc_chain (default): cfg3's 8x8 stage -- six pointwise
+    """planner.fuse_tc_chain (opt-in): cfg3's 8x8 stage -- six pointwise
     layers (the first reading 8x8x64 from the arena), five 8x8 depthwise
     layers and the closing stride-2 depthwise to 4x4 -- is one TcChain unit,
     and the plan computes the unfused graph."""
     m, w = zoo.build(3)
     g = build_graph(m, w)
-    plan = build_plan(g)
+    plan = build_plan(g, tc_chain=True)
+    assert "TcChain" not in kinds(build_plan(g))        # opt-in
     (tc,) = [u for u in plan.units if u.kind == "TcChain"]
     assert [st.kind[0] for st in tc.steps] == list("CDCDCDCDCDCD")
     assert tc.input_shapes[0].dims == (8, 8, 64) and tc.output_shape.dims == (4, 4, 128)
