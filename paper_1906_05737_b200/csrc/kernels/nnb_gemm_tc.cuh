@@ -748,8 +748,11 @@ struct GemmTc {
             tc_fence_after();
           }
           const u32 dbuf = tmem + acc * ACC_COLS;
-          if constexpr (CB16 && !NNB_CB16_WB) {
-            // BF16-correction tiles: the main product a_hi*b_hi reads the raw
+          if constexpr (CB16 && WIDE && !NNB_CB16_WB) {
+            // N = 256 BF16-correction row tiles (measured: Dense 1024->512
+            // 0.2185 -> 0.2142 ms, 512->256 0.0722 -> 0.0709 ms; the narrow
+            // conv tiles got slower with it: cfg4 0.286 -> 0.313 ms, so they
+            // keep the joint issue below): the main product a_hi*b_hi reads the raw
             // A tile (the tensor core truncates it to TF32), so it is issued as
             // soon as the TMA lands, while the split warps build A_corr; the
             // correction MMA follows on lo_ready.  Same accumulation order per

@@ -223,7 +223,7 @@ class Specializer:
                  kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, corr_bf16="auto", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
@@ -761,9 +761,11 @@ class Specializer:
         # ms -- but K = 32 pointwise convs then miss the plain FP32 gate on
         # 0.03% of outputs near zero (|d| 1.5e-5: within the stated bf16
         # bound, not within atol 1e-5), so narrow tiles keep the TF32 split.
-        # "auto" (default): the N = 256 row tiles and the implicit-GEMM conv
-        # tiles with K >= CB16_CONV_MIN_K (the K = 32 pointwise convs keep the
-        # TF32 split: their near-zero outputs missed atol 1e-5 by 1.5e-5)
+        # "wide" (default): the N = 256 row tiles only.  "auto" adds the
+        # implicit-GEMM conv tiles with K >= CB16_CONV_MIN_K (cfg4 @64: 0.897
+        # -> 0.857 ms), but their outputs then sit within the stated BF16
+        # bound, not the plain FP32 gate (cfg4's reference golden: 3 of 57600
+        # outputs off by 1.3e-5 > atol 1e-5), so it is opt-in
         cb16_on = (wide if self.corr_bf16 == "wide" else
                    (wide or (conv is not None and K >= CB16_CONV_MIN_K)) if self.corr_bf16 == "auto"
                    else bool(self.corr_bf16))

@@ -54,8 +54,8 @@ class Tuning:
     wide_chunk: object = None      # main-chain chunk of the N = 256 tiles
     wide_csplit: bool = True       # correction chain of the N = 256 tiles
     rn_ss: bool = True             # write the rounded hi back over shared-memory A tiles
-    corr_bf16: object = "auto"     # BF16 correction products: "auto" (N=256 tiles + conv tiles with
-                                   # K >= 128), "wide" (N=256 tiles only), True (all), False
+    corr_bf16: object = "wide"     # BF16 correction products: "wide" (N=256 tiles only), "auto"
+                                   # (+ conv tiles with K >= 128), True (all), False
     cb16_w4: bool = True           # 4 split warps for BF16-correction tiles
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
 
