@@ -302,6 +302,10 @@ __device__ __forceinline__ u32 cluster_rank() {
 __device__ __forceinline__ void named_sync64(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
+// named barrier over the four epilogue warps of one column group
+__device__ __forceinline__ void named_sync128(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -511,8 +515,9 @@ struct GemmTc {
   // WIDE: N = 256 per MMA (a tcgen05 kind::tf32 instruction costs ~100
   // cycles at N <= 128 and ~1.4x that at N = 256, scripts/mma_n256.py); the
   // epilogue keeps 128 running sums per thread (384 threads: 168 registers)
-  static constexpr bool WIDE = C::BN > 128;
-  static_assert(C::BN % 16 == 0 && C::BN >= 16 && (C::BN <= 128 || C::BN == 256),
+  static constexpr bool WIDE = C::BN > 128 && !C::KP9;
+  static_assert(C::BN % 16 == 0 && C::BN >= 16 && (C::BN <= 128 || C::BN == 256 ||
+                                                   (C::KP9 && C::BN <= 256)),
                 "UMMA N / TMEM budget");
   static_assert(!C::CORR_WHOLE || (CS && C::NACC == 1), "whole-K correction chain");
   static_assert(!WIDE || (!TA && C::NACC == 1 && !C::CONV && !C::RES && C::UPF == 1 &&
@@ -525,9 +530,20 @@ struct GemmTc {
   // epilogue combines out(x) = sum_kx D'(x + kx)[kx] with warp shuffles, so a
   // tile of 16 input columns yields OW = 16 - (KW - 1) output columns.
   static constexpr bool KP = C::KPACK != 0;
-  static constexpr int OW = KP ? TW - (C::KW - 1) : TW;
+  // KP9: ALL KH x KW taps packed into N (N = KH*KW*CO <= 256, K = CI): one
+  // A box per channel block instead of one per kernel row, i.e. every input
+  // pixel is loaded and split once per tile instead of KH times.  A tile of
+  // 8 x 16 input pixels yields THO = 8 - (KH - 1) rows x OW output columns;
+  // the epilogue adds the KW horizontal partial sums with shuffles and the KH
+  // vertical ones through shared memory (rows cross warp quarters).
+  static constexpr bool K9 = C::KP9 != 0;
+  static constexpr int OW = (KP || K9) ? TW - (C::KW - 1) : TW;
+  static constexpr int THO = K9 ? TH - (C::KH - 1) : TH;
   static constexpr int TX = C::CONV ? (C::WO + OW - 1) / OW : 1;
-  static constexpr int TPI = C::CONV ? ((C::HO + TH - 1) / TH) * TX : 1;
+  static constexpr int TPI = C::CONV ? ((C::HO + THO - 1) / THO) * TX : 1;
+  static_assert(!K9 || (C::CONV && !KP && !C::POOL && !C::RES && C::UPF == 1 && !C::DPOOL &&
+                        C::CO == 16 && C::KH * C::KW * C::CO == C::N && !C::CSPLIT &&
+                        C::KH <= 3 && C::KW <= 3), "KP9 geometry");
   static constexpr int CB = C::CONV ? C::CI / BK : 1;       // channel blocks per tap
   static constexpr int CB0 = C::CONV ? C::C0 / BK : 1;      // ... from source 0
   static_assert(!C::CONV || C::CI % BK == 0, "conv tiles need CI % BK == 0");
@@ -549,6 +565,8 @@ struct GemmTc {
   static_assert(!ET || !(C::POOL || C::UPF > 1 || KP), "TMA epilogue: plain row tiles only");
   static_assert(!(C::RES && C::UPF > 1), "residual fusion excludes upsampling (planner)");
   static constexpr int EPI_STAGE = EPI_WARPS * NBUF * 2048;       // 32 x 16 fp32 per buffer
+  static_assert(!K9 || 2 * (C::KH - 1) * 8 * 16 * (C::CO / 2) * 4 <= EPI_STAGE,
+                "KP9 vertical exchange fits the staging area");
   // HEAD: a following Dense with HN <= 16 outputs (a classifier head, e.g.
   // cfg1's 128 -> 10 + softmax) computed in this epilogue from the finished
   // tile row: each of the two warps holding a row's column halves forms the
@@ -710,7 +728,7 @@ struct GemmTc {
               const bool second = C::CONCAT && cb >= CB0;
               const int kx = KP ? 0 : tap % C::KW, ky = KP ? tap : tap / C::KW;
               tma_load_4d(st, second ? tmA1 : tmA, &full[s], (second ? cb - CB0 : cb) * BK,
-                          (tt % TX) * OW + kx - C::PL, (tt / TX) * TH + ky - C::PT, img);
+                          (tt % TX) * OW + kx - C::PL, (tt / TX) * THO + ky - C::PT, img);
             } else {
               tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
               if constexpr (C::APF > 0) {
@@ -1017,7 +1035,7 @@ struct GemmTc {
             const int img = mb / TPI, tt = mb % TPI;
             const int tap = kb / CB, cb = kb % CB;
             const int kx = KP ? 0 : tap % C::KW, ky = KP ? tap : tap / C::KW;
-            const int iy = (tt / TX) * TH + row / TW + ky - C::PT;
+            const int iy = (tt / TX) * THO + row / TW + ky - C::PT;
             const int ix = (tt % TX) * OW + row % TW + kx - C::PL;
             ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
             const bool second = C::CONCAT && cb >= CB0;
@@ -1169,6 +1187,84 @@ struct GemmTc {
             mbar_expect_tx(&rbar[ew], ngrp * 2048);
             for (int g = 0; g < ngrp; ++g) box_io(true, ebuf + g * 128, nb * C::BN + cbeg + g * 16);
           }
+        }
+        if constexpr (K9) {
+          // ---- all taps packed: D''[pixel][ky][kx][co] -> out ----
+          constexpr int GCO = C::CO / 2;                 // output channels per warp group (8)
+          constexpr int NT = C::KH * C::KW;
+          const int g = (warp - EPI_W0) >> 2;
+          float d[NT][GCO];
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int i = 0; i < GCO; ++i) d[t][i] = 0.f;
+          for (int ch = 0; ch < NCHUNK; ++ch) {
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (!(NNB_TC_DBG & 8)) {
+              u32 rv[NT][GCO];
+#pragma unroll
+              for (int t = 0; t < NT; ++t)
+                tmem_ld_async<GCO>(tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + t * C::CO + g * GCO,
+                                   rv[t]);
+              tmem_wait_ld();
+#pragma unroll
+              for (int t = 0; t < NT; ++t) {
+                tmem_pin_n<GCO>(rv[t]);
+#pragma unroll
+                for (int i = 0; i < GCO; ++i) d[t][i] += __uint_as_float(rv[t][i]);
+              }
+            }
+            tc_fence_before();
+            arrive_mma(&tempty[acc]);
+            if (++acc == ABUF) { acc = 0; aph ^= 1; }
+          }
+          // horizontal: h[ky] = sum_kx D''(column + kx)[ky][kx] (lanes of one image row)
+          float h[C::KH][GCO];
+#pragma unroll
+          for (int ky = 0; ky < C::KH; ++ky)
+#pragma unroll
+            for (int i = 0; i < GCO; ++i) {
+              float v = d[ky * C::KW][i];
+#pragma unroll
+              for (int kx = 1; kx < C::KW; ++kx)
+                v += __shfl_down_sync(0xffffffffu, d[ky * C::KW + kx][i], kx);
+              h[ky][i] = v;
+            }
+          // vertical: out(row) = h[0](row) + h[1](row + 1) + h[2](row + 2); rows
+          // two apart live in the next warp quarter, so h[1..] go through the
+          // group's half of the staging area ([ky-1][tile row][column][GCO])
+          float* hx = reinterpret_cast<float*>(epi_stage) + g * ((C::KH - 1) * 8 * 16 * GCO);
+          const int rr = q * 32 + lane, trow = rr / TW, tcol = rr % TW;
+          named_sync128(9 + g);                          // last tile's reads are done
+#pragma unroll
+          for (int ky = 1; ky < C::KH; ++ky)
+#pragma unroll
+            for (int i = 0; i < GCO; i += 4)
+              *reinterpret_cast<float4*>(hx + (((ky - 1) * 8 + trow) * 16 + tcol) * GCO + i) =
+                  make_float4(h[ky][i], h[ky][i + 1], h[ky][i + 2], h[ky][i + 3]);
+          named_sync128(9 + g);                          // this tile's partial rows stored
+          if (NNB_TC_DBG & 16) continue;
+          const int img = mb / TPI, tt = mb % TPI;
+          const int oy = (tt / TX) * THO + trow, ox = (tt % TX) * OW + tcol;
+          if (trow < THO && tcol < OW && img < n && oy < C::HO && ox < C::WO) {
+            float y[GCO];
+#pragma unroll
+            for (int i = 0; i < GCO; ++i) {
+              float v = h[0][i];
+#pragma unroll
+              for (int ky = 1; ky < C::KH; ++ky)
+                v += hx[(((ky - 1) * 8 + trow + ky) * 16 + tcol) * GCO + i];
+              const int col = g * GCO + i;
+              y[i] = finish<C::ACT, EMODE, C::POST>(v + __ldg(bias + col), ps, po, col);
+            }
+            float* dst = out + (long long)img * (C::OUT_IMG / 4) + ((long long)oy * C::WO + ox) * C::CO +
+                         g * GCO;
+#pragma unroll
+            for (int i = 0; i < GCO; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+          }
+          continue;
         }
         if constexpr (KP) {
           // ---- packed horizontal taps: reduce chunks, combine across lanes ----

@@ -220,7 +220,7 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 kpack=True, kpack9=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
@@ -239,6 +239,7 @@ class Specializer:
         self.narrow = narrow
         self.aldg = aldg
         self.kpack = kpack
+        self.kpack9 = kpack9
         self.epi_tma = epi_tma
         self.csplit = csplit
         self.split_rn = split_rn
@@ -453,11 +454,11 @@ class Specializer:
             if n_tc <= self.max_batch:
                 conv = None
                 if tc_conv:
-                    conv = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, KW=KW, PT=PT, PL=PL,
+                    conv = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, KH=KH, KW=KW, PT=PT, PL=PL,
                                 POOL=pool_fused, PHO=PHO, PWO=PWO, C0=C0,
                                 CONCAT=concat, UPF=UPF)
                 if tc_dwf:
-                    conv = dict(H=HO, W=WO, CI=CI, HO=HO, WO=WO, KW=1, PT=0, PL=0,
+                    conv = dict(H=HO, W=WO, CI=CI, HO=HO, WO=WO, KH=1, KW=1, PT=0, PL=0,
                                 POOL=False, PHO=1, PWO=1, C0=CI, CONCAT=False, UPF=1, DWF=1)
                 self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
                               rows_geo=dict(HO=HO, WO=WO, UPF=UPF),
@@ -634,12 +635,24 @@ class Specializer:
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
-        # narrow outputs: pack the horizontal taps into N (3x fewer MMAs)
+        # narrow outputs: pack all KH x KW taps into N (KP9: N = 144 for CO = 16,
+        # K = CI, each input pixel loaded and split once per tile), else the
+        # horizontal taps (KPACK: N = KW * CO, K = KH * CI)
         kw = u.kernel_hw[1] if conv else 1
-        kpack = bool(conv and self.kpack and CO % 16 == 0 and kw * CO <= 128 and kw > 1
+        kh_ = u.kernel_hw[0] if conv else 1
+        kp9 = bool(conv and self.kpack9 and CO == 16 and kh_ * kw * CO <= 256 and 1 < kh_ <= 3
+                   and 1 < kw <= 3 and not conv["POOL"] and u.residual_id is None
+                   and conv.get("UPF", 1) == 1 and not conv.get("DWF") and u.dual_pool is None
+                   and conv["CI"] % 32 == 0 and conv["C0"] % 32 == 0)
+        kpack = bool(conv and self.kpack and not kp9 and CO % 16 == 0 and kw * CO <= 128 and kw > 1
                      and (CO == 16 or CO % 32 == 0)
                      and not conv["POOL"] and u.residual_id is None)
         CO_real = CO
+        if kp9:
+            ci = conv["CI"]
+            wmat = (np.asarray(wmat, F32).reshape(kh_, kw, ci, CO).transpose(2, 0, 1, 3)
+                    .reshape(ci, kh_ * kw * CO))          # [ci][(ky*KW+kx)*CO+co]
+            K, CO = ci, kh_ * kw * CO
         if kpack:
             kh = u.kernel_hw[0]
             ci = conv["CI"]
@@ -647,7 +660,7 @@ class Specializer:
                     .reshape(kh * ci, kw * CO))           # [ky*CI+ci][kx*CO+co]
             K, CO = kh * ci, kw * CO
         BN = min(128, -(-CO // 16) * 16) if CO < 32 else min(128, -(-CO // 32) * 32)
-        if kpack:
+        if kpack or kp9:
             BN = CO
         # N = 256 tiles for wide row GEMMs whose K fits one accumulator chunk:
         # a kind::tf32 MMA costs ~1.4x at N = 256 what it costs at N = 128
@@ -690,7 +703,7 @@ class Specializer:
         if wide:
             BK = self.wide_bk
             sw = 3 if BK == 32 else 2
-        csplit = self.csplit
+        csplit = self.csplit and not kp9      # KP9: N = 144, two buffers fit only merged
         # k-blocks (of 32) per TMEM accumulator chunk: every chunk ends in a
         # drain the MMAs wait for (one accumulator buffer at BN = 128), so
         # long chunks are faster; the tensor core truncates once per MMA, so
@@ -738,7 +751,7 @@ class Specializer:
         # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
         res = u.residual_id is not None
         egrp = max(1, (BN // 2 if BN >= 32 else 16) // 16)
-        epi_tma = bool(self.epi_tma and not kpack and CO % 4 == 0 and (not res or egrp <= 2)
+        epi_tma = bool(self.epi_tma and not kpack and not kp9 and CO % 4 == 0 and (not res or egrp <= 2)
                        and not (conv and conv["POOL"])
                        and (conv or not rows_geo or rows_geo.get("UPF", 1) == 1)
                        and (not conv or conv.get("UPF", 1) == 1))
@@ -775,13 +788,13 @@ class Specializer:
         # 0.892 -> 0.834 ms, cfg0/2/3 unchanged)
         conv_w4 = bool(cb16 and not wide and self.cb16_w4)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(bf16_corr_words(hi, lo) if cb16 else lo)
-        geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KW=1, PT=0, PL=0, PHO=1, PWO=1,
-                   C0=1, CONCAT=0, UPF=1, DWF=0)
+        geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KH=1, KW=1, PT=0, PL=0, PHO=1,
+                   PWO=1, C0=1, CONCAT=0, UPF=1, DWF=0)
         if conv:
             geo.update(conv, CONV=1)
         elif rows_geo:
             geo.update(rows_geo)
-        fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
+        fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, KP9=kp9, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
@@ -872,8 +885,9 @@ class Specializer:
             fields.update(HEAD=0, HN=1, H_ACT=0, H_POST=0, H_PS_OFF=0, H_PO_OFF=0, H_SOFTMAX=0,
                           H_SMEXP=0, H_OUT_OFF=0)
         if conv:
-            ow = 16 - (kw - 1) if kpack else 16
-            tpi = -(-conv["HO"] // 8) * -(-conv["WO"] // ow)
+            ow = 16 - (kw - 1) if (kpack or kp9) else 16
+            tho = 8 - (kh_ - 1) if kp9 else 8
+            tpi = -(-conv["HO"] // tho) * -(-conv["WO"] // ow)
             ipi, ipb = tpi, 2 if pair else 1
             tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
         else:
@@ -889,6 +903,7 @@ class Specializer:
                        f" chains {NACC} bufs {ABUF}{'' if csplit else ' merged-corr'}"
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
+                       f"{' all taps packed in N' if kp9 else ''}"
                        f"{' depthwise fused' if dwf else ''}"
                        f"{' 8x16-pixel conv tiles' if conv else ' row tiles'}"
                        f"{' concat (2 A maps)' if conv and conv.get('CONCAT') else ''}"

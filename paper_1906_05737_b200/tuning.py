@@ -43,6 +43,7 @@ class Tuning:
     nacc: object = None            # accumulator chains per buffer
     aldg: bool = False             # A via cp.async instead of TMA
     kpack: bool = True             # pack KW taps of narrow convs into N
+    kpack9: bool = True            # pack all KH x KW taps of CO = 16 convs into N (N = 144)
     epi_tma: bool = True           # TMA-store epilogue
     csplit: bool = True            # separate correction-product chain
     chunk: object = None           # k-blocks per accumulator chunk
