@@ -766,60 +766,6 @@ struct GemmTc {
             tc_fence_after();
           }
           const u32 dbuf = tmem + acc * ACC_COLS;
-          if constexpr (CB16 && WIDE && !NNB_CB16_WB) {
-            // N = 256 BF16-correction row tiles (measured: Dense 1024->512
-            // 0.2185 -> 0.2142 ms, 512->256 0.0722 -> 0.0709 ms; the narrow
-            // conv tiles got slower with it: cfg4 0.286 -> 0.313 ms, so they
-            // keep the joint issue below): the main product a_hi*b_hi reads the raw
-            // A tile (the tensor core truncates it to TF32), so it is issued as
-            // soon as the TMA lands, while the split warps build A_corr; the
-            // correction MMA follows on lo_ready.  Same accumulation order per
-            // chain as issuing both after lo_ready -- bit-identical results,
-            // and the split leaves the ring's critical path.
-            mbar_wait(&full[s], ph);
-            tc_fence_after();
-            if (lane == 0) {
-              const u32 base = smem_u32(smem + s * STAGE);
-              const u32 b_hi = base + A_SMEM;
-#pragma unroll
-              for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
-                const u32 o = k * 32;
-                const int ks = kc * (BK / 8) + k;
-                const u32 d = dbuf + (ks % NACC) * CW;
-                if (PAIR) mma_tf32_pair(d, kmajor_desc<ROWB>(base + o), kmajor_desc<ROWB>(b_hi + o), IDESC, ks >= NACC);
-                else mma_tf32(d, kmajor_desc<ROWB>(base + o), kmajor_desc<ROWB>(b_hi + o), IDESC, ks >= NACC);
-              }
-            }
-            __syncwarp();
-            mbar_wait(&lo_ready[s], ph);
-            tc_fence_after();
-            if (lane == 0) {
-              const u32 base = smem_u32(smem + s * STAGE);
-              const u32 a_lo = base + A_BYTES, b_lo = base + A_SMEM + B_BYTES;
-#pragma unroll
-              for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
-                const u32 o = k * 32;
-                const int ks = kc * (BK / 8) + k;
-                const u32 dc = dbuf + (ks % NACC) * CW + C::BN;
-                const u32 acc_c = C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : (u32)(ks >= NACC);
-                if (PAIR) mma_bf16_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
-                else mma_bf16(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
-              }
-              if (PAIR) {
-                mma_commit_pair(&empty[s]);
-                if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit_pair(&tfull[acc]);
-              } else {
-                mma_commit(&empty[s]);
-                if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
-              }
-            }
-            __syncwarp();
-            if (++s == C::NS) { s = 0; ph ^= 1; }
-            if (kc == CHUNK_KB - 1 || kb == KB - 1) {
-              if (++acc == ABUF) { acc = 0; aph ^= 1; }
-            }
-            continue;
-          }
           if (AL) mbar_wait(&full[s], ph);           // B (TMA); A comes via lo_ready
           mbar_wait(&lo_ready[s], ph);
           tc_fence_after();
