@@ -11,3 +11,4 @@
 #include "nnb_conv_direct.cuh"
 #include "nnb_chain.cuh"
 #include "nnb_tcchain.cuh"
+#include "nnb_tiny.cuh"

@@ -62,7 +62,10 @@ SEP_BLOCK = 128
 # weights and a rolled kernel-row loop keep NVRTC under the compile budget
 DIRECT_UNROLL_MAX = 2048
 DIRECT_SPLIT_MAX = 2304
-CB16_CONV_MIN_K = 128     # conv tiles from this K take the BF16 correction products   # ... and with a pool window split over two lanes
+CB16_CONV_MIN_K = 128     # conv tiles from this K take the BF16 correction products
+TINY_MAX_N = 64           # batches up to this run the whole net as one TinyNet launch ...
+TINY_ARENA_MAX = 160 * 1024   # ... when the per-image arena fits shared memory
+TINY_WEIGHTS_MAX = 512 * 1024  # ... and the weights are small   # ... and with a pool window split over two lanes
 
 
 @dataclass
@@ -106,6 +109,14 @@ class DevicePool:
 
     def zeros_offset(self, n):
         return self.add(np.zeros(max(n, 1), F32))
+
+    def mark(self):
+        return len(self.data), dict(self._seen)
+
+    def rollback(self, mark):
+        """Forget every entry added since ``mark``."""
+        self.data = self.data[:mark[0]]
+        self._seen = mark[1]
 
 
 @dataclass
@@ -220,7 +231,7 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, kpack9=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 kpack=True, kpack9=True, tiny=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
@@ -240,6 +251,7 @@ class Specializer:
         self.aldg = aldg
         self.kpack = kpack
         self.kpack9 = kpack9
+        self.tiny = tiny
         self.epi_tma = epi_tma
         self.csplit = csplit
         self.split_rn = split_rn
@@ -256,6 +268,7 @@ class Specializer:
         self.rn_ss = rn_ss
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self._dual_from = 1 << 30     # lowest batch whose conv launch stores the dual pool
+        self._n_floor = 1             # regular launches serve batches >= this (TinyNet below)
         self.chunk = chunk
         self.nacc = nacc
         self.tmem_a = tmem_a
@@ -283,6 +296,10 @@ class Specializer:
              tmaps=(), grid_cap=0, cluster=1, code=""):
         if self._n_cap is not None:          # batches above the cap run fused elsewhere
             n_max = min(n_max, self._n_cap)
+            if n_min > n_max:
+                return
+        if self._n_floor > 1:                # batches below the floor run as one TinyNet launch
+            n_min = max(n_min, self._n_floor)
             if n_min > n_max:
                 return
         kname = f"nnb_u{unit_pos:02d}_{tag}_{len(self.names)}"
@@ -980,6 +997,129 @@ class Specializer:
                   32 * KS, 0, rows, MB, grid_mult=nj, n_min=n_min, n_max=n_max,
                   note=f"split-K rows K={K} N={CO} ks={KS} rows/block {MB}")
 
+    def _tiny_step(self, i, u):
+        """(struct text, call) of one unit inside the TinyNet kernel, or None
+        when the unit kind / fusion is outside it."""
+        off = lambda t: self.asg.offsets[t][0]
+        ep = lambda co: self.epilogue_fields(u, co)
+        res = off(u.residual_id) if u.residual_id is not None else -1
+        if u.kind == "Conv2D":
+            if u.dw is not None or u.concat_in or u.upsample_after != 1 or u.softmax_after:
+                return None
+            H, W, CI = u.input_shapes[0].dims
+            co = u.kernel.shape[3]
+            pre = u.pre_pool_shape if u.pool_after else u.output_shape
+            HO, WO = pre.h, pre.w
+            KH, KW = u.kernel_hw
+            PT = same_padding(H, KH, u.stride)[0] if u.padding == "same" else 0
+            PL = same_padding(W, KW, u.stride)[0] if u.padding == "same" else 0
+            f = dict(H=H, W=W, CI=CI, HO=HO, WO=WO, CO=co, KH=KH, KW=KW, S=u.stride, PT=PT, PL=PL,
+                     POOL=u.pool_after, PHO=u.output_shape.h, PWO=u.output_shape.w,
+                     IN=off(u.input_ids[0]), OUT=off(u.output_id), RES=res,
+                     W_OFF=self.pool.add(np.asarray(u.kernel, F32)), B_OFF=self.pool.add(u.bias),
+                     **ep(co))
+            return f, "TinyConv"
+        if u.kind == "DepthwiseConv2D":
+            if (u.residual_id is not None or u.pool_after or u.upsample_after != 1
+                    or u.softmax_after):
+                return None
+            H, W, C = u.input_shapes[0].dims
+            HO, WO, _ = u.output_shape.dims
+            KH, KW = u.kernel_hw
+            PT = same_padding(H, KH, u.stride)[0] if u.padding == "same" else 0
+            PL = same_padding(W, KW, u.stride)[0] if u.padding == "same" else 0
+            f = dict(H=H, W=W, C=C, HO=HO, WO=WO, KH=KH, KW=KW, S=u.stride, PT=PT, PL=PL,
+                     IN=off(u.input_ids[0]), OUT=off(u.output_id), W_OFF=self.pool.add(u.kernel),
+                     B_OFF=self.pool.add(u.bias), **ep(C))
+            return f, "TinyDw"
+        if u.kind == "Dense":
+            K, CO = u.kernel.shape
+            if u.softmax_after and CO > 32:
+                return None
+            f = dict(K=K, CO=CO, IN=off(u.input_ids[0]), OUT=off(u.output_id), RES=res,
+                     W_OFF=self.pool.add(np.asarray(u.kernel, F32)), B_OFF=self.pool.add(u.bias),
+                     SOFTMAX=bool(u.softmax_after), SMEXP=SMEXP_CODE[self.opt.softmax_exp], **ep(CO))
+            return f, "TinyDense"
+        if u.kind == "Pool":
+            if u.upsample_after != 1 or u.input_shapes[0].rank != 3:
+                return None
+            H, W, C = u.input_shapes[0].dims
+            o = u.output_shape
+            HO, WO = (1, 1) if o.rank == 1 else (o.h, o.w)
+            PH, PW = u.kernel_hw
+            PT = same_padding(H, PH, u.stride)[0] if u.padding == "same" else 0
+            PL = same_padding(W, PW, u.stride)[0] if u.padding == "same" else 0
+            f = dict(H=H, W=W, C=C, HO=HO, WO=WO, PH=PH, PW=PW, S=u.stride, PT=PT, PL=PL,
+                     AVG=u.pool_op == "avg", IN=off(u.input_ids[0]), OUT=off(u.output_id))
+            return f, "TinyPool"
+        if u.kind in ("ElementwiseActivation", "Add"):
+            if len(u.input_ids) > 4:
+                return None
+            ins = [off(t) for t in u.input_ids] + [0] * (4 - len(u.input_ids))
+            aff = u.scale is not None
+            f = dict(N=u.output_shape.elements, C=u.output_shape.c, NIN=len(u.input_ids),
+                     IN0=ins[0], IN1=ins[1], IN2=ins[2], IN3=ins[3], OUT=off(u.output_id),
+                     AFFINE=aff, SC_OFF=self.pool.add(u.scale) if aff else 0,
+                     OF_OFF=self.pool.add(u.offset) if aff else 0,
+                     ACT=ACT_CODE[u.activation], MODE=MODE_CODE[self.opt.activation_mode])
+            return f, "TinyElem"
+        if u.kind == "Softmax":
+            if u.output_shape.rank != 1 or u.output_shape.elements > 32:
+                return None
+            f = dict(L=u.output_shape.elements, IN=off(u.input_ids[0]), OUT=off(u.output_id),
+                     SMEXP=SMEXP_CODE[self.opt.softmax_exp])
+            return f, "TinySoftmax"
+        return None
+
+    def _tiny(self):
+        """The whole network as ONE launch for batches up to TINY_MAX_N (one
+        CTA per image over a shared-memory copy of its arena;
+        nnb_tiny.cuh) when every unit has a TinyNet step, the per-image
+        arena fits shared memory and the weights are small (read through
+        L1).  Regular launches then serve the larger batches only."""
+        if (self.asg.arena_size > TINY_ARENA_MAX or not self.plan.units
+                or len(self.plan.units) < 2):
+            return
+        wbytes = sum(4 * a.size for u in self.plan.units
+                     for a in (u.kernel, u.bias, u.post_scale, u.post_offset, u.scale, u.offset)
+                     if a is not None)
+        if wbytes > TINY_WEIGHTS_MAX:
+            return
+        pool_mark = self.pool.mark()
+        steps = []
+        for i, u in enumerate(self.plan.units):
+            st = self._tiny_step(i, u)
+            if st is None:
+                self.pool.rollback(pool_mark)   # nothing of it is referenced
+                return
+            steps.append(st)
+        n_max = min(self.max_batch, TINY_MAX_N)
+        structs = [_cfg_struct(f"T{i}", f).replace("\n", "\n  ") for i, (f, _) in enumerate(steps)]
+        body = ["  __device__ static __forceinline__ void body(const float* __restrict__ pool, "
+                "float* a) {"]
+        for i, (_, t) in enumerate(steps):
+            body += [f"    nnb::{t}<T{i}>::run(pool, a);", "    __syncthreads();"]
+        body.append("  }")
+
+        def copies(tids, load):
+            lines = [f"  __device__ static __forceinline__ void {'load' if load else 'store'}("
+                     "float* __restrict__ arena, int img, float* a) {"]
+            for t in tids:
+                o, b = self.asg.offsets[t][0], self.img_bytes(t)
+                g = f"nnb::at<float>(arena, {self.arena_off(t)}LL + (long long)img * {b}LL)"
+                lines.append(f"    nnb::tiny_copy<{b}>({'a + ' + str(o // 4) if load else g}, "
+                             f"{g if load else 'a + ' + str(o // 4)});")
+            lines.append("  }")
+            return lines
+        code = "\n".join(["  " + x for x in structs] + body + copies(self.plan.input_ids, True)
+                         + copies(self.plan.output_ids, False))
+        arena_floats = -(-self.asg.arena_size // 16) * 4
+        self.emit(0, "tinynet", "nnb::TinyNet", dict(ARENA_FLOATS=arena_floats), 256,
+                  4 * arena_floats, 1, 1, dynamic_smem=True, n_max=n_max, code=code,
+                  note=f"whole network ({len(steps)} units) in one launch, one CTA per image, "
+                       f"{self.asg.arena_size // 1024} KB arena in shared memory")
+        self._n_floor = n_max + 1
+
     def chain(self, pos, u):
         """A run of small depthwise / pointwise convs (+ closing global average
         pool) in one kernel, one CTA per image (nnb_chain.cuh,
@@ -1254,6 +1394,8 @@ class Specializer:
                   ELEM_BLOCK)
 
     def run(self):
+        if self.tiny and not self.mega:
+            self._tiny()
         for pos, u in enumerate(self.plan.units):
             self._n_cap = self.head_cap.get(pos)
             if u.kind in ("Dense", "Conv2D"):

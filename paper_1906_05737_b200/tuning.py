@@ -44,6 +44,7 @@ class Tuning:
     aldg: bool = False             # A via cp.async instead of TMA
     kpack: bool = True             # pack KW taps of narrow convs into N
     kpack9: bool = True            # pack all KH x KW taps of CO = 16 convs into N (N = 144)
+    tiny: bool = True              # small nets at small batches as one TinyNet launch
     epi_tma: bool = True           # TMA-store epilogue
     csplit: bool = True            # separate correction-product chain
     chunk: object = None           # k-blocks per accumulator chunk

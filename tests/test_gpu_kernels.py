@@ -772,3 +772,35 @@ def test_tc_chain_vs_oracle(case, n):
     unf, net3 = gpu(m, wt, x)
     assert "TcChain" not in [u.kind for u in net3.plan.units]
     np.testing.assert_allclose(got, unf, **TOL)
+
+
+@pytest.mark.parametrize("n", [1, 3, 64])
+@pytest.mark.parametrize("opts", [EXACT, ApproximationOptions()], ids=["exact", "default"])
+def test_tinynet_whole_network_launch(n, opts):
+    """kernels.Specializer._tiny / nnb_tiny.cuh: cfg0 and a small net with a
+    residual, BatchNorm, depthwise, avg-pool, padding-valid stride-2 conv and a
+    softmax run as ONE launch at small batches, against the oracle."""
+    nets = [zoo.build(0)]
+    rng = np.random.default_rng(n)
+    b = NetBuilder()
+    x = b.input((12, 10, 4))
+    c1 = b.layer("Conv2D", [x], {"filters": 8, "kernel_size": 3, "padding": "same", "activation": "relu"},
+                 [("kernel", he(rng, (3, 3, 4, 8), 36)), ("bias", (rng.standard_normal(8) * .1).astype(F32))])
+    d = b.layer("DepthwiseConv2D", [c1], {"kernel_size": 3, "padding": "same", "activation": "tanh"},
+                [("kernel", he(rng, (3, 3, 8), 9)), ("bias", (rng.standard_normal(8) * .1).astype(F32))])
+    a = b.layer("Add", [c1, d])
+    bn = b.layer("BatchNorm", [a], None, bn_params(rng, 8))
+    c2 = b.layer("Conv2D", [bn], {"filters": 6, "kernel_size": 3, "strides": 2, "padding": "valid",
+                                  "activation": "sigmoid"},
+                 [("kernel", he(rng, (3, 3, 8, 6), 72)), ("bias", np.zeros(6, F32))])
+    p = b.layer("AvgPool2D", [c2], {"pool_size": 2, "strides": 1})
+    f = b.layer("Flatten", [p])
+    y = b.layer("Dense", [f], {"units": 7, "activation": "linear"},
+                [("kernel", he(rng, (3 * 3 * 6, 7), 54)), ("bias", np.zeros(7, F32))])
+    nets.append(b.build([b.layer("Softmax", [y])]))
+    for k, (m, w) in enumerate(nets):
+        xin = (zoo.inputs(0, n) if k == 0 else rng.uniform(-2, 2, (n, 12, 10, 4)).astype(F32))
+        got, net = gpu(m, w, xin, opts)
+        act = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
+        assert [("tinynet" in l.kernel) for l in act] == [True], [l.kernel for l in act]
+        np.testing.assert_allclose(got, ref(m, w, xin, "exact" if opts == EXACT else opts), **TOL)
