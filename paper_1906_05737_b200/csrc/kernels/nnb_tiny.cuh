@@ -45,49 +45,53 @@ struct TinyConv {
     const float* po = at<float>(pool, S::PO_OFF);
     constexpr int NP = S::POOL ? 4 : 1;
     constexpr int ITEMS = (S::POOL ? S::PHO * S::PWO : S::HO * S::WO) * CQ;
+    static_assert(S::CO % 4 == 0, "tiny conv: channel quads");
     for (int it = threadIdx.x; it < ITEMS; it += blockDim.x) {
       const int q = it % CQ, pix = it / CQ, co = 4 * q;
       const int py = S::POOL ? pix / S::PWO : pix / S::WO, px = S::POOL ? pix % S::PWO : pix % S::WO;
-      float bias[4], m[4];
+      // a thread owns a channel quad of NP pixels (a whole pool window): each
+      // tap's weight quad is one float4 load feeding 4*NP FFMAs
+      float acc[NP][4];
+      {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bs + co));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        bias[j] = co + j < S::CO ? __ldg(bs + co + j) : 0.f;
-        m[j] = 0.f;
+        for (int p = 0; p < NP; ++p) {
+          acc[p][0] = b4.x; acc[p][1] = b4.y; acc[p][2] = b4.z; acc[p][3] = b4.w;
+        }
       }
-      // the pixels of a pool window one after the other (rolled: NVRTC time);
-      // each is finished (activation / post-BN) before the max, as unfused
-#pragma unroll 1
-      for (int p = 0; p < NP; ++p) {
-        const int oy = S::POOL ? 2 * py + p / 2 : py, ox = S::POOL ? 2 * px + p % 2 : px;
-        float acc[4] = {bias[0], bias[1], bias[2], bias[3]};
-        for (int ky = 0; ky < S::KH; ++ky) {
-          const int iy = oy * S::S - S::PT + ky;
-          if (iy < 0 || iy >= S::H) continue;
-          for (int kx = 0; kx < S::KW; ++kx) {
-            const int ix = ox * S::S - S::PL + kx;
-            if (ix < 0 || ix >= S::W) continue;
-            const float* xin = in + (iy * S::W + ix) * S::CI;
-            const float* wr = wk + ((ky * S::KW + kx) * S::CI) * S::CO + co;
-#pragma unroll 4
-            for (int ci = 0; ci < S::CI; ++ci) {
-              const float x = xin[ci];
+      for (int ky = 0; ky < S::KH; ++ky) {
+        for (int kx = 0; kx < S::KW; ++kx) {
+          int off[NP];
+          bool ok[NP];
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (co + j < S::CO) acc[j] = fmaf(x, __ldg(wr + ci * S::CO + j), acc[j]);
+          for (int p = 0; p < NP; ++p) {
+            const int oy = S::POOL ? 2 * py + p / 2 : py, ox = S::POOL ? 2 * px + p % 2 : px;
+            const int iy = oy * S::S - S::PT + ky, ix = ox * S::S - S::PL + kx;
+            ok[p] = iy >= 0 && iy < S::H && ix >= 0 && ix < S::W;
+            off[p] = ok[p] ? (iy * S::W + ix) * S::CI : 0;
+          }
+          const float* wr = wk + ((ky * S::KW + kx) * S::CI) * S::CO + co;
+#pragma unroll 2
+          for (int ci = 0; ci < S::CI; ++ci) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(wr + ci * S::CO));
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+              if (ok[p]) {
+                const float x = in[off[p] + ci];
+                acc[p][0] = fmaf(x, w4.x, acc[p][0]); acc[p][1] = fmaf(x, w4.y, acc[p][1]);
+                acc[p][2] = fmaf(x, w4.z, acc[p][2]); acc[p][3] = fmaf(x, w4.w, acc[p][3]);
+              }
             }
           }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float y = finish<S::ACT, S::MODE, S::POST>(acc[j], ps, po, co + j < S::CO ? co + j : 0);
-          m[j] = p == 0 ? y : fmaxf(m[j], y);
-        }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (co + j >= S::CO) continue;
+        float y = finish<S::ACT, S::MODE, S::POST>(acc[0][j], ps, po, co + j);
+#pragma unroll
+        for (int p = 1; p < NP; ++p) y = fmaxf(y, finish<S::ACT, S::MODE, S::POST>(acc[p][j], ps, po, co + j));
         const int o = pix * S::CO + co + j;
-        out[o] = S::RES >= 0 ? add(m[j], a[S::RES / 4 + o]) : m[j];
+        out[o] = S::RES >= 0 ? add(y, a[S::RES / 4 + o]) : y;
       }
     }
   }
@@ -124,32 +128,47 @@ struct TinyDw {
 };
 
 // Dense K -> CO (+ residual, + softmax over the row when SOFTMAX, CO <= 32).
-// A warp per output: lanes split K, partial sums added in a fixed tree order.
+// Lanes take 32 consecutive outputs (coalesced weight rows), the 8 warps
+// split K into slices whose partial sums are added in slice order after the
+// bias.
 // S: K, CO, IN, OUT, RES, W_OFF (K, CO), B_OFF, ACT, MODE, POST, PS_OFF,
 //    PO_OFF, SOFTMAX, SMEXP
 template <class S>
 struct TinyDense {
   __device__ static __forceinline__ void run(const float* __restrict__ pool, float* a) {
+    __shared__ float part[8][33];
     const float* in = a + S::IN / 4;
     float* out = a + S::OUT / 4;
     const float* wk = at<float>(pool, S::W_OFF);
     const float* bs = at<float>(pool, S::B_OFF);
     const float* ps = at<float>(pool, S::PS_OFF);
     const float* po = at<float>(pool, S::PO_OFF);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int j = warp; j < S::CO; j += nw) {
-      float s = 0.f;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int KS = S::K >= 128 ? 8 : S::K >= 32 ? 4 : 1;        // K slices
+    constexpr int KL = (S::K + KS - 1) / KS;
+    for (int j0 = 0; j0 < S::CO; j0 += 32) {
+      const int j = j0 + lane;
+      if (warp < KS) {
+        float s = 0.f;
+        const int k0 = warp * KL, k1 = k0 + KL < S::K ? k0 + KL : S::K;
+        if (j < S::CO) {
 #pragma unroll 4
-      for (int k = lane; k < S::K; k += 32) s = fmaf(in[k], __ldg(wk + k * S::CO + j), s);
-      s = warp_sum(s);
-      if (lane == 0) {
-        float y = finish<S::ACT, S::MODE, S::POST>(add(__ldg(bs + j), s), ps, po, j);
+          for (int k = k0; k < k1; ++k) s = fmaf(in[k], __ldg(wk + k * S::CO + j), s);
+        }
+        part[warp][lane] = s;
+      }
+      __syncthreads();
+      if (warp == 0 && j < S::CO) {
+        float y = __ldg(bs + j);
+#pragma unroll
+        for (int sl = 0; sl < KS; ++sl) y = add(y, part[sl][lane]);
+        y = finish<S::ACT, S::MODE, S::POST>(y, ps, po, j);
         if (S::RES >= 0) y = add(y, a[S::RES / 4 + j]);
         out[j] = y;
       }
+      __syncthreads();
     }
     if constexpr (S::SOFTMAX) {
-      __syncthreads();
       if (warp == 0) {
         const float v = softmax_warp_row<S::SMEXP>(lane < S::CO ? out[lane] : 0.f, lane < S::CO);
         if (lane < S::CO) out[lane] = v;

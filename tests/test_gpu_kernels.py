@@ -796,7 +796,7 @@ def test_tinynet_whole_network_launch(n, opts):
     p = b.layer("AvgPool2D", [c2], {"pool_size": 2, "strides": 1})
     f = b.layer("Flatten", [p])
     y = b.layer("Dense", [f], {"units": 7, "activation": "linear"},
-                [("kernel", he(rng, (3 * 3 * 6, 7), 54)), ("bias", np.zeros(7, F32))])
+                [("kernel", he(rng, (4 * 3 * 6, 7), 72)), ("bias", np.zeros(7, F32))])
     nets.append(b.build([b.layer("Softmax", [y])]))
     for k, (m, w) in enumerate(nets):
         xin = (zoo.inputs(0, n) if k == 0 else rng.uniform(-2, 2, (n, 12, 10, 4)).astype(F32))
