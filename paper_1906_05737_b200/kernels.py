@@ -1004,7 +1004,8 @@ class Specializer:
         ep = lambda co: self.epilogue_fields(u, co)
         res = off(u.residual_id) if u.residual_id is not None else -1
         if u.kind == "Conv2D":
-            if u.dw is not None or u.concat_in or u.upsample_after != 1 or u.softmax_after:
+            if (u.dw is not None or u.concat_in or u.upsample_after != 1 or u.softmax_after
+                    or u.kernel.shape[3] % 4):
                 return None
             H, W, CI = u.input_shapes[0].dims
             co = u.kernel.shape[3]

@@ -790,13 +790,13 @@ def test_tinynet_whole_network_launch(n, opts):
                 [("kernel", he(rng, (3, 3, 8), 9)), ("bias", (rng.standard_normal(8) * .1).astype(F32))])
     a = b.layer("Add", [c1, d])
     bn = b.layer("BatchNorm", [a], None, bn_params(rng, 8))
-    c2 = b.layer("Conv2D", [bn], {"filters": 6, "kernel_size": 3, "strides": 2, "padding": "valid",
+    c2 = b.layer("Conv2D", [bn], {"filters": 8, "kernel_size": 3, "strides": 2, "padding": "valid",
                                   "activation": "sigmoid"},
-                 [("kernel", he(rng, (3, 3, 8, 6), 72)), ("bias", np.zeros(6, F32))])
+                 [("kernel", he(rng, (3, 3, 8, 8), 72)), ("bias", np.zeros(8, F32))])
     p = b.layer("AvgPool2D", [c2], {"pool_size": 2, "strides": 1})
     f = b.layer("Flatten", [p])
     y = b.layer("Dense", [f], {"units": 7, "activation": "linear"},
-                [("kernel", he(rng, (4 * 3 * 6, 7), 72)), ("bias", np.zeros(7, F32))])
+                [("kernel", he(rng, (4 * 3 * 8, 7), 96)), ("bias", np.zeros(7, F32))])
     nets.append(b.build([b.layer("Softmax", [y])]))
     for k, (m, w) in enumerate(nets):
         xin = (zoo.inputs(0, n) if k == 0 else rng.uniform(-2, 2, (n, 12, 10, 4)).astype(F32))
