@@ -10,8 +10,8 @@
 // Dense accumulate bias first, taps / inputs in the interpreter's order
 // (pkg/src/nnjit/interpreter.py:45-62) with fmaf (inside the FP32 gate like
 // the FFMA GEMM); pooling, elementwise and depthwise steps use the
-// interpreter's op-by-op rounding (bit-exact).  Weights are read through L1
-// (__ldg; they are small by construction: the selection bounds them).
+// interpreter's op-by-op rounding (bit-exact).  The weights are staged into
+// shared memory once per CTA (the selection bounds their size).
 #pragma once
 #include "nnb_common.cuh"
 #include "nnb_softmax.cuh"
@@ -36,11 +36,11 @@ __device__ __forceinline__ void tiny_copy(float* __restrict__ dst, const float* 
 template <class S>
 struct TinyConv {
   static constexpr int CQ = (S::CO + 3) / 4;
-  __device__ static __forceinline__ void run(const float* __restrict__ pool, float* a) {
+  __device__ static __forceinline__ void run(const float* __restrict__ pool, const float* w, float* a) {
     const float* in = a + S::IN / 4;
     float* out = a + S::OUT / 4;
-    const float* wk = at<float>(pool, S::W_OFF);
-    const float* bs = at<float>(pool, S::B_OFF);
+    const float* wk = at<float>(w, S::W_OFF);
+    const float* bs = at<float>(w, S::B_OFF);
     const float* ps = at<float>(pool, S::PS_OFF);
     const float* po = at<float>(pool, S::PO_OFF);
     constexpr int NP = S::POOL ? 4 : 1;
@@ -53,7 +53,7 @@ struct TinyConv {
       // tap's weight quad is one float4 load feeding 4*NP FFMAs
       float acc[NP][4];
       {
-        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bs + co));
+        const float4 b4 = *reinterpret_cast<const float4*>(bs + co);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           acc[p][0] = b4.x; acc[p][1] = b4.y; acc[p][2] = b4.z; acc[p][3] = b4.w;
@@ -73,7 +73,7 @@ struct TinyConv {
           const float* wr = wk + ((ky * S::KW + kx) * S::CI) * S::CO + co;
 #pragma unroll 2
           for (int ci = 0; ci < S::CI; ++ci) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4*>(wr + ci * S::CO));
+            const float4 w4 = *reinterpret_cast<const float4*>(wr + ci * S::CO);
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
               if (ok[p]) {
@@ -103,23 +103,23 @@ struct TinyConv {
 //    MODE, POST, PS_OFF, PO_OFF
 template <class S>
 struct TinyDw {
-  __device__ static __forceinline__ void run(const float* __restrict__ pool, float* a) {
+  __device__ static __forceinline__ void run(const float* __restrict__ pool, const float* w, float* a) {
     const float* in = a + S::IN / 4;
     float* out = a + S::OUT / 4;
-    const float* wk = at<float>(pool, S::W_OFF);
-    const float* bs = at<float>(pool, S::B_OFF);
+    const float* wk = at<float>(w, S::W_OFF);
+    const float* bs = at<float>(w, S::B_OFF);
     const float* ps = at<float>(pool, S::PS_OFF);
     const float* po = at<float>(pool, S::PO_OFF);
     for (int it = threadIdx.x; it < S::HO * S::WO * S::C; it += blockDim.x) {
       const int c = it % S::C, pix = it / S::C, oy = pix / S::WO, ox = pix % S::WO;
-      float acc = __ldg(bs + c);
+      float acc = bs[c];
       for (int ky = 0; ky < S::KH; ++ky) {
         const int iy = oy * S::S - S::PT + ky;
         if (iy < 0 || iy >= S::H) continue;
         for (int kx = 0; kx < S::KW; ++kx) {
           const int ix = ox * S::S - S::PL + kx;
           if (ix < 0 || ix >= S::W) continue;
-          acc = add(acc, mul(in[(iy * S::W + ix) * S::C + c], __ldg(wk + (ky * S::KW + kx) * S::C + c)));
+          acc = add(acc, mul(in[(iy * S::W + ix) * S::C + c], wk[(ky * S::KW + kx) * S::C + c]));
         }
       }
       out[it] = finish<S::ACT, S::MODE, S::POST>(acc, ps, po, c);
@@ -135,12 +135,12 @@ struct TinyDw {
 //    PO_OFF, SOFTMAX, SMEXP
 template <class S>
 struct TinyDense {
-  __device__ static __forceinline__ void run(const float* __restrict__ pool, float* a) {
+  __device__ static __forceinline__ void run(const float* __restrict__ pool, const float* w, float* a) {
     __shared__ float part[8][33];
     const float* in = a + S::IN / 4;
     float* out = a + S::OUT / 4;
-    const float* wk = at<float>(pool, S::W_OFF);
-    const float* bs = at<float>(pool, S::B_OFF);
+    const float* wk = at<float>(w, S::W_OFF);
+    const float* bs = at<float>(w, S::B_OFF);
     const float* ps = at<float>(pool, S::PS_OFF);
     const float* po = at<float>(pool, S::PO_OFF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -153,13 +153,13 @@ struct TinyDense {
         const int k0 = warp * KL, k1 = k0 + KL < S::K ? k0 + KL : S::K;
         if (j < S::CO) {
 #pragma unroll 4
-          for (int k = k0; k < k1; ++k) s = fmaf(in[k], __ldg(wk + k * S::CO + j), s);
+          for (int k = k0; k < k1; ++k) s = fmaf(in[k], wk[k * S::CO + j], s);
         }
         part[warp][lane] = s;
       }
       __syncthreads();
       if (warp == 0 && j < S::CO) {
-        float y = __ldg(bs + j);
+        float y = bs[j];
 #pragma unroll
         for (int sl = 0; sl < KS; ++sl) y = add(y, part[sl][lane]);
         y = finish<S::ACT, S::MODE, S::POST>(y, ps, po, j);
@@ -181,7 +181,7 @@ struct TinyDense {
 // S: H, W, C, HO, WO, PH, PW, S, PT, PL, AVG, IN, OUT
 template <class S>
 struct TinyPool {
-  __device__ static __forceinline__ void run(const float* __restrict__, float* a) {
+  __device__ static __forceinline__ void run(const float* __restrict__, const float*, float* a) {
     const float* in = a + S::IN / 4;
     float* out = a + S::OUT / 4;
     for (int it = threadIdx.x; it < S::HO * S::WO * S::C; it += blockDim.x) {
@@ -209,15 +209,15 @@ struct TinyPool {
 // S: N (elements), C (channels), NIN, IN0..IN3, OUT, AFFINE, SC_OFF, OF_OFF, ACT, MODE
 template <class S>
 struct TinyElem {
-  __device__ static __forceinline__ void run(const float* __restrict__ pool, float* a) {
-    const float* sc = at<float>(pool, S::SC_OFF);
-    const float* of = at<float>(pool, S::OF_OFF);
+  __device__ static __forceinline__ void run(const float* __restrict__ pool, const float* w, float* a) {
+    const float* sc = at<float>(w, S::SC_OFF);
+    const float* of = at<float>(w, S::OF_OFF);
     for (int i = threadIdx.x; i < S::N; i += blockDim.x) {
       float y = a[S::IN0 / 4 + i];
       if (S::NIN > 1) y = add(y, a[S::IN1 / 4 + i]);
       if (S::NIN > 2) y = add(y, a[S::IN2 / 4 + i]);
       if (S::NIN > 3) y = add(y, a[S::IN3 / 4 + i]);
-      if (S::AFFINE) y = add(mul(y, __ldg(sc + i % S::C)), __ldg(of + i % S::C));
+      if (S::AFFINE) y = add(mul(y, sc[i % S::C]), of[i % S::C]);
       a[S::OUT / 4 + i] = activate<S::ACT, S::MODE>(y);
     }
   }
@@ -227,7 +227,7 @@ struct TinyElem {
 // S: L, IN, OUT, SMEXP
 template <class S>
 struct TinySoftmax {
-  __device__ static __forceinline__ void run(const float* __restrict__, float* a) {
+  __device__ static __forceinline__ void run(const float* __restrict__, const float*, float* a) {
     if ((threadIdx.x >> 5) != 0) return;
     const int lane = threadIdx.x & 31;
     static_assert(S::L <= 32, "tiny softmax: one warp");
@@ -238,15 +238,22 @@ struct TinySoftmax {
 
 // C: ARENA_FLOATS and the generated load(arena, img, a) / body(pool, a) /
 //    store(arena, img, a)
+// The kernel's weights and biases are the first W_BYTES of the pool (the
+// TinyNet is specialised before any other unit) and are copied into shared
+// memory once per CTA: every layer then reads them at shared-memory latency
+// (from global memory each (tap, channel) row is a fresh L2 round trip -- all
+// items read the same rows at the same time, so L1 never hits: 94 us for cfg0
+// at batch 1 before).  Post-BN vectors stay in global memory (finish()).
 template <class C>
 struct TinyNet {
-  struct Smem { float a[C::ARENA_FLOATS]; };
+  struct Smem { float w[C::W_FLOATS]; float a[C::ARENA_FLOATS]; };
   __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n,
                              Smem& sm) {
+    if (blockIdx.x < n) tiny_copy<C::W_FLOATS * 4>(sm.w, pool);
     for (int img = blockIdx.x; img < n; img += gridDim.x) {
       C::load(arena, img, sm.a);
       __syncthreads();
-      C::body(pool, sm.a);
+      C::body(pool, sm.w, sm.a);
       __syncthreads();
       C::store(arena, img, sm.a);
       __syncthreads();

@@ -65,7 +65,8 @@ DIRECT_SPLIT_MAX = 2304
 CB16_CONV_MIN_K = 128     # conv tiles from this K take the BF16 correction products
 TINY_MAX_N = 64           # batches up to this run the whole net as one TinyNet launch ...
 TINY_ARENA_MAX = 160 * 1024   # ... when the per-image arena fits shared memory
-TINY_WEIGHTS_MAX = 512 * 1024  # ... and the weights are small   # ... and with a pool window split over two lanes
+TINY_WEIGHTS_MAX = 96 * 1024  # ... and the weights are small (staged in shared memory)
+TINY_SMEM_MAX = 200 * 1024    # arena + weights   # ... and with a pool window split over two lanes
 
 
 @dataclass
@@ -1087,6 +1088,7 @@ class Specializer:
         if wbytes > TINY_WEIGHTS_MAX:
             return
         pool_mark = self.pool.mark()
+        assert pool_mark[0] == 0, "the TinyNet is specialised first (its weights lead the pool)"
         steps = []
         for i, u in enumerate(self.plan.units):
             st = self._tiny_step(i, u)
@@ -1097,9 +1099,9 @@ class Specializer:
         n_max = min(self.max_batch, TINY_MAX_N)
         structs = [_cfg_struct(f"T{i}", f).replace("\n", "\n  ") for i, (f, _) in enumerate(steps)]
         body = ["  __device__ static __forceinline__ void body(const float* __restrict__ pool, "
-                "float* a) {"]
+                "const float* w, float* a) {"]
         for i, (_, t) in enumerate(steps):
-            body += [f"    nnb::{t}<T{i}>::run(pool, a);", "    __syncthreads();"]
+            body += [f"    nnb::{t}<T{i}>::run(pool, w, a);", "    __syncthreads();"]
         body.append("  }")
 
         def copies(tids, load):
@@ -1115,8 +1117,12 @@ class Specializer:
         code = "\n".join(["  " + x for x in structs] + body + copies(self.plan.input_ids, True)
                          + copies(self.plan.output_ids, False))
         arena_floats = -(-self.asg.arena_size // 16) * 4
-        self.emit(0, "tinynet", "nnb::TinyNet", dict(ARENA_FLOATS=arena_floats), 256,
-                  4 * arena_floats, 1, 1, dynamic_smem=True, n_max=n_max, code=code,
+        w_floats = -(-len(self.pool.data) // 16) * 4          # every entry so far is this kernel's
+        if 4 * (arena_floats + w_floats) > TINY_SMEM_MAX:
+            self.pool.rollback(pool_mark)
+            return
+        self.emit(0, "tinynet", "nnb::TinyNet", dict(ARENA_FLOATS=arena_floats, W_FLOATS=w_floats),
+                  256, 4 * (arena_floats + w_floats), 1, 1, dynamic_smem=True, n_max=n_max, code=code,
                   note=f"whole network ({len(steps)} units) in one launch, one CTA per image, "
                        f"{self.asg.arena_size // 1024} KB arena in shared memory")
         self._n_floor = n_max + 1
