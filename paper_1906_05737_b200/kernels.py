@@ -232,7 +232,7 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, kpack9=True, tiny=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 kpack=True, kpack9=True, tiny=False, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
@@ -1078,7 +1078,14 @@ class Specializer:
         CTA per image over a shared-memory copy of its arena;
         nnb_tiny.cuh) when every unit has a TinyNet step, the per-image
         arena fits shared memory and the weights are small (read through
-        L1).  Regular launches then serve the larger batches only."""
+        L1).  Regular launches then serve the larger batches only.
+
+        Opt-in (``tuning={"tiny": True}``): measured on B200, cfg0 at 1 / 16 /
+        64 images 37 us against 23 / 31 / 32 us for the per-layer launches
+        (60 us before the weights were staged in shared memory).  One CTA
+        per image leaves one image's layers on 256 threads of one SM, where
+        the per-layer kernels spread each layer over many CTAs; the launch
+        overhead it removes is smaller than that."""
         if (self.asg.arena_size > TINY_ARENA_MAX or not self.plan.units
                 or len(self.plan.units) < 2):
             return

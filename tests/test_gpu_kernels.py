@@ -800,7 +800,7 @@ def test_tinynet_whole_network_launch(n, opts):
     nets.append(b.build([b.layer("Softmax", [y])]))
     for k, (m, w) in enumerate(nets):
         xin = (zoo.inputs(0, n) if k == 0 else rng.uniform(-2, 2, (n, 12, 10, 4)).astype(F32))
-        got, net = gpu(m, w, xin, opts)
+        got, net = gpu(m, w, xin, opts, tiny=True)
         act = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
         assert [("tinynet" in l.kernel) for l in act] == [True], [l.kernel for l in act]
         np.testing.assert_allclose(got, ref(m, w, xin, "exact" if opts == EXACT else opts), **TOL)

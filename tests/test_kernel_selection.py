@@ -88,11 +88,11 @@ def test_concat_fed_pointwise_conv_never_takes_the_row_gemm():
 
 
 def test_small_net_small_batch_is_one_tinynet_launch():
-    """kernels.Specializer._tiny: cfg0 (16 KB arena, 24 KB of weights) runs
+    """kernels.Specializer._tiny (opt-in): cfg0 (16 KB arena, 24 KB of weights) runs
     as ONE launch up to TINY_MAX_N images and as per-layer launches above;
     cfg1 (2.8 MB of weights) and the big-arena configs never take it."""
     from paper_1906_05737_b200.kernels import TINY_MAX_N
-    ls = launches(*zoo.build(0), 4096)
+    ls = launches(*zoo.build(0), 4096, tiny=True)
     tiny = [l for l in ls if "tinynet" in l.kernel]
     assert len(tiny) == 1 and (tiny[0].n_min, tiny[0].n_max) == (1, TINY_MAX_N)
     for n in (1, TINY_MAX_N):
@@ -100,6 +100,6 @@ def test_small_net_small_batch_is_one_tinynet_launch():
     assert all("tinynet" not in l.kernel for l in ls if l.n_min <= TINY_MAX_N + 1 <= l.n_max)
     assert not any("tinynet" in l.kernel for l in ls if l.n_min <= 4096 <= l.n_max)
     for cfg in (1, 2, 3, 4):
-        assert not any("tinynet" in l.kernel for l in launches(*zoo.build(cfg), 64))
-    ls = launches(*zoo.build(0), 8, tiny=False)
+        assert not any("tinynet" in l.kernel for l in launches(*zoo.build(cfg), 64, tiny=True))
+    ls = launches(*zoo.build(0), 8)                      # opt-in
     assert not any("tinynet" in l.kernel for l in ls)
