@@ -19,9 +19,12 @@ struct ConvDirect {
   // PSPLIT: a 2x2 pool window is shared by two lanes (2l: top row, 2l+1:
   // bottom row), halving the unrolled FFMAs per thread (NVRTC time) at the
   // same instruction mix; the window max crosses lanes with one shuffle
-  static constexpr bool PSPLIT = C::POOL && C::PSPLIT;
-  static constexpr int PY = C::POOL && !PSPLIT ? 2 : 1;
-  static constexpr int PX = C::POOL ? 2 : C::PXT;
+  // PSPLIT = 4: one pixel per lane, a window over lanes 4l..4l+3 (max by two
+  // shuffles) -- a quarter of the unrolled body again.
+  static constexpr int NSPLIT = C::POOL ? (C::PSPLIT == 4 ? 4 : C::PSPLIT ? 2 : 1) : 1;
+  static constexpr bool PSPLIT = NSPLIT > 1;
+  static constexpr int PY = C::POOL && NSPLIT == 1 ? 2 : 1;
+  static constexpr int PX = C::POOL ? (NSPLIT == 4 ? 1 : 2) : C::PXT;
   static constexpr int NP = PY * PX;
   static constexpr int CV = (C::CI % 4 == 0) ? 4 : 1;        // channels per load
   static constexpr int WN = C::KH * C::KW * C::CI * C::CO;   // weight floats
@@ -51,16 +54,16 @@ struct ConvDirect {
     i64 imgp[NP];
     bool live[NP];
     if (C::POOL) {
-      const int half = PSPLIT ? (int)(cell & 1) : 0;
-      const i64 win = PSPLIT ? cell >> 1 : cell;
+      const int half = (int)(cell & (NSPLIT - 1));
+      const i64 win = cell / NSPLIT;
       const bool ok = win < (i64)n * CELLS_Y * CELLS_X;
       const int cx = (int)(win % CELLS_X);
       const int cy = (int)((win / CELLS_X) % CELLS_Y);
       const i64 img = ok ? win / ((i64)CELLS_X * CELLS_Y) : 0;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        oyp[p] = cy * 2 + (PSPLIT ? half : p / PX);
-        oxp[p] = cx * PX + p % PX;
+        oyp[p] = cy * 2 + (NSPLIT == 4 ? half >> 1 : NSPLIT == 2 ? half : p / PX);
+        oxp[p] = NSPLIT == 4 ? cx * 2 + (half & 1) : cx * PX + p % PX;
         imgp[p] = img;
         live[p] = ok;
       }
@@ -177,15 +180,17 @@ struct ConvDirect {
       const unsigned mask = __activemask();
       float* dst = at<float>(arena, C::OUT_OFF + imgp[0] * C::OUT_IMG) +
                    ((i64)(oyp[0] / 2) * C::PWO + oxp[0] / 2) * C::CO;
-      const bool top = (oyp[0] & 1) == 0;
+      const bool top = (oyp[0] & 1) == 0 && (NSPLIT == 2 || (oxp[0] & 1) == 0);
 #pragma unroll
       for (int o = 0; o < C::CO; o += 4) {
         float m4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (o + i < C::CO) {
-            const float m = fmaxf(acc[0][o + i], acc[1][o + i]);
-            m4[i] = fmaxf(m, __shfl_xor_sync(mask, m, 1));
+            float m = NP > 1 ? fmaxf(acc[0][o + i], acc[NP > 1 ? 1 : 0][o + i]) : acc[0][o + i];
+            m = fmaxf(m, __shfl_xor_sync(mask, m, 1));
+            if (NSPLIT == 4) m = fmaxf(m, __shfl_xor_sync(mask, m, 2));
+            m4[i] = m;
           }
         }
         if (top) {

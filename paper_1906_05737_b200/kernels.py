@@ -428,7 +428,9 @@ class Specializer:
 
         # narrow inputs: direct FFMA convolution (all batch sizes)
         if (u.kind == "Conv2D" and not softmax and CO <= 32 and u.dw is None
-                and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16))):
+                and (CI <= 4 or (CI <= 8 and pool_fused and CO <= 16)
+                     or (CI <= 16 and pool_fused and CO <= 16 and self.direct_imm
+                         and KH * KW * CI * CO <= DIRECT_SPLIT_MAX))):
             assert not concat
             self._conv_direct(pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL,
                               pool_fused, PHO, PWO, UPF, n_min=n_min)
@@ -950,10 +952,12 @@ class Specializer:
         # a pool window split over two lanes halves the unrolled body (cfg0's
         # 16x16x8 -> 16 conv: 4608 -> 2304 FFMAs, immediates kept: 88 -> ~53 us
         # at 4096 images against the shared-memory form)
-        psplit = bool(pool_fused and unrolled > DIRECT_UNROLL_MAX
-                      and unrolled // 2 <= DIRECT_SPLIT_MAX)
-        if psplit:
-            unrolled //= 2
+        psplit = 0
+        if pool_fused and unrolled > DIRECT_UNROLL_MAX:
+            # a 2x2 window over 2 lanes (one row each) or 4 (one pixel each;
+            # cfg0's 8x8x16 -> 16 conv: the SIMT GEMM took 44 us)
+            psplit = 2 if unrolled // 2 <= DIRECT_SPLIT_MAX else 4
+            unrolled //= psplit
         wimm = bool(self.direct_imm) and unrolled <= (DIRECT_SPLIT_MAX if psplit
                                                       else DIRECT_UNROLL_MAX)
         if self.direct_imm == "force":
@@ -967,13 +971,13 @@ class Specializer:
         code = _imm_tables(wt=wmat, bias=u.bias) if wimm else ""
         # pool: one 2x2 window per thread; else pxt pixels per thread, the
         # 128-thread block covering 128*pxt consecutive pixels
-        ipi, ipb = ((PHO * PWO * (2 if psplit else 1), 128) if pool_fused
+        ipi, ipb = ((PHO * PWO * max(psplit, 1), 128) if pool_fused
                     else (HO * WO, 128 * pxt))
         smem = 4 * ((4 if wimm else KH * KW * CI * CO) + CO)
         self.emit(pos, f"conv{KH}x{KW}_direct", "nnb::ConvDirect", fields, 128, smem, ipi, ipb,
                   dynamic_smem=True, n_min=n_min, code=code,
                   note=f"direct conv CI={CI} CO={CO} {'pool2 ' if pool_fused else ''}px/thread "
-                       f"{(2 if psplit else 4) if pool_fused else pxt}"
+                       f"{(4 // psplit if psplit else 4) if pool_fused else pxt}"
                        f"{' weights as immediates' if wimm else ' weights in smem'}")
 
     def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None, n_min=1):

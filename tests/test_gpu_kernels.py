@@ -804,3 +804,24 @@ def test_tinynet_whole_network_launch(n, opts):
         act = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
         assert [("tinynet" in l.kernel) for l in act] == [True], [l.kernel for l in act]
         np.testing.assert_allclose(got, ref(m, w, xin, "exact" if opts == EXACT else opts), **TOL)
+
+
+@pytest.mark.parametrize("h,w,ci,co,n", [(8, 8, 16, 16, 5), (9, 7, 12, 16, 3), (16, 16, 8, 16, 2),
+                                         (10, 6, 16, 8, 4)])
+def test_direct_conv_pool_window_split_over_lanes(h, w, ci, co, n):
+    """ConvDirect with a fused 2x2 max-pool whose window is split over 2
+    lanes (PSPLIT 2: one row each) or 4 (one pixel each) so the weights stay
+    instruction immediates within the compile budget (odd maps: the last
+    row / column has no window)."""
+    rng = np.random.default_rng(h * ci + co)
+    b = NetBuilder()
+    x = b.input((h, w, ci))
+    y = b.maxpool(b.layer("Conv2D", [x], {"filters": co, "kernel_size": 3, "padding": "same",
+                                          "activation": "relu"},
+                          [("kernel", he(rng, (3, 3, ci, co), 9 * ci)),
+                           ("bias", (rng.standard_normal(co) * 0.1).astype(F32))]))
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
+    got, net = gpu(m, wt, xin)
+    assert any("direct" in l.kernel and "immediates" in l.note for l in net.artifact.launches)
+    np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
