@@ -61,7 +61,7 @@ def test_direct_conv_is_not_fully_unrolled_beyond_the_budget():
     plan = build_plan(build_graph(m, w))
     spec = specialize(plan, plan_buffers(plan, reserve_heads=True), EXACT, 1, 16, tiny=False)
     src = spec.sources[spec.kernel_source[spec.kernel_names.index("nnb_u01_conv3x3_direct_1")]]
-    assert "PSPLIT = 1LL" in src and "WIMM = 1LL" in src and "ROLL_KY = 0LL" in src
+    assert "PSPLIT = 2LL" in src and "WIMM = 1LL" in src and "ROLL_KY = 0LL" in src
     stem = spec.sources[spec.kernel_source[0]]
     assert "WIMM = 1LL" in stem and "__device__ const float nnb_Cfg_0_wt" in stem
     assert kernels.DIRECT_UNROLL_MAX >= 3 * 3 * 1 * 8 * 4
