@@ -60,7 +60,7 @@ def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
         y = b.layer("MaxPool2D", [y], {"pool_size": 2, "strides": 2})
     m, wt = b.build([y])
     xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
-    got, net = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0)
+    got, net = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0, direct_imm=False)
     assert any("_tc_" in l.kernel for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
 
