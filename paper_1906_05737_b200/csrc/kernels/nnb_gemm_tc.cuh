@@ -497,6 +497,9 @@ struct GemmTc {
   static constexpr u32 IDESC_B16 = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(C::BN >> 3) << 17) |
                                    ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
   static_assert(!CB16 || (!TA && !C::ALDG && !C::DWF && BK == 32 && C::CSPLIT), "bf16 correction split");
+  // EARLY main products (N = 256 BF16-correction row tiles; the raw A tile is
+  // never rewritten by the split there)
+  static constexpr bool EARLY = CB16 && C::EARLY && !NNB_CB16_WB;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
@@ -642,7 +645,8 @@ struct GemmTc {
     u64* tfull = bars + 3 * C::NS;    // [ABUF] accumulator ready
     u64* tempty = tfull + ABUF;       // [ABUF] accumulator drained (epilogue arrivals)
     u64* rbar = tempty + ABUF;        // [EPI_WARPS] residual boxes landed (EPI_TMA)
-    u32* tmem_slot = reinterpret_cast<u32*>(rbar + EPI_WARPS);
+    u64* pfull = rbar + EPI_WARPS;    // [NS]  EARLY pairs: the peer's stage landed (leader)
+    u32* tmem_slot = reinterpret_cast<u32*>(pfull + C::NS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
@@ -676,6 +680,7 @@ struct GemmTc {
         mbar_init(&tempty[a], PAIR ? 2 * EPI_WARPS : EPI_THREADS);
       }
       for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
+      for (int st = 0; st < C::NS; ++st) mbar_init(&pfull[st], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -766,6 +771,58 @@ struct GemmTc {
             tc_fence_after();
           }
           const u32 dbuf = tmem + acc * ACC_COLS;
+          if constexpr (EARLY) {
+            // N = 256 BF16-correction tiles: the main product a_hi*b_hi reads
+            // the raw A tile (the tensor core truncates it to TF32), so it is
+            // issued once both CTAs' stage has landed (local TMA barrier + the
+            // peer's pfull arrival), while the split warps build A_corr; the
+            // correction MMA follows on lo_ready.  Same accumulation order per
+            // chain as issuing both after lo_ready.
+            mbar_wait(&full[s], ph);
+            if (PAIR) mbar_wait(&pfull[s], ph);
+            tc_fence_after();
+            if (lane == 0) {
+              const u32 base = smem_u32(smem + s * STAGE);
+              const u32 b_hi = base + A_SMEM;
+#pragma unroll
+              for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
+                const u32 o = k * 32;
+                const int ks = kc * (BK / 8) + k;
+                const u32 d = dbuf + (ks % NACC) * CW;
+                if (PAIR) mma_tf32_pair(d, kmajor_desc<ROWB>(base + o), kmajor_desc<ROWB>(b_hi + o), IDESC, ks >= NACC);
+                else mma_tf32(d, kmajor_desc<ROWB>(base + o), kmajor_desc<ROWB>(b_hi + o), IDESC, ks >= NACC);
+              }
+            }
+            __syncwarp();
+            mbar_wait(&lo_ready[s], ph);
+            tc_fence_after();
+            if (lane == 0) {
+              const u32 base = smem_u32(smem + s * STAGE);
+              const u32 a_lo = base + A_BYTES, b_lo = base + A_SMEM + B_BYTES;
+#pragma unroll
+              for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
+                const u32 o = k * 32;
+                const int ks = kc * (BK / 8) + k;
+                const u32 dc = dbuf + (ks % NACC) * CW + C::BN;
+                const u32 acc_c = C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : (u32)(ks >= NACC);
+                if (PAIR) mma_bf16_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
+                else mma_bf16(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
+              }
+              if (PAIR) {
+                mma_commit_pair(&empty[s]);
+                if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit_pair(&tfull[acc]);
+              } else {
+                mma_commit(&empty[s]);
+                if (kc == CHUNK_KB - 1 || kb == KB - 1) mma_commit(&tfull[acc]);
+              }
+            }
+            __syncwarp();
+            if (++s == C::NS) { s = 0; ph ^= 1; }
+            if (kc == CHUNK_KB - 1 || kb == KB - 1) {
+              if (++acc == ABUF) { acc = 0; aph ^= 1; }
+            }
+            continue;
+          }
           if (AL) mbar_wait(&full[s], ph);           // B (TMA); A comes via lo_ready
           mbar_wait(&lo_ready[s], ph);
           tc_fence_after();
@@ -1041,6 +1098,9 @@ struct GemmTc {
       for (int t = t0; t < tiles; t += tstep) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
+          // EARLY: the peer's A / B halves of this stage have landed -- the
+          // leader may issue the main products before the split is done
+          if (EARLY && PAIR && rank != 0 && ct == 0) mbar_arrive_leader(&pfull[s]);
           float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
           float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + A_BYTES);
           if constexpr (CB16) {

@@ -232,7 +232,7 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, kpack9=True, tiny=False, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 kpack=True, kpack9=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
@@ -253,6 +253,7 @@ class Specializer:
         self.kpack = kpack
         self.kpack9 = kpack9
         self.tiny = tiny
+        self.early_mma = early_mma
         self.epi_tma = epi_tma
         self.csplit = csplit
         self.split_rn = split_rn
@@ -819,6 +820,7 @@ class Specializer:
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
                       CORR_BF16=int(cb16), CONV_W4=int(conv_w4),
+                      EARLY=int(cb16 and wide and self.early_mma),
                       APF=(self.a_prefetch if (wide and not conv) else 0),
                       PAIR=int(pair),
                       # shared-memory transposed epilogue (coalesced residual

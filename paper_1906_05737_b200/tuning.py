@@ -61,6 +61,7 @@ class Tuning:
                                    # (+ conv tiles with K >= 128), True (all), False
     cb16_w4: bool = True           # 4 split warps for BF16-correction tiles
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
+    early_mma: bool = True         # N = 256 BF16-correction tiles: main MMAs before the split
 
     def specializer_kwargs(self):
         """Keyword arguments of kernels.Specializer (the selection constants
