@@ -518,9 +518,9 @@ struct GemmTc {
   // WIDE: N = 256 per MMA (a tcgen05 kind::tf32 instruction costs ~100
   // cycles at N <= 128 and ~1.4x that at N = 256, scripts/mma_n256.py); the
   // epilogue keeps 128 running sums per thread (384 threads: 168 registers)
-  static constexpr bool WIDE = C::BN > 128 && !C::KP9;
+  static constexpr bool WIDE = C::BN > 128 && !C::KP9 && !C::KPACK;
   static_assert(C::BN % 16 == 0 && C::BN >= 16 && (C::BN <= 128 || C::BN == 256 ||
-                                                   (C::KP9 && C::BN <= 256)),
+                                                   ((C::KP9 || C::KPACK) && C::BN <= 256)),
                 "UMMA N / TMEM budget");
   static_assert(!C::CORR_WHOLE || (CS && C::NACC == 1), "whole-K correction chain");
   static_assert(!WIDE || (!TA && C::NACC == 1 && !C::CONV && !C::RES && C::UPF == 1 &&
@@ -1272,7 +1272,78 @@ struct GemmTc {
           }
           continue;
         }
-        if constexpr (KP) {
+        if constexpr (KP && C::CO / 2 > 16 && NCHUNK == 1 && NACC == 1) {
+          // ---- packed horizontal taps, wide groups (CO = 64: N = 192): one
+          // chunk, so each 16-channel group is drained, combined, finished and
+          // stored on its own (registers: KW x 16 loaded values at a time) ----
+          constexpr int GCO = C::CO / 2;
+          const int g = (warp - EPI_W0) >> 2;
+          const int img = mb / TPI, tt = mb % TPI;
+          const int rr0 = q * 32 + lane, w0 = rr0 % TW;
+          auto pix = [&](int rr, long long& ob) {
+            const int w = rr % TW;
+            const int oy = (tt / TX) * TH + rr / TW, ox = (tt % TX) * OW + w;
+            ob = (long long)img * (C::OUT_IMG / 4) +
+                 ((long long)(oy * C::UPF) * C::WO * C::UPF + ox * C::UPF) * C::CO + g * GCO;
+            return img < n && w < OW && oy < C::HO && ox < C::WO;
+          };
+          mbar_wait(&tfull[acc], aph);
+          tc_fence_after();
+#pragma unroll 1
+          for (int h = 0; h < GCO / 16; ++h) {
+            u32 rv[C::KW][16], rc[C::KW][16];
+#pragma unroll
+            for (int kx = 0; kx < C::KW; ++kx) {
+              const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + kx * C::CO + g * GCO + h * 16;
+              tmem_ld16_async(ta, rv[kx]);
+              if (CS) tmem_ld16_async(ta + C::BN, rc[kx]);
+            }
+            tmem_wait_ld();
+            float y[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float part[C::KW];
+#pragma unroll
+              for (int kx = 0; kx < C::KW; ++kx) {
+                tmem_pin_n<16>(rv[kx]);
+                if (CS) tmem_pin_n<16>(rc[kx]);
+                part[kx] = CS ? __uint_as_float(rv[kx][i]) + __uint_as_float(rc[kx][i])
+                              : __uint_as_float(rv[kx][i]);
+              }
+              float sacc = part[0];
+#pragma unroll
+              for (int kx = 1; kx < C::KW; ++kx) sacc += __shfl_down_sync(0xffffffffu, part[kx], kx);
+              const int col = g * GCO + h * 16 + i;
+              y[i] = finish<C::ACT, EMODE, C::POST>(sacc + __ldg(bias + col), ps, po, col);
+            }
+            if (NNB_TC_DBG & 16) continue;
+            if constexpr (C::DPOOL) {
+              dual_pool_store<16>(arena, y, (rr0 & 17) == 0 && w0 + 1 < OW, img,
+                                  (tt / TX) * TH + rr0 / TW, (tt % TX) * OW + w0, g * GCO + h * 16, n);
+            }
+            float4* st = epi_stage + (warp - EPI_W0) * 128;
+            stage_rows<16>(st, y, lane);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int row = p * 8 + lane / 4, c = lane % 4;
+              long long ob;
+              if (pix(q * 32 + row, ob)) {
+                const float4 x = st[stage_slot<16>(row, c)];
+#pragma unroll
+                for (int rep = 0; rep < C::UPF * C::UPF; ++rep)
+                  *reinterpret_cast<float4*>(
+                      out + ob + ((long long)(rep / C::UPF) * C::WO * C::UPF + rep % C::UPF) * C::CO +
+                      h * 16 + 4 * c) = x;
+              }
+            }
+            __syncwarp();
+          }
+          tc_fence_before();
+          arrive_mma(&tempty[acc]);
+          if (++acc == ABUF) { acc = 0; aph ^= 1; }
+          continue;
+        }
+        if constexpr (KP && !(C::CO / 2 > 16 && NCHUNK == 1 && NACC == 1)) {
           // ---- packed horizontal taps: reduce chunks, combine across lanes ----
           constexpr int GCO = C::CO / 2;                 // output channels per warp group
           static_assert(GCO == 8 || GCO % 16 == 0, "KPACK staged store width");

@@ -232,7 +232,7 @@ def _pad4(x):
 class Specializer:
     def __init__(self, plan, assignment, options, max_batch, capacity, use_tc=True,
                  sm_count=148, tc_min_rows=TC_MIN_ROWS, tmem_a=True, nacc=None, aldg=False,
-                 kpack=True, kpack9=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
+                 kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
                  wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
@@ -254,6 +254,7 @@ class Specializer:
         self.kpack9 = kpack9
         self.tiny = tiny
         self.early_mma = early_mma
+        self.kpack_wide = kpack_wide
         self.epi_tma = epi_tma
         self.csplit = csplit
         self.split_rn = split_rn
@@ -665,7 +666,12 @@ class Specializer:
                    and 1 < kw <= 3 and not conv["POOL"] and u.residual_id is None
                    and conv.get("UPF", 1) == 1 and not conv.get("DWF") and u.dual_pool is None
                    and conv["CI"] % 32 == 0 and conv["C0"] % 32 == 0)
-        kpack = bool(conv and self.kpack and not kp9 and CO % 16 == 0 and kw * CO <= 128 and kw > 1
+        # (KW * CO up to 192: CO = 64 convs pack into N = 192 with the
+        # correction products merged into the main chain -- two accumulator
+        # buffers of 192 columns fit TMEM, the short K = KH*CI keeps the merged
+        # chain accurate)
+        kpack = bool(conv and self.kpack and not kp9 and CO % 16 == 0 and kw > 1
+                     and (kw * CO <= 128 or (kw * CO <= 192 and CO % 32 == 0 and self.kpack_wide))
                      and (CO == 16 or CO % 32 == 0)
                      and not conv["POOL"] and u.residual_id is None)
         CO_real = CO
@@ -724,7 +730,7 @@ class Specializer:
         if wide:
             BK = self.wide_bk
             sw = 3 if BK == 32 else 2
-        csplit = self.csplit and not kp9      # KP9: N = 144, two buffers fit only merged
+        csplit = self.csplit and not kp9 and BN <= 128   # N = 144 / 192: two buffers fit only merged
         # k-blocks (of 32) per TMEM accumulator chunk: every chunk ends in a
         # drain the MMAs wait for (one accumulator buffer at BN = 128), so
         # long chunks are faster; the tensor core truncates once per MMA, so

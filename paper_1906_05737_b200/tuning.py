@@ -44,6 +44,7 @@ class Tuning:
     aldg: bool = False             # A via cp.async instead of TMA
     kpack: bool = True             # pack KW taps of narrow convs into N
     kpack9: bool = True            # pack all KH x KW taps of CO = 16 convs into N (N = 144)
+    kpack_wide: bool = True        # pack the KW taps of CO = 64 convs into N = 192 (merged correction)
     tiny: bool = False             # small nets at small batches as one TinyNet launch (opt-in:
                                    # cfg0 batch 1 37 us vs 23 us for the per-layer launches)
     epi_tma: bool = True           # TMA-store epilogue

@@ -45,10 +45,12 @@ def test_conv_sweep(h, w, ci, co, k, s, pad, act, n):
     (10, 18, 32, 16, "same", False, 3), (17, 23, 32, 48, "same", True, 2),
     (12, 40, 64, 32, "valid", True, 2), (9, 16, 32, 40, "same", False, 1),
     (60, 80, 32, 64, "same", True, 2), (14, 20, 16, 32, "same", False, 2),
-    (11, 30, 16, 16, "same", True, 2), (9, 12, 48, 32, "valid", False, 2)])
+    (11, 30, 16, 16, "same", True, 2), (9, 12, 48, 32, "valid", False, 2),
+    (14, 20, 32, 64, "same", False, 2), (10, 37, 64, 64, "valid", False, 3)])
 def test_tensor_core_conv3x3(h, w, ci, co, pad, pool, n):
     """Implicit-GEMM tcgen05 conv (4-D TMA boxes, zero-filled borders), with
-    and without the fused 2x2 max-pool epilogue, ragged 8x16 tiles."""
+    and without the fused 2x2 max-pool epilogue, ragged 8x16 tiles; CO = 16
+    (all taps in N), 32 (KW taps in N = 96) and 64 (KW taps in N = 192)."""
     rng = np.random.default_rng(ci + co + h)
     b = NetBuilder()
     x = b.input((h, w, ci))
