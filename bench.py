@@ -368,7 +368,7 @@ def dominant_roofline(net, B, lt, peaks, ffma):
     from paper_1906_05737_b200 import roofline
     dom = max(lt, key=lt.get)
     L = net.artifact.launches[dom]
-    r = roofline.launch_roofline(net.plan.units[L.unit], L, B, peaks, ffma)
+    r = roofline.launch_roofline(net.plan.units[L.unit], L, B, peaks, ffma[0])
     t = lt[dom] / 1e3
     share = lt[dom] / sum(lt.values())
     if r["bound"] == "hbm":
