@@ -72,3 +72,21 @@ def test_reference_cpu_path_is_the_real_reference():
     np.testing.assert_array_equal(got, rec["compiled_default"])
     us, calls = refbench.batch1_latency_us(0, seconds=0.2, net=net)
     assert us > 0 and calls >= 5
+
+
+@pytest.mark.parametrize("cfg,batch", [(1, 65536), (3, 256), (0, 4096)])
+def test_bench_dominant_roofline_any_pipe(cfg, batch):
+    """bench.dominant_roofline on the real launch lists: tensor-, FFMA- and
+    HBM-bound dominant launches all yield a fraction of their own peak."""
+    import pathlib
+    import sys
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+    import bench
+    net = fake_net(cfg, batch)
+    idx = net.launches_for(batch)
+    lt = {i: 0.01 * (k + 1) for k, i in enumerate(idx)}          # the last launch dominates
+    roof = bench.dominant_roofline(net, batch, lt, PEAKS, (FFMA, "test"))
+    assert roof["bound"] in ("tensor", "fp32_ffma", "hbm") and 0 < roof["frac"]
+    assert roof["kernel"] == net.artifact.launches[idx[-1]].kernel
+    rows, roof_us, meas = bench.launch_table(net, batch, lt, PEAKS, (FFMA, "test"))
+    assert len(rows) == len(idx) and roof_us > 0 and meas > 0
