@@ -104,6 +104,28 @@ struct ConvDirect {
     // slow (kernels.py DIRECT_UNROLL_MAX)
     // ROLL_KY = 1: the ky loop is rolled; 2: ky and kx are (one rolled loop
     // over the KH*KW taps)
+    // PATCH: a stride-1 pooled window over <= 4 channels reads its whole
+    // (PY+KH-1) x (PX+KW-1) input patch once into registers (16 loads for a
+    // 3x3 conv instead of 36 per-tap loads with their bounds arithmetic --
+    // the stems were issue-bound: cfg0's 32x32x1 -> 8 conv 79% issue-active
+    // at 50% FMA-pipe use); the FFMAs keep the (ky, kx, ci) order
+    constexpr bool PATCH = C::POOL && NSPLIT == 1 && C::S == 1 && C::CI <= 4 && C::WIMM &&
+                           C::ROLL_KY == 0;
+    constexpr int PR = PATCH ? PY + C::KH - 1 : 1, PCC = PATCH ? PX + C::KW - 1 : 1;
+    float pt[PR][PCC][PATCH ? C::CI : 1];
+    if constexpr (PATCH) {
+      const int iy0 = oyp[0] - C::PT, ix0 = oxp[0] - C::PL;
+#pragma unroll
+      for (int r = 0; r < PR; ++r)
+#pragma unroll
+        for (int c = 0; c < PCC; ++c) {
+          const int iy = iy0 + r, ix = ix0 + c;
+          const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
+          const float* src = inp[0] + ((i64)(ok ? iy : 0) * C::W + (ok ? ix : 0)) * C::CI;
+#pragma unroll
+          for (int ci = 0; ci < C::CI; ++ci) pt[r][c][ci] = ok ? lda(src + ci) : 0.f;
+        }
+    }
     constexpr int TAPS_ROLLED = C::ROLL_KY == 2 ? C::KH * C::KW : C::ROLL_KY == 1 ? C::KH : 1;
     constexpr int KX_UNROLLED = C::ROLL_KY == 2 ? 1 : C::KW;
 #pragma unroll
@@ -119,6 +141,11 @@ struct ConvDirect {
           float xv[NP][CV];
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
+            if constexpr (PATCH) {
+#pragma unroll
+              for (int c = 0; c < CV; ++c) xv[p][c] = pt[p / PX + ky_][p % PX + kx][c0 + c];
+              continue;
+            }
             const int iy = oyp[p] * C::S - C::PT + ky_;
             const int ix = oxp[p] * C::S - C::PL + kx;
             const bool ok = iy >= 0 && iy < C::H && ix >= 0 && ix < C::W;
