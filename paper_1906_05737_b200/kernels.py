@@ -408,7 +408,10 @@ class Specializer:
             # (narrow layers hand over to the tensor cores earlier: cfg0's
             # Dense 256->32 at 256 rows 0.039 -> 0.033 ms replay on tcgen05,
             # cfg1's 1024->512 at 256 rows 0.062 here vs 0.070 there)
-            sdr = self.small_dense_rows if CO > 64 else min(self.small_dense_rows, 128)
+            # (and so do wide ones with a short K: cfg3's Dense 256->1000 at 256
+            # rows 16.7 -> 12.7 us on tcgen05)
+            sdr = (self.small_dense_rows if 64 < CO <= 512 or CI > 256
+                   else min(self.small_dense_rows, 128))
             if sdr > SMALL_M:
                 hi = min(sdr, self.max_batch)
                 self._dense_small(pos, u, wmat, CI, CO, softmax, n_max=hi, mb=8, n_min=n_min)
