@@ -39,6 +39,16 @@
 #ifndef NNB_TC_DBG
 #define NNB_TC_DBG 0
 #endif
+// NNB_DRAIN2: mid-tile drains of whole-K correction chains read two column
+// groups per TMEM wait (dense 1024->512 at 65536 rows 0.2137 -> 0.2105 ms)
+#ifndef NNB_DRAIN2
+#define NNB_DRAIN2 1
+#endif
+// NNB_SPLIT_UNROLL: unroll of the BF16-correction split loop (8: the whole
+// stage per thread in flight; 0.2110 -> 0.2096 ms)
+#ifndef NNB_SPLIT_UNROLL
+#define NNB_SPLIT_UNROLL 8
+#endif
 // The tensor core reads FP32 operands of kind::tf32 with the 13 low mantissa
 // bits ignored (verified on B200 by scripts/tc_hi.py: bit-identical results
 // with and without writing hi = a & 0xffffe000 back), so only lo = a - hi is
@@ -500,6 +510,7 @@ struct GemmTc {
   // EARLY main products (N = 256 BF16-correction row tiles; the raw A tile is
   // never rewritten by the split there)
   static constexpr bool EARLY = CB16 && C::EARLY && !NNB_CB16_WB;
+  static constexpr int SPLIT_UNROLL = NNB_SPLIT_UNROLL;
   static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
@@ -1109,8 +1120,8 @@ struct GemmTc {
             // A_corr row keeps the same swizzle: bf16(hi) x 8 in chunk 2g,
             // bf16(lo) x 8 in chunk 2g+1
             uint4* corr = reinterpret_cast<uint4*>(lo);
-#pragma unroll 2
-            for (int i = ct; i < A_BYTES / 32; i += 32 * CONV_WARPS) {
+#pragma unroll (SPLIT_UNROLL)
+            for (int i = ct; i < ((NNB_TC_DBG & 4) ? 0 : A_BYTES / 32); i += 32 * CONV_WARPS) {
               const int row = i >> 2, g = i & 3, x = row & 7;
               const int p0 = row * 8 + ((2 * g) ^ x), p1 = row * 8 + ((2 * g + 1) ^ x);
               const float4 v0 = a[p0], v1 = a[p1];
@@ -1446,6 +1457,35 @@ struct GemmTc {
           // registers next to them)
           constexpr int GB = (EPI_COLS / 16 >= 2 && !CS) ? 2 : 1;
           const bool rd_c = CS && (!C::CORR_WHOLE || ch == NCHUNK - 1);   // correction read
+          if constexpr (C::CORR_WHOLE && NACC == 1 && NNB_DRAIN2 && EPI_COLS % 32 == 0) {
+            // mid-tile chunk of a whole-K correction chain: only the main
+            // columns are read, two 16-column groups per wait (the correction
+            // registers hold the second) -- half the load round trips while
+            // the MMAs wait for this drain
+            if (!rd_c) {
+#pragma unroll
+              for (int g0 = 0; g0 < ((NNB_TC_DBG & 8) ? 0 : EPI_COLS / 16); g0 += 2) {
+                if (cbeg + g0 * 16 < C::BN) {
+                  u32 rv[16], rw[16];
+                  const u32 ta = tmem + ((u32)(q * 32) << 16) + acc * ACC_COLS + cbeg + g0 * 16;
+                  tmem_ld16_async(ta, rv);
+                  tmem_ld16_async(ta + 16, rw);
+                  tmem_wait_ld();
+                  tmem_pin(rv);
+                  tmem_pin(rw);
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) {
+                    run[g0 * 16 + i] += __uint_as_float(rv[i]);
+                    run[g0 * 16 + 16 + i] += __uint_as_float(rw[i]);
+                  }
+                }
+              }
+              tc_fence_before();
+              arrive_mma(&tempty[acc]);
+              if (++acc == ABUF) { acc = 0; aph ^= 1; }
+              continue;
+            }
+          }
 #pragma unroll
           for (int g0 = 0; g0 < ((NNB_TC_DBG & 8) ? 0 : EPI_COLS / 16); g0 += GB) {
             if (cbeg + g0 * 16 < C::BN) {            // warp-uniform (whole batch valid)
