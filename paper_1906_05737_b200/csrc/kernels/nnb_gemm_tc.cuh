@@ -1141,8 +1141,22 @@ struct GemmTc {
             }
           } else {
 #pragma unroll 4
-          for (int i = ct; i < A_BYTES / 16; i += 32 * CONV_WARPS) {
+          for (int i = ct; i < ((NNB_TC_DBG & 4) ? 0 : A_BYTES / 16); i += 32 * CONV_WARPS) {
             float4 v = a[i], h, l;
+            if (C::RN_SS == 2) {
+              // truncated hi left to the hardware (the raw tile), lo rounded
+              // to TF32 here: its rounding error is unbiased and the tile is
+              // not written back (one store per 4 elements instead of two)
+              float4 r;
+              r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+              r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+              r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+              r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+              l.x = __uint_as_float(split_hi(r.x)); l.y = __uint_as_float(split_hi(r.y));
+              l.z = __uint_as_float(split_hi(r.z)); l.w = __uint_as_float(split_hi(r.w));
+              lo[i] = l;
+              continue;
+            }
             if (C::RN_SS) {
               // round-to-nearest split written back: lo of either sign, so
               // its own TF32 truncation is unbiased (the raw tile would be

@@ -235,10 +235,11 @@ class Specializer:
                  kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=True, corr_bf16="wide", cb16_w4=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
+        self.conv_w4 = conv_w4
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
         self.tc_min_images = tc_min_images
@@ -816,7 +817,13 @@ class Specializer:
         # narrow tiles with the bf16 split: four converter warps (with two the
         # extra split work made cfg4's convs slower; with four cfg4 @64
         # 0.892 -> 0.834 ms, cfg0/2/3 unchanged)
-        conv_w4 = bool(cb16 and not wide and self.cb16_w4)
+        # conv tiles whose MMA work per k-block is short next to the split of
+        # their A tile (all taps in N, 16-channel k-blocks, N = 192): four
+        # split warps too (cfg4 @64: KP9 conv 0.195 -> 0.170 ms, BK = 16 conv
+        # 0.138 -> 0.131, N = 192 0.085 -> 0.084; the N = 96 concat conv with
+        # K = 384 gets slower, 0.178 -> 0.194, and keeps two)
+        conv_w4 = bool((cb16 and not wide and self.cb16_w4)
+                       or (conv and (self.conv_w4 is True or (self.conv_w4 == "auto" and (kp9 or BK == 16 or BN > 128)))))
         hi_off, lo_off = self.pool.add(hi), self.pool.add(bf16_corr_words(hi, lo) if cb16 else lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KH=1, KW=1, PT=0, PL=0, PHO=1,
                    PWO=1, C0=1, CONCAT=0, UPF=1, DWF=0)
@@ -827,7 +834,7 @@ class Specializer:
         fields = dict(K=K, N=CO, CO=CO_real, KPACK=kpack, KP9=kp9, NPAD=NPAD, BN=BN, BK=BK, NS=NS,
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
-                      CORR_WHOLE=int(corr_whole), RN_SS=int(self.rn_ss and self.split_rn),
+                      CORR_WHOLE=int(corr_whole), RN_SS=(2 if self.rn_ss == 2 else int(bool(self.rn_ss))) if self.split_rn else 0,
                       CORR_BF16=int(cb16), CONV_W4=int(conv_w4),
                       EARLY=int(cb16 and wide and self.early_mma),
                       APF=(self.a_prefetch if (wide and not conv) else 0),

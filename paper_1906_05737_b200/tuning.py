@@ -57,10 +57,12 @@ class Tuning:
     wide_bk: int = 32              # k-block of the N = 256 tiles
     wide_chunk: object = None      # main-chain chunk of the N = 256 tiles
     wide_csplit: bool = True       # correction chain of the N = 256 tiles
-    rn_ss: bool = True             # write the rounded hi back over shared-memory A tiles
+    rn_ss: object = 2              # shared-memory A split: 2 = lo rounded to TF32 (hi left to the
+                                   # hardware), True = rounded hi written back, False = truncation
     corr_bf16: object = "wide"     # BF16 correction products: "wide" (N=256 tiles only), "auto"
                                    # (+ conv tiles with K >= 128), True (all), False
     cb16_w4: bool = True           # 4 split warps for BF16-correction tiles
+    conv_w4: object = "auto"       # 4 split warps for conv tiles: "auto" (short k-block work), True, False
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
     early_mma: bool = True         # N = 256 BF16-correction tiles: main MMAs before the split
 
