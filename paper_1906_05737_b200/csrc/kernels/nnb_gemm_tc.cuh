@@ -428,7 +428,16 @@ template <class C>
 struct GemmTc {
   static constexpr int BM = 128, BK = C::BK;                // 32 (SW128) or 16 (SW64)
   static constexpr int ROWB = BK * 4;
-  static constexpr int A_BYTES = BM * BK * 4;
+  // RS: vertical taps sharing one A box (KPACK conv tiles): the box holds the
+  // TH + RS - 1 input rows of the tile (16 pixels each) and the MMAs of kernel
+  // row ky read it from pixel row ky on -- a 16-row offset is a whole number
+  // of swizzle atoms -- so each input pixel is loaded and split once per
+  // channel block instead of once per kernel row.  A k-block then carries RS
+  // B sub-tiles (W^T columns ky * CI + channel block) and RS x BK/8 k-steps.
+  static constexpr int RS = C::RS;
+  static constexpr int A_ROWS = BM + (RS - 1) * 16;
+  static constexpr int A_BYTES = A_ROWS * BK * 4;
+  static constexpr int KSTEPS = RS * (BK / 8);             // k-steps per k-block
   // PAIR: CTA pairs (cluster of 2, tcgen05 cta_group::2).  The pair computes a
   // 256 x BN tile: each CTA loads its own 128 rows of A and HALF of B (BN/2
   // rows of W^T), the leader issues M=256 MMAs that read both CTAs' operands,
@@ -438,6 +447,7 @@ struct GemmTc {
   static constexpr bool PAIR = C::PAIR != 0;
   static constexpr int B_ROWS = PAIR ? C::BN / 2 : C::BN;   // B rows held per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 4;
+  static constexpr int B_SMEM = RS * B_BYTES;               // hi (or lo) B sub-tiles of a stage
   // TMEM_A: the split A operand lives in tensor memory (MMA "ts" form), so the
   // tensor core reads only B from shared memory -- for narrow N the A re-reads
   // (three products per k-step) otherwise saturate shared-memory bandwidth.
@@ -453,8 +463,8 @@ struct GemmTc {
   static constexpr int HALO_TX = HALO_W * HALO_H * BK * 4;           // bytes the box delivers
   static constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
   static constexpr int A_SMEM = (TA ? (DWF ? 0 : A_BYTES) : 2 * A_BYTES);  // A (+ A_lo) in smem
-  static constexpr int STAGE = A_SMEM + 2 * B_BYTES + HALO_BYTES;
-  static constexpr int KB = (C::K + BK - 1) / BK;
+  static constexpr int STAGE = A_SMEM + 2 * B_SMEM + HALO_BYTES;
+  static constexpr int KB = (C::K + BK * RS - 1) / (BK * RS);
   static constexpr int NTN = C::NPAD / C::BN;
   // One accumulator buffer = main (a_hi*b_hi) + correction (a_hi*b_lo + a_lo*b_hi)
   // columns.  Tensor-core accumulation truncates once per MMA instruction, so the
@@ -567,6 +577,7 @@ struct GemmTc {
   static_assert(!KP || (C::CONV && !C::POOL && !C::RES && C::CO % 16 == 0 &&
                         C::KW * C::CO == C::N), "KPACK geometry");
   static_assert(STAGE % 1024 == 0, "stage alignment");
+  static_assert(RS == 1 || (KP && C::CONV && !TA && !AL && !DWF && !CB16 && RS == C::KH), "row-shared taps");
   static_assert(!DWF || (C::CONV && !KP && !AL && C::KW == 1 && C::CI % BK == 0),
                 "depthwise fusion: 1x1 conv tiles");
   // EPI_TMA: the epilogue writes the tile into 64B-swizzled shared-memory
@@ -724,7 +735,7 @@ struct GemmTc {
             mbar_wait(&empty[s], ph ^ 1);
             unsigned char* st = smem + s * STAGE;
             mbar_expect_tx(&full[s], (NNB_TC_DBG & 2) ? 0
-                                     : (AL ? 0 : DWF ? HALO_TX : A_BYTES) + 2 * B_BYTES);
+                                     : (AL ? 0 : DWF ? HALO_TX : A_BYTES) + 2 * B_SMEM);
             if (NNB_TC_DBG & 2) {
               // diagnostic: no operand traffic
             } else if (AL) {
@@ -732,7 +743,7 @@ struct GemmTc {
             } else if (DWF) {
               // depthwise input halo of the tile, channel block kb
               const int img = mb / TPI, tt = mb % TPI;
-              tma_load_4d(st + A_SMEM + 2 * B_BYTES, tmA, &full[s], kb * BK,
+              tma_load_4d(st + A_SMEM + 2 * B_SMEM, tmA, &full[s], kb * BK,
                           (tt % TX) * TW * C::DW_S - C::DW_PL,
                           (tt / TX) * TH * C::DW_S - C::DW_PT, img);
             } else if (C::CONV) {
@@ -757,8 +768,11 @@ struct GemmTc {
             }
             if (!(NNB_TC_DBG & 2)) {
               const int brow = nb * C::BN + rank * B_ROWS;         // this CTA's B rows
-              tma_load_2d(st + A_SMEM, tmB, &full[s], kb * BK, brow);
-              tma_load_2d(st + A_SMEM + B_BYTES, tmBlo, &full[s], kb * BK, brow);
+#pragma unroll
+              for (int r = 0; r < RS; ++r) {                       // RS: kernel row r's W^T block
+                tma_load_2d(st + A_SMEM + r * B_BYTES, tmB, &full[s], (r * KB + kb) * BK, brow);
+                tma_load_2d(st + A_SMEM + B_SMEM + r * B_BYTES, tmBlo, &full[s], (r * KB + kb) * BK, brow);
+              }
             }
             if (++s == C::NS) { s = 0; ph ^= 1; }
           }
@@ -809,7 +823,7 @@ struct GemmTc {
             tc_fence_after();
             if (lane == 0) {
               const u32 base = smem_u32(smem + s * STAGE);
-              const u32 a_lo = base + A_BYTES, b_lo = base + A_SMEM + B_BYTES;
+              const u32 a_lo = base + A_BYTES, b_lo = base + A_SMEM + B_SMEM;
 #pragma unroll
               for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
                 const u32 o = k * 32;
@@ -839,13 +853,15 @@ struct GemmTc {
           tc_fence_after();
           if (lane == 0) {
             const u32 base = smem_u32(smem + s * STAGE);
-            const u32 a_hi = base, a_lo = base + A_BYTES;
-            const u32 b_hi = base + A_SMEM, b_lo = b_hi + B_BYTES;
+#pragma unroll
+            for (int r = 0; r < RS; ++r) {
+            const u32 a_hi = base + r * 16 * ROWB, a_lo = a_hi + A_BYTES;
+            const u32 b_hi = base + A_SMEM + r * B_BYTES, b_lo = b_hi + B_SMEM;
             const u32 ta = tmem + A_TCOL + s * 2 * BK;                // TMEM A slot
 #pragma unroll
             for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
               const u32 o = k * 32;   // 8 tf32 = 32 bytes along the swizzled row
-              const int ks = kc * (BK / 8) + k;                  // k-step within the chunk
+              const int ks = kc * KSTEPS + r * (BK / 8) + k;     // k-step within the chunk
 #ifdef NNB_TC_NDBG
               const u32 d = tmem, dc = tmem;                     // diagnostic width test
 #else
@@ -856,7 +872,7 @@ struct GemmTc {
               // CORR_WHOLE: the correction chain runs over the whole K (its
               // values are ~2^-11 of the main sum, so its truncations are
               // negligible); only the main chain restarts per chunk
-              const u32 acc_c = CS ? (C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : accum) : 1u;
+              const u32 acc_c = CS ? (C::CORR_WHOLE ? (u32)(kb * KSTEPS + r * (BK / 8) + k > 0) : accum) : 1u;
               if (PAIR && TA) {
                 mma_tf32_ts_pair(d, ta + 8 * k, kmajor_desc<ROWB>(b_hi + o), IDESC, accum);
                 mma_tf32_ts_pair(dc, ta + 8 * k, kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
@@ -880,6 +896,7 @@ struct GemmTc {
                 mma_tf32(dc, kmajor_desc<ROWB>(a_hi + o), kmajor_desc<ROWB>(b_lo + o), IDESC, acc_c);
                 mma_tf32(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_hi + o), IDESC, 1);
               }
+            }
             }
             if (PAIR) {
               mma_commit_pair(&empty[s]);
@@ -913,7 +930,7 @@ struct GemmTc {
       for (int t = t0; t < tiles; t += tstep) {
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
-          const unsigned char* halo = smem + s * STAGE + A_SMEM + 2 * B_BYTES;
+          const unsigned char* halo = smem + s * STAGE + A_SMEM + 2 * B_SMEM;
           unsigned char* arow = smem + s * STAGE + r * ROWB;
           const int c0 = kb * BK;
           const u32 ta = tmem + ((u32)(q * 32) << 16) + A_TCOL + s * 2 * BK;
@@ -1381,7 +1398,7 @@ struct GemmTc {
           for (int ch = 0; ch < NCHUNK; ++ch) {
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * (BK / 8);
+            const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * KSTEPS;
             // every tap of a chain in flight, one wait (the drain is the KPACK
             // epilogue's critical path: 12 serial load+wait pairs per tile before)
 #pragma unroll
@@ -1465,7 +1482,7 @@ struct GemmTc {
           mbar_wait(&tfull[acc], aph);
           tc_fence_after();
           // chains written in this chunk (a short last chunk may not reach all)
-          const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * (BK / 8);
+          const int ksteps = (ch == NCHUNK - 1 ? KB - ch * CHUNK_KB : CHUNK_KB) * KSTEPS;
           // batches of GB 16-column groups: all their loads in flight, one wait
           // (32 loaded registers per batch: the 64-column running sums stay in
           // registers next to them)

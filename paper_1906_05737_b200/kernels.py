@@ -235,11 +235,12 @@ class Specializer:
                  kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
         self.conv_w4 = conv_w4
+        self.rowshare = rowshare
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
         self.tc_min_images = tc_min_images
@@ -675,7 +676,8 @@ class Specializer:
         # buffers of 192 columns fit TMEM, the short K = KH*CI keeps the merged
         # chain accurate)
         kpack = bool(conv and self.kpack and not kp9 and CO % 16 == 0 and kw > 1
-                     and (kw * CO <= 128 or (kw * CO <= 192 and CO % 32 == 0 and self.kpack_wide))
+                     and (kw * CO <= 128 or (kw * CO <= 192 and CO % 32 == 0 and self.kpack_wide
+                                             and kh_ * conv["CI"] <= 512))
                      and (CO == 16 or CO % 32 == 0)
                      and not conv["POOL"] and u.residual_id is None)
         CO_real = CO
@@ -775,9 +777,17 @@ class Specializer:
         pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0
                     and ((not conv and tmem_a and BN == 128 and K >= 256)
                          or conv or wide))
-        a_smem = (0 if dwf else 128 * BK * 4) if tmem_a else 2 * 128 * BK * 4
+        # row-shared vertical taps (KPACK conv tiles, A in shared memory): one
+        # A box of 8 + KH - 1 input rows serves every kernel row (nnb_gemm_tc.cuh
+        # RS), so each input pixel is loaded and split once per channel block
+        rs = (kh_ if (kpack and self.rowshare and kh_ > 1 and not tmem_a and not aldg and not dwf
+                      and self.corr_bf16 not in (True, "auto")) else 1)
+        # (cfg4 @64: 0.659 -> 0.607 ms; the 120x160x16->32 conv 0.131 -> 0.111,
+        # the 60x80x128->32 concat conv 0.180 -> 0.146)
+        a_rows = 128 + 16 * (rs - 1)
+        a_smem = (0 if dwf else 128 * BK * 4) if tmem_a else 2 * a_rows * BK * 4
         halo_bytes = -(-(halo_w * halo_h * BK * 4) // 1024) * 1024
-        stage = a_smem + 2 * (BN // 2 if pair else BN) * BK * 4 + halo_bytes
+        stage = a_smem + 2 * rs * (BN // 2 if pair else BN) * BK * 4 + halo_bytes
         # epilogue through TMA stores (and a TMA-prefetched residual) for plain
         # row tiles; 64B-swizzled 32 x 16 boxes, NBUF per epilogue warp
         res = u.residual_id is not None
@@ -789,6 +799,22 @@ class Specializer:
         nbuf = (egrp if res else min(egrp, 2)) if epi_tma else 1
         epi_bytes = 8 * nbuf * 2048
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
+        room = SMEM_MAX - 1024 - 512 - epi_bytes
+        if rs > 1 and room // stage < 2 and BK == 32:
+            # row-shared stages of 16-channel k-blocks (N = 192: 112 KB -> 56 KB;
+            # cfg4 @64 0.084 -> 0.078 ms; where two 32-channel stages fit they
+            # are faster: N = 96, K = 384 0.146 vs 0.169 ms at 16)
+            bk16 = 2 * a_rows * 16 * 4 + 2 * rs * (BN // 2 if pair else BN) * 16 * 4
+            if room // bk16 >= 3:
+                BK, sw, stage = 16, 2, bk16
+        if rs > 1 and room // stage < 2:
+            # two row-shared stages do not fit: per-row boxes
+            rs = 1
+            chunk = self.chunk or (16 if K <= 1024 else 8)
+            stage = 2 * 128 * BK * 4 + 2 * (BN // 2 if pair else BN) * BK * 4 + halo_bytes
+        if rs > 1 and not self.chunk:
+            # a chunk counts k-blocks of RS x BK k values: keep its K span
+            chunk = max(1, chunk * 32 // (rs * BK))
         NS = max(2, min(8, (SMEM_MAX - 1024 - 512 - epi_bytes) // stage))
         if tmem_a:
             NS = min(NS, (512 - ABUF * NACC * cw) // (2 * BK))
@@ -835,7 +861,7 @@ class Specializer:
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=(2 if self.rn_ss == 2 else int(bool(self.rn_ss))) if self.split_rn else 0,
-                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4),
+                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4), RS=rs,
                       EARLY=int(cb16 and wide and self.early_mma),
                       APF=(self.a_prefetch if (wide and not conv) else 0),
                       PAIR=int(pair),
@@ -871,7 +897,7 @@ class Specializer:
 
             def act_map(tid, ch):
                 return dict(space=1, offset=self.arena_off(tid), dims=(ch, W, H, self.cap),
-                            box=(BK, 16, 8, 1), strides=(4 * ch, 4 * ch * W, 4 * ch * W * H),
+                            box=(BK, 16, 8 + rs - 1, 1), strides=(4 * ch, 4 * ch * W, 4 * ch * W * H),
                             swizzle=sw)
             tm_a = act_map(u.input_ids[0], conv["C0"])
             tm_a1 = (act_map(u.input_ids[1], conv["CI"] - conv["C0"]) if conv["CONCAT"]
@@ -941,6 +967,7 @@ class Specializer:
                        f" chains {NACC} bufs {ABUF}{'' if csplit else ' merged-corr'}"
                        f"{' A via cp.async' if aldg else ''}"
                        f"{' taps packed in N' if kpack else ''}"
+                       f"{' rows shared by the kernel rows' if rs > 1 else ''}"
                        f"{' all taps packed in N' if kp9 else ''}"
                        f"{' depthwise fused' if dwf else ''}"
                        f"{' 8x16-pixel conv tiles' if conv else ' row tiles'}"

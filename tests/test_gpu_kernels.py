@@ -827,3 +827,29 @@ def test_direct_conv_pool_window_split_over_lanes(h, w, ci, co, n):
     got, net = gpu(m, wt, xin)
     assert any("direct" in l.kernel and "immediates" in l.note for l in net.artifact.launches)
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("h,w,ci,co,k,pad,n", [
+    (19, 35, 32, 32, 3, "same", 2), (12, 21, 16, 32, 5, "same", 2), (13, 18, 32, 64, 3, "valid", 2),
+    (20, 33, 128, 32, 3, "same", 1)])
+def test_row_shared_kpack_conv(h, w, ci, co, k, pad, n):
+    """KPACK conv tiles with one A box of 8 + KH - 1 rows shared by every
+    kernel row (RS, 16-row descriptor offsets; 16-channel k-blocks when two
+    32-channel stages do not fit), against the oracle and the per-row-box form."""
+    rng = np.random.default_rng(ci * k + co)
+    b = NetBuilder()
+    x = b.input((h, w, ci))
+    y = b.layer("Conv2D", [x], {"filters": co, "kernel_size": k, "padding": pad, "activation": "tanh"},
+                [("kernel", he(rng, (k, k, ci, co), k * k * ci)),
+                 ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    m, wt = b.build([y])
+    xin = rng.uniform(-2, 2, (n, h, w, ci)).astype(F32)
+    got, net = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0, direct_imm=False)
+    assert any("rows shared" in l.note for l in net.artifact.launches), \
+        [l.note for l in net.artifact.launches]
+    want = ref(m, wt, xin)
+    np.testing.assert_allclose(got, want, **TOL)
+    per_row, net1 = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0, direct_imm=False, rowshare=False)
+    assert not any("rows shared" in l.note for l in net1.artifact.launches)
+    np.testing.assert_allclose(per_row, want, **TOL)

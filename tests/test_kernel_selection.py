@@ -103,3 +103,55 @@ def test_small_net_small_batch_is_one_tinynet_launch():
         assert not any("tinynet" in l.kernel for l in launches(*zoo.build(cfg), 64, tiny=True))
     ls = launches(*zoo.build(0), 8)                      # opt-in
     assert not any("tinynet" in l.kernel for l in ls)
+
+
+def test_tc_tiles_fit_shared_memory_and_share_rows():
+    """Every tcgen05 launch of the BASELINE configs fits the 227 KB opt-in
+    shared memory at its bench batch (row-shared KPACK stages fall back to
+    per-row boxes when two do not fit), and cfg4's narrow KPACK convs use the
+    row-shared A boxes (one box of 8 + KH - 1 rows)."""
+    from paper_1906_05737_b200.kernels import SMEM_MAX
+    shared = 0
+    for cfg, batch in ((0, 4096), (1, 65536), (2, 1024), (3, 256), (4, 64)):
+        m, w = zoo.build(cfg)
+        for l in launches(m, w, batch):
+            if "_tc_" not in l.kernel:
+                continue
+            assert l.smem <= SMEM_MAX, (cfg, l.kernel, l.smem)
+            if "rows shared" in l.note:
+                shared += 1
+                assert l.tmaps[0]["box"][2] == 10, l.tmaps[0]
+    assert shared >= 2
+
+
+def _cfg_fields(src, kernel):
+    """The specialised Cfg constants of one kernel's translation unit."""
+    import re
+    return {k: int(v) for k, v in re.findall(r"static constexpr long long (\w+) = (-?\d+)LL;", src)}
+
+
+def test_wide_kpack_tiles_drain_one_chunk():
+    """The N > 128 KPACK epilogue drains one accumulator chunk (nnb_gemm_tc.cuh
+    static_assert): on every tcgen05 conv tile of the randomised tensor-core
+    networks (tests/test_gpu_fuzz_tc.py) a wide KPACK tile's K fits one chunk,
+    with and without row-shared boxes."""
+    from test_gpu_fuzz_tc import tc_network
+    from paper_1906_05737_b200.tuning import make_tuning
+    seen = 0
+    for seed in range(48):
+        rng = np.random.default_rng(1000 + seed)
+        m, w, _ = tc_network(rng)
+        n = int(rng.choice([1, 2, 5, 17]))
+        for rowshare in (True, False):
+            tn = make_tuning(dict(tc_min_rows=1, tc_tile_use=0, dw_fusion=bool(seed % 2), rowshare=rowshare))
+            plan = build_plan(build_graph(m, w), dw_fusion=tn.dw_fusion)
+            sp = specialize(plan, plan_buffers(plan), EXACT, n, n, **tn.specializer_kwargs())
+            for l in sp.launches:
+                if "_tc_" not in l.kernel or not l.n_min <= n <= l.n_max:
+                    continue
+                f = _cfg_fields(sp.sources[sp.kernel_source[sp.kernel_names.index(l.kernel)]], l.kernel)
+                if f.get("KPACK") and f["N"] > 128:
+                    seen += 1
+                    kb = -(-f["K"] // (f["BK"] * f["RS"]))
+                    assert kb <= f["CHUNK"], (seed, l.kernel, f["K"], f["BK"], f["RS"], f["CHUNK"])
+    assert seen > 0
