@@ -733,6 +733,13 @@ class Specializer:
         NACC = max(1, min(8, 128 // BN)) if self.nacc is None else max(1, min(self.nacc, 128 // BN))
         aldg = self.aldg
         tmem_a = self.tmem_a and NACC == 1 and not aldg and (BN <= 64 or BN == 128)
+        if (tmem_a and BN > 64 and head is not None and -(-CO // BN) == 1 and not wide
+                and u.residual_id is None and not kpack):
+            # A in TMEM leaves one accumulator buffer at BN = 128, which keeps a
+            # following head out of the epilogue; shared-memory A with two
+            # buffers + the fused head (cfg1 @65536: 256->128 + 128->10 0.0371
+            # + 0.0108 -> 0.0379 ms, replay 0.3214 -> 0.3160 ms)
+            tmem_a = False
         if wide:
             BK = self.wide_bk
             sw = 3 if BK == 32 else 2
@@ -933,7 +940,7 @@ class Specializer:
         # the head's FFMAs lengthen the epilogue: only when a second accumulator
         # buffer keeps the MMA from waiting on it (measured: cfg0 Dense 256->32
         # + 32->2, two buffers: replay -1.3%; cfg1 256->128 + 128->10, one
-        # buffer: +1%)
+        # buffer (A in TMEM): +1%, two (A in shared memory): -1.7%)
         if (head is not None and ntn == 1 and BN >= 32 and not wide and not res and not kpack
                 and ABUF >= 2):
             hn = head.kernel.shape[1]

@@ -221,7 +221,10 @@ def test_specialised_launches_cover_every_unit_once_per_batch(cfg, batch):
             continue
         units = [l.unit for l in act]
         assert sorted(units) == sorted(set(units)), (n, units)
-        assert set(units) == set(range(len(plan.units))), (n, units)
+        # a tcgen05 launch with a fused head (kernels.py HEAD) also covers the next unit
+        heads = [l.unit + 1 for l in act if "fused Dense head" in l.note]
+        assert not set(heads) & set(units), (n, units, heads)
+        assert set(units) | set(heads) == set(range(len(plan.units))), (n, units)
 
 
 def _reference_nnjit():
