@@ -235,12 +235,14 @@ class Specializer:
                  kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, small_conv=True, small_conv_kper=16, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
         self.conv_w4 = conv_w4
         self.rowshare = rowshare
+        self.small_conv = small_conv
+        self.small_conv_kper = small_conv_kper
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
         self.tc_min_images = tc_min_images
@@ -422,6 +424,32 @@ class Specializer:
                 n_min = hi + 1
         else:
             n_min = 1
+            # few-pixel pointwise convs (batch-1 latency): while the tiled GEMM
+            # (16 x 64 tiles) would not fill one wave of CTAs, the split-K row
+            # kernel (1 / 2 / 4 pixels per block, 16 k per warp) -- the GEMM
+            # runs a handful of CTAs through a serial K loop.  Measured (warm
+            # replays): cfg3 @1 0.103 -> 0.058 ms, @16 0.113 -> 0.100, cfg2
+            # @1 0.033 -> 0.029 ms; from a full wave on it loses (cfg3 @64
+            # 0.142 -> 0.152 ms with it on the 4x4 layers)
+            n_hi = 0
+            if (u.kind == "Conv2D" and KH == KW == S == 1 and PT == PL == 0 and not concat
+                    and not pool_fused and UPF == 1 and u.dw is None and not softmax
+                    and self.small_conv and self.max_batch > 0):
+                n_hi = min(self.max_batch, 16 * ((self.sm_count - 1) // -(-CO // 64)) // rows)
+            if n_hi > 0:
+                lo = 1
+                for mb, m_cap in ((1, 256), (2, 1024), (4, 1 << 30)):
+                    hi = min(n_hi, m_cap // rows)
+                    if hi >= lo:
+                        # (the opt-in persistent kernel takes blocks of <= MEGA_THREADS)
+                        kper = max(self.small_conv_kper, CI // (MEGA_THREADS // 32)) if self.mega \
+                            else self.small_conv_kper
+                        self._dense_small(pos, u, wmat, CI, CO, False, n_min=lo, n_max=hi, rows=rows,
+                                          mb=mb, kper=kper)
+                        lo = hi + 1
+                if self.max_batch <= n_hi:
+                    return
+                n_min = n_hi + 1
 
         # depthwise producer + narrow pointwise conv: one fused kernel
         # (nnb_sep.cuh, all batch sizes)
@@ -1032,12 +1060,12 @@ class Specializer:
                        f"{(4 // psplit if psplit else 4) if pool_fused else pxt}"
                        f"{' weights as immediates' if wimm else ' weights in smem'}")
 
-    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None, n_min=1):
+    def _dense_small(self, pos, u, wmat, K, CO, softmax, n_max, rows=1, mb=None, n_min=1, kper=32):
         """Split-K GEMV/GEMM for few rows: Dense at n <= n_max (MB = n_max
         rows per block), or a 1x1 conv whose n*rows pixels are the rows (MB
         = ``mb`` per block)."""
         MB = mb or n_max
-        KS = max(1, min(32, K // 32))
+        KS = max(1, min(32, K // kper))
         fields = dict(K=K, CO=CO, MB=MB, KS=KS, ROWS=rows,
                       IN_OFF=self.arena_off(u.input_ids[0]),
                       IN_IMG=self.img_bytes(u.input_ids[0]),

@@ -64,6 +64,8 @@ class Tuning:
     cb16_w4: bool = True           # 4 split warps for BF16-correction tiles
     conv_w4: object = "auto"       # 4 split warps for conv tiles: "auto" (short k-block work), True, False
     rowshare: bool = True          # KPACK conv tiles: one A box of 8+KH-1 rows serves every kernel row
+    small_conv: bool = True        # few-pixel 1x1 convs (one wave of GEMM tiles or less): split-K row kernel
+    small_conv_kper: int = 16
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
     early_mma: bool = True         # N = 256 BF16-correction tiles: main MMAs before the split
 
