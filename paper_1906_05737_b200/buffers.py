@@ -71,7 +71,9 @@ def _reads(u):
 
 def _writes(u):
     dp = getattr(u, "dual_pool", None)
-    return (u.output_id,) + ((dp.output_id,) if dp is not None else ())
+    da = getattr(u, "dw_after", None)
+    return ((u.output_id,) + ((dp.output_id,) if dp is not None else ())
+            + ((da.output_id,) if da is not None else ()))
 
 
 def head_pairs(plan):

@@ -313,6 +313,9 @@ __device__ __forceinline__ void named_sync64(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 // named barrier over the four epilogue warps of one column group
+__device__ __forceinline__ void named_sync256(int id) {
+  asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
 __device__ __forceinline__ void named_sync128(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
@@ -589,7 +592,26 @@ struct GemmTc {
   static constexpr int NBUF = ET ? (C::RES ? EGRP : (EGRP < 2 ? EGRP : 2)) : 1;
   static_assert(!ET || !(C::POOL || C::UPF > 1 || KP), "TMA epilogue: plain row tiles only");
   static_assert(!(C::RES && C::UPF > 1), "residual fusion excludes upsampling (planner)");
-  static constexpr int EPI_STAGE = EPI_WARPS * NBUF * 2048;       // 32 x 16 fp32 per buffer
+  // EDW: the DepthwiseConv2D consuming this 1x1 conv computed in the epilogue
+  // (planner.fuse_pw_dw).  A 128-row tile holds 128 / (E_H * E_W) whole images
+  // (cfg3's 8x8 and 4x4 maps), so the finished tile -- bias, activation,
+  // post-BN applied -- is parked in shared memory as [row][BN + 4] floats
+  // (lane = row float4 stores and channel-quad = lane float4 loads are both
+  // conflict-free) and the eight epilogue warps run the depthwise taps over
+  // it: a thread owns one output row of one image and one channel quad,
+  // reads each input row of the window once into registers and slides the
+  // taps over it (reference order: bias, then (ky, kx), out-of-image taps
+  // skipped -- pkg/src/nnjit/interpreter.py:65-73), then stores the depthwise
+  // output (512 contiguous bytes per warp and pixel).  The pointwise output
+  // itself is never written.
+  static constexpr bool EDW = C::EDW != 0;
+  static constexpr int ETS = C::BN + 4;                           // parked tile row stride (floats)
+  static constexpr int EDW_BYTES = EDW ? (BM * ETS * 4 + 1023) / 1024 * 1024 : 0;
+  static_assert(!EDW || (!C::CONV && !C::RES && C::UPF == 1 && !C::HEAD && !KP && !K9 && !WIDE && !ET &&
+                         !C::DPOOL && BM % (C::E_H * C::E_W) == 0 && C::BN % 32 == 0 && C::N % 4 == 0 &&
+                         C::ROWS == C::E_H * C::E_W && C::E_W <= 16),
+                "depthwise epilogue: row tiles holding whole images");
+  static constexpr int EPI_STAGE = EDW ? EDW_BYTES : EPI_WARPS * NBUF * 2048;   // 32 x 16 fp32 per buffer
   static_assert(!K9 || 2 * (C::KH - 1) * 8 * 16 * (C::CO / 2) * 4 <= EPI_STAGE,
                 "KP9 vertical exchange fits the staging area");
   // HEAD: a following Dense with HN <= 16 outputs (a classifier head, e.g.
@@ -1210,6 +1232,8 @@ struct GemmTc {
       float4* ebuf = epi_stage + ew * NBUF * 128;      // this warp's 2 KB boxes
       int acc = 0;
       u32 aph = 0, rph = 0;
+      constexpr int ECQ = C::BN / 4, ETAPS = EDW ? C::E_KH * C::E_KW : 1;
+      const int et = threadIdx.x - 32 * EPI_W0, ecq = et % ECQ;
       for (int t = t0; t < tiles; t += tstep) {
         const int mb = mb_of(t), nb = t % NTN;
         // TMA box (32 rows of this warp x 16 columns from `col`) load / store
@@ -1659,7 +1683,13 @@ struct GemmTc {
             dual_pool_store<16>(arena, v, (r & 17) == 0, img, (tt / TX) * TH + r / TW,
                                 (tt % TX) * TW + r % TW, col0, n);
           }
-          if constexpr (ET) {
+          if constexpr (EDW) {
+            float* trow = reinterpret_cast<float*>(epi_stage) + r * ETS + cbeg + g * 16;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<float4*>(trow + 4 * j) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else if constexpr (ET) {
             float4* b = ebuf + (g % NBUF) * 128;
             if (C::RES) {
               if (g == 0) mbar_wait(&rbar[ew], rph);
@@ -1731,6 +1761,76 @@ struct GemmTc {
               }
             }
           }
+        }
+        if constexpr (EDW) {
+          // this thread's channel quad of the depthwise kernel and bias (the
+          // same for every row task it takes); the loads fly across the barrier
+          const int ch = nb * C::BN + 4 * ecq;
+          const int chl = ch < C::N ? ch : 0;
+          float4 ewq[ETAPS];
+#pragma unroll
+          for (int k = 0; k < ETAPS; ++k)
+            ewq[k] = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::E_W_OFF) + k * C::N + chl));
+          const float4 eb4 = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::E_B_OFF) + chl));
+          named_sync256(9);                          // the tile is parked
+          constexpr int P = C::E_H * C::E_W, IMGS = BM / P, RT = IMGS * C::E_HO;
+          constexpr int OXC = C::E_WO < 4 ? C::E_WO : 4;       // outputs per register window
+          const float* T = reinterpret_cast<const float*>(epi_stage) + 4 * ecq;
+          const float* eps = at<float>(pool, C::E_PS_OFF);
+          const float* epo = at<float>(pool, C::E_PO_OFF);
+          constexpr int TPR = EPI_THREADS / ECQ;               // row tasks in flight
+#pragma unroll 1
+          for (int rt = et < TPR * ECQ ? et / ECQ : RT; rt < RT; rt += TPR) {
+            const int li = rt / C::E_HO, oy = rt - li * C::E_HO;
+            const long long img = (long long)mb * IMGS + li;
+            if (img >= n || ch >= C::N) continue;
+            float* d = at<float>(arena, C::E_OUT_OFF + img * C::E_OUT_IMG) +
+                       (long long)oy * C::E_WO * C::N + ch;
+#pragma unroll
+            for (int ox0 = 0; ox0 < C::E_WO; ox0 += OXC) {
+              constexpr int XW = (OXC - 1) * C::E_S + C::E_KW;   // input columns of the window
+              const int ixb = ox0 * C::E_S - C::E_PL;            // its first column (compile-time)
+              float4 a[OXC];
+#pragma unroll
+              for (int o = 0; o < OXC; ++o) a[o] = eb4;
+#pragma unroll
+              for (int ky = 0; ky < C::E_KH; ++ky) {
+                const int iy = oy * C::E_S - C::E_PT + ky;
+                if (iy < 0 || iy >= C::E_H) continue;
+                const float* row = T + (li * P + iy * C::E_W) * ETS;
+                float4 x[XW];
+#pragma unroll
+                for (int j = 0; j < XW; ++j)
+                  if (ixb + j >= 0 && ixb + j < C::E_W)
+                    x[j] = *reinterpret_cast<const float4*>(row + (ixb + j) * ETS);
+#pragma unroll
+                for (int kx = 0; kx < C::E_KW; ++kx) {
+                  const float4 w4 = ewq[ky * C::E_KW + kx];
+#pragma unroll
+                  for (int o = 0; o < OXC; ++o) {
+                    const int j = o * C::E_S + kx;
+                    if (ox0 + o >= C::E_WO || ixb + j < 0 || ixb + j >= C::E_W) continue;
+                    if (C::E_FMA) {     // one rounding per tap (within the FP32 gate)
+                      a[o].x = fmaf(x[j].x, w4.x, a[o].x); a[o].y = fmaf(x[j].y, w4.y, a[o].y);
+                      a[o].z = fmaf(x[j].z, w4.z, a[o].z); a[o].w = fmaf(x[j].w, w4.w, a[o].w);
+                    } else {            // the interpreter's mul-then-add
+                      a[o].x = add(a[o].x, mul(x[j].x, w4.x)); a[o].y = add(a[o].y, mul(x[j].y, w4.y));
+                      a[o].z = add(a[o].z, mul(x[j].z, w4.z)); a[o].w = add(a[o].w, mul(x[j].w, w4.w));
+                    }
+                  }
+                }
+              }
+#pragma unroll
+              for (int o = 0; o < OXC; ++o)
+                if (ox0 + o < C::E_WO)
+                  *reinterpret_cast<float4*>(d + (ox0 + o) * C::N) = make_float4(
+                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].x, eps, epo, ch),
+                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].y, eps, epo, ch + 1),
+                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].z, eps, epo, ch + 2),
+                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].w, eps, epo, ch + 3));
+            }
+          }
+          if (t + tstep < tiles) named_sync256(9);   // the next tile parks over this one
         }
         if (C::RES && ngrp > 0) rph ^= 1;
       }

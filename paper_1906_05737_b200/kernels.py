@@ -275,6 +275,7 @@ class Specializer:
         self.rn_ss = rn_ss
         self.unit_src = {}            # launch index -> (cfg name, struct, template, dynamic smem)
         self._dual_from = 1 << 30     # lowest batch whose conv launch stores the dual pool
+        self._edw_from = 1 << 30      # ... whose 1x1 conv launch computes the following depthwise conv
         self._n_floor = 1             # regular launches serve batches >= this (TinyNet below)
         self.chunk = chunk
         self.nacc = nacc
@@ -515,9 +516,11 @@ class Specializer:
                 if tc_dwf:
                     conv = dict(H=HO, W=WO, CI=CI, HO=HO, WO=WO, KH=1, KW=1, PT=0, PL=0,
                                 POOL=False, PHO=1, PWO=1, C0=CI, CONCAT=False, UPF=1, DWF=1)
+                edw = u.dw_after if (tc_rows and u.dw_after is not None and u.kind == "Conv2D"
+                                     and u.residual_id is None and UPF == 1) else None
                 self._gemm_tc(pos, u, wmat, K, CO, rows, n_tc, conv,
                               rows_geo=dict(HO=HO, WO=WO, UPF=UPF),
-                              head=self._head_candidate(pos, u) if not conv else None)
+                              head=self._head_candidate(pos, u) if not conv else None, edw=edw)
                 n_max = n_tc - 1
                 if n_max < n_min:
                     return
@@ -686,7 +689,7 @@ class Specializer:
         return v
 
     def _gemm_tc(self, pos, u, wmat, K, CO, rows, n_min, conv=None, rows_geo=None, head=None,
-                 n_max=1 << 30):
+                 n_max=1 << 30, edw=None):
         """tcgen05 3xTF32 GEMM (csrc/kernels/nnb_gemm_tc.cuh) for n >= n_min.
         ``conv`` switches the A operand to 8x16-pixel implicit-GEMM tiles of a
         stride-1 convolution loaded as 4-D TMA boxes (zero-filled borders)."""
@@ -726,7 +729,9 @@ class Specializer:
         # N = 256 tiles for wide row GEMMs whose K fits one accumulator chunk:
         # a kind::tf32 MMA costs ~1.4x at N = 256 what it costs at N = 128
         res_ = u.residual_id is not None
-        wide = bool(self.wide and not conv and CO >= 256 and K <= 1024 and not res_
+        if edw is not None:
+            head = None
+        wide = bool(self.wide and not conv and edw is None and CO >= 256 and K <= 1024 and not res_
                     and self.pair and not self.aldg and CO % 4 == 0
                     and (not rows_geo or rows_geo.get("UPF", 1) == 1))
         if wide:
@@ -831,8 +836,12 @@ class Specializer:
                        and not (conv and conv["POOL"])
                        and (conv or not rows_geo or rows_geo.get("UPF", 1) == 1)
                        and (not conv or conv.get("UPF", 1) == 1))
+        if edw is not None:
+            epi_tma = False        # the finished tile is parked in shared memory instead
         nbuf = (egrp if res else min(egrp, 2)) if epi_tma else 1
         epi_bytes = 8 * nbuf * 2048
+        if edw is not None:
+            epi_bytes = -(-(128 * (BN + 4) * 4) // 1024) * 1024
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
         room = SMEM_MAX - 1024 - 512 - epi_bytes
         if rs > 1 and room // stage < 2 and BK == 32:
@@ -927,6 +936,26 @@ class Specializer:
             self._dual_from = min(self._dual_from, n_min)
         else:
             fields.update(DPOOL=0, DP_OFF=0, DP_IMG=0, DP_UPF=1, DP_PHO=1, DP_PWO=1)
+        # the depthwise conv consuming this 1x1 conv, in the epilogue (planner.fuse_pw_dw)
+        if edw is not None:
+            eh, ew_, _ = u.output_shape.dims
+            eho, ewo, _ = edw.output_shape.dims
+            ekh, ekw = edw.kernel_hw
+            same = edw.padding == "same"
+            eep = self.epilogue_fields(edw, CO)
+            fields.update(EDW=1, E_H=eh, E_W=ew_, E_HO=eho, E_WO=ewo, E_KH=ekh, E_KW=ekw,
+                          E_S=edw.stride,
+                          E_PT=same_padding(eh, ekh, edw.stride)[0] if same else 0,
+                          E_PL=same_padding(ew_, ekw, edw.stride)[0] if same else 0,
+                          E_W_OFF=self.pool.add(edw.kernel), E_B_OFF=self.pool.add(edw.bias),
+                          E_ACT=eep["ACT"], E_POST=eep["POST"], E_PS_OFF=eep["PS_OFF"],
+                          E_PO_OFF=eep["PO_OFF"], E_OUT_OFF=self.arena_off(edw.output_id),
+                          E_OUT_IMG=self.img_bytes(edw.output_id), E_FMA=int(bool(self.sep_fma)))
+            self._edw_from = min(self._edw_from, n_min)
+        else:
+            fields.update(EDW=0, E_H=1, E_W=1, E_HO=1, E_WO=1, E_KH=1, E_KW=1, E_S=1, E_PT=0, E_PL=0,
+                          E_W_OFF=0, E_B_OFF=0, E_ACT=0, E_POST=0, E_PS_OFF=0, E_PO_OFF=0,
+                          E_OUT_OFF=0, E_OUT_IMG=0, E_FMA=0)
         if conv:
             H, W = conv["H"], conv["W"]
 
@@ -992,6 +1021,8 @@ class Specializer:
         else:
             ipi, ipb = rows, 256 if pair else 128
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
+            if edw is not None:
+                tag = f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc"
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
@@ -1010,6 +1041,7 @@ class Specializer:
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
                        f"{' bf16 corr' if cb16 else ''}"
                        f"{' + pooled second store' if dp is not None else ''}"
+                       f"{' + depthwise conv in the epilogue' if edw is not None else ''}"
                        f"{f' + fused Dense head N={hn}' if hn else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,
@@ -1353,7 +1385,7 @@ class Specializer:
                        f"{len(blocks)} weight blocks in a {nstage}-stage ring, {smem // 1024} KB "
                        "shared")
 
-    def depthwise(self, pos, u):
+    def depthwise(self, pos, u, n_cap=1 << 30):
         H, W, C = u.input_shapes[0].dims
         HO, WO, _ = u.output_shape.dims
         KH, KW = u.kernel_hw
@@ -1369,6 +1401,9 @@ class Specializer:
         base.update(self.epilogue_fields(u, C))
 
         def variant(px, n_min, n_max):
+            n_max = min(n_max, n_cap)
+            if n_min > n_max:
+                return
             per_img = HO * -(-WO // px) * (C // vec)
             self.emit(pos, f"dw{KH}x{KW}", "nnb::Depthwise",
                       dict(base, PX=px, IDX32=int(self.cap * per_img < 2 ** 31)),
@@ -1497,11 +1532,14 @@ class Specializer:
         for pos, u in enumerate(self.plan.units):
             self._n_cap = self.head_cap.get(pos)
             if u.kind in ("Dense", "Conv2D"):
-                self._dual_from = 1 << 30
+                self._dual_from = self._edw_from = 1 << 30
                 self.gemm(pos, u)
                 if u.dual_pool is not None and self._dual_from > 1:
                     # batches whose conv kernel has no second (pooled) store
                     self.pool_unit(pos, u.dual_pool, n_max=self._dual_from - 1)
+                if u.dw_after is not None and self._edw_from > 1:
+                    # batches whose conv kernel has no depthwise epilogue
+                    self.depthwise(pos, u.dw_after, n_cap=self._edw_from - 1)
             elif u.kind == "DepthwiseConv2D":
                 if u.residual_id is not None or u.pool_after or u.softmax_after:
                     raise UnsupportedLayer("depthwise epilogue fusion")

@@ -77,6 +77,10 @@ class CompilationUnit:
     steps: list = None              # Chain: the fused units, in order
     dual_pool: object = None        # a 2x2 max-pool (Pool unit) computed from this conv's
                                     # output in its epilogue while the full output is stored
+    dw_after: object = None         # the DepthwiseConv2D (a unit) consuming this 1x1 conv's output,
+                                    # computed in the conv's tcgen05 epilogue (fuse_pw_dw): the unit
+                                    # then writes the depthwise output; its own output_id is only
+                                    # written at batch sizes whose kernel lacks that epilogue
 
     def describe(self):
         bits = [self.kind, ",".join(map(str, self.input_shapes)) + f" -> {self.output_shape}"]
@@ -103,6 +107,9 @@ class CompilationUnit:
             bits.append(f"+maxpool2->t{self.dual_pool.output_id}"
                         + (f"+upsample{self.dual_pool.upsample_after}"
                            if self.dual_pool.upsample_after > 1 else ""))
+        if self.dw_after is not None:
+            kh, kw = self.dw_after.kernel_hw
+            bits.append(f"+dw{kh}x{kw}/s{self.dw_after.stride}->t{self.dw_after.output_id}")
         if self.steps:
             bits.append("[" + " | ".join(
                 f"{st.kind}{'%dx%d/s%d' % (*st.kernel_hw, st.stride) if st.kernel_hw else ''}"
@@ -125,7 +132,7 @@ class FusionPlan:
     node_units: dict = field(default_factory=dict)
 
     def producer_positions(self):
-        return {u.output_id: p for p, u in enumerate(self.units)}
+        return {t: p for p, u in enumerate(self.units) for t in unit_writes(u)}
 
     def consumer_count(self, tid):
         return (sum(t == tid for u in self.units for t in self._reads(u))
@@ -449,9 +456,12 @@ def fuse_upsample(plan):
 
 
 def unit_writes(u):
-    """Tensors a unit writes: its output, and a dual-stored pooled map."""
+    """Tensors a unit writes: its output, a dual-stored pooled map, and the
+    output of a depthwise conv computed in its epilogue."""
     dp = getattr(u, "dual_pool", None)
-    return (u.output_id,) + ((dp.output_id,) if dp is not None else ())
+    da = getattr(u, "dw_after", None)
+    return ((u.output_id,) + ((dp.output_id,) if dp is not None else ())
+            + ((da.output_id,) if da is not None else ()))
 
 
 def fuse_pool_dual(plan):
@@ -580,6 +590,49 @@ def fuse_dw_pw(plan, narrow_only=False):
             plan.tensors.pop(d.output_id, None)
             _delete(plan, pos - 1, u)
             continue
+        pos += 1
+    return plan
+
+
+PW_DW_TILE_ROWS = 128      # rows of a tcgen05 row tile (nnb_gemm_tc.cuh BM)
+PW_DW_MIN_CO = 32
+
+
+def pw_dw_ok(u, d):
+    """Geometry of a pointwise conv ``u`` whose consumer ``d`` (depthwise) the
+    tcgen05 epilogue can compute: a 128-row tile holds whole images (8x8 and
+    4x4 maps: 2 and 8 images), so every tap of the depthwise window lies in
+    the tile the CTA has just finished."""
+    h, w, c = u.output_shape.dims
+    kh, kw = d.kernel_hw
+    return (PW_DW_TILE_ROWS % (h * w) == 0 and w <= 16 and c % 4 == 0 and c >= PW_DW_MIN_CO
+            and kh <= 5 and kw <= 5 and d.stride in (1, 2)
+            and u.input_shapes[0].c % 4 == 0)
+
+
+def fuse_pw_dw(plan):
+    """A pointwise (1x1, stride 1) Conv2D whose only consumer is a
+    DepthwiseConv2D over a map small enough that a 128-row GEMM tile holds
+    whole images (cfg3's 8x8 and 4x4 stages) computes that depthwise conv in
+    its tcgen05 epilogue (nnb_gemm_tc.cuh EDW): the finished tile stays in
+    shared memory, the depthwise taps read it there, and only the depthwise
+    output is stored -- one launch and one round trip through memory less per
+    separable block.  The pointwise output keeps its buffer: batch sizes
+    served by kernels without that epilogue write it and run the depthwise
+    conv as its own launch (kernels.py)."""
+    pos = 0
+    while pos + 1 < len(plan.units):
+        u, d = plan.units[pos], plan.units[pos + 1]
+        if (u.kind == "Conv2D" and d.kind == "DepthwiseConv2D" and u.kernel_hw == (1, 1)
+                and u.stride == 1 and d.input_ids == (u.output_id,) and u.dw is None
+                and u.dw_after is None and u.dual_pool is None and not u.concat_in
+                and not u.pool_after and u.upsample_after == 1 and not u.softmax_after
+                and u.residual_id is None and d.residual_id is None and not d.pool_after
+                and d.upsample_after == 1 and not d.softmax_after and d.dw_after is None
+                and u.output_shape.rank == 3 and pw_dw_ok(u, d)
+                and _private(plan, u.output_id)):
+            u.dw_after = d
+            _delete(plan, pos + 1, u)
         pos += 1
     return plan
 
@@ -794,7 +847,8 @@ def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
     return plan
 
 
-def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False):
+def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False,
+               pw_dw=True):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -807,11 +861,11 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain
     depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
-        apply_gpu_fusions(plan, dw_fusion, chain, tc_chain)
+        apply_gpu_fusions(plan, dw_fusion, chain, tc_chain, pw_dw)
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False, pw_dw=True):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -825,6 +879,8 @@ def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False):
         fuse_tc_chain(plan)
     if chain:
         fuse_chain(plan)
+    if pw_dw and not chain and not tc_chain:
+        fuse_pw_dw(plan)
     return plan
 
 
@@ -835,7 +891,8 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
                          "pool_op", "factor", "in_place_preference")
 
 
-def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False):
+def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False,
+               pw_dw=True):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions
@@ -863,7 +920,7 @@ def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=
     ours = FusionPlan(units, {t: shape(s) for t, s in plan.tensors.items()},
                       tuple(plan.input_ids), tuple(plan.output_ids), dict(plan.node_units))
     if gpu_fusion:
-        apply_gpu_fusions(ours, dw_fusion, chain, tc_chain)
+        apply_gpu_fusions(ours, dw_fusion, chain, tc_chain, pw_dw)
     return ours
 
 

@@ -146,6 +146,12 @@ def unit_work(u, plan=None):
         pf, _, _ = unit_work(dp)
         f += pf
         out += 4 * dp.output_shape.elements
+    da = getattr(u, "dw_after", None)
+    if da is not None:             # depthwise conv in the epilogue: only its output is stored
+        df, _, dwb = unit_work(da)
+        f += df
+        wb += dwb
+        out += 4 * (da.output_shape.elements - u.output_shape.elements)
     d = getattr(u, "dw", None)
     if d is not None:              # fused depthwise producer
         df, _, dwb = unit_work(d)

@@ -21,6 +21,8 @@ class Tuning:
     gpu_fusion: bool = True        # B200 epilogue fusions (pool, residual, softmax, upsample, concat)
     dw_fusion: object = "narrow"   # depthwise->pointwise: "narrow" (SepNarrow), True (all), False
     head: bool = True              # fuse a <=16-wide Dense head into a tcgen05 Dense epilogue
+    pw_dw: bool = True             # pointwise conv + the depthwise conv consuming it, computed in the
+                                   # tcgen05 epilogue where a 128-row tile holds whole images (fuse_pw_dw)
     tc_chain: bool = False         # 8x8-stage pointwise/depthwise runs as one tcgen05 kernel
                                    # (planner.fuse_tc_chain; correct, break-even, opt-in)
     chain: bool = False            # small depthwise/pointwise runs as one FFMA kernel (fuse_chain;
@@ -74,7 +76,7 @@ class Tuning:
         filled in where the field is None)."""
         from .kernels import (MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_IMAGES, TC_MIN_K,
                               TC_MIN_ROWS)
-        skip = {"gpu_fusion", "dw_fusion", "chain", "tc_chain"}
+        skip = {"gpu_fusion", "dw_fusion", "chain", "tc_chain", "pw_dw"}
         kw = {f.name: getattr(self, f.name) for f in fields(self) if f.name not in skip}
         if kw["tc_min_rows"] is None:
             kw["tc_min_rows"] = MEGA_TC_MIN_ROWS if self.mega else TC_MIN_ROWS

@@ -91,3 +91,6 @@ def _run_unit(u, vals):
         dp = getattr(u, "dual_pool", None)
         if dp is not None:                # the conv's second, pooled store
             _run_unit(dp, vals)
+        da = getattr(u, "dw_after", None)
+        if da is not None:                # the depthwise conv computed in the epilogue
+            _run_unit(da, vals)

@@ -748,6 +748,48 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
         np.testing.assert_allclose(g, wv, **TOL)
 
 
+@pytest.mark.parametrize("n", [1, 3, 40, 77])
+@pytest.mark.parametrize("case", [
+    # cfg3's 8x8 stage: pw -> dw pairs (stride 1, then stride 2 to 4x4), post-BN after some
+    (8, 8, 64, [("p", 128, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 128, "relu6"),
+                ("d", 3, 2, "same", "relu6"), ("p", 256, "relu6"), ("d", 3, 1, "same", "relu6"),
+                ("p", 256, "linear")], True, True),
+    # 4x8 maps (four images per tile), 5x5 and 'valid' windows, 96 channels (BN = 96 -> 128),
+    # two N tiles (160 channels), tanh / sigmoid epilogues
+    (4, 8, 32, [("p", 96, "tanh"), ("d", 5, 1, "same", "relu"), ("p", 160, "sigmoid"),
+                ("d", 3, 1, "valid", "elu"), ("p", 32, "linear")], False, False),
+    # 2x2 maps (32 images per tile) and a 16x8 map (one image per tile)
+    (16, 8, 16, [("p", 64, "relu"), ("d", 3, 2, "same", "relu6"), ("p", 64, "relu6"),
+                 ("d", 3, 2, "valid", "linear"), ("p", 32, "relu"), ("d", 3, 2, "same", "tanh")],
+     False, True)])
+@pytest.mark.parametrize("opts", [EXACT, ApproximationOptions()], ids=["exact", "default"])
+def test_pointwise_with_depthwise_epilogue(case, n, opts):
+    """planner.fuse_pw_dw + nnb_gemm_tc.cuh EDW: a 1x1 conv whose consumer is a
+    depthwise conv over a map that fits a 128-row tile computes that conv in
+    its tcgen05 epilogue (ragged batches leave part of a tile empty); batch
+    sizes below the tcgen05 threshold run the depthwise conv as a second
+    launch of the unit.  Against the oracle and the unfused plan."""
+    h, w, c, spec, gap, post_bn = case
+    rng = np.random.default_rng(len(spec) * 13 + c + n)
+    m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
+    x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
+    want = ref(m, wt, x, "exact" if opts == EXACT else opts)
+    for tune in (dict(tc_min_rows=1, tc_min_images=1, small_conv=False), {}):
+        got, net = gpu(m, wt, x, opts, **tune)
+        fused = [u for u in net.plan.units if u.dw_after is not None]
+        assert fused, net.plan.describe()
+        act = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
+        if tune:
+            assert any("depthwise conv in the epilogue" in l.note for l in act), [l.kernel for l in act]
+        for u in fused:      # one fused launch, or the pointwise kernel + a depthwise launch
+            mine = [l for l in act if net.plan.units[l.unit] is u]
+            assert len(mine) == (1 if "depthwise conv in the epilogue" in mine[0].note else 2)
+        np.testing.assert_allclose(got, want, **TOL)
+    unf, net0 = gpu(m, wt, x, opts, pw_dw=False)
+    assert not [u for u in net0.plan.units if u.dw_after is not None]
+    np.testing.assert_allclose(got, unf, **TOL)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 64])
 @pytest.mark.parametrize("case", [
     # cfg3-like: pw 64->128 reading an 8x8 map from the arena, dw/pw pairs at 8x8,
