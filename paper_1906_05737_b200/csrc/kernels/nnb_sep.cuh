@@ -26,6 +26,11 @@
 //   * the tile's outputs (contiguous rows) are staged in shared memory as
 //     16-byte rows and written back as coalesced float4 stores (storing each
 //     pixel's CO floats straight from registers was 5-10% slower).
+//   * SP = 2 (wide layers, whose band leaves room for only a few CTAs per SM):
+//     two threads per pixel in neighbouring WARPS -- each runs the depthwise
+//     taps of half the channels, the halves meet in a shared-memory exchange
+//     row, and each forms half of the pointwise outputs -- so the same band
+//     feeds twice the warps (cfg3's 32-channel blocks ran 8 warps per SM).
 // Measured alternatives (cfg3 @256, dw 64x64x8 + pw 16): a band version with
 // per-tap bounds checks and weights loaded from shared memory spent 700
 // instructions per pixel (36.9 us, 64% issue-busy); a register version with
@@ -48,14 +53,19 @@ struct SepNarrow {
   static constexpr int PXT = TH * WO;                               // output pixels per tile
   static constexpr int CQ = CI / 4;
   static constexpr int BAND = RI * WB * CP;                         // floats per stage
-  static_assert(CI % 4 == 0 && CI <= 128 && CO <= 128 && PXT <= NT && NT % 32 == 0 && NT <= 1024,
+  static constexpr int SP = C::SP;                                  // threads per pixel
+  static constexpr int CQH = CQ / SP, COH = CO / SP;                // quads / outputs per thread
+  static_assert(CI % 4 == 0 && CI <= 128 && CO <= 128 && SP * PXT <= NT && NT % (32 * SP) == 0 &&
+                NT <= 1024 && (SP == 1 || (SP == 2 && CQ % 2 == 0 && CO % 8 == 0)),
                 "depthwise + narrow pointwise");
   // staging row stride: 16-byte rows at an odd 16-byte stride (conflict-free
   // float4 writes) when CO % 4 == 0, else an odd float stride
   static constexpr int RS = CO % 4 ? (CO | 1) : (((CO + 4) / 4) % 2 ? CO + 4 : CO + 8);
   struct Smem {
     float a[NS][BAND];
-    float o[PXT * RS];
+    // output staging; with SP = 2 first the exchange rows of the depthwise
+    // outputs (one padded row per pixel), read back before any output lands
+    float o[PXT * (SP == 2 && CP > RS ? CP : RS)];
   };
 
   __device__ static void load_tile(Smem& sm, int stage, const float* in, i64 tile) {
@@ -110,7 +120,10 @@ struct SepNarrow {
     const float* dpo = at<float>(pool, C::DW_PO_OFF);
     const float* ps = at<float>(pool, C::PS_OFF);
     const float* po = at<float>(pool, C::PO_OFF);
-    const int py = t / WO, ox = t - py * WO;
+    // SP = 2: warps 2g and 2g + 1 own the same 32 pixels, half the channels each
+    const int h = SP == 2 ? (t >> 5) & 1 : 0;
+    const int pix = SP == 2 ? ((t >> 6) << 5) + (t & 31) : t;
+    const int py = pix / WO, ox = pix - py * WO;
     const int boff = (py * S * WB + ox * S) * CP;       // the pixel's first tap in the band
 
     int stage = 0;
@@ -127,53 +140,92 @@ struct SepNarrow {
       const int oy0 = (int)(tile - img * TPI) * TH;
       const int live = (HO - oy0 < TH ? HO - oy0 : TH) * WO;
       const i64 p0 = img * (HO * WO) + (i64)oy0 * WO;      // first output pixel of the tile
-      if (t < live) {
+      float a[CI];
+      if (pix < live) {
         const float* band = &sm.a[stage][boff];
-        float a[CI];
 #pragma unroll
-        for (int q = 0; q < CQ; ++q) {
-          float4 acc = make_float4(C::dwb(4 * q), C::dwb(4 * q + 1), C::dwb(4 * q + 2), C::dwb(4 * q + 3));
+        for (int qq = 0; qq < CQH; ++qq) {
+          // (the two halves branch on the warp's parity so that every weight
+          // index below is a compile-time constant)
+          float4 r4;
 #pragma unroll
-          for (int ky = 0; ky < KH; ++ky)
+          for (int hh = 0; hh < SP; ++hh) {
+            if (hh != h) continue;
+            const int q = hh * CQH + qq;
+            float4 acc = make_float4(C::dwb(4 * q), C::dwb(4 * q + 1), C::dwb(4 * q + 2), C::dwb(4 * q + 3));
 #pragma unroll
-            for (int kx = 0; kx < KW; ++kx) {
-              const float4 x = *reinterpret_cast<const float4*>(band + (ky * WB + kx) * CP + 4 * q);
-              const int wi = (ky * KW + kx) * CI + 4 * q;
-              if (C::DW_FMA) {       // one rounding per tap (within the FP32 gate)
-                acc.x = fmaf(x.x, C::dww(wi + 0), acc.x);
-                acc.y = fmaf(x.y, C::dww(wi + 1), acc.y);
-                acc.z = fmaf(x.z, C::dww(wi + 2), acc.z);
-                acc.w = fmaf(x.w, C::dww(wi + 3), acc.w);
-              } else {               // the interpreter's mul-then-add: bit-exact
-                acc.x = add(acc.x, mul(x.x, C::dww(wi + 0)));
-                acc.y = add(acc.y, mul(x.y, C::dww(wi + 1)));
-                acc.z = add(acc.z, mul(x.z, C::dww(wi + 2)));
-                acc.w = add(acc.w, mul(x.w, C::dww(wi + 3)));
+            for (int ky = 0; ky < KH; ++ky)
+#pragma unroll
+              for (int kx = 0; kx < KW; ++kx) {
+                const float4 x = *reinterpret_cast<const float4*>(band + (ky * WB + kx) * CP + 4 * q);
+                const int wi = (ky * KW + kx) * CI + 4 * q;
+                if (C::DW_FMA) {       // one rounding per tap (within the FP32 gate)
+                  acc.x = fmaf(x.x, C::dww(wi + 0), acc.x);
+                  acc.y = fmaf(x.y, C::dww(wi + 1), acc.y);
+                  acc.z = fmaf(x.z, C::dww(wi + 2), acc.z);
+                  acc.w = fmaf(x.w, C::dww(wi + 3), acc.w);
+                } else {               // the interpreter's mul-then-add: bit-exact
+                  acc.x = add(acc.x, mul(x.x, C::dww(wi + 0)));
+                  acc.y = add(acc.y, mul(x.y, C::dww(wi + 1)));
+                  acc.z = add(acc.z, mul(x.z, C::dww(wi + 2)));
+                  acc.w = add(acc.w, mul(x.w, C::dww(wi + 3)));
+                }
               }
+            r4.x = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.x, dps, dpo, 4 * q + 0);
+            r4.y = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.y, dps, dpo, 4 * q + 1);
+            r4.z = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.z, dps, dpo, 4 * q + 2);
+            r4.w = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.w, dps, dpo, 4 * q + 3);
+            if (SP == 2) {
+              *reinterpret_cast<float4*>(&sm.o[pix * CP + 4 * q]) = r4;
+            } else {
+              a[4 * q + 0] = r4.x; a[4 * q + 1] = r4.y; a[4 * q + 2] = r4.z; a[4 * q + 3] = r4.w;
             }
-          a[4 * q + 0] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.x, dps, dpo, 4 * q + 0);
-          a[4 * q + 1] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.y, dps, dpo, 4 * q + 1);
-          a[4 * q + 2] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.z, dps, dpo, 4 * q + 2);
-          a[4 * q + 3] = finish<C::DW_ACT, C::MODE, C::DW_POST>(acc.w, dps, dpo, 4 * q + 3);
+          }
         }
-        float acc[CO];
+      }
+      if (SP == 2) __syncthreads();          // both halves of every pixel's depthwise row stored
+      if (SP == 2) {
+        if (pix < live) {
 #pragma unroll
-        for (int j = 0; j < CO; ++j) acc[j] = C::bias(j);
-        C::dotr(a, acc);
+          for (int q = 0; q < CQ; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(&sm.o[pix * CP + 4 * q]);
+            a[4 * q + 0] = v.x; a[4 * q + 1] = v.y; a[4 * q + 2] = v.z; a[4 * q + 3] = v.w;
+          }
+        }
+        __syncthreads();                     // the exchange rows are read: outputs may land
+      }
+      if (pix < live) {
+        float acc[COH];
+        bool upper = false;
+        if constexpr (SP == 2) {
+          if (h == 1) {          // the upper half of the output channels
+            upper = true;
 #pragma unroll
-        for (int j = 0; j < CO; ++j) acc[j] = finish<C::ACT, C::MODE, C::POST>(acc[j], ps, po, j);
+            for (int j = 0; j < COH; ++j) acc[j] = C::bias(COH + j);
+            C::dotr1(a, acc);
+          }
+        }
+        if (!upper) {
+#pragma unroll
+          for (int j = 0; j < COH; ++j) acc[j] = C::bias(j);
+          C::dotr(a, acc);
+        }
+        const int j0 = h * COH;
+#pragma unroll
+        for (int j = 0; j < COH; ++j) acc[j] = finish<C::ACT, C::MODE, C::POST>(acc[j], ps, po, j0 + j);
         if (C::RES) {
-          const float* res = at<float>(arena, C::RES_OFF) + (p0 + t) * CO;
+          const float* res = at<float>(arena, C::RES_OFF) + (p0 + pix) * CO + j0;
 #pragma unroll
-          for (int j = 0; j < CO; ++j) acc[j] = add(acc[j], __ldg(res + j));
+          for (int j = 0; j < COH; ++j) acc[j] = add(acc[j], __ldg(res + j));
         }
-        if (CO % 4 == 0) {
+        if (COH % 4 == 0) {
 #pragma unroll
-          for (int j = 0; j < CO; j += 4)
-            *reinterpret_cast<float4*>(&sm.o[t * RS + j]) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+          for (int j = 0; j < COH; j += 4)
+            *reinterpret_cast<float4*>(&sm.o[pix * RS + j0 + j]) =
+                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < CO; ++j) sm.o[t * RS + j] = acc[j];
+          for (int j = 0; j < COH; ++j) sm.o[pix * RS + j0 + j] = acc[j];
         }
       }
       __syncthreads();

@@ -203,7 +203,7 @@ def _narrow_code(wmat, bias, K, CO, KS):
     return "\n".join(out)
 
 
-def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias):
+def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias, sp=1):
     """Members of a SepNarrow config: ``dww(i)`` / ``dwb(c)`` (depthwise
     weights in (ky, kx, c) order and bias, folded to immediates once the
     kernel's loops are unrolled), ``bias(j)`` and ``dotr(a, acc)``: the
@@ -211,10 +211,17 @@ def _sep_code(wmat, bias, K, CO, dw_kernel, dw_bias):
     weight an immediate (k ascending, columns innermost: RowsNarrow's order
     with one K slice)."""
     w = np.asarray(wmat, F32).reshape(K, CO)
-    out = [f"  __device__ static __forceinline__ void dotr(const float (&a)[{K}], float* acc) {{"]
-    for k in range(K):
-        out.extend(f"    acc[{j}] = fmaf(a[{k}], {_flit(w[k, j])}, acc[{j}]);" for j in range(CO))
-    out.append("  }")
+    out = []
+    # sp = 2: ``dotr`` forms the lower half of the output channels and
+    # ``dotr1`` the upper half (two threads per pixel, nnb_sep.cuh SP)
+    coh = CO // sp
+    for half in range(sp):
+        out.append(f"  __device__ static __forceinline__ void dotr{half or ''}"
+                   f"(const float (&a)[{K}], float* acc) {{")
+        for k in range(K):
+            out.extend(f"    acc[{j}] = fmaf(a[{k}], {_flit(w[k, half * coh + j])}, acc[{j}]);"
+                       for j in range(coh))
+        out.append("  }")
     return [ImmTables(dww=dw_kernel, dwb=dw_bias, bias=bias), "\n".join(out)]
 
 
@@ -637,7 +644,7 @@ class Specializer:
         dwf = self._dw_fields(u)
         fields = dict(H=dwf["DW_H"], W=dwf["DW_W"], CI=CI, S=dwf["DW_S"], KH=dwf["DW_KH"],
                       KW=dwf["DW_KW"], PT=dwf["DW_PT"], PL=dwf["DW_PL"], HO=HO, WO=WO, CO=CO,
-                      TH=geo["TH"], NS=geo["NS"], NT=geo["NT"],
+                      TH=geo["TH"], NS=geo["NS"], NT=geo["NT"], SP=geo.get("SP", 1),
                       IN_OFF=self.arena_off(u.input_ids[0]), OUT_OFF=self.arena_off(u.output_id),
                       RES=u.residual_id is not None,
                       RES_OFF=self.arena_off(u.residual_id) if u.residual_id is not None else 0,
@@ -649,9 +656,10 @@ class Specializer:
         kh, kw = d.kernel_hw
         self.emit(pos, f"sep{kh}x{kw}_narrow", "nnb::SepNarrow", fields, geo["NT"], geo["smem"],
                   tpi, 1, dynamic_smem=True, grid_cap=self.sm_count * per_sm,
-                  code=_sep_code(wmat, u.bias, CI, CO, d.kernel, d.bias),
+                  code=_sep_code(wmat, u.bias, CI, CO, d.kernel, d.bias, geo.get("SP", 1)),
                   note=f"dw{kh}x{kw}/s{d.stride} C={CI} + pw N={CO}: {geo['TH']}x{WO}-pixel tiles, "
-                       f"{geo['NS']}-stage cp.async ring, zero halo, weights as immediates")
+                       f"{geo['NS']}-stage cp.async ring, zero halo, weights as immediates"
+                       f"{', two threads per pixel' if geo.get('SP', 1) == 2 else ''}")
 
     def _dw_fields(self, u):
         """Fields of a fused depthwise producer (GemmSimt DW loader, tcgen05

@@ -518,6 +518,8 @@ def fuse_concat(plan):
 SEP_SMEM_MAX = 232448      # dynamic shared memory per block (227 KB opt-in)
 SEP_CI_MAX = 32            # depthwise channels = pointwise K of the fused kernel
 SEP_CO_MAX = 32            # pointwise outputs (weights as FFMA immediates)
+SEP_SPLIT_MAX_WARPS = 0    # resident warps per SM up to which a pixel is shared by two threads
+                           # (0: never -- measured slower on B200, see sep_narrow_geometry.split)
 
 
 def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
@@ -540,11 +542,34 @@ def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
     cp = c + 4 if ((c + 4) // 4) % 2 else c + 8
     wb = (wo - 1) * s + kw
     rs = (co | 1) if co % 4 else (co + 4 if ((co + 4) // 4) % 2 else co + 8)
-    if force:                                       # (TH, NS) for experiments
-        th, ns = force
+    def split(g):
+        """Two threads per pixel (nnb_sep.cuh SP) when the band leaves the SM
+        at most SEP_SPLIT_MAX_WARPS warps: the same shared memory then feeds
+        twice the warps (cfg3's 32-channel blocks run 2 CTAs x 4 warps per
+        SM).  Measured on B200 (bit-identical outputs): cfg3 @256 dw C=16 +
+        pw 32 27.2 -> 29.2 us, dw C=32 + pw 32 26.3 -> 31.2 us, cfg2 @1024 dw
+        C=16 + pw 32 63.7 -> 73.9 us -- these kernels are bound by shared-memory
+        wavefronts and issue slots (ncu: short scoreboard / MIO stalls), not by
+        latency, and the exchange row adds to both.  Kept behind
+        ``sep_geo=(TH, NS, 2)``; off by default."""
+        nt, smem = g["NT"], g["smem"]
+        warps = max(1, min(smem_max // (smem + 1024), 2048 // nt)) * nt // 32
+        px = g["TH"] * wo
+        smem2 = smem + 4 * px * max(0, cp - rs)      # the exchange rows share the output staging
+        if (c % 8 == 0 and co % 8 == 0 and warps <= SEP_SPLIT_MAX_WARPS and 2 * nt <= 1024
+                and smem2 + 1024 <= smem_max):
+            return dict(g, NT=2 * nt, smem=smem2, SP=2)
+        return dict(g, SP=1)
+
+    if force:                                       # (TH, NS[, SP]) for experiments
+        th, ns = force[:2]
         ri = (th - 1) * s + kh
         smem = 4 * (ns * ri * wb * cp + th * wo * rs)
-        return dict(TH=th, NS=ns, NT=-(-th * wo // 32) * 32, smem=smem)
+        g = dict(TH=th, NS=ns, NT=-(-th * wo // 32) * 32, smem=smem)
+        if len(force) > 2:
+            return (dict(g, NT=2 * g["NT"], smem=smem + 4 * th * wo * max(0, cp - rs), SP=2) if force[2] == 2
+                    else dict(g, SP=1))
+        return split(g)
     # two ring stages, tiles of 4-8 warps; the band height that issues the
     # fewest warps per image (idle lanes of a tile's last warp, ragged last
     # band), then the smaller tile (more CTAs per SM).  Measured (cfg2 block 1,
@@ -565,7 +590,7 @@ def sep_narrow_geometry(d, u, smem_max=SEP_SMEM_MAX, force=None):
         if best is None or key < best[0]:
             best = (key, dict(TH=th, NS=2, NT=nt, smem=smem))
     if best:
-        return best[1]
+        return split(best[1])
     return None
 
 

@@ -176,6 +176,13 @@ def test_sep_narrow(h, w, c, co, k, s, pad, dwbias, res, n):
         assert [l.kernel.split("_")[2] for l in net.artifact.launches] == [f"sep{k}x{k}"], \
             net.describe()
     np.testing.assert_allclose(got, ref(m, wt, xin), **TOL)
+    if len(net.plan.units) == 1 and c % 8 == 0 and co % 8 == 0:
+        # one and two threads per pixel (nnb_sep.cuh SP) form every output in
+        # the same order: bit-identical
+        geo = sep_narrow_geometry(net.plan.units[0].dw, net.plan.units[0])
+        alt, net1 = gpu(m, wt, xin, sep_geo=(geo["TH"], geo["NS"], 3 - geo["SP"]))
+        assert ("two threads per pixel" in net1.artifact.launches[0].note) == (geo["SP"] == 1)
+        assert np.array_equal(alt, got)
     # (the tiled pointwise GEMM: the split-K row kernel of few-pixel 1x1
     # convs sums in another order)
     unf, net2 = gpu(m, wt, xin, dw_fusion=False, small_conv=False)
