@@ -1810,9 +1810,12 @@ struct GemmTc {
                   for (int o = 0; o < OXC; ++o) {
                     const int j = o * C::E_S + kx;
                     if (ox0 + o >= C::E_WO || ixb + j < 0 || ixb + j >= C::E_W) continue;
-                    if (C::E_FMA) {     // one rounding per tap (within the FP32 gate)
-                      a[o].x = fmaf(x[j].x, w4.x, a[o].x); a[o].y = fmaf(x[j].y, w4.y, a[o].y);
-                      a[o].z = fmaf(x[j].z, w4.z, a[o].z); a[o].w = fmaf(x[j].w, w4.w, a[o].w);
+                    if (C::E_FMA) {     // one rounding per tap (within the FP32 gate), FFMA2
+                      const float2 lo = __ffma2_rn(make_float2(x[j].x, x[j].y), make_float2(w4.x, w4.y),
+                                                   make_float2(a[o].x, a[o].y));
+                      const float2 hi = __ffma2_rn(make_float2(x[j].z, x[j].w), make_float2(w4.z, w4.w),
+                                                   make_float2(a[o].z, a[o].w));
+                      a[o] = make_float4(lo.x, lo.y, hi.x, hi.y);
                     } else {            // the interpreter's mul-then-add
                       a[o].x = add(a[o].x, mul(x[j].x, w4.x)); a[o].y = add(a[o].y, mul(x[j].y, w4.y));
                       a[o].z = add(a[o].z, mul(x[j].z, w4.z)); a[o].w = add(a[o].w, mul(x[j].w, w4.w));

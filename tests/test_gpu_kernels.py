@@ -755,7 +755,7 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
         np.testing.assert_allclose(g, wv, **TOL)
 
 
-@pytest.mark.parametrize("n", [1, 3, 40, 77])
+@pytest.mark.parametrize("n", [1, 3, 40, 77, 330])     # 330: persistent CTAs take a second tile
 @pytest.mark.parametrize("case", [
     # cfg3's 8x8 stage: pw -> dw pairs (stride 1, then stride 2 to 4x4), post-BN after some
     (8, 8, 64, [("p", 128, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 128, "relu6"),
