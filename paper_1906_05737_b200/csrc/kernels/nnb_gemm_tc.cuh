@@ -604,13 +604,26 @@ struct GemmTc {
   // skipped -- pkg/src/nnjit/interpreter.py:65-73), then stores the depthwise
   // output (512 contiguous bytes per warp and pixel).  The pointwise output
   // itself is never written.
+  // Maps larger than a tile but 16 pixels wide or less (cfg3's 16x16 stage)
+  // run as BANDS: a tile is EB_TR = 128 / E_W consecutive image rows starting
+  // at input row tt * EB_OT * E_S - E_PT (a 2-D TMA box at that row of the
+  // [pixels x K] matrix; rows above the image or of the neighbouring image
+  // are loaded but never used as taps), and yields the EB_OT output rows whose
+  // windows it holds -- the 1x1 conv of the overlap rows is recomputed (x1.5
+  // for 3x3 taps on 16x16 maps), which costs less than a launch.
   static constexpr bool EDW = C::EDW != 0;
+  static constexpr int EP = EDW ? C::E_H * C::E_W : 1;            // pixels per image
+  static constexpr bool EBAND = EDW && BM % EP != 0;
+  static constexpr int EB_TR = EDW ? BM / C::E_W : 1;             // image rows per band tile
+  static constexpr int EB_OT = EDW ? (EB_TR - C::E_KH) / C::E_S + 1 : 1;   // output rows per band tile
+  static constexpr int EB_TPI = EDW ? (C::E_HO + EB_OT - 1) / EB_OT : 1;   // band tiles per image
+  static_assert(!EBAND || (BM % C::E_W == 0 && EB_TR >= C::E_KH && !PAIR), "depthwise epilogue: band tiles");
   static constexpr int ETS = C::BN + 4;                           // parked tile row stride (floats)
   static constexpr int EDW_BYTES = EDW ? (BM * ETS * 4 + 1023) / 1024 * 1024 : 0;
   static_assert(!EDW || (!C::CONV && !C::RES && C::UPF == 1 && !C::HEAD && !KP && !K9 && !WIDE && !ET &&
-                         !C::DPOOL && BM % (C::E_H * C::E_W) == 0 && C::BN % 32 == 0 && C::N % 4 == 0 &&
+                         !C::DPOOL && C::BN % 32 == 0 && C::N % 4 == 0 &&
                          C::ROWS == C::E_H * C::E_W && C::E_W <= 16),
-                "depthwise epilogue: row tiles holding whole images");
+                "depthwise epilogue: row tiles holding whole images or bands of one");
   static constexpr int EPI_STAGE = EDW ? EDW_BYTES : EPI_WARPS * NBUF * 2048;   // 32 x 16 fp32 per buffer
   static_assert(!K9 || 2 * (C::KH - 1) * 8 * 16 * (C::CO / 2) * 4 <= EPI_STAGE,
                 "KP9 vertical exchange fits the staging area");
@@ -694,7 +707,7 @@ struct GemmTc {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rows = (long long)n * C::ROWS;
-    const int mtiles = C::CONV ? n * TPI : (int)((rows + BM - 1) / BM);
+    const int mtiles = C::CONV ? n * TPI : EBAND ? n * EB_TPI : (int)((rows + BM - 1) / BM);
     // pairs walk 256-row tile pairs: CTA `rank` of the pair takes 128 of them
     const int rank = PAIR ? (int)cluster_rank() : 0;
     const int tiles = (PAIR ? (mtiles + 1) / 2 : mtiles) * NTN;
@@ -779,7 +792,11 @@ struct GemmTc {
               tma_load_4d(st, second ? tmA1 : tmA, &full[s], (second ? cb - CB0 : cb) * BK,
                           (tt % TX) * OW + kx - C::PL, (tt / TX) * THO + ky - C::PT, img);
             } else {
-              tma_load_2d(st, tmA, &full[s], kb * BK, mb * BM);
+              // (EDW bands: the tile starts at an input row of its image, possibly
+              // above it -- negative coordinates are zero-filled)
+              tma_load_2d(st, tmA, &full[s], kb * BK,
+                          EBAND ? (mb / EB_TPI) * EP + ((mb % EB_TPI) * EB_OT * C::E_S - C::E_PT) * C::E_W
+                                : mb * BM);
               if constexpr (C::APF > 0) {
                 // the A box APF k-blocks ahead into L2: its TMA load then
                 // waits on L2, not HBM, latency (the ring is latency-bound)
@@ -1773,65 +1790,73 @@ struct GemmTc {
             ewq[k] = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::E_W_OFF) + k * C::N + chl));
           const float4 eb4 = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::E_B_OFF) + chl));
           named_sync256(9);                          // the tile is parked
-          constexpr int P = C::E_H * C::E_W, IMGS = BM / P, RT = IMGS * C::E_HO;
+          constexpr int IMGS = EBAND ? 1 : BM / EP;
+          constexpr int RT = EBAND ? EB_OT : IMGS * C::E_HO;   // output rows of the tile
           constexpr int OXC = C::E_WO < 4 ? C::E_WO : 4;       // outputs per register window
+          constexpr int NWIN = (C::E_WO + OXC - 1) / OXC;      // windows per output row
+          constexpr int XW = (OXC - 1) * C::E_S + C::E_KW;     // input columns of a window
+          constexpr int TPR = EPI_THREADS / ECQ;               // (row, window) tasks in flight
           const float* T = reinterpret_cast<const float*>(epi_stage) + 4 * ecq;
           const float* eps = at<float>(pool, C::E_PS_OFF);
           const float* epo = at<float>(pool, C::E_PO_OFF);
-          constexpr int TPR = EPI_THREADS / ECQ;               // row tasks in flight
 #pragma unroll 1
-          for (int rt = et < TPR * ECQ ? et / ECQ : RT; rt < RT; rt += TPR) {
-            const int li = rt / C::E_HO, oy = rt - li * C::E_HO;
-            const long long img = (long long)mb * IMGS + li;
+          for (int rw = et < TPR * ECQ ? et / ECQ : RT * NWIN; rw < RT * NWIN; rw += TPR) {
+            const int rt = rw / NWIN, ox0 = (rw - rt * NWIN) * OXC;
+            int li, oy, trow;          // image of the tile, output row, tile row of input row iy = 0
+            long long img;
+            if (EBAND) {
+              const int tt = mb % EB_TPI;
+              li = 0; oy = tt * EB_OT + rt; img = mb / EB_TPI;
+              trow = -(tt * EB_OT * C::E_S - C::E_PT);
+              if (oy >= C::E_HO) continue;
+            } else {
+              li = rt / C::E_HO; oy = rt - li * C::E_HO; img = (long long)mb * IMGS + li;
+              trow = li * C::E_H;
+            }
             if (img >= n || ch >= C::N) continue;
-            float* d = at<float>(arena, C::E_OUT_OFF + img * C::E_OUT_IMG) +
-                       (long long)oy * C::E_WO * C::N + ch;
+            const int ixb = ox0 * C::E_S - C::E_PL;              // first input column of the window
+            float4 a[OXC];
 #pragma unroll
-            for (int ox0 = 0; ox0 < C::E_WO; ox0 += OXC) {
-              constexpr int XW = (OXC - 1) * C::E_S + C::E_KW;   // input columns of the window
-              const int ixb = ox0 * C::E_S - C::E_PL;            // its first column (compile-time)
-              float4 a[OXC];
+            for (int o = 0; o < OXC; ++o) a[o] = eb4;
 #pragma unroll
-              for (int o = 0; o < OXC; ++o) a[o] = eb4;
+            for (int ky = 0; ky < C::E_KH; ++ky) {
+              const int iy = oy * C::E_S - C::E_PT + ky;
+              if (iy < 0 || iy >= C::E_H) continue;              // taps outside the image are skipped
+              const float* row = T + ((trow + iy) * C::E_W + ixb) * ETS;
+              float4 x[XW];
 #pragma unroll
-              for (int ky = 0; ky < C::E_KH; ++ky) {
-                const int iy = oy * C::E_S - C::E_PT + ky;
-                if (iy < 0 || iy >= C::E_H) continue;
-                const float* row = T + (li * P + iy * C::E_W) * ETS;
-                float4 x[XW];
+              for (int j = 0; j < XW; ++j)                        // ... or read as zeros
+                x[j] = (ixb + j >= 0 && ixb + j < C::E_W) ? *reinterpret_cast<const float4*>(row + j * ETS)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int j = 0; j < XW; ++j)
-                  if (ixb + j >= 0 && ixb + j < C::E_W)
-                    x[j] = *reinterpret_cast<const float4*>(row + (ixb + j) * ETS);
+              for (int kx = 0; kx < C::E_KW; ++kx) {
+                const float4 w4 = ewq[ky * C::E_KW + kx];
 #pragma unroll
-                for (int kx = 0; kx < C::E_KW; ++kx) {
-                  const float4 w4 = ewq[ky * C::E_KW + kx];
-#pragma unroll
-                  for (int o = 0; o < OXC; ++o) {
-                    const int j = o * C::E_S + kx;
-                    if (ox0 + o >= C::E_WO || ixb + j < 0 || ixb + j >= C::E_W) continue;
-                    if (C::E_FMA) {     // one rounding per tap (within the FP32 gate), FFMA2
-                      const float2 lo = __ffma2_rn(make_float2(x[j].x, x[j].y), make_float2(w4.x, w4.y),
-                                                   make_float2(a[o].x, a[o].y));
-                      const float2 hi = __ffma2_rn(make_float2(x[j].z, x[j].w), make_float2(w4.z, w4.w),
-                                                   make_float2(a[o].z, a[o].w));
-                      a[o] = make_float4(lo.x, lo.y, hi.x, hi.y);
-                    } else {            // the interpreter's mul-then-add
-                      a[o].x = add(a[o].x, mul(x[j].x, w4.x)); a[o].y = add(a[o].y, mul(x[j].y, w4.y));
-                      a[o].z = add(a[o].z, mul(x[j].z, w4.z)); a[o].w = add(a[o].w, mul(x[j].w, w4.w));
-                    }
+                for (int o = 0; o < OXC; ++o) {
+                  const int j = o * C::E_S + kx;
+                  if (C::E_FMA) {     // one rounding per tap (within the FP32 gate), FFMA2
+                    const float2 lo = __ffma2_rn(make_float2(x[j].x, x[j].y), make_float2(w4.x, w4.y),
+                                                 make_float2(a[o].x, a[o].y));
+                    const float2 hi = __ffma2_rn(make_float2(x[j].z, x[j].w), make_float2(w4.z, w4.w),
+                                                 make_float2(a[o].z, a[o].w));
+                    a[o] = make_float4(lo.x, lo.y, hi.x, hi.y);
+                  } else {            // the interpreter's mul-then-add
+                    a[o].x = add(a[o].x, mul(x[j].x, w4.x)); a[o].y = add(a[o].y, mul(x[j].y, w4.y));
+                    a[o].z = add(a[o].z, mul(x[j].z, w4.z)); a[o].w = add(a[o].w, mul(x[j].w, w4.w));
                   }
                 }
               }
-#pragma unroll
-              for (int o = 0; o < OXC; ++o)
-                if (ox0 + o < C::E_WO)
-                  *reinterpret_cast<float4*>(d + (ox0 + o) * C::N) = make_float4(
-                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].x, eps, epo, ch),
-                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].y, eps, epo, ch + 1),
-                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].z, eps, epo, ch + 2),
-                      finish<C::E_ACT, EMODE, C::E_POST>(a[o].w, eps, epo, ch + 3));
             }
+            float* d = at<float>(arena, C::E_OUT_OFF + img * C::E_OUT_IMG) +
+                       ((long long)oy * C::E_WO + ox0) * C::N + ch;
+#pragma unroll
+            for (int o = 0; o < OXC; ++o)
+              if (ox0 + o < C::E_WO)
+                *reinterpret_cast<float4*>(d + o * C::N) = make_float4(
+                    finish<C::E_ACT, EMODE, C::E_POST>(a[o].x, eps, epo, ch),
+                    finish<C::E_ACT, EMODE, C::E_POST>(a[o].y, eps, epo, ch + 1),
+                    finish<C::E_ACT, EMODE, C::E_POST>(a[o].z, eps, epo, ch + 2),
+                    finish<C::E_ACT, EMODE, C::E_POST>(a[o].w, eps, epo, ch + 3));
           }
           if (t + tstep < tiles) named_sync256(9);   // the next tile parks over this one
         }

@@ -737,8 +737,15 @@ class Specializer:
         # N = 256 tiles for wide row GEMMs whose K fits one accumulator chunk:
         # a kind::tf32 MMA costs ~1.4x at N = 256 what it costs at N = 128
         res_ = u.residual_id is not None
+        eband = 0
         if edw is not None:
             head = None
+            eh_, ew__, _ = u.output_shape.dims
+            if 128 % (eh_ * ew__):
+                # band tiles (nnb_gemm_tc.cuh EBAND): 128 / W image rows per tile
+                etr = 128 // ew__
+                eot = (etr - edw.kernel_hw[0]) // edw.stride + 1
+                eband = -(-edw.output_shape.h // eot)          # tiles per image
         wide = bool(self.wide and not conv and edw is None and CO >= 256 and K <= 1024 and not res_
                     and self.pair and not self.aldg and CO % 4 == 0
                     and (not rows_geo or rows_geo.get("UPF", 1) == 1))
@@ -822,7 +829,7 @@ class Specializer:
         # Narrow-N convs are bound by tcgen05 instruction dispatch, not MMA
         # math (ncu: TC pipe 66% busy, tensor math 23% at N=48): a pair issues
         # one M=256 instruction where two CTAs issued two.
-        pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0
+        pair = bool(self.pair and not aldg and BN % 16 == 0 and (BN // 2) % 8 == 0 and not eband
                     and ((not conv and tmem_a and BN == 128 and K >= 256)
                          or conv or wide))
         # row-shared vertical taps (KPACK conv tiles, A in shared memory): one
@@ -1028,6 +1035,8 @@ class Specializer:
             tag = f"conv{u.kernel_hw[0]}x{u.kernel_hw[1]}_tc"
         else:
             ipi, ipb = rows, 256 if pair else 128
+            if eband:
+                ipi, ipb = eband, 1
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
             if edw is not None:
                 tag = f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc"
@@ -1050,6 +1059,7 @@ class Specializer:
                        f"{' bf16 corr' if cb16 else ''}"
                        f"{' + pooled second store' if dp is not None else ''}"
                        f"{' + depthwise conv in the epilogue' if edw is not None else ''}"
+                       f"{f' ({eband} bands of {128 // u.output_shape.w} rows per image)' if eband else ''}"
                        f"{f' + fused Dense head N={hn}' if hn else ''}")
 
     def _conv_direct(self, pos, u, wmat, H, W, CI, HO, WO, CO, KH, KW, S, PT, PL, pool_fused,

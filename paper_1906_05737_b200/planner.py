@@ -623,22 +623,35 @@ PW_DW_TILE_ROWS = 128      # rows of a tcgen05 row tile (nnb_gemm_tc.cuh BM)
 PW_DW_MIN_CO = 32
 
 
-def pw_dw_ok(u, d):
+def pw_dw_ok(u, d, bands=False):
     """Geometry of a pointwise conv ``u`` whose consumer ``d`` (depthwise) the
     tcgen05 epilogue can compute: a 128-row tile holds whole images (8x8 and
     4x4 maps: 2 and 8 images), so every tap of the depthwise window lies in
     the tile the CTA has just finished."""
     h, w, c = u.output_shape.dims
     kh, kw = d.kernel_hw
-    return (PW_DW_TILE_ROWS % (h * w) == 0 and w <= 16 and c % 4 == 0 and c >= PW_DW_MIN_CO
+    whole = PW_DW_TILE_ROWS % (h * w) == 0
+    # larger maps of <= 16 columns as bands of 128 / w image rows: the overlap
+    # rows of neighbouring bands are recomputed by the 1x1 conv (cfg3's 16x16
+    # stage: 3 bands of 8 rows per image for 3x3 taps, stride 1 or 2)
+    # Measured on B200 (cfg3 @256): the two band kernels take 19.6 + 17.2 us
+    # against 11.4 + 11.3 and 13.8 + 7.2 us for the separate launches, but the
+    # replay goes 0.2377 -> 0.2452 ms: a CTA walks ~5 band tiles and its eight
+    # epilogue warps run drain, park, taps and stores of each one after the
+    # other, while the separate depthwise launch overlaps its neighbours
+    # (PDL).  Opt-in (``pw_dw="bands"``).
+    band = (bands and not whole and PW_DW_TILE_ROWS % w == 0 and PW_DW_TILE_ROWS // w >= max(8, kh)
+            and h * w > PW_DW_TILE_ROWS)
+    return ((whole or band) and w <= 16 and c % 4 == 0 and c >= PW_DW_MIN_CO
             and kh <= 5 and kw <= 5 and d.stride in (1, 2)
             and u.input_shapes[0].c % 4 == 0)
 
 
-def fuse_pw_dw(plan):
+def fuse_pw_dw(plan, bands=False):
     """A pointwise (1x1, stride 1) Conv2D whose only consumer is a
     DepthwiseConv2D over a map small enough that a 128-row GEMM tile holds
-    whole images (cfg3's 8x8 and 4x4 stages) computes that depthwise conv in
+    whole images (cfg3's 8x8 and 4x4 stages) or a band of 8 or more rows of a
+    map at most 16 pixels wide (its 16x16 stage) computes that depthwise conv in
     its tcgen05 epilogue (nnb_gemm_tc.cuh EDW): the finished tile stays in
     shared memory, the depthwise taps read it there, and only the depthwise
     output is stored -- one launch and one round trip through memory less per
@@ -654,7 +667,7 @@ def fuse_pw_dw(plan):
                 and not u.pool_after and u.upsample_after == 1 and not u.softmax_after
                 and u.residual_id is None and d.residual_id is None and not d.pool_after
                 and d.upsample_after == 1 and not d.softmax_after and d.dw_after is None
-                and u.output_shape.rank == 3 and pw_dw_ok(u, d)
+                and u.output_shape.rank == 3 and pw_dw_ok(u, d, bands)
                 and _private(plan, u.output_id)):
             u.dw_after = d
             _delete(plan, pos + 1, u)
@@ -905,7 +918,7 @@ def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False, pw_
     if chain:
         fuse_chain(plan)
     if pw_dw and not chain and not tc_chain:
-        fuse_pw_dw(plan)
+        fuse_pw_dw(plan, bands=pw_dw == "bands")
     return plan
 
 

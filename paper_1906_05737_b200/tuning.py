@@ -21,8 +21,9 @@ class Tuning:
     gpu_fusion: bool = True        # B200 epilogue fusions (pool, residual, softmax, upsample, concat)
     dw_fusion: object = "narrow"   # depthwise->pointwise: "narrow" (SepNarrow), True (all), False
     head: bool = True              # fuse a <=16-wide Dense head into a tcgen05 Dense epilogue
-    pw_dw: bool = True             # pointwise conv + the depthwise conv consuming it, computed in the
-                                   # tcgen05 epilogue where a 128-row tile holds whole images (fuse_pw_dw)
+    pw_dw: object = True           # pointwise conv + the depthwise conv consuming it, computed in the
+                                   # tcgen05 epilogue where a 128-row tile holds whole images (fuse_pw_dw);
+                                   # "bands": also maps <= 16 pixels wide as bands of rows (measured slower)
     tc_chain: bool = False         # 8x8-stage pointwise/depthwise runs as one tcgen05 kernel
                                    # (planner.fuse_tc_chain; correct, break-even, opt-in)
     chain: bool = False            # small depthwise/pointwise runs as one FFMA kernel (fuse_chain;

@@ -768,7 +768,16 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
     # 2x2 maps (32 images per tile) and a 16x8 map (one image per tile)
     (16, 8, 16, [("p", 64, "relu"), ("d", 3, 2, "same", "relu6"), ("p", 64, "relu6"),
                  ("d", 3, 2, "valid", "linear"), ("p", 32, "relu"), ("d", 3, 2, "same", "tanh")],
-     False, True)])
+     False, True),
+    # band tiles: cfg3's 16x16 stage (3 bands of 8 rows per image; stride 1, then 2 to 8x8)
+    (16, 16, 32, [("p", 64, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 64, "relu6"),
+                  ("d", 3, 2, "same", "relu6"), ("p", 128, "relu6"), ("d", 3, 1, "same", "linear"),
+                  ("p", 32, "linear")], False, True),
+    # bands of 16 rows of a 32x8 map (5x5 taps), then 8 rows of a 24x16 map with 'valid' windows
+    (32, 8, 16, [("p", 32, "tanh"), ("d", 5, 1, "same", "relu"), ("p", 64, "sigmoid"),
+                 ("d", 3, 2, "valid", "linear"), ("p", 32, "relu")], False, False),
+    (24, 16, 32, [("p", 96, "relu"), ("d", 3, 1, "valid", "relu6"), ("p", 40, "elu"),
+                  ("d", 3, 2, "same", "tanh")], False, True)])
 @pytest.mark.parametrize("opts", [EXACT, ApproximationOptions()], ids=["exact", "default"])
 def test_pointwise_with_depthwise_epilogue(case, n, opts):
     """planner.fuse_pw_dw + nnb_gemm_tc.cuh EDW: a 1x1 conv whose consumer is a
@@ -781,12 +790,16 @@ def test_pointwise_with_depthwise_epilogue(case, n, opts):
     m, wt = _chain_net(rng, h, w, c, spec, gap, post_bn)
     x = rng.uniform(-1, 2, (n, h, w, c)).astype(F32)
     want = ref(m, wt, x, "exact" if opts == EXACT else opts)
-    for tune in (dict(tc_min_rows=1, tc_min_images=1, small_conv=False), {}):
+    bands = 128 % (h * w) != 0            # maps larger than a tile: the opt-in band tiles
+    for forced in (True, False):
+        tune = dict(tc_min_rows=1, tc_min_images=1, small_conv=False) if forced else {}
+        if bands:
+            tune = dict(tune, pw_dw="bands")
         got, net = gpu(m, wt, x, opts, **tune)
         fused = [u for u in net.plan.units if u.dw_after is not None]
         assert fused, net.plan.describe()
         act = [l for l in net.artifact.launches if l.n_min <= n <= l.n_max]
-        if tune:
+        if forced:
             assert any("depthwise conv in the epilogue" in l.note for l in act), [l.kernel for l in act]
         for u in fused:      # one fused launch, or the pointwise kernel + a depthwise launch
             mine = [l for l in act if net.plan.units[l.unit] is u]
