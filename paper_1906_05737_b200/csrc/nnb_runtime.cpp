@@ -70,7 +70,7 @@ struct Cu {
   CU_FN(cuGraphExecDestroy) CU_FN(cuEventCreate) CU_FN(cuEventRecord)
   CU_FN(cuEventSynchronize) CU_FN(cuEventElapsedTime) CU_FN(cuEventDestroy)
   CU_FN(cuGetErrorString) CU_FN(cuTensorMapEncodeTiled) CU_FN(cuLaunchKernelEx)
-  CU_FN(cuMemsetD32Async) CU_FN(cuCtxGetCurrent)
+  CU_FN(cuMemsetD32Async) CU_FN(cuCtxGetCurrent) CU_FN(cuStreamWaitEvent)
 #undef CU_FN
   void load() {
     const char *names[] = {"libcuda.so.1", "libcuda.so"};
@@ -94,6 +94,7 @@ struct Cu {
     CU_LOAD(cuEventRecord) CU_LOAD(cuEventSynchronize) CU_LOAD(cuEventElapsedTime)
     CU_LOAD(cuEventDestroy) CU_LOAD(cuGetErrorString) CU_LOAD(cuTensorMapEncodeTiled)
     CU_LOAD(cuLaunchKernelEx) CU_LOAD(cuMemsetD32Async) CU_LOAD(cuCtxGetCurrent)
+    CU_LOAD(cuStreamWaitEvent)
 #undef CU_LOAD
     CUresult r = p_cuInit(0);
     if (r != CUDA_SUCCESS) {
@@ -334,6 +335,18 @@ struct nnb_net {
   double compile_ms = 0;
   bool cache_hit = false;
   CUevent ev0 = nullptr, ev1 = nullptr;
+  // Weight prefetch (small batches): a replay over n <= prefetch_max_n images
+  // is a chain of short launches, each of which starts by pulling its weights
+  // from HBM when they are not in L2 (a cold start, or other work on the GPU
+  // since the last replay).  Such graphs get a second branch next to the
+  // chain: one small kernel that issues prefetch.global.L2 over the whole
+  // constant pool, so later layers find their weights in L2 while the first
+  // layers run.  NNB_PREFETCH_MAX_N (default 16, 0 = off).
+  int prefetch_max_n = 16;
+  CUstream side_stream = nullptr;
+  CUevent fork_ev = nullptr, join_ev = nullptr;
+  CUmodule pf_mod = nullptr;
+  CUfunction pf_fn = nullptr;
 };
 
 namespace {
@@ -477,6 +490,49 @@ nnb_status enqueue(nnb_net *net, int n, CUstream s) {
   return NNB_OK;
 }
 
+const char *kPrefetchSrc = R"(
+extern "C" __global__ void __launch_bounds__(256) nnb_l2_prefetch(const char* p, unsigned long long bytes) {
+  const unsigned long long step = (unsigned long long)gridDim.x * blockDim.x * 128ull;
+  for (unsigned long long off = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * 128ull;
+       off < bytes; off += step)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+}
+)";
+
+// The prefetch branch of a small-batch graph (see nnb_net): forked from the
+// capture stream before the first launch.  Failures only disable it.
+bool prefetch_branch(nnb_net *net, int n) {
+  Cu *C = cu();
+  if (n > net->prefetch_max_n || net->pool_bytes < 4096 || !C->p_cuStreamWaitEvent) return false;
+  if (!net->pf_fn) {
+    std::string cubin;
+    double cms = 0;
+    bool hit = false;
+    if (compile_cubin(kPrefetchSrc, ".", net->cache_dir.empty() ? nullptr : net->cache_dir.c_str(), "",
+                      &cubin, &cms, &hit) != NNB_OK ||
+        C->p_cuModuleLoadData(&net->pf_mod, cubin.data()) != CUDA_SUCCESS ||
+        C->p_cuModuleGetFunction(&net->pf_fn, net->pf_mod, "nnb_l2_prefetch") != CUDA_SUCCESS ||
+        C->p_cuStreamCreate(&net->side_stream, CU_STREAM_NON_BLOCKING) != CUDA_SUCCESS ||
+        C->p_cuEventCreate(&net->fork_ev, CU_EVENT_DISABLE_TIMING) != CUDA_SUCCESS ||
+        C->p_cuEventCreate(&net->join_ev, CU_EVENT_DISABLE_TIMING) != CUDA_SUCCESS) {
+      net->pf_fn = nullptr;
+      net->prefetch_max_n = 0;
+      return false;
+    }
+  }
+  if (C->p_cuEventRecord(net->fork_ev, net->capture_stream) != CUDA_SUCCESS ||
+      C->p_cuStreamWaitEvent(net->side_stream, net->fork_ev, 0) != CUDA_SUCCESS)
+    return false;
+  CUdeviceptr pool = net->pool;
+  unsigned long long bytes = net->pool_bytes;
+  void *args[] = {&pool, &bytes};
+  const unsigned blocks = (unsigned)std::min<uint64_t>(32, (bytes / 128 + 255) / 256);
+  C->p_cuLaunchKernel(net->pf_fn, blocks ? blocks : 1, 1, 1, 256, 1, 1, 0, net->side_stream, args, nullptr);
+  // (the side stream is now part of the capture: it must be joined before
+  // the capture ends)
+  return C->p_cuEventRecord(net->join_ev, net->side_stream) == CUDA_SUCCESS;
+}
+
 nnb_status graph_for(nnb_net *net, int n, CUgraphExec *out) {
   auto it = net->graphs.find(n);
   if (it != net->graphs.end()) { *out = it->second; return NNB_OK; }
@@ -484,7 +540,9 @@ nnb_status graph_for(nnb_net *net, int n, CUgraphExec *out) {
   nnb_status lst = ensure_loaded(net, n);
   if (lst != NNB_OK) return lst;
   CU_CHECK(C->p_cuStreamBeginCapture(net->capture_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+  const bool forked = prefetch_branch(net, n);
   nnb_status st = enqueue(net, n, net->capture_stream);
+  if (forked) C->p_cuStreamWaitEvent(net->capture_stream, net->join_ev, 0);
   CUgraph g = nullptr;
   CUresult r = C->p_cuStreamEndCapture(net->capture_stream, &g);
   if (st != NNB_OK) { if (g) C->p_cuGraphDestroy(g); return st; }
@@ -653,6 +711,7 @@ nnb_status nnb_create(const nnb_net_desc *d, nnb_net **out) {
   net->device = d->device;
   net->max_batch = d->max_batch;
   if (const char *e = getenv("NNB_PDL")) net->pdl = atoi(e) != 0;
+  if (const char *e = getenv("NNB_PREFETCH_MAX_N")) net->prefetch_max_n = atoi(e);
   CUdevice dev;
   nnb_status st = device_ctx(d->device, &net->ctx, &dev);
   if (st != NNB_OK) { delete net; return st; }
@@ -956,6 +1015,10 @@ void nnb_destroy(nnb_net *net) {
     if (net->ev0) C->p_cuEventDestroy(net->ev0);
     if (net->ev1) C->p_cuEventDestroy(net->ev1);
     if (net->capture_stream) C->p_cuStreamDestroy(net->capture_stream);
+    if (net->side_stream) C->p_cuStreamDestroy(net->side_stream);
+    if (net->fork_ev) C->p_cuEventDestroy(net->fork_ev);
+    if (net->join_ev) C->p_cuEventDestroy(net->join_ev);
+    if (net->pf_mod) C->p_cuModuleUnload(net->pf_mod);
     if (net->arena) C->p_cuMemFree(net->arena);
     if (net->pool) C->p_cuMemFree(net->pool);
     for (CUmodule m : net->mods)

@@ -917,3 +917,24 @@ def test_row_shared_kpack_conv(h, w, ci, co, k, pad, n):
     per_row, net1 = gpu(m, wt, xin, tc_min_rows=1, tc_tile_use=0, direct_imm=False, rowshare=False)
     assert not any("rows shared" in l.note for l in net1.artifact.launches)
     np.testing.assert_allclose(per_row, want, **TOL)
+
+
+def test_weight_prefetch_branch(monkeypatch):
+    """nnb_runtime.cpp prefetch_branch: graphs of small batches carry a second
+    branch that prefetches the constant pool into L2 (NNB_PREFETCH_MAX_N, default
+    16).  It changes no result, and larger batches keep the single chain."""
+    m, w = zoo.build(2)
+    for n in (1, 16, 17):
+        x = zoo.inputs(2, n)
+        outs = []
+        for env in ("0", None):
+            if env is None:
+                monkeypatch.delenv("NNB_PREFETCH_MAX_N", raising=False)
+            else:
+                monkeypatch.setenv("NNB_PREFETCH_MAX_N", env)
+            got, net = gpu(m, w, x, ApproximationOptions())
+            got2 = net.run([x])[0].cpu().numpy()          # the cached graph replays
+            assert np.array_equal(got, got2)
+            outs.append(got)
+        assert np.array_equal(outs[0], outs[1])
+        np.testing.assert_allclose(outs[1], ref(m, w, x, ApproximationOptions()), **TOL)
