@@ -204,16 +204,17 @@ def test_random_networks_fusion_soundness():
         np.testing.assert_allclose(got, want, rtol=2e-4, atol=2e-5, err_msg=f"trial {trial}")
 
 
+@pytest.mark.parametrize("mega", [True, False])
 @pytest.mark.parametrize("cfg", range(5))
 @pytest.mark.parametrize("batch", [1, 3, 64, 300])
-def test_specialised_launches_cover_every_unit_once_per_batch(cfg, batch):
+def test_specialised_launches_cover_every_unit_once_per_batch(cfg, batch, mega):
     """For every n in [1, batch] each plan unit is covered by exactly one
     launch (n-range variants must tile the batch axis without overlap)."""
     from paper_1906_05737_b200 import plan_buffers
     from paper_1906_05737_b200.kernels import specialize
     from paper_1906_05737_b200.options import EXACT
     plan = build_plan(build_graph(*zoo.build(cfg)))
-    spec = specialize(plan, plan_buffers(plan), EXACT, batch, -(-batch // 16) * 16, mega=True)
+    spec = specialize(plan, plan_buffers(plan), EXACT, batch, -(-batch // 16) * 16, mega=mega)
     for n in sorted({1, min(2, batch), batch // 2 or 1, batch}):
         act = [l for l in spec.launches if l.n_min <= n <= l.n_max]
         if any(l.cooperative for l in act):        # the batch-1 persistent kernel runs alone
