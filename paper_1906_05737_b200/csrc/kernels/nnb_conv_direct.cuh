@@ -126,10 +126,50 @@ struct ConvDirect {
           for (int ci = 0; ci < C::CI; ++ci) pt[r][c][ci] = ok ? lda(src + ci) : 0.f;
         }
     }
+    // RUN: the KW * CI floats a kernel row reads for one pixel are one
+    // contiguous run of the input; with CI % 4 != 0 (the RGB stems) the
+    // per-tap path issued one scalar load with its own bounds arithmetic per
+    // (tap, channel) -- 27 loads for a 3x3x3 window, and the stems are
+    // issue-bound.  Here each kernel row's run is read once per pixel, as
+    // 8-byte loads where the run starts 8-byte aligned (even S*CI, W*CI,
+    // PL*CI: the stride-2 stems), with one row test and one test per column;
+    // the FFMAs keep the (ky, kx, ci) order.
+    constexpr bool RUN = !PATCH && CV == 1 && C::WIMM && C::ROLL_KY == 0 && C::KW * C::CI <= 16 &&
+                         C::KW * C::CI > 1;
+    constexpr bool RUN2 = RUN && (C::S * C::CI) % 2 == 0 && (C::W * C::CI) % 2 == 0 &&
+                          (C::PL * C::CI) % 2 == 0 && C::IN_IMG % 8 == 0 && C::IN_OFF % 8 == 0;
+    constexpr int RL = RUN ? C::KW * C::CI : 1;
     constexpr int TAPS_ROLLED = C::ROLL_KY == 2 ? C::KH * C::KW : C::ROLL_KY == 1 ? C::KH : 1;
     constexpr int KX_UNROLLED = C::ROLL_KY == 2 ? 1 : C::KW;
 #pragma unroll
     for (int ky = 0; ky < C::KH * C::KW / (TAPS_ROLLED * KX_UNROLLED); ++ky) {
+     float rn[NP][RL];
+     if constexpr (RUN) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int iy = oyp[p] * C::S - C::PT + ky;
+        const int ix0 = oxp[p] * C::S - C::PL;
+        const bool rowok = iy >= 0 && iy < C::H;
+        const float* src = inp[p] + ((i64)(rowok ? iy : 0) * C::W + ix0) * C::CI;
+        bool ok[C::KW];
+#pragma unroll
+        for (int c = 0; c < C::KW; ++c) ok[c] = rowok && ix0 + c >= 0 && ix0 + c < C::W;
+#pragma unroll
+        for (int e = 0; e < RL; e += (RUN2 ? 2 : 1)) {
+          if (RUN2 && e + 1 < RL) {
+            const bool o0 = ok[e / C::CI], o1 = ok[(e + 1) / C::CI];
+            float2 v = make_float2(0.f, 0.f);
+            if (o0 && o1) v = lda(reinterpret_cast<const float2*>(src + e));
+            else if (o0) v.x = lda(src + e);
+            else if (o1) v.y = lda(src + e + 1);
+            rn[p][e] = v.x;
+            rn[p][e + 1] = v.y;
+          } else {
+            rn[p][e] = ok[e / C::CI] ? lda(src + e) : 0.f;
+          }
+        }
+      }
+     }
 #pragma unroll 1
      for (int tr = 0; tr < TAPS_ROLLED; ++tr) {
 #pragma unroll
@@ -144,6 +184,10 @@ struct ConvDirect {
             if constexpr (PATCH) {
 #pragma unroll
               for (int c = 0; c < CV; ++c) xv[p][c] = pt[p / PX + ky_][p % PX + kx][c0 + c];
+              continue;
+            }
+            if constexpr (RUN) {
+              xv[p][0] = rn[p][kx * C::CI + c0];
               continue;
             }
             const int iy = oyp[p] * C::S - C::PT + ky_;
