@@ -245,6 +245,67 @@ struct Pool {
 };
 
 // ---------------------------------------------------------------------------
+// GlobalAveragePooling2D + the narrow Dense consuming it (planner.
+// fuse_gap_dense: a classifier / regression head such as cfg2's 128 -> 4),
+// one warp per image: lanes own channel quads and sum them over the pixels in
+// (y, x) order, divide by the count (the Pool kernel's operations, pkg/src/
+// nnjit/interpreter.py:85-95), park the pooled row in shared memory, then
+// lane j forms output j = bias, k ascending (interpreter.py:45-50), applies
+// the activation / post-BN / softmax and stores it.  One launch instead of two
+// that each move a few kilobytes per image.
+template <class C>
+struct GapDense {
+  static constexpr int CQ = C::CH / 4, QPL = (CQ + 31) / 32, WPB = 4;   // quads, quads per lane, warps
+  static_assert(C::CH % 4 == 0 && C::CO <= 32, "pooled row in channel quads, one output per lane");
+  __device__ static void run(const float* __restrict__ pool, float* __restrict__ arena, int n) {
+    __shared__ __align__(16) float row[WPB][C::CH];
+    const int lane_ = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const i64 img = nnb_bid() * WPB + wp;
+    if (img >= n) return;
+    const float4* in = at<float4>(arena, C::IN_OFF + img * C::IN_IMG);
+    float4 s[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) s[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int p = 0; p < C::H * C::W; ++p) {
+#pragma unroll
+      for (int i = 0; i < QPL; ++i) {
+        const int q = lane_ + 32 * i;
+        if (q < CQ) {
+          const float4 v = lda(in + (i64)p * CQ + q);
+          s[i].x = add(s[i].x, v.x); s[i].y = add(s[i].y, v.y);
+          s[i].z = add(s[i].z, v.z); s[i].w = add(s[i].w, v.w);
+        }
+      }
+    }
+    const float cf = (float)(C::H * C::W);
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+      const int q = lane_ + 32 * i;
+      if (q < CQ)
+        *reinterpret_cast<float4*>(&row[wp][4 * q]) =
+            make_float4(dvd(s[i].x, cf), dvd(s[i].y, cf), dvd(s[i].z, cf), dvd(s[i].w, cf));
+    }
+    __syncwarp();
+    const bool live = lane_ < C::CO;
+    const int j = live ? lane_ : 0;
+    const float* w = at<float>(pool, C::W_OFF) + j;
+    float acc = __ldg(at<float>(pool, C::B_OFF) + j);
+#pragma unroll 4
+    for (int k = 0; k < C::CH; k += 4) {
+      const float4 a = *reinterpret_cast<const float4*>(&row[wp][k]);
+      acc = fmaf(a.x, __ldg(w + (i64)k * C::CO), acc);
+      acc = fmaf(a.y, __ldg(w + (i64)(k + 1) * C::CO), acc);
+      acc = fmaf(a.z, __ldg(w + (i64)(k + 2) * C::CO), acc);
+      acc = fmaf(a.w, __ldg(w + (i64)(k + 3) * C::CO), acc);
+    }
+    float v = finish<C::ACT, C::MODE, C::POST>(acc, at<float>(pool, C::PS_OFF), at<float>(pool, C::PO_OFF), j);
+    if (C::SOFTMAX) v = softmax_warp_row<C::SMEXP>(v, live);
+    if (live) at<float>(arena, C::OUT_OFF + img * C::OUT_IMG)[j] = v;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // Elementwise: n-ary Add (left to right), BatchNorm affine (x*s + o, two
 // roundings), activation -- in the order of emitters.py:115-121.
 template <class C>

@@ -1492,6 +1492,19 @@ class Specializer:
                       elems // vec, ELEM_BLOCK)
             first = False
 
+    def gap_dense(self, pos, u):
+        """GlobalAveragePooling2D + narrow Dense, one warp per image (nnb_small.cuh GapDense)."""
+        H, W, CH = u.input_shapes[0].dims
+        CO = u.kernel.shape[1]
+        fields = dict(H=H, W=W, CH=CH, CO=CO, IN_OFF=self.arena_off(u.input_ids[0]),
+                      IN_IMG=self.img_bytes(u.input_ids[0]), OUT_OFF=self.arena_off(u.output_id),
+                      OUT_IMG=self.img_bytes(u.output_id),
+                      W_OFF=self.pool.add(np.asarray(u.kernel, F32)), B_OFF=self.pool.add(u.bias),
+                      SOFTMAX=bool(u.softmax_after), SMEXP=SMEXP_CODE[self.opt.softmax_exp])
+        fields.update(self.epilogue_fields(u, CO))
+        self.emit(pos, "gap_dense", "nnb::GapDense", fields, 128, 0, 32, 128,
+                  note=f"global average pool {H}x{W}x{CH} + Dense N={CO}, one warp per image")
+
     def softmax(self, pos, u):
         shape = u.output_shape
         L = shape.dims[-1]
@@ -1549,7 +1562,9 @@ class Specializer:
             self._tiny()
         for pos, u in enumerate(self.plan.units):
             self._n_cap = self.head_cap.get(pos)
-            if u.kind in ("Dense", "Conv2D"):
+            if u.kind == "Dense" and u.gap is not None:
+                self.gap_dense(pos, u)
+            elif u.kind in ("Dense", "Conv2D"):
                 self._dual_from = self._edw_from = 1 << 30
                 self.gemm(pos, u)
                 if u.dual_pool is not None and self._dual_from > 1:

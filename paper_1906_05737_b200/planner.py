@@ -77,6 +77,8 @@ class CompilationUnit:
     steps: list = None              # Chain: the fused units, in order
     dual_pool: object = None        # a 2x2 max-pool (Pool unit) computed from this conv's
                                     # output in its epilogue while the full output is stored
+    gap: object = None              # Dense: the GlobalAveragePooling2D (a Pool unit) producing its
+                                    # input, computed by the same launch (fuse_gap_dense)
     dw_after: object = None         # the DepthwiseConv2D (a unit) consuming this 1x1 conv's output,
                                     # computed in the conv's tcgen05 epilogue (fuse_pw_dw): the unit
                                     # then writes the depthwise output; its own output_id is only
@@ -107,6 +109,8 @@ class CompilationUnit:
             bits.append(f"+maxpool2->t{self.dual_pool.output_id}"
                         + (f"+upsample{self.dual_pool.upsample_after}"
                            if self.dual_pool.upsample_after > 1 else ""))
+        if self.gap is not None:
+            bits.append("gap-loader")
         if self.dw_after is not None:
             kh, kw = self.dw_after.kernel_hw
             bits.append(f"+dw{kh}x{kw}/s{self.dw_after.stride}->t{self.dw_after.output_id}")
@@ -619,6 +623,34 @@ def fuse_dw_pw(plan, narrow_only=False):
     return plan
 
 
+GAP_DENSE_MAX_CO = 32      # one output per lane (nnb_small.cuh GapDense)
+
+
+def fuse_gap_dense(plan):
+    """GlobalAveragePooling2D feeding only a Dense with <= 32 outputs (cfg2's
+    128 -> 4 head) becomes that Dense's loader: one warp per image pools the
+    map and forms the outputs, one launch instead of two that each move a few
+    kilobytes per image."""
+    pos = 1
+    while pos < len(plan.units):
+        u, p = plan.units[pos], plan.units[pos - 1]
+        if (u.kind == "Dense" and p.kind == "Pool" and p.pool_op == "avg" and u.gap is None
+                and u.input_ids == (p.output_id,) and p.input_shapes[0].rank == 3
+                and tuple(p.kernel_hw) == tuple(p.input_shapes[0].dims[:2])
+                and p.output_shape.elements == p.input_shapes[0].c and p.padding == "valid"
+                and p.upsample_after == 1 and p.residual_id is None and u.residual_id is None
+                and p.input_shapes[0].c % 4 == 0 and u.kernel.shape[1] <= GAP_DENSE_MAX_CO
+                and u.kernel.shape[0] == p.input_shapes[0].c and _private(plan, p.output_id)):
+            u.gap = p
+            u.input_ids = p.input_ids
+            u.input_shapes = p.input_shapes
+            plan.tensors.pop(p.output_id, None)
+            _delete(plan, pos - 1, u)
+            continue
+        pos += 1
+    return plan
+
+
 PW_DW_TILE_ROWS = 128      # rows of a tcgen05 row tile (nnb_gemm_tc.cuh BM)
 PW_DW_MIN_CO = 32
 
@@ -886,7 +918,7 @@ def fuse_tc_chain(plan, min_pw=TC_CHAIN_MIN_PW):
 
 
 def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False,
-               pw_dw=True):
+               pw_dw=True, gap_dense=True):
     """Reference fusions to a fixpoint, then the B200 epilogue fusions.
     ``dw_fusion`` folds depthwise convs into the pointwise conv that consumes
     them.  "narrow" (default): only pairs whose pointwise conv has <= 32
@@ -899,11 +931,12 @@ def build_plan(graph, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain
     depthwise math on its four split warps.  False: no depthwise fusion."""
     plan = build_reference_plan(graph)
     if gpu_fusion:
-        apply_gpu_fusions(plan, dw_fusion, chain, tc_chain, pw_dw)
+        apply_gpu_fusions(plan, dw_fusion, chain, tc_chain, pw_dw, gap_dense)
     return plan
 
 
-def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False, pw_dw=True):
+def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False, pw_dw=True,
+                      gap_dense=True):
     """The B200 epilogue fusions, in place, on a reference-fused plan."""
     fuse_pool(plan)
     fuse_residual(plan)
@@ -919,6 +952,8 @@ def apply_gpu_fusions(plan, dw_fusion="narrow", chain=False, tc_chain=False, pw_
         fuse_chain(plan)
     if pw_dw and not chain and not tc_chain:
         fuse_pw_dw(plan, bands=pw_dw == "bands")
+    if gap_dense and not chain and not tc_chain:
+        fuse_gap_dense(plan)
     return plan
 
 
@@ -930,7 +965,7 @@ REFERENCE_UNIT_FIELDS = ("uid", "kind", "name", "input_ids", "output_id", "input
 
 
 def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=False,
-               pw_dw=True):
+               pw_dw=True, gap_dense=True):
     """A plan made by the REFERENCE's planner (``nnjit.build_plan``,
     pkg/src/nnjit/optimizer.py:328-341: a FusionPlan of CompilationUnits,
     :35-91) as this package's FusionPlan, with the B200 epilogue fusions
@@ -958,7 +993,7 @@ def adopt_plan(plan, gpu_fusion=True, dw_fusion="narrow", chain=False, tc_chain=
     ours = FusionPlan(units, {t: shape(s) for t, s in plan.tensors.items()},
                       tuple(plan.input_ids), tuple(plan.output_ids), dict(plan.node_units))
     if gpu_fusion:
-        apply_gpu_fusions(ours, dw_fusion, chain, tc_chain, pw_dw)
+        apply_gpu_fusions(ours, dw_fusion, chain, tc_chain, pw_dw, gap_dense)
     return ours
 
 

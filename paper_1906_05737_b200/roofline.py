@@ -126,6 +126,8 @@ def unit_work(u, plan=None):
     if k == "Dense":
         kin, units = u.kernel.shape
         f = 2 * kin * units
+        if getattr(u, "gap", None) is not None:      # pooled by the same launch
+            f += u.input_shapes[0].elements
     elif k == "Conv2D":
         kh, kw, ci, co = u.kernel.shape
         conv_out = (u.pre_pool_shape if getattr(u, "pool_after", False) else

@@ -104,7 +104,8 @@ class CompiledNetwork:
             dw_fusion = False      # the persistent kernel walks the unfused templates
         self.plan = build_plan(self.graph, gpu_fusion=tn.gpu_fusion, dw_fusion=dw_fusion,
                                chain=tn.chain and not tn.mega, tc_chain=tn.tc_chain and not tn.mega,
-                               pw_dw=tn.pw_dw and tn.use_tc and not tn.mega and not tn.tiny)
+                               pw_dw=tn.pw_dw if (tn.use_tc and not tn.mega and not tn.tiny) else False,
+                               gap_dense=tn.gap_dense and not tn.mega and not tn.tiny)
         self.assignment = plan_buffers(self.plan, reserve_heads=tn.head)
         cap = _capacity(self.max_batch)
         spec = specialize(self.plan, self.assignment, self.options, self.max_batch, cap,

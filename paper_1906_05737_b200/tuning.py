@@ -24,6 +24,7 @@ class Tuning:
     pw_dw: object = True           # pointwise conv + the depthwise conv consuming it, computed in the
                                    # tcgen05 epilogue where a 128-row tile holds whole images (fuse_pw_dw);
                                    # "bands": also maps <= 16 pixels wide as bands of rows (measured slower)
+    gap_dense: bool = True         # GlobalAveragePooling2D + the <=32-wide Dense consuming it as one launch
     tc_chain: bool = False         # 8x8-stage pointwise/depthwise runs as one tcgen05 kernel
                                    # (planner.fuse_tc_chain; correct, break-even, opt-in)
     chain: bool = False            # small depthwise/pointwise runs as one FFMA kernel (fuse_chain;
@@ -77,7 +78,7 @@ class Tuning:
         filled in where the field is None)."""
         from .kernels import (MEGA_TC_MIN_ROWS, SMALL_DENSE_ROWS, TC_MIN_IMAGES, TC_MIN_K,
                               TC_MIN_ROWS)
-        skip = {"gpu_fusion", "dw_fusion", "chain", "tc_chain", "pw_dw"}
+        skip = {"gpu_fusion", "dw_fusion", "chain", "tc_chain", "pw_dw", "gap_dense"}
         kw = {f.name: getattr(self, f.name) for f in fields(self) if f.name not in skip}
         if kw["tc_min_rows"] is None:
             kw["tc_min_rows"] = MEGA_TC_MIN_ROWS if self.mega else TC_MIN_ROWS

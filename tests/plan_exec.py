@@ -37,6 +37,10 @@ def _run_unit(u, vals):
         x = vals[u.input_ids[0]]
         n = x.shape[0]
         if u.kind == "Dense":
+            g = getattr(u, "gap", None)
+            if g is not None:               # global average pool computed by the same launch
+                x = oracle.pool(x.reshape((n,) + g.input_shapes[0].dims), g.kernel_hw[0], g.kernel_hw[1],
+                                g.stride, g.padding, True)
             y = _post(oracle.dense(x.reshape(n, -1), u.kernel, u.bias, 1), u)
         elif u.kind in ("Conv2D", "DepthwiseConv2D"):
             dw = u.kind == "DepthwiseConv2D"

@@ -938,3 +938,33 @@ def test_weight_prefetch_branch(monkeypatch):
             outs.append(got)
         assert np.array_equal(outs[0], outs[1])
         np.testing.assert_allclose(outs[1], ref(m, w, x, ApproximationOptions()), **TOL)
+
+
+@pytest.mark.parametrize("h,w,c,co,act,softmax,n", [
+    (8, 10, 128, 4, "linear", False, 37), (4, 4, 256, 10, "linear", True, 5), (3, 5, 8, 1, "tanh", False, 1),
+    (7, 7, 40, 32, "relu", False, 130), (1, 1, 16, 3, "sigmoid", True, 9)])
+@pytest.mark.parametrize("opts", [EXACT, ApproximationOptions()], ids=["exact", "default"])
+def test_gap_dense_head(h, w, c, co, act, softmax, n, opts):
+    """planner.fuse_gap_dense + nnb_small.cuh GapDense: GlobalAveragePooling2D
+    and the narrow Dense consuming it as one launch (one warp per image; more
+    than 32 channel quads per lane group, softmax, ragged last block)."""
+    rng = np.random.default_rng(h * w + c + co)
+    b = NetBuilder()
+    x = b.input((h, w, c))
+    y = b.layer("Conv2D", [x], {"filters": c, "kernel_size": 1, "activation": "relu"},
+                [("kernel", he(rng, (1, 1, c, c), c)), ("bias", (rng.standard_normal(c) * 0.1).astype(F32))])
+    g = b.layer("GlobalAveragePooling2D", [y])
+    d = b.layer("Dense", [g], {"units": co, "activation": act},
+                [("kernel", he(rng, (c, co), c)), ("bias", (rng.standard_normal(co) * 0.1).astype(F32))])
+    if softmax:
+        d = b.layer("Softmax", [d])
+    m, wt = b.build([d])
+    xin = rng.uniform(-2, 2, (n, h, w, c)).astype(F32)
+    got, net = gpu(m, wt, xin, opts)
+    assert [u.kind for u in net.plan.units][-1] == "Dense" and net.plan.units[-1].gap is not None, \
+        net.plan.describe()
+    assert [l.kernel.split("_", 2)[2] for l in net.artifact.launches][-1].startswith("gap_dense")
+    np.testing.assert_allclose(got, ref(m, wt, xin, "exact" if opts == EXACT else opts), **TOL)
+    sep, net2 = gpu(m, wt, xin, opts, gap_dense=False)
+    assert "Pool" in [u.kind for u in net2.plan.units]
+    np.testing.assert_allclose(got, sep, rtol=1e-5, atol=2e-6)

@@ -34,7 +34,7 @@ def test_every_specializer_knob_is_a_tuning_field():
         "self", "plan", "assignment", "options", "max_batch", "capacity", "sm_count"}
     kw = Tuning().specializer_kwargs()
     assert set(kw) == spec, set(kw) ^ spec
-    assert set(FIELDS) == spec | {"gpu_fusion", "dw_fusion", "chain", "tc_chain", "pw_dw"}
+    assert set(FIELDS) == spec | {"gpu_fusion", "dw_fusion", "chain", "tc_chain", "pw_dw", "gap_dense"}
     assert kw["tc_min_rows"] == 256 and make_tuning({"mega": True}).specializer_kwargs()[
         "tc_min_rows"] == 2048
 
