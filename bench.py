@@ -550,10 +550,12 @@ def main():
                     rp = build_reference_plan(build_graph(*zoo.build(c)))
                     t_s = roofline.survey_layerwise_roof_s(rp, big, peaks["hbm_gbs"],
                                                            roofline.fp32_peak_tflops())
+                    lr_us, _ = roofline.layer_roofline(netb, rp, big, peaks, ffma[0])
                     e = {"batch": big, "ms": ms_b, "images_per_s": big / (ms_b / 1e3),
                          "batch1_latency_us": ms_1 * 1e3,
                          "launches": len(netb.launches_for(big)),
                          "roof_us": r_us, "roofline_frac": r_us / (ms_b * 1e3),
+                         "layer_roof_us": lr_us, "layer_roofline_frac": lr_us / (ms_b * 1e3),
                          "sum_launch_us": m_us,
                          "launch_rows": [{k: (round(v, 3) if isinstance(v, float) else v)
                                           for k, v in r.items()} for r in rws],

@@ -162,6 +162,53 @@ def unit_work(u, plan=None):
     return f, ins + out, wb
 
 
+def layer_roofline(net, ref_plan, n, peaks, ffma_tflops):
+    """north_star's "per-layer memory or compute roofline" with the per-pipe
+    peaks of ``launch_roofline``: the sum over the LAYERS of the reference-
+    style plan (BatchNorm folded, activations fused, nothing else -- one unit
+    per Dense / conv / depthwise / pool / ... layer, ``planner.build_reference_plan``)
+    of max(compute at the pipe that runs the layer, its own bytes / HBM
+    bandwidth).  Compute pipe of a layer: Dense / Conv2D take the pipe of the
+    launch that covers them in the compiled network at batch ``n`` (tcgen05
+    with its 3 or 2 products per MAC, else FFMA); every other layer --
+    depthwise taps, pooling, elementwise, also when a tcgen05 launch carries
+    them in its epilogue -- is FFMA work.  Unlike ``net_roofline`` (per fused
+    LAUNCH) this bound keeps the activation traffic between layers that the
+    compiled network's fusions remove, so a fused launch can beat its layers'
+    sum.  Returns (µs, rows)."""
+    by_uid = {u.uid: pos for pos, u in enumerate(net.plan.units)}
+    for pos, u in enumerate(net.plan.units):          # units carried inside another one
+        for inner in (getattr(u, "dw", None), getattr(u, "dw_after", None),
+                      getattr(u, "dual_pool", None), getattr(u, "gap", None)):
+            if inner is not None:
+                by_uid.setdefault(inner.uid, pos)
+        for st in getattr(u, "steps", None) or ():
+            by_uid.setdefault(st.uid, pos)
+    node_of = {}
+    for node, uid in ref_plan.node_units.items():
+        if uid is not None:
+            node_of.setdefault(uid, node)
+    active = [net.artifact.launches[i] for i in net.launches_for(n)]
+    total, rows = 0.0, []
+    for ru in ref_plan.units:
+        pipe, mult = "ffma", 1
+        if ru.kind in ("Dense", "Conv2D"):
+            ours = net.plan.node_units.get(node_of.get(ru.uid))
+            pos = by_uid.get(ours)
+            main = [L for L in active if L.unit == pos]
+            if main:
+                pipe, mult = launch_pipe(main[0])
+        f, io, w = unit_work(ru)
+        p = tf32_peak_tflops(peaks) if pipe == "tensor" else ffma_tflops
+        t_c = n * f * mult / (p * 1e12)
+        t_m = (n * io + w) / (peaks["hbm_gbs"] * 1e9)
+        t = max(t_c, t_m)
+        total += t
+        rows.append({"layer": ru.name, "kind": ru.kind, "pipe": pipe, "products_per_mac": mult,
+                     "roof_us": t * 1e6, "bound": "compute" if t_c >= t_m else "hbm"})
+    return total * 1e6, rows
+
+
 def survey_layerwise_roof_s(plan, n, hbm_gbs, peak_tflops):
     t = 0.0
     for u in plan.units:

@@ -27,15 +27,18 @@ def main(bench, ref=None):
           f"{rl['achieved']:.0f} {rl['unit']} = **{rl['frac']:.2f}** of {rl['peak']:.0f}; "
           f"share of step {rl['share_of_step']:.2f}; DRAM traffic {rl['traffic'] / 1e6:.0f} MB vs "
           f"{rl['algorithmic_per_launch']['bytes'] / 1e6:.0f} MB algorithmic.\n")
-    print("| config | batch | ms | images/s | roof µs | roofline frac | launches | batch-1 µs (L2 flushed) "
+    print("| config | batch | ms | images/s | roof µs | roofline frac (per fused launch) | per-layer roof µs "
+          "| frac of the per-layer roofline | launches | batch-1 µs (L2 flushed) "
           "| reference CPU batch-1 µs | speed-up at batch 1 |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for name, v in d["configs"].items():
         rc = (r or {}).get("configs", {}).get(name, {}) if r else {}
         rb1 = rc.get("batch1_latency_us") or (v.get("reference_cpu") or {}).get("batch1_latency_us")
         tail = f"{rb1:.1f} | {rb1 / v['batch1_latency_us']:.2f}" if rb1 else "— | —"
         print(f"| {name} | {v['batch']} | {v['ms']:.4f} | {v['images_per_s'] / 1e6:.3f} M | {v['roof_us']:.1f} "
-              f"| {v['roofline_frac']:.3f} | {v['launches']} | {v['batch1_latency_us']:.1f} | {tail} |")
+              f"| {v['roofline_frac']:.3f} | {v.get('layer_roof_us', float('nan')):.1f} "
+              f"| {v.get('layer_roofline_frac', float('nan')):.3f} | {v['launches']} "
+              f"| {v['batch1_latency_us']:.1f} | {tail} |")
     for name, v in d["configs"].items():
         print(f"\n### {name} @ {v['batch']}: replay {v['ms'] * 1e3:.1f} µs, roof {v['roof_us']:.1f} µs\n")
         print("| launch | pipe | GFLOP | MB | roof µs (bound) | measured µs | frac |")

@@ -51,6 +51,27 @@ def test_every_launch_has_work_and_a_pipe(cfg):
         assert r["frac"] == pytest.approx(r["roof_us"] / 1e3)
 
 
+@pytest.mark.parametrize("cfg", range(5))
+def test_layer_roofline_keeps_the_traffic_fusion_removes(cfg):
+    """roofline.layer_roofline: the per-LAYER bound over the reference-style
+    plan (north_star's wording) with the compiled network's pipes.  It is at
+    least the per-launch bound wherever launches fuse layers (cfg2-cfg4), and
+    every Dense / conv layer a tcgen05 launch covers is on the tensor pipe."""
+    from paper_1906_05737_b200.planner import build_reference_plan
+    B = {0: 4096, 1: 65536, 2: 1024, 3: 256, 4: 64}[cfg]
+    net = fake_net(cfg, B)
+    rp = build_reference_plan(build_graph(*zoo.build(cfg)))
+    us, rows = roofline.layer_roofline(net, rp, B, PEAKS, FFMA)
+    _, launch_us = roofline.net_roofline(net, B, PEAKS, FFMA)
+    assert len(rows) == len(rp.units) and us == pytest.approx(sum(r["roof_us"] for r in rows))
+    assert us >= 0.99 * launch_us, (us, launch_us)
+    if cfg in (2, 3, 4):
+        assert us > 1.05 * launch_us
+    n_tc = sum("_tc_" in net.artifact.launches[i].kernel for i in net.launches_for(B))
+    assert sum(r["pipe"] == "tensor" for r in rows) >= n_tc - (1 if cfg == 1 else 0)   # cfg1: fused head
+    assert all(r["pipe"] == "ffma" for r in rows if r["kind"] not in ("Dense", "Conv2D"))
+
+
 def test_ffma_peak_source_order(tmp_path):
     assert roofline.ffma_peak_tflops(70.0) == (70.0, "nnb_ffma_peak measured in this run")
     tf, src = roofline.ffma_peak_tflops(None)
