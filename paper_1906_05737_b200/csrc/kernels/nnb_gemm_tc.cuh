@@ -617,7 +617,8 @@ struct GemmTc {
   static constexpr int EB_TR = EDW ? BM / C::E_W : 1;             // image rows per band tile
   static constexpr int EB_OT = EDW ? (EB_TR - C::E_KH) / C::E_S + 1 : 1;   // output rows per band tile
   static constexpr int EB_TPI = EDW ? (C::E_HO + EB_OT - 1) / EB_OT : 1;   // band tiles per image
-  static_assert(!EBAND || (BM % C::E_W == 0 && EB_TR >= C::E_KH && !PAIR), "depthwise epilogue: band tiles");
+  static_assert(!EBAND || (BM % C::E_W == 0 && EB_TR >= C::E_KH && !PAIR && !C::E_GAP),
+                "depthwise epilogue: band tiles");
   static constexpr int ETS = C::BN + 4;                           // parked tile row stride (floats)
   static constexpr int EDW_BYTES = EDW ? (BM * ETS * 4 + 1023) / 1024 * 1024 : 0;
   static_assert(!EDW || (!C::CONV && !C::RES && C::UPF == 1 && !C::HEAD && !KP && !K9 && !WIDE && !ET &&
@@ -1791,6 +1792,27 @@ struct GemmTc {
           const float4 eb4 = __ldg(reinterpret_cast<const float4*>(at<float>(pool, C::E_B_OFF) + chl));
           named_sync256(9);                          // the tile is parked
           constexpr int IMGS = EBAND ? 1 : BM / EP;
+          if constexpr (C::E_GAP != 0) {
+            // global average pool: (image of the tile, channel quad) tasks sum the
+            // image's parked rows in pixel order and divide by the count (the Pool
+            // kernel's operations, pkg/src/nnjit/interpreter.py:85-95)
+            constexpr int TPG = EPI_THREADS / ECQ;
+            const float* Tg = reinterpret_cast<const float*>(epi_stage) + 4 * ecq;
+#pragma unroll 1
+            for (int li = et < TPG * ECQ ? et / ECQ : IMGS; li < IMGS; li += TPG) {
+              const long long img = (long long)mb * IMGS + li;
+              if (img >= n || ch >= C::N) continue;
+              float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+              for (int p = 0; p < EP; ++p) {
+                const float4 v = *reinterpret_cast<const float4*>(Tg + (li * EP + p) * ETS);
+                a.x = add(a.x, v.x); a.y = add(a.y, v.y); a.z = add(a.z, v.z); a.w = add(a.w, v.w);
+              }
+              const float cf = (float)EP;
+              *reinterpret_cast<float4*>(at<float>(arena, C::E_OUT_OFF + img * C::E_OUT_IMG) + ch) =
+                  make_float4(dvd(a.x, cf), dvd(a.y, cf), dvd(a.z, cf), dvd(a.w, cf));
+            }
+          } else {
           constexpr int RT = EBAND ? EB_OT : IMGS * C::E_HO;   // output rows of the tile
           constexpr int OXC = C::E_WO < 4 ? C::E_WO : 4;       // outputs per register window
           constexpr int NWIN = (C::E_WO + OXC - 1) / OXC;      // windows per output row
@@ -1857,6 +1879,7 @@ struct GemmTc {
                     finish<C::E_ACT, EMODE, C::E_POST>(a[o].y, eps, epo, ch + 1),
                     finish<C::E_ACT, EMODE, C::E_POST>(a[o].z, eps, epo, ch + 2),
                     finish<C::E_ACT, EMODE, C::E_POST>(a[o].w, eps, epo, ch + 3));
+          }
           }
           if (t + tstep < tiles) named_sync256(9);   // the next tile parks over this one
         }

@@ -741,7 +741,7 @@ class Specializer:
         if edw is not None:
             head = None
             eh_, ew__, _ = u.output_shape.dims
-            if 128 % (eh_ * ew__):
+            if 128 % (eh_ * ew__) and edw.kind != "Pool":
                 # band tiles (nnb_gemm_tc.cuh EBAND): 128 / W image rows per tile
                 etr = 128 // ew__
                 eot = (etr - edw.kernel_hw[0]) // edw.stride + 1
@@ -952,13 +952,22 @@ class Specializer:
         else:
             fields.update(DPOOL=0, DP_OFF=0, DP_IMG=0, DP_UPF=1, DP_PHO=1, DP_PWO=1)
         # the depthwise conv consuming this 1x1 conv, in the epilogue (planner.fuse_pw_dw)
-        if edw is not None:
+        if edw is not None and edw.kind == "Pool":
+            # global average pool of the parked tile (E_GAP)
+            eh, ew_, _ = u.output_shape.dims
+            zo = self.pool.zeros_offset(CO)
+            fields.update(EDW=1, E_GAP=1, E_H=eh, E_W=ew_, E_HO=1, E_WO=1, E_KH=1, E_KW=1, E_S=1, E_PT=0,
+                          E_PL=0, E_W_OFF=zo, E_B_OFF=zo, E_ACT=0, E_POST=0, E_PS_OFF=zo, E_PO_OFF=zo,
+                          E_OUT_OFF=self.arena_off(edw.output_id),
+                          E_OUT_IMG=self.img_bytes(edw.output_id), E_FMA=0)
+            self._edw_from = min(self._edw_from, n_min)
+        elif edw is not None:
             eh, ew_, _ = u.output_shape.dims
             eho, ewo, _ = edw.output_shape.dims
             ekh, ekw = edw.kernel_hw
             same = edw.padding == "same"
             eep = self.epilogue_fields(edw, CO)
-            fields.update(EDW=1, E_H=eh, E_W=ew_, E_HO=eho, E_WO=ewo, E_KH=ekh, E_KW=ekw,
+            fields.update(EDW=1, E_GAP=0, E_H=eh, E_W=ew_, E_HO=eho, E_WO=ewo, E_KH=ekh, E_KW=ekw,
                           E_S=edw.stride,
                           E_PT=same_padding(eh, ekh, edw.stride)[0] if same else 0,
                           E_PL=same_padding(ew_, ekw, edw.stride)[0] if same else 0,
@@ -968,7 +977,7 @@ class Specializer:
                           E_OUT_IMG=self.img_bytes(edw.output_id), E_FMA=int(bool(self.sep_fma)))
             self._edw_from = min(self._edw_from, n_min)
         else:
-            fields.update(EDW=0, E_H=1, E_W=1, E_HO=1, E_WO=1, E_KH=1, E_KW=1, E_S=1, E_PT=0, E_PL=0,
+            fields.update(EDW=0, E_GAP=0, E_H=1, E_W=1, E_HO=1, E_WO=1, E_KH=1, E_KW=1, E_S=1, E_PT=0, E_PL=0,
                           E_W_OFF=0, E_B_OFF=0, E_ACT=0, E_POST=0, E_PS_OFF=0, E_PO_OFF=0,
                           E_OUT_OFF=0, E_OUT_IMG=0, E_FMA=0)
         if conv:
@@ -1039,7 +1048,8 @@ class Specializer:
                 ipi, ipb = eband, 1
             tag = "dense_tc" if u.kind == "Dense" else "conv1x1_tc"
             if edw is not None:
-                tag = f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc"
+                tag = ("conv1x1_gap_tc" if edw.kind == "Pool"
+                       else f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc")
         self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
@@ -1058,7 +1068,7 @@ class Specializer:
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
                        f"{' bf16 corr' if cb16 else ''}"
                        f"{' + pooled second store' if dp is not None else ''}"
-                       f"{' + depthwise conv in the epilogue' if edw is not None else ''}"
+                       f"{' + global average pool in the epilogue' if edw is not None and edw.kind == 'Pool' else ' + depthwise conv in the epilogue' if edw is not None else ''}"
                        f"{f' ({eband} bands of {128 // u.output_shape.w} rows per image)' if eband else ''}"
                        f"{f' + fused Dense head N={hn}' if hn else ''}")
 
@@ -1572,7 +1582,10 @@ class Specializer:
                     self.pool_unit(pos, u.dual_pool, n_max=self._dual_from - 1)
                 if u.dw_after is not None and self._edw_from > 1:
                     # batches whose conv kernel has no depthwise epilogue
-                    self.depthwise(pos, u.dw_after, n_cap=self._edw_from - 1)
+                    if u.dw_after.kind == "Pool":
+                        self.pool_unit(pos, u.dw_after, n_max=self._edw_from - 1)
+                    else:
+                        self.depthwise(pos, u.dw_after, n_cap=self._edw_from - 1)
             elif u.kind == "DepthwiseConv2D":
                 if u.residual_id is not None or u.pool_after or u.softmax_after:
                     raise UnsupportedLayer("depthwise epilogue fusion")

@@ -111,7 +111,9 @@ class CompilationUnit:
                            if self.dual_pool.upsample_after > 1 else ""))
         if self.gap is not None:
             bits.append("gap-loader")
-        if self.dw_after is not None:
+        if self.dw_after is not None and self.dw_after.kind == "Pool":
+            bits.append(f"+gap->t{self.dw_after.output_id}")
+        elif self.dw_after is not None:
             kh, kw = self.dw_after.kernel_hw
             bits.append(f"+dw{kh}x{kw}/s{self.dw_after.stride}->t{self.dw_after.output_id}")
         if self.steps:
@@ -663,6 +665,12 @@ def pw_dw_ok(u, d, bands=False):
     h, w, c = u.output_shape.dims
     kh, kw = d.kernel_hw
     whole = PW_DW_TILE_ROWS % (h * w) == 0
+    if d.kind == "Pool":
+        # GlobalAveragePooling2D of a map the tile holds whole: the same parked
+        # tile, summed over each image's rows (cfg3's 4x4x256 map ahead of the classifier)
+        return (whole and w <= 16 and c % 4 == 0 and c >= PW_DW_MIN_CO and d.pool_op == "avg"
+                and (kh, kw) == (h, w) and d.padding == "valid" and d.output_shape.elements == c
+                and u.input_shapes[0].c % 4 == 0)
     # larger maps of <= 16 columns as bands of 128 / w image rows: the overlap
     # rows of neighbouring bands are recomputed by the 1x1 conv (cfg3's 16x16
     # stage: 3 bands of 8 rows per image for 3x3 taps, stride 1 or 2)
@@ -693,7 +701,7 @@ def fuse_pw_dw(plan, bands=False):
     pos = 0
     while pos + 1 < len(plan.units):
         u, d = plan.units[pos], plan.units[pos + 1]
-        if (u.kind == "Conv2D" and d.kind == "DepthwiseConv2D" and u.kernel_hw == (1, 1)
+        if (u.kind == "Conv2D" and d.kind in ("DepthwiseConv2D", "Pool") and u.kernel_hw == (1, 1)
                 and u.stride == 1 and d.input_ids == (u.output_id,) and u.dw is None
                 and u.dw_after is None and u.dual_pool is None and not u.concat_in
                 and not u.pool_after and u.upsample_after == 1 and not u.softmax_after

@@ -4,7 +4,7 @@
 tag=${1:-r02}
 out=gpurun_out/prof_$tag; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || exit 1
-for spec in "0 4096 conv3x3_direct_1" "1 65536 dense_tc_3" "2 1024 sep3x3_narrow_1" "3 256 sep3x3_narrow_1" "4 64 conv3x3_tc_4"; do
+for spec in "0 4096 conv3x3_direct_1" "1 65536 dense_tc_3" "2 1024 sep3x3_narrow_1" "3 256 sep3x3_narrow_1" "3 256 conv1x1_dw3x3_tc" "4 64 conv3x3_tc_4"; do
   set -- $spec
   name=${tag}_cfg$1_$3
   timeout 300 python scripts/prof_net.py --config $1 --batch $2 --mode default --reps 1 > $out/$name.prof.log 2>&1 || continue
