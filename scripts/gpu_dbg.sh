@@ -1,4 +1,13 @@
 #!/bin/bash
+# NNB_TC_DBG ablation of a config's tcgen05 launches (bit 0 no MMAs, 1 no TMA loads, 2 no A split,
+# 3 no TMEM reads, 4 no output path): where a launch's time goes.
+# usage: gpurun -- bash scripts/gpu_dbg.sh CONFIG BATCH [BITS...]      (default bits: 1 2 4 8 16 7 24 31)
+cfg=${1:-3}; batch=${2:-256}; shift 2
+bits=${*:-1 2 4 8 16 7 24 31}
 out=gpurun_out/dbg; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { tail $out/build.log; exit 1; }
-timeout 600 python scripts/ab_kw.py 3 256 'pw_dw=True M:rational S:fast' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=1' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=2' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=4' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=8' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=15' 'pw_dw=True M:rational S:fast D:NNB_TC_DBG=31' 2>&1 | grep "replay\|u10_\|u11_\|u15_\|u16_\|u07_" | cut -c1-90 > $out/ab.log; cat $out/ab.log
+v='M:rational S:fast'
+args=("use_tc=True $v")
+for b in $bits; do args+=("use_tc=True $v D:NNB_TC_DBG=$b"); done
+timeout 900 python scripts/ab_kw.py $cfg $batch "${args[@]}" 2>&1 | grep "replay\|_tc_" | cut -c1-100 > $out/ab_cfg$cfg.log
+cat $out/ab_cfg$cfg.log
