@@ -141,7 +141,10 @@ nnb_status nnb_compile_parallel(const char *const *sources, int32_t n_sources,
  * max_batch images runs, upload the pool, allocate and zero the arena.  The
  * kernels of other batch sizes are compiled on their first replay (or every
  * kernel up front with NNB_EAGER=1); CUDA graphs are captured lazily per
- * batch size. */
+ * batch size.  Graphs over n <= NNB_PREFETCH_MAX_N images (default 16, 0 =
+ * off) carry a second branch that prefetches the constant pool into L2 while
+ * the first launches run (cold-start latency); NNB_PDL=0 turns programmatic
+ * dependent launch off. */
 nnb_status nnb_create(const nnb_net_desc *desc, nnb_net **out);
 
 /* Device address of arena byte `offset` (for zero-copy tensor views). */
