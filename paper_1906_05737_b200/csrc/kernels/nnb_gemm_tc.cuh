@@ -533,7 +533,16 @@ struct GemmTc {
   static_assert(!PAIR || (!AL && C::BN % 16 == 0 && (C::BN / 2) % 8 == 0), "CTA-pair tile shape");
   // A splitters: 4 for A in TMEM / cp.async / depthwise producers and for
   // the bf16 correction split of narrow tiles (C::CONV_W4), else 2
-  static constexpr int CONV_WARPS = (TA || AL || DWF || C::CONV_W4) ? 4 : 2;
+  // SETREG (N = 256 BF16-correction row tiles): SIX split warps and 512
+  // threads -- the launch gives every thread 128 registers, then the two
+  // producer / split warpgroups hand registers back (setmaxnreg.dec 88) and
+  // the two epilogue warpgroups, which hold 128 running sums per thread, take
+  // them (setmaxnreg.inc 168): 256 x 88 + 256 x 168 = the whole register file.
+  // Without the reallocation 168 registers x 384 threads left room for two
+  // split warps only, and the split sat on every stage's critical path.
+  static constexpr bool SETREG = C::SETREG != 0;
+  static constexpr int CONV_WARPS = SETREG ? 6 : (TA || AL || DWF || C::CONV_W4) ? 4 : 2;
+  static_assert(!SETREG || (CB16 && !TA && !AL && !DWF), "register reallocation: BF16-correction tiles");
   static constexpr int EPI_W0 = 2 + CONV_WARPS;                   // first epilogue warp
   static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;
   static constexpr int EPI_COLS = C::BN >= 32 ? C::BN / 2 : 16;  // columns per epilogue warp
@@ -759,8 +768,14 @@ struct GemmTc {
     else __syncthreads();
     tc_fence_after();
     const u32 tmem = *tmem_slot;
+    // SETREG: warpgroups 0-1 (TMA, MMA, six split warps) release registers, 2-3
+    // (epilogue) take them -- issued inside each role's branch, so that ptxas
+    // allocates every role within its own budget
+#define NNB_SETREG_DEC() do { if constexpr (SETREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); } while (0)
+#define NNB_SETREG_INC() do { if constexpr (SETREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;"); } while (0)
 
     if (warp == 0) {
+      NNB_SETREG_DEC();
       // ---------------- TMA producer ----------------
       if (lane == 0) {
         int s = 0;
@@ -819,6 +834,7 @@ struct GemmTc {
         }
       }
     } else if (warp == 1) {
+      NNB_SETREG_DEC();
       // ---------------- MMA issuer (the leader CTA of a pair) ----------------
       if (PAIR && rank != 0) {
         // the peer's MMA warp only owns the TMEM allocation
@@ -955,6 +971,7 @@ struct GemmTc {
       }
       }
     } else if (warp < EPI_W0) {
+      NNB_SETREG_DEC();
      // (role bodies selected at compile time: only the instantiated form is
      // compiled -- NVRTC time)
      if constexpr (DWF) {
@@ -1238,6 +1255,7 @@ struct GemmTc {
       }
      }
     } else {
+      NNB_SETREG_INC();
       // ---------------- epilogue ----------------
       const int q = warp & 3;                    // TMEM lane quarter of this warp
       const int r = q * 32 + lane;               // row within the tile

@@ -242,13 +242,14 @@ class Specializer:
                  kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, small_conv=True, small_conv_kper=16, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None):
+                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, small_conv=True, small_conv_kper=16, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None, setreg=True):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
         self.conv_w4 = conv_w4
         self.rowshare = rowshare
         self.small_conv = small_conv
+        self.setreg = setreg
         self.small_conv_kper = small_conv_kper
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
@@ -909,6 +910,9 @@ class Specializer:
         # K = 384 gets slower, 0.178 -> 0.194, and keeps two)
         conv_w4 = bool((cb16 and not wide and self.cb16_w4)
                        or (conv and (self.conv_w4 is True or (self.conv_w4 == "auto" and (kp9 or BK == 16 or BN > 128)))))
+        # N = 256 BF16-correction row tiles: six split warps, registers moved from the
+        # producer / split warpgroups to the epilogue ones (nnb_gemm_tc.cuh SETREG)
+        setreg = bool(cb16 and wide and self.setreg and not tmem_a and not aldg)
         hi_off, lo_off = self.pool.add(hi), self.pool.add(bf16_corr_words(hi, lo) if cb16 else lo)
         geo = dict(CONV=0, POOL=0, H=1, W=1, CI=1, HO=1, WO=1, KH=1, KW=1, PT=0, PL=0, PHO=1,
                    PWO=1, C0=1, CONCAT=0, UPF=1, DWF=0)
@@ -920,7 +924,7 @@ class Specializer:
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=(2 if self.rn_ss == 2 else int(bool(self.rn_ss))) if self.split_rn else 0,
-                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4), RS=rs,
+                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4), SETREG=int(setreg), RS=rs,
                       EARLY=int(cb16 and wide and self.early_mma),
                       APF=(self.a_prefetch if (wide and not conv) else 0),
                       PAIR=int(pair),
@@ -1050,7 +1054,8 @@ class Specializer:
             if edw is not None:
                 tag = ("conv1x1_gap_tc" if edw.kind == "Pool"
                        else f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc")
-        self.emit(pos, tag, "nnb::GemmTc", fields, 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
+        self.emit(pos, tag, "nnb::GemmTc", fields,
+                  512 if setreg else 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
                   n_min=n_min, n_max=n_max, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
@@ -1066,7 +1071,7 @@ class Specializer:
                        f"{' 8x16-pixel conv tiles' if conv else ' row tiles'}"
                        f"{' concat (2 A maps)' if conv and conv.get('CONCAT') else ''}"
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
-                       f"{' bf16 corr' if cb16 else ''}"
+                       f"{' bf16 corr' if cb16 else ''}{' 6 split warps (setmaxnreg)' if setreg else ''}"
                        f"{' + pooled second store' if dp is not None else ''}"
                        f"{' + global average pool in the epilogue' if edw is not None and edw.kind == 'Pool' else ' + depthwise conv in the epilogue' if edw is not None else ''}"
                        f"{f' ({eband} bands of {128 // u.output_shape.w} rows per image)' if eband else ''}"

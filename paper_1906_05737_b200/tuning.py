@@ -72,6 +72,7 @@ class Tuning:
     small_conv_kper: int = 16
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
     early_mma: bool = True         # N = 256 BF16-correction tiles: main MMAs before the split
+    setreg: bool = True            # ... with six split warps and setmaxnreg register reallocation
 
     def specializer_kwargs(self):
         """Keyword arguments of kernels.Specializer (the selection constants
