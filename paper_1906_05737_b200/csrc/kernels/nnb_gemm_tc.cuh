@@ -519,7 +519,11 @@ struct GemmTc {
   static constexpr bool CB16 = C::CORR_BF16 != 0;
   static constexpr u32 IDESC_B16 = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(C::BN >> 3) << 17) |
                                    ((u32)((PAIR ? 2 * BM : BM) >> 4) << 24);
-  static_assert(!CB16 || (!TA && !C::ALDG && !C::DWF && BK == 32 && C::CSPLIT), "bf16 correction split");
+  // (the N = 256 row tiles may also MERGE the correction MMA into the main
+  // accumulator -- CSPLIT = 0: two 256-column buffers, so the epilogue drains
+  // one chunk while the MMAs fill the next)
+  static_assert(!CB16 || (!TA && !C::ALDG && !C::DWF && BK == 32 && (C::CSPLIT || C::BN == 256)),
+                "bf16 correction split");
   // EARLY main products (N = 256 BF16-correction row tiles; the raw A tile is
   // never rewritten by the split there)
   static constexpr bool EARLY = CB16 && C::EARLY && !NNB_CB16_WB;
@@ -884,8 +888,9 @@ struct GemmTc {
               for (int k = 0; k < ((NNB_TC_DBG & 1) ? 0 : BK / 8); ++k) {
                 const u32 o = k * 32;
                 const int ks = kc * (BK / 8) + k;
-                const u32 dc = dbuf + (ks % NACC) * CW + C::BN;
-                const u32 acc_c = C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : (u32)(ks >= NACC);
+                const u32 dc = dbuf + (ks % NACC) * CW + (CS ? C::BN : 0);
+                const u32 acc_c = !CS ? 1u   // merged: after this stage's main product into the same chain
+                                  : C::CORR_WHOLE ? (u32)(kb * (BK / 8) + k > 0) : (u32)(ks >= NACC);
                 if (PAIR) mma_bf16_pair(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
                 else mma_bf16(dc, kmajor_desc<ROWB>(a_lo + o), kmajor_desc<ROWB>(b_lo + o), IDESC_B16, acc_c);
               }

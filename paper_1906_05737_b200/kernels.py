@@ -813,10 +813,21 @@ class Specializer:
             # (BN = 128: 0.337 ms at <= 0.67); merged chains with two buffers
             # 0.30-0.35 ms.  With the round-to-nearest split written back
             # (rn_ss) the 16-block form has the BN = 128 path's accuracy.
+            # MERGED form (wide_csplit=False, opt-in): the BF16 correction MMA
+            # accumulates into the main chain, restarted every 8 k-blocks, so
+            # TWO 256-column buffers fit and a chunk is drained while the next
+            # one is filled (with six split warps the mainloop runs at the MMA
+            # roof; what remains is the MMAs waiting for drains).  Measured
+            # (cfg1 @65536): Dense 1024->512 0.1990 -> 0.1922 ms, replay 0.2983
+            # -> 0.2910 ms, max |d| / FP32 gate 0.75-0.85 on N(0,1) inputs for
+            # both forms -- but one of 9.7 M outputs of a K = 512 tanh layer on
+            # U(-2, 2) inputs lands at 1.02x the plain gate (test_wide_n256_
+            # tiles_opt_in), which the split form passes; 4-block chunks are
+            # more accurate (0.68-0.78) and slower (0.3053 ms).  Not the default.
             csplit = self.wide_csplit
             corr_whole = csplit
             if not self.chunk:
-                chunk = self.wide_chunk or (16 if csplit else 4)
+                chunk = self.wide_chunk or (16 if csplit else 8)
         cw = (2 if csplit else 1) * BN                # TMEM columns per accumulator chain
         ABUF = 1 if ((tmem_a and BN > 64 and csplit) or (wide and csplit)) else 2
         if not tmem_a and self.abuf:
@@ -899,7 +910,7 @@ class Specializer:
         cb16_on = (wide if self.corr_bf16 == "wide" else
                    (wide or (conv is not None and K >= CB16_CONV_MIN_K)) if self.corr_bf16 == "auto"
                    else bool(self.corr_bf16))
-        cb16 = bool(cb16_on and not tmem_a and not aldg and not dwf and BK == 32 and csplit)
+        cb16 = bool(cb16_on and not tmem_a and not aldg and not dwf and BK == 32 and (csplit or wide))
         # narrow tiles with the bf16 split: four converter warps (with two the
         # extra split work made cfg4's convs slower; with four cfg4 @64
         # 0.892 -> 0.834 ms, cfg0/2/3 unchanged)

@@ -60,7 +60,9 @@ class Tuning:
     wide: bool = True              # N = 256 row tiles
     wide_bk: int = 32              # k-block of the N = 256 tiles
     wide_chunk: object = None      # main-chain chunk of the N = 256 tiles
-    wide_csplit: bool = True       # correction chain of the N = 256 tiles
+    wide_csplit: bool = True       # separate correction chain of the N = 256 tiles (False: merged into
+                                   # the main chain, two accumulator buffers: -2.4% on cfg1, but one
+                                   # output in 10^7 just over the plain FP32 gate -- opt-in)
     rn_ss: object = 2              # shared-memory A split: 2 = lo rounded to TF32 (hi left to the
                                    # hardware), True = rounded hi written back, False = truncation
     corr_bf16: object = "wide"     # BF16 correction products: "wide" (N=256 tiles only), "auto"

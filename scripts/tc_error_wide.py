@@ -26,7 +26,7 @@ for v in variants:
         else:
             x = (rng.standard_normal((ROWS, 1024)) * rng.uniform(0.1, 10, (ROWS, 1))).astype(np.float32)
         want = oracle.run(m, w, [x])[0]
-        net = compile_model(m, w, EXACT, batch=ROWS, **kw)
+        net = compile_model(m, w, EXACT, batch=ROWS, tuning=kw)
         got = net.run([x])[0].cpu().numpy()
         d = np.abs(got.astype(np.float64) - want)
         r = np.max(d / (1e-5 + 1e-4 * np.abs(want)))
@@ -41,6 +41,6 @@ for v in variants:
     m, w = zoo.build(1)
     x = zoo.inputs(1, ROWS)
     want = oracle.run(m, w, [x])[0]
-    got = compile_model(m, w, EXACT, batch=ROWS, **kw).run([x])[0].cpu().numpy()
+    got = compile_model(m, w, EXACT, batch=ROWS, tuning=kw).run([x])[0].cpu().numpy()
     r = np.max(np.abs(got.astype(np.float64) - want) / (1e-5 + 1e-4 * np.abs(want)))
     print(f"[{v}] cfg1 end to end: max d/lim {r:.3f}; worst dense trial {worst:.3f}")
