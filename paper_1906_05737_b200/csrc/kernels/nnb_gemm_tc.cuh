@@ -528,7 +528,19 @@ struct GemmTc {
   // never rewritten by the split there)
   static constexpr bool EARLY = CB16 && C::EARLY && !NNB_CB16_WB;
   static constexpr int SPLIT_UNROLL = NNB_SPLIT_UNROLL;
-  static constexpr int EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
+  // EPI16 (KPACK conv tiles with CO = 32): SIXTEEN epilogue warps -- four
+  // per TMEM lane quarter, each draining and combining a quarter of the
+  // output channels.  Those tiles are bound by the epilogue's dependent chain
+  // per tile (drain, shuffles, pooled store, staged store: cfg4's 120x160x16
+  // -> 32 conv runs 88 us with the mainloop ablated, 78 us with the epilogue
+  // ablated); half the channels per warp was meant to shorten the chain.
+  // Measured: bit-identical but SLOWER (109.5 -> 118 us; the 60x80x128 -> 32
+  // conv 145.8 -> 153 us) -- 8-channel groups halve the bytes per store and
+  // the extra warps add TMEM / shuffle contention.  Opt-in (tuning epi16).
+  static constexpr int EPI_WARPS = C::EPI16 ? 16 : 8, EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int EPI_GROUPS = EPI_WARPS / 4;               // column groups (warps per lane quarter)
+  static_assert(!C::EPI16 || (C::KPACK && C::CO == 32 && C::CONV && !C::EPI_TMA && !C::EDW && !C::HEAD &&
+                              !C::SETREG), "sixteen epilogue warps: KPACK conv tiles with 32 outputs");
   // ALDG: the A operand is gathered by the four loader/converter warps with
   // cp.async (16-byte LDGSTS, zero-fill for padding) straight into the swizzled
   // layout, instead of per-row TMA requests (which cap A at ~16-28 B/cycle/SM).
@@ -1452,7 +1464,7 @@ struct GemmTc {
         }
         if constexpr (KP && !(C::CO / 2 > 16 && NCHUNK == 1 && NACC == 1)) {
           // ---- packed horizontal taps: reduce chunks, combine across lanes ----
-          constexpr int GCO = C::CO / 2;                 // output channels per warp group
+          constexpr int GCO = C::CO / EPI_GROUPS;        // output channels per warp group
           static_assert(GCO == 8 || GCO % 16 == 0, "KPACK staged store width");
           const int g = (warp - EPI_W0) >> 2;
           float run[C::KW][GCO];

@@ -242,7 +242,7 @@ class Specializer:
                  kpack=True, kpack9=True, kpack_wide=True, tiny=False, early_mma=True, epi_tma=True, csplit=True, chunk=None, split_rn=True,
                  pair=True, tc_tile_use=0.75, mega=False, abuf=None, small_dense_rows=SMALL_DENSE_ROWS, tc_min_images=TC_MIN_IMAGES,
                  tc_min_k=TC_MIN_K, wide=True, wide_bk=32, wide_chunk=None,
-                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, small_conv=True, small_conv_kper=16, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None, setreg=True):
+                 wide_csplit=True, rn_ss=2, corr_bf16="wide", cb16_w4=True, conv_w4="auto", rowshare=True, small_conv=True, small_conv_kper=16, a_prefetch=0, narrow=True, direct_imm=True, sep_fma=True, narrow_geo=None, head=True, sep_geo=None, setreg=True, epi16=False):
         self.use_tc = use_tc
         self.sep_geo = sep_geo
         self.corr_bf16 = corr_bf16
@@ -250,6 +250,7 @@ class Specializer:
         self.rowshare = rowshare
         self.small_conv = small_conv
         self.setreg = setreg
+        self.epi16 = epi16
         self.small_conv_kper = small_conv_kper
         self.cb16_w4 = cb16_w4
         self.a_prefetch = a_prefetch
@@ -866,7 +867,10 @@ class Specializer:
         if edw is not None:
             epi_tma = False        # the finished tile is parked in shared memory instead
         nbuf = (egrp if res else min(egrp, 2)) if epi_tma else 1
-        epi_bytes = 8 * nbuf * 2048
+        # KPACK conv tiles with 32 outputs: sixteen epilogue warps (nnb_gemm_tc.cuh EPI16) --
+        # bit-identical, measured SLOWER (cfg4 @64: 109.5 -> 118 us, 145.8 -> 153 us): opt-in
+        epi16 = bool(kpack and CO_real == 32 and self.epi16 and edw is None)
+        epi_bytes = (16 if epi16 else 8) * nbuf * 2048
         if edw is not None:
             epi_bytes = -(-(128 * (BN + 4) * 4) // 1024) * 1024
         # deep rings hide the TMA/L2 latency when a stage carries little MMA work
@@ -935,7 +939,7 @@ class Specializer:
                       ROWS=rows, TMEM_A=tmem_a,
                       NACC=NACC, ALDG=aldg, ABUF=ABUF, CSPLIT=int(csplit), CHUNK=chunk,
                       CORR_WHOLE=int(corr_whole), RN_SS=(2 if self.rn_ss == 2 else int(bool(self.rn_ss))) if self.split_rn else 0,
-                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4), SETREG=int(setreg), RS=rs,
+                      CORR_BF16=int(cb16), CONV_W4=int(conv_w4), SETREG=int(setreg), EPI16=int(epi16), RS=rs,
                       EARLY=int(cb16 and wide and self.early_mma),
                       APF=(self.a_prefetch if (wide and not conv) else 0),
                       PAIR=int(pair),
@@ -1066,7 +1070,8 @@ class Specializer:
                 tag = ("conv1x1_gap_tc" if edw.kind == "Pool"
                        else f"conv1x1_dw{edw.kernel_hw[0]}x{edw.kernel_hw[1]}_tc")
         self.emit(pos, tag, "nnb::GemmTc", fields,
-                  512 if setreg else 448 if (tmem_a or aldg or dwf or conv_w4) else 384, smem,
+                  (512 if setreg else 448 if (tmem_a or aldg or dwf or conv_w4) else 384)
+                  + (256 if epi16 else 0), smem,
                   ipi, ipb,
                   grid_mult=ntn * (2 if pair else 1), cluster=2 if pair else 1,
                   n_min=n_min, n_max=n_max, tmaps=[tm_a, tm_b, tm_bl, tm_a1, tm_o, tm_r], code=code,
@@ -1083,6 +1088,7 @@ class Specializer:
                        f"{' concat (2 A maps)' if conv and conv.get('CONCAT') else ''}"
                        f"{' A in TMEM' if tmem_a else ''}{' TMA epilogue' if epi_tma and not hn else ''}"
                        f"{' bf16 corr' if cb16 else ''}{' 6 split warps (setmaxnreg)' if setreg else ''}"
+                       f"{' 16 epilogue warps' if epi16 else ''}"
                        f"{' + pooled second store' if dp is not None else ''}"
                        f"{' + global average pool in the epilogue' if edw is not None and edw.kind == 'Pool' else ' + depthwise conv in the epilogue' if edw is not None else ''}"
                        f"{f' ({eband} bands of {128 // u.output_shape.w} rows per image)' if eband else ''}"

@@ -75,6 +75,7 @@ class Tuning:
     a_prefetch: int = 0            # L2 prefetch distance of A boxes (k-blocks)
     early_mma: bool = True         # N = 256 BF16-correction tiles: main MMAs before the split
     setreg: bool = True            # ... with six split warps and setmaxnreg register reallocation
+    epi16: bool = False            # KPACK conv tiles with 32 outputs: sixteen epilogue warps (measured slower)
 
     def specializer_kwargs(self):
         """Keyword arguments of kernels.Specializer (the selection constants
