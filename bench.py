@@ -551,6 +551,10 @@ def main():
                     t_s = roofline.survey_layerwise_roof_s(rp, big, peaks["hbm_gbs"],
                                                            roofline.fp32_peak_tflops())
                     lr_us, _ = roofline.layer_roofline(netb, rp, big, peaks, ffma[0])
+                    # cold compile(): NVRTC of every kernel of a replay over `big` images, no cubin cache
+                    cold = compile_model(*zoo.build(c), opts, batch=big, device=local, cache_dir="")
+                    cold_ms = cold.compile_ms
+                    del cold
                     e = {"batch": big, "ms": ms_b, "images_per_s": big / (ms_b / 1e3),
                          "batch1_latency_us": ms_1 * 1e3,
                          "launches": len(netb.launches_for(big)),
@@ -561,7 +565,7 @@ def main():
                                           for k, v in r.items()} for r in rws],
                          "survey_ffma_only_frac": t_s * 1e3 / ms_b,
                          "gflop_per_batch": big * roofline.total_flops(rp) / 1e9,
-                         "compile_ms": netb.compile_ms}
+                         "compile_ms": netb.compile_ms, "cold_compile_ms": cold_ms}
                     if name in ref_b1 and "batch1_latency_us" in ref_b1[name]:
                         e["reference_cpu"] = ref_b1[name]
                         e["batch1_speedup_vs_reference_cpu"] = (

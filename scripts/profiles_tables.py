@@ -29,8 +29,9 @@ def main(bench, ref=None):
           f"{rl['algorithmic_per_launch']['bytes'] / 1e6:.0f} MB algorithmic.\n")
     print("| config | batch | ms | images/s | roof µs | roofline frac (per fused launch) | per-layer roof µs "
           "| frac of the per-layer roofline | launches | batch-1 µs (L2 flushed) "
-          "| reference CPU batch-1 µs | speed-up at batch 1 |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
+          "| reference CPU batch-1 µs | speed-up at batch 1 | cold compile() ms (no cubin cache) "
+          "| reference compile ms |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for name, v in d["configs"].items():
         rc = (r or {}).get("configs", {}).get(name, {}) if r else {}
         rb1 = rc.get("batch1_latency_us") or (v.get("reference_cpu") or {}).get("batch1_latency_us")
@@ -38,7 +39,8 @@ def main(bench, ref=None):
         print(f"| {name} | {v['batch']} | {v['ms']:.4f} | {v['images_per_s'] / 1e6:.3f} M | {v['roof_us']:.1f} "
               f"| {v['roofline_frac']:.3f} | {v.get('layer_roof_us', float('nan')):.1f} "
               f"| {v.get('layer_roofline_frac', float('nan')):.3f} | {v['launches']} "
-              f"| {v['batch1_latency_us']:.1f} | {tail} |")
+              f"| {v['batch1_latency_us']:.1f} | {tail} | {v.get('cold_compile_ms', float('nan')):.0f} "
+              f"| {(v.get('reference_cpu') or {}).get('compile_ms', float('nan')):.0f} |")
     for name, v in d["configs"].items():
         print(f"\n### {name} @ {v['batch']}: replay {v['ms'] * 1e3:.1f} µs, roof {v['roof_us']:.1f} µs\n")
         print("| launch | pipe | GFLOP | MB | roof µs (bound) | measured µs | frac |")
