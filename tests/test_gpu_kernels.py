@@ -769,6 +769,10 @@ def test_dual_pooled_store(h, w, ci, co, up, n, tc):
     (16, 8, 16, [("p", 64, "relu"), ("d", 3, 2, "same", "relu6"), ("p", 64, "relu6"),
                  ("d", 3, 2, "valid", "linear"), ("p", 32, "relu"), ("d", 3, 2, "same", "tanh")],
      False, True),
+    # one image per tile (16x8 = 128 pixels), then a 1x1 map (128 images per tile: only the centre tap)
+    (16, 8, 32, [("p", 64, "relu"), ("d", 3, 1, "same", "relu6"), ("p", 32, "linear"),
+                 ("d", 5, 2, "same", "relu")], False, False),
+    (1, 1, 32, [("p", 64, "tanh"), ("d", 3, 1, "same", "relu"), ("p", 32, "linear")], False, True),
     # band tiles: cfg3's 16x16 stage (3 bands of 8 rows per image; stride 1, then 2 to 8x8)
     (16, 16, 32, [("p", 64, "relu6"), ("d", 3, 1, "same", "relu6"), ("p", 64, "relu6"),
                   ("d", 3, 2, "same", "relu6"), ("p", 128, "relu6"), ("d", 3, 1, "same", "linear"),
